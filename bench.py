@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""RBGS QR throughput benchmark (BASELINE.json metric: GB/s of W processed,
+% of HBM roofline, at 1/2/4/8 B200).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2|c1|c3|c5shard]
+                    [--order reference|fma] [--impl b200|reference]
+
+A step is one complete RBGS QR factorization (`rbgs.rbgs`, every block:
+sketch, LS solve, projection, inter-block QR, final certification) of the
+synthetic W of the chosen BASELINE config, W resident in HBM.  Default:
+configs[1] (C2: n = 1e6 x m = 800, p = 40, gaussian k = 1600, two-precision).
+With N > 1 (torchrun) the rows are sharded, n = N x n_config (weak scaling),
+and each block's sketches are summed with one NCCL allreduce.
+
+`e2e` is the same metric through the public API with host buffers: a pinned
+host W is copied to the device inside every timed step and R is read back.
+`--impl reference` times the CPU restatement of the reference (oracle/) on a
+bounded row sample of the same workload with all host threads.
+"""
+
+from __future__ import annotations
+
+import os
+
+_CORES = len(os.sched_getaffinity(0))
+if "--impl" in os.sys.argv and "reference" in os.sys.argv:
+    for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ.setdefault(_v, str(_CORES))
+
+import argparse  # noqa: E402
+import json  # noqa: E402
+import math  # noqa: E402
+import statistics  # noqa: E402
+import subprocess  # noqa: E402
+import sys  # noqa: E402
+import threading  # noqa: E402
+import time  # noqa: E402
+
+import numpy as np  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "c2": dict(name="C2", n=1_000_000, m=800, p=40, k=1600, kind="gaussian", gen="trig", dtype="f32",
+               coarse="coarse", desc="RBGS QR two-precision, trig family 1e6 x 800, p=40, gaussian k=1600"),
+    "c1": dict(name="C1", n=20_000, m=200, p=10, k=400, kind="gaussian", gen="trig", dtype="f64",
+               coarse="fine", desc="RBGS QR fp64 throughout, trig family 20000 x 200, p=10, gaussian k=400"),
+    "c3": dict(name="C3", n=1 << 24, m=512, p=32, k=1024, kind="srht", gen="lowrank", dtype="f32",
+               coarse="coarse", desc="RBGS QR two-precision, U diag(s) V^T 2^24 x 512, p=32, SRHT k=1024"),
+    "c5shard": dict(name="C5-shard", n=1 << 24, m=1024, p=64, k=2048, kind="gaussian", gen="colscaled",
+                    dtype="f32", coarse="coarse",
+                    desc="RBGS QR two-precision, per-GPU shard of C5: 2^24 x 1024, p=64, gaussian k=2048"),
+}
+SEED_W, SEED_THETA = 7, 11
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops", 1658.3)), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and
+                          r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU restatement (oracle) -- the reference arm and the cpu_baseline leg
+
+def _oracle_sample(cfgd, n_s):
+    """One RBGS QR of an n_s-row sample of the workload with the CPU oracle;
+    the gaussian table is materialised beforehand (operator construction),
+    like the reference's SRHT tables.  Returns seconds."""
+    from oracle import sketches as osk
+    from oracle import sweep as osw
+    from paper_2111_14641_b200 import workloads as WL
+
+    m, p, k = cfgd["m"], cfgd["p"], min(cfgd["k"], n_s)
+    if cfgd["gen"] == "trig":
+        W = WL.trig_host(n_s, m, SEED_W)
+    else:
+        g = np.random.Generator(np.random.Philox(SEED_W))
+        W = g.standard_normal((n_s, m)) * np.logspace(0, -6, m)
+    if cfgd["dtype"] == "f32":
+        W = W.astype(np.float32).astype(np.float64)
+    op = osk.materialize(osk.OracleSketch(cfgd["kind"], k, n_s, SEED_THETA))
+    cfg = osw.OracleConfig(osw.uniform_widths(m, p), interblock="sketched_cholqr(1)",
+                           coarse=cfgd["coarse"])
+    t0 = time.perf_counter()
+    osw.rbgs(W, op, cfg)
+    return time.perf_counter() - t0
+
+
+def reference_arm(args, cfgd):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_s = args.sample_rows or 4096
+    times = []
+    for it in range(args.warmup + args.steps):
+        t = _oracle_sample(cfgd, n_s)
+        if it >= args.warmup:
+            times.append(t)
+    sec = sum(times) / len(times)
+    s = 4 if cfgd["dtype"] == "f32" else 8
+    val = s * n_s * cfgd["m"] / sec / 1e9
+    cpu = {"value": val, "unit": "GB/s", "cores": _CORES, "kind": "port",
+           "sample": f"{n_s} x {cfgd['m']} rows of {cfgd['name']} (same m, p, k-kind), one factorization "
+                     f"per step, oracle/ restatement (numpy + OpenBLAS, {_CORES} threads)"}
+    line = {"metric": "RBGS QR GB/s of W processed", "value": val, "unit": "GB/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32-coarse/f64-fine" if cfgd["dtype"] == "f32" else "f64", "data": "synthetic",
+            "config": {"workload": cfgd["desc"], "sample_rows": n_s},
+            "cpu_baseline": cpu, "e2e": {"value": val, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                                         "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the GPU arm
+
+def gpu_arm(args, cfgd):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2111_14641_b200 import _device as D
+    from paper_2111_14641_b200 import _lib, sketching, workloads
+    from paper_2111_14641_b200.comm import Comm, RowShard
+    from paper_2111_14641_b200.kernels import COARSE, FINE, BlockPartition
+    from paper_2111_14641_b200.rbgs import DeviceConfig, RbgsConfig, rbgs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    n_per, m, p, k = cfgd["n"], cfgd["m"], cfgd["p"], cfgd["k"]
+    n = n_per * world
+    shard = RowShard(n, rank * n_per, n_per)
+    dtype = torch.float32 if cfgd["dtype"] == "f32" else torch.float64
+    esz = 4 if dtype == torch.float32 else 8
+    # --- inputs (not timed) ---
+    if cfgd["gen"] == "trig":
+        W = workloads.trig_device(n, m, SEED_W, shard.row0, n_per, dtype, dev)
+    elif cfgd["gen"] == "lowrank":
+        W = workloads.lowrank_device(n_per, m, SEED_W, dtype=dtype, device=dev, rank=rank)
+    else:
+        W = workloads.colscaled_gaussian_device(n_per, m, SEED_W, dtype=dtype, device=dev, rank=rank)
+    if cfgd["kind"] == "gaussian":
+        theta = sketching.gaussian_operator(k, n, SEED_THETA)
+        theta.device_tables(dev, shard.row0, n_per)
+    else:
+        theta = sketching.SketchOperator(cfgd["kind"], k, n, SEED_THETA)
+        theta.device_tables(dev)
+    cfg = RbgsConfig(partition=BlockPartition.uniform(m, p), interblock="sketched_cholqr(1)",
+                     coarse=COARSE if cfgd["coarse"] == "coarse" else FINE)
+    dc = DeviceConfig(device=dev, projection_order=args.order, comm=Comm(group) if group else None,
+                      shard=shard if world > 1 else None)
+    torch.cuda.synchronize()
+
+    def step():
+        return rbgs(W, theta, cfg, dc)
+
+    for _ in range(args.warmup):
+        f = step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if group is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # --- timed region: K factorizations, W resident in HBM ---
+    n0 = _lib.launch_count()
+    with Clocks(local) as clk, D.timed_kernels() as timer:
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            f = step()
+        e1.record()
+        barrier()
+    launches = _lib.launch_count() - n0
+    ms = e0.elapsed_time(e1) / args.steps
+    if group is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ksum = timer.summary()
+    cert = f.cert
+    wbytes = esz * n * m
+    value = wbytes / (ms * 1e-3) / 1e9
+
+    # --- e2e: pinned host W -> device inside the step, R read back ---
+    e2e = None
+    if not args.no_e2e:
+        Wh = torch.empty((m, n_per), dtype=dtype).pin_memory().t()
+        Wh.copy_(W)
+        del W
+        torch.cuda.empty_cache()
+        e2e_steps = max(1, min(args.steps, 3))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            fe = rbgs(Wh, theta, cfg, dc)
+            Rh = fe.R.data  # device -> host read of the result
+        barrier()
+        sec = (time.perf_counter() - t0) / e2e_steps
+        if group is not None:
+            t = torch.tensor([sec], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sec = float(t.item())
+        e2e = {"value": wbytes / sec / 1e9, "unit": "GB/s", "h2d_bytes_per_step": esz * n_per * m,
+               "d2h_bytes_per_step": int(Rh.nbytes), "ms_per_step": sec * 1e3}
+
+    # --- roofline of the dominant kernel ---
+    hbm, bf16, src = _peaks()
+    dom = max(ksum.items(), key=lambda kv: kv[1]["ms"]) if ksum else None
+    roof = None
+    if dom:
+        name, d = dom
+        per_ms = d["ms"] / d["calls"]
+        ach = d["bytes"] / d["calls"] / (per_ms * 1e-3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+                traffic = json.load(fh).get(f"{cfgd['name']}:{name}")
+        except Exception:
+            pass
+        roof = {"bound": "hbm", "kernel": name, "achieved": ach, "peak": hbm, "unit": "GB/s",
+                "frac": ach / hbm, "traffic": traffic, "peak_source": src,
+                "share_of_step": d["ms"] / args.steps / ms,
+                "bytes_per_launch": d["bytes"] / d["calls"], "ms_per_launch": per_ms}
+    kernels = {kname: {"ms_per_step": d["ms"] / args.steps, "calls_per_step": d["calls"] / args.steps,
+                       "GBps": d["bytes"] / (d["ms"] * 1e-3) / 1e9,
+                       "TFLOPs": d["flops"] / (d["ms"] * 1e-3) / 1e12}
+               for kname, d in ksum.items()}
+    alg = esz * n * p * (cfg.partition.num_blocks * (cfg.partition.num_blocks + 1) / 2
+                         + 4 * cfg.partition.num_blocks - 2)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n_s = args.sample_rows or 8192
+        sec = _oracle_sample(cfgd, n_s)
+        cpu = {"value": esz * n_s * m / sec / 1e9, "unit": "GB/s", "cores": _CORES, "kind": "port",
+               "sample": f"{n_s} x {m} rows of {cfgd['name']}, one factorization, oracle/ restatement "
+                         f"(numpy + OpenBLAS)"}
+    if rank == 0:
+        line = {
+            "metric": "RBGS QR GB/s of W processed", "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32-coarse/f64-fine" if cfgd["coarse"] == "coarse" else "f64", "data": "synthetic",
+            "config": {"workload": cfgd["desc"], "n": n, "m": m, "p": p, "k": k, "sketch": cfgd["kind"],
+                       "interblock": "sketched_cholqr(1)", "ls_solver": "richardson(5)",
+                       "projection_order": args.order, "parallelism": f"rows{world}",
+                       "l2": "inputs larger than L2 (W = %.1f GB)" % (wbytes / 1e9)},
+            "roofline": roof,
+            "algorithmic_roofline": {"bytes_per_factorization": alg, "GBps": alg / (ms * 1e-3) / 1e9,
+                                     "frac": alg / (ms * 1e-3) / 1e9 / hbm / world},
+            "kernels": kernels,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "cert": {"delta": cert.delta, "delta_tilde": cert.delta_tilde},
+        }
+        print(json.dumps(line), flush=True)
+    if group is not None:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--order", default="reference", choices=["reference", "fma"])
+    ap.add_argument("--sample-rows", type=int, default=None,
+                    help="rows of the CPU sample (default 4096 reference arm, 8192 cpu_baseline)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfgd = CONFIGS[args.config]
+    if args.impl == "reference":
+        reference_arm(args, cfgd)
+    else:
+        gpu_arm(args, cfgd)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,178 @@
+/*
+ * rbgs_b200.h -- C ABI of the B200-native RBGS hot path (libs rbgs_b200.so).
+ *
+ * The reference (`sketch_krylov`, pure Python) has no FFI layer: its
+ * boundary is the Python API of `rbgs.py` / `sketching.py` / `krylov.py`.
+ * Each entry point below replaces one numeric site of that API (SURVEY.md
+ * section 2, "kernel sites" K1-K10); the citation on each names the
+ * reference lines it stands in for.  The Python host layer
+ * (`paper_2111_14641_b200/rbgs.py` etc.) mirrors the reference API and calls
+ * these through ctypes; INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - every matrix pointer is DEVICE memory, column-major, leading dimension
+ *     in elements (ld >= rows);
+ *   - `dtype` arguments take RB_F32 / RB_F64;
+ *   - `row0` is the global index of local row 0 (row sharding: the sketch
+ *     operators are keyed by global row, so shards compose by summation);
+ *   - every call is asynchronous on `stream` (a cudaStream_t, NULL = legacy
+ *     default stream) and never synchronises the host;
+ *   - return value: RB_OK, or a negative RB_E* code with a message in
+ *     rb_last_error();  numerical failures (non-PD pivot) are reported
+ *     through device-side `info` words, as LAPACK does;
+ *   - reductions over rows are two-stage with a fixed grid, so results are
+ *     bit-reproducible run to run on the same device.
+ */
+#ifndef RBGS_B200_H
+#define RBGS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RB_OK 0
+#define RB_EINVAL (-1)   /* bad argument or shape                        */
+#define RB_ECUDA (-2)    /* CUDA launch / runtime error                  */
+#define RB_EWS (-3)      /* workspace too small                          */
+
+#define RB_F32 0
+#define RB_F64 1
+
+/* Step-3 arithmetic order in coarse mode */
+#define RB_ORDER_REFERENCE 0  /* separately rounded multiply and subtract  */
+#define RB_ORDER_FMA 1        /* fused multiply-subtract (not bit-exact)    */
+
+const char* rb_version(void);
+const char* rb_last_error(void);
+/* Number of kernels this process has launched through the library. */
+unsigned long long rb_launch_count(void);
+/* Bytes of device workspace the sketch / reduction calls below may use for
+ * an n-row, ncols-column, k-row problem (upper bound). */
+size_t rb_workspace_bytes(int64_t n, int ncols, int k);
+
+/* ---- K3  Step 3 projection (rbgs.py:369-370 -> kernels.py:171-209) -------
+ * Qp = fl(W - Q X) in the reference's elementary order: acc = fl_c(W); for
+ * l = 0..c-1 ascending: acc = fl_c(acc - fl_c(fl_c(Q[:,l]) * fl_c(X[l,:]))),
+ * every multiply and subtract separately rounded in the compute format
+ * (coarse: binary32, fine: binary64; no FMA contraction).  c may be 0.
+ * order = RB_ORDER_FMA (coarse only) fuses each multiply-subtract into one
+ * rounding instead: faster, not bit-identical to the reference.
+ * norms2 (may be NULL) receives { sum W^2, sum Qp^2 } over these rows in
+ * fp64 (rbgs.py:373-374 before the square root).                         */
+int rb_project(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t n, int c, int p,
+               const void* Q, int64_t ldq, const double* X, int64_t ldx,
+               const void* W, int64_t ldw, void* Qp, int64_t ldqp, double* norms2,
+               void* ws, size_t ws_bytes, void* stream);
+
+/* ---- K1/K2  sketches (sketching.py:140-155 and the north-star kinds) -----
+ * out (k x ncols, fp64, col-major, ld ldo) = Theta[:, row0:row0+n] @ X,
+ * summed in fp64.  accumulate != 0 adds into out instead of overwriting.  */
+
+/* gaussian kind: materialise the int16 table q (k x nrows, K-major: entry
+ * (r, i) at theta[r * ldt + i]) for global rows row0..row0+nrows-1.
+ * Definition in DESIGN.md section 3 (Philox4x32-10 + Box-Muller, 2^-11). */
+int rb_gaussian_fill(uint64_t seed, int k, int64_t row0, int64_t nrows,
+                     int16_t* theta, int64_t ldt, void* stream);
+/* out = scale * (q @ X) for an int16 table (gaussian kind; scale =
+ * 1 / (2048 sqrt(k))). */
+int rb_sketch_dense_i16(int x_dtype, int64_t n, int ncols, const void* X, int64_t ldx,
+                        const int16_t* theta, int64_t ldt, int k, double scale,
+                        double* out, int64_t ldo, int accumulate,
+                        void* ws, size_t ws_bytes, void* stream);
+/* srht kind (sketching.py:129-137): signs as a bitmask over the GLOBAL
+ * padded index space (bit i set <=> sign_diagonal[i] = -1), sample = the
+ * k global sample indices, scale = 1/sqrt(k).  Rows >= n_valid (global)
+ * are the zero padding.  row0 must be a multiple of 2048 unless n_pad <= 2048. */
+int rb_sketch_srht(int x_dtype, int64_t n, int ncols, const void* X, int64_t ldx,
+                   int64_t row0, int64_t n_pad, const uint32_t* sign_bits,
+                   const int64_t* sample, int k, double scale,
+                   double* out, int64_t ldo, int accumulate,
+                   void* ws, size_t ws_bytes, void* stream);
+/* sparse_sign kind: s = min(nnz, k) nonzeros +-1/sqrt(s) per column of
+ * Theta, rows from the Philox word stream. */
+int rb_sketch_sparse_sign(int x_dtype, int64_t n, int ncols, const void* X, int64_t ldx,
+                          int64_t row0, uint64_t seed, int k, int nnz,
+                          double* out, int64_t ldo, int accumulate,
+                          void* ws, size_t ws_bytes, void* stream);
+/* rademacher kind (sketching.py:151-155): k x n sign bits (row r at
+ * bits + r * ldb words, bit i set <=> sign -1), out = scale * S @ X. */
+int rb_sketch_signs(int x_dtype, int64_t n, int ncols, const void* X, int64_t ldx,
+                    const uint32_t* bits, int64_t ldb, int k, double scale,
+                    double* out, int64_t ldo, int accumulate,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* ---- K5  tall triangular scaling (rbgs.py:284, kernels.py:250-270) ------
+ * Xout = B R^{-1} (R p x p upper, fp64), each row solved in fp64 and
+ * rounded to out_dtype.  In place (Xout == B, same dtype) is allowed.     */
+int rb_trsm_right(int in_dtype, int out_dtype, int64_t n, int p, const void* B, int64_t ldb,
+                  const double* R, int64_t ldr, void* Xout, int64_t ldx, void* stream);
+
+/* ---- small fp64 kernels (Steps 2, 4-5, 7; rbgs.py:144-225, 267-290, 428-443)
+ * C = alpha op(A) op(B) + beta C, fp64, op = transpose when trans != 0.    */
+int rb_gemm_f64(int transA, int transB, int m, int n, int k, double alpha,
+                const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                double* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
+/* Tall Gram / cross product: out (p x q fp64) = A^T B for n-row A (n x p)
+ * and B (n x q), inputs f32 or f64, fp64 accumulation (fused l2 stage).  */
+int rb_cross(int a_dtype, int b_dtype, int64_t n, int p, int q, const void* A, int64_t lda,
+             const void* B, int64_t ldb, double* out, int64_t ldo, int accumulate,
+             void* ws, size_t ws_bytes, void* stream);
+/* Upper Cholesky R^T R = G (dpotrf, kernels.py:234-247); *info (device) =
+ * 0 or the 1-based column of the first non-positive pivot.  R's strictly
+ * lower part is zeroed.  G and R may alias.  p <= 1024.                  */
+int rb_potrf_upper(int p, const double* G, int64_t ldg, double* R, int64_t ldr,
+                   int* info, void* stream);
+/* Left solve R X = B (R m x m upper), B m x nrhs overwritten with X.
+ * *info (device) = 0, or 1 + index of the first zero diagonal.          */
+int rb_trsm_left_upper(int m, int nrhs, const double* R, int64_t ldr, double* B, int64_t ldb,
+                       int* info, void* stream);
+/* Economic Householder QR of A (m x q, m >= q, fp64, overwritten by the
+ * explicit Q) with R (q x q upper) and diag(R) >= 0 (kernels.py:216-231).
+ * Single CTA; for the k-dimensional and Hessenberg problems only.        */
+int rb_geqrf_small(int m, int q, double* A, int64_t lda, double* R, int64_t ldr,
+                   void* ws, size_t ws_bytes, void* stream);
+/* Sum of squares of an m x n fp64/f32 matrix, minus the identity when
+ * minus_identity != 0 (certify, rbgs.py:441-442); result written (not
+ * accumulated) to *out.                                                   */
+int rb_sumsq(int dtype, int64_t m, int n, const void* A, int64_t lda, int minus_identity,
+             double* out, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- composite Step-2 / Step-4-5 solvers ---------------------------------
+ * Richardson (rbgs.py:144-156): X (c x p) after l sweeps of
+ * X <- X + S^T (P - S X) from X = 0.  T is a k x p fp64 scratch.         */
+int rb_ls_richardson(int k, int c, int p, const double* S, int64_t lds, const double* P,
+                     int64_t ldp, int l, double* X, int64_t ldx, double* T, int64_t ldt,
+                     void* ws, size_t ws_bytes, void* stream);
+/* One sketched-CholQR pass on the k x p sketch Sp (rbgs.py:282-289):
+ * G = Sp^T Sp, R = chol(G) (info as rb_potrf_upper), Sout = Sp R^{-1}.   */
+int rb_sketched_cholqr_small(int k, int p, const double* Sp, int64_t lds, double* R,
+                             int64_t ldr, double* Sout, int64_t ldso, int* info,
+                             void* ws, size_t ws_bytes, void* stream);
+
+/* ---- K10  operator: 7-point Dirichlet Laplacian (C4, krylov.py:129-130) --
+ * Y = A X on an nx*ny*nz_local slab (x fastest) of the global grid; halo
+ * planes (nx*ny rows each, NULL = Dirichlet boundary) supply the z
+ * neighbours of the first / last local plane.                             */
+int rb_stencil7(int x_dtype, int y_dtype, int nx, int ny, int nz_local, int ncols,
+                const void* X, int64_t ldx, const void* halo_lo, const void* halo_hi,
+                int64_t ldh, void* Y, int64_t ldy, void* stream);
+
+/* General CSR operator (operators.py:57-73): Y = A X, A n x n CSR with
+ * int64 indptr / indices and fp64 values; each output row accumulates its
+ * entries in stored order from 0 (scipy csr_matvecs order).             */
+int rb_csr_spmm(int x_dtype, int y_dtype, int64_t n, int ncols, const int64_t* indptr,
+                const int64_t* indices, const double* values, const void* X, int64_t ldx,
+                void* Y, int64_t ldy, void* stream);
+
+/* ---- misc ---------------------------------------------------------------- */
+/* Y = (out dtype) X elementwise for an m x n matrix (rounding to nearest). */
+int rb_convert(int in_dtype, int out_dtype, int64_t m, int n, const void* X, int64_t ldx,
+               void* Y, int64_t ldy, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RBGS_B200_H */

@@ -196,6 +196,15 @@ def apply(op: OracleSketch, X) -> np.ndarray:
     return np.asfortranarray(_apply(op, X))
 
 
+def materialize(op: OracleSketch) -> OracleSketch:
+    """Cache the dense fp64 matrix of a gaussian operator (operator
+    construction, as the reference does for its SRHT tables), so apply is
+    one BLAS product.  For timing the CPU baseline on row samples."""
+    if op.kind == "gaussian":
+        op.dense = gaussian_int16(op.seed, op.k, np.arange(op.n)).astype(np.float64) * gaussian_scale(op.k)
+    return op
+
+
 def _apply(op: OracleSketch, X) -> np.ndarray:
     X = np.asarray(X, dtype=np.float64)
     if X.ndim == 1:
@@ -209,6 +218,8 @@ def _apply(op: OracleSketch, X) -> np.ndarray:
     if op.kind == "rademacher":
         return rademacher_apply(op, X)
     if op.kind == "gaussian":
+        if getattr(op, "dense", None) is not None:
+            return op.dense @ X
         return gaussian_apply(op.seed, op.k, X)
     M = sparse_sign_matrix(op.seed, op.k, op.nnz, op.n)
     return np.asarray(M @ X)

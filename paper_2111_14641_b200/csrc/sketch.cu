@@ -1,0 +1,415 @@
+// K1/K2: sketches  out = Theta[:, row0:row0+n] @ X  in fp64
+// (rbgs.py:363, :282, :390 -> sketching.py:140-155).
+//
+//  * dense kinds (gaussian int16 table, rademacher sign bits): split-K
+//    register-tiled fp64 GEMM, M = k sketch rows, N = ncols, K = n rows;
+//    per-split partials are reduced in a fixed order (deterministic).
+//  * srht: pruned subsampled Walsh-Hadamard.  Rows are cut in tiles of
+//    T = 2048; with global row i = (g, l), H[s, i] = (-1)^popc(g_s & g) *
+//    (-1)^popc(l_s & l), so each tile needs its own 2048-point FWHT (three
+//    register stages, five warp-shuffle stages, three stages after one
+//    shared-memory transpose) and then only a signed gather at the k sampled
+//    local indices.  This is the Kronecker split H_n = H_G (x) H_T of
+//    SURVEY.md 8(e), with CTAs playing the role of shards.
+//  * sparse_sign: each row i scatters s signed copies of X[i, :] into a
+//    shared-memory k x CG accumulator.
+#include "common.cuh"
+
+namespace rb {
+
+int sm_count();
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// ======================= dense (split-K fp64 GEMM) ==========================
+constexpr int BM = 128, BK = 16, TM = 8;
+
+struct I16Src {
+  const int16_t* t;
+  int64_t ld;
+  __device__ __forceinline__ double at(int r, int64_t i) const { return (double)t[(int64_t)r * ld + i]; }
+};
+struct BitSrc {
+  const uint32_t* b;
+  int64_t ld;  // words per sketch row
+  __device__ __forceinline__ double at(int r, int64_t i) const {
+    const uint32_t w = b[(int64_t)r * ld + (i >> 5)];
+    return ((w >> (i & 31)) & 1u) ? -1.0 : 1.0;
+  }
+};
+
+template <typename TX, typename Src, int TN>
+__global__ void __launch_bounds__(kThreads)
+dense_partial(int64_t n, int ncols, const TX* __restrict__ X, int64_t ldx, Src src, int k,
+              int64_t chunk, double* __restrict__ ws) {
+  constexpr int BN = 16 * TN;
+  __shared__ __align__(16) double sA[BK][BM];
+  __shared__ __align__(16) double sB[BK][BN];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.x * BM;
+  const int64_t kbeg = (int64_t)blockIdx.y * chunk;
+  const int64_t kend = min(n, kbeg + chunk);
+  double acc[TM][TN];
+#pragma unroll
+  for (int a = 0; a < TM; ++a)
+#pragma unroll
+    for (int b = 0; b < TN; ++b) acc[a][b] = 0.0;
+
+  for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
+    __syncthreads();
+    // A tile: BM sketch rows x BK W-rows (K-major source: contiguous in i)
+    for (int e = threadIdx.x; e < BM * BK; e += kThreads) {
+      const int r = e / BK, kk = e % BK;
+      const int64_t i = k0 + kk;
+      sA[kk][r] = (m0 + r < k && i < kend) ? src.at(m0 + r, i) : 0.0;
+    }
+    for (int e = threadIdx.x; e < BN * BK; e += kThreads) {
+      const int j = e / BK, kk = e % BK;
+      const int64_t i = k0 + kk;
+      sB[kk][j] = (j < ncols && i < kend) ? (double)X[i + (int64_t)j * ldx] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      double a[TM], b[TN];
+#pragma unroll
+      for (int q = 0; q < TM; ++q) a[q] = sA[kk][ty * TM + q];
+#pragma unroll
+      for (int q = 0; q < TN; ++q) b[q] = sB[kk][tx * TN + q];
+#pragma unroll
+      for (int q = 0; q < TM; ++q)
+#pragma unroll
+        for (int t = 0; t < TN; ++t) acc[q][t] = fma(a[q], b[t], acc[q][t]);
+    }
+  }
+  // partial layout: ws[split][j][r] (column-major k x ncols per split)
+  double* dst = ws + (int64_t)blockIdx.y * k * ncols;
+#pragma unroll
+  for (int q = 0; q < TM; ++q) {
+    const int r = m0 + ty * TM + q;
+#pragma unroll
+    for (int t = 0; t < TN; ++t) {
+      const int j = tx * TN + t;
+      if (r < k && j < ncols) dst[r + (int64_t)j * k] = acc[q][t];
+    }
+  }
+}
+
+// out[r, j] = scale * sum_s ws[s][j][r]  (+ out when accumulate)
+__global__ void reduce_splits(const double* __restrict__ ws, int splits, int k, int ncols,
+                              double scale, double* __restrict__ out, int64_t ldo, int accumulate) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tot = (int64_t)k * ncols;
+  if (e >= tot) return;
+  double s = 0.0;
+  for (int q = 0; q < splits; ++q) s += ws[(int64_t)q * tot + e];
+  const int r = (int)(e % k), j = (int)(e / k);
+  double* o = out + r + (int64_t)j * ldo;
+  *o = accumulate ? *o + scale * s : scale * s;
+}
+
+template <typename TX, typename Src>
+int dense_sketch(int64_t n, int ncols, const TX* X, int64_t ldx, Src src, int k, double scale,
+                 double* out, int64_t ldo, int accumulate, void* ws, size_t ws_bytes,
+                 cudaStream_t st) {
+  const int mt = ceil_div(k, BM);
+  const int target = 4 * sm_count();
+  int splits = (int)std::max<int64_t>(1, std::min<int64_t>((n + 2047) / 2048, (target + mt - 1) / mt));
+  const size_t per = (size_t)k * ncols * sizeof(double);
+  if ((size_t)splits * per > ws_bytes) splits = (int)std::max<size_t>(1, ws_bytes / per);
+  RB_REQUIRE(ws && (size_t)splits * per <= ws_bytes, "sketch: workspace too small");
+  int64_t chunk = (n + splits - 1) / splits;
+  chunk = (chunk + BK - 1) / BK * BK;
+  splits = (int)std::max<int64_t>(1, (n + chunk - 1) / chunk);
+  dim3 grid(mt, splits);
+  double* w = (double*)ws;
+  if (n == 0) {
+    splits = 0;
+  } else if (ncols <= 16) {
+    RB_KLAUNCH dense_partial<TX, Src, 1><<<grid, kThreads, 0, st>>>(n, ncols, X, ldx, src, k, chunk, w);
+  } else if (ncols <= 32) {
+    RB_KLAUNCH dense_partial<TX, Src, 2><<<grid, kThreads, 0, st>>>(n, ncols, X, ldx, src, k, chunk, w);
+  } else if (ncols <= 48) {
+    RB_KLAUNCH dense_partial<TX, Src, 3><<<grid, kThreads, 0, st>>>(n, ncols, X, ldx, src, k, chunk, w);
+  } else {
+    RB_KLAUNCH dense_partial<TX, Src, 4><<<grid, kThreads, 0, st>>>(n, ncols, X, ldx, src, k, chunk, w);
+  }
+  const int64_t tot = (int64_t)k * ncols;
+  RB_KLAUNCH reduce_splits<<<ceil_div(tot, 256), 256, 0, st>>>(w, splits, k, ncols, scale, out, ldo, accumulate);
+  return check_launch("dense sketch");
+}
+
+// ======================= gaussian table fill ================================
+__global__ void gaussian_fill_kernel(uint64_t seed, int k, int64_t row0, int64_t nrows,
+                                     int16_t* __restrict__ theta, int64_t ldt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int q = blockIdx.y;  // quad of sketch rows 4q..4q+3
+  if (i >= nrows) return;
+  const uint64_t gi = (uint64_t)(row0 + i);
+  const u32x4 w = philox4x32_10(u32x4{(uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)q, kTagGauss},
+                                (uint32_t)seed, (uint32_t)(seed >> 32));
+  const double sc = 2.3283064365386963e-10;  // 2^-32
+  const double ua = ((double)w.x + 0.5) * sc, ub = ((double)w.y + 0.5) * sc;
+  const double uc = ((double)w.z + 0.5) * sc, ud = ((double)w.w + 0.5) * sc;
+  const double r1 = sqrt(-2.0 * log(ua)), r2 = sqrt(-2.0 * log(uc));
+  const double t1 = 6.283185307179586 * ub, t2 = 6.283185307179586 * ud;
+  double s1, c1, s2, c2;
+  sincos(t1, &s1, &c1);
+  sincos(t2, &s2, &c2);
+  const double g[4] = {r1 * c1, r1 * s1, r2 * c2, r2 * s2};
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int r = 4 * q + t;
+    if (r < k) {
+      double v = rint(2048.0 * g[t]);
+      v = fmin(fmax(v, -32767.0), 32767.0);
+      theta[(int64_t)r * ldt + i] = (int16_t)v;
+    }
+  }
+}
+
+// ======================= SRHT ==============================================
+constexpr int kT = 2048;  // tile rows (2^11)
+
+template <int MS, int CG, typename TX>
+__global__ void __launch_bounds__(kThreads)
+srht_partial(int64_t n, int ncols, const TX* __restrict__ X, int64_t ldx, int64_t row0,
+             const uint32_t* __restrict__ sign_bits, const int64_t* __restrict__ sample, int k,
+             int tiles_per_cta, int ntiles, double* __restrict__ ws) {
+  __shared__ __align__(16) double z[kT];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c0 = blockIdx.y * CG;
+  const int cg = min(CG, ncols - c0);
+  // my samples: s = tid + 256 m
+  int ls[MS];
+  int64_t gs[MS];
+#pragma unroll
+  for (int m = 0; m < MS; ++m) {
+    const int s = tid + kThreads * m;
+    const int64_t idx = s < k ? sample[s] : 0;
+    ls[m] = (int)(idx & (kT - 1));
+    gs[m] = idx >> 11;
+  }
+  double acc[MS][CG];
+#pragma unroll
+  for (int m = 0; m < MS; ++m)
+#pragma unroll
+    for (int c = 0; c < CG; ++c) acc[m][c] = 0.0;
+
+  const int tbeg = blockIdx.x * tiles_per_cta;
+  const int tend = min(ntiles, tbeg + tiles_per_cta);
+  const int64_t gtile0 = row0 >> 11;  // global tile of local tile 0
+  for (int t = tbeg; t < tend; ++t) {
+    const int64_t lbase = (int64_t)t * kT;          // local row of element 0
+    const int64_t g = gtile0 + t;                   // global tile index
+    const int64_t gbase = (row0 & ~(int64_t)(kT - 1)) + lbase;  // global row of element 0
+    // sign bits for my 8 rows: elements e = warp*256 + lane*8 + v
+    const int e0 = warp * 256 + lane * 8;
+    const uint32_t word = sign_bits[(gbase + e0) >> 5];
+    const uint32_t sb = (word >> ((gbase + e0) & 31)) & 0xFFu;
+    const int64_t off = (row0 & (kT - 1));  // local row of element e is lbase + e - off
+    // per-sample sign of H_G[g_s, g]
+    double hs[MS];
+#pragma unroll
+    for (int m = 0; m < MS; ++m) hs[m] = (__popcll((unsigned long long)(gs[m] & g)) & 1) ? -1.0 : 1.0;
+    for (int c = 0; c < cg; ++c) {
+      const TX* xc = X + (int64_t)(c0 + c) * ldx;
+      double v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int64_t lr = lbase + e0 + q - off;
+        double x = (lr >= 0 && lr < n) ? (double)xc[lr] : 0.0;
+        v[q] = ((sb >> q) & 1u) ? -x : x;
+      }
+      // stages on bits 0..2 (in register)
+#pragma unroll
+      for (int h = 1; h < 8; h <<= 1)
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (!(q & h)) {
+            const double a = v[q], b = v[q + h];
+            v[q] = a + b;
+            v[q + h] = a - b;
+          }
+      // stages on bits 3..7 (lane bits 0..4)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const bool hi = lane & o;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const double pv = __shfl_xor_sync(0xffffffffu, v[q], o);
+          v[q] = hi ? pv - v[q] : v[q] + pv;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) z[e0 + q] = v[q];
+      __syncthreads();
+      // stages on bits 8..10: element j*256 + tid
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = z[q * 256 + tid];
+#pragma unroll
+      for (int h = 1; h < 8; h <<= 1)
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (!(q & h)) {
+            const double a = v[q], b = v[q + h];
+            v[q] = a + b;
+            v[q + h] = a - b;
+          }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 8; ++q) z[q * 256 + tid] = v[q];
+      __syncthreads();
+#pragma unroll
+      for (int m = 0; m < MS; ++m)
+        if (tid + kThreads * m < k) acc[m][c] += hs[m] * z[ls[m]];
+    }
+  }
+  // partial layout: ws[blockIdx.x][col][s]
+  double* dst = ws + (int64_t)blockIdx.x * k * ncols;
+#pragma unroll
+  for (int m = 0; m < MS; ++m) {
+    const int s = tid + kThreads * m;
+    if (s < k)
+#pragma unroll
+      for (int c = 0; c < CG; ++c)
+        if (c < cg) dst[s + (int64_t)(c0 + c) * k] = acc[m][c];
+  }
+}
+
+template <typename TX>
+int srht_sketch(int64_t n, int ncols, const TX* X, int64_t ldx, int64_t row0, int64_t n_pad,
+                const uint32_t* bits, const int64_t* sample, int k, double scale, double* out,
+                int64_t ldo, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st) {
+  RB_REQUIRE(k <= 8 * kThreads, "srht: k=%d > 2048 unsupported", k);
+  RB_REQUIRE(n_pad <= kT || (row0 % kT) == 0, "srht: row0 must be a multiple of 2048");
+  const int64_t span = (row0 % kT) + n;  // rows covered from the first tile start
+  const int ntiles = ceil_div(span, kT);
+  const int MS = k <= 256 ? 1 : k <= 512 ? 2 : k <= 1024 ? 4 : 8;
+  const int CG = MS >= 8 ? 4 : 8;
+  const int cgroups = ceil_div(ncols, CG);
+  const size_t per = (size_t)k * ncols * sizeof(double);
+  int ctas = std::max(1, std::min(ntiles, (2 * sm_count() + cgroups - 1) / cgroups));
+  if ((size_t)ctas * per > ws_bytes) ctas = (int)std::max<size_t>(1, ws_bytes / per);
+  RB_REQUIRE(ws && (size_t)ctas * per <= ws_bytes, "srht: workspace too small");
+  const int tpc = ceil_div(ntiles, ctas);
+  ctas = ceil_div(ntiles, tpc);
+  dim3 grid(ctas, cgroups);
+  double* w = (double*)ws;
+#define RB_SRHT(M, C) RB_KLAUNCH srht_partial<M, C, TX><<<grid, kThreads, 0, st>>>(n, ncols, X, ldx, row0, bits, sample, k, tpc, ntiles, w)
+  if (MS == 1) RB_SRHT(1, 8);
+  else if (MS == 2) RB_SRHT(2, 8);
+  else if (MS == 4) RB_SRHT(4, 8);
+  else RB_SRHT(8, 4);
+#undef RB_SRHT
+  const int64_t tot = (int64_t)k * ncols;
+  RB_KLAUNCH reduce_splits<<<ceil_div(tot, 256), 256, 0, st>>>(w, ctas, k, ncols, scale, out, ldo, accumulate);
+  return check_launch("srht sketch");
+}
+
+// ======================= sparse sign ========================================
+template <typename TX>
+__global__ void __launch_bounds__(kThreads)
+sparse_partial(int64_t n, int ncols, const TX* __restrict__ X, int64_t ldx, int64_t row0,
+               uint64_t seed, int k, int s, int cg, int64_t rows_per_cta, double* __restrict__ ws) {
+  extern __shared__ double sacc[];  // k x cg
+  const int c0 = blockIdx.y * cg;
+  const int cc = min(cg, ncols - c0);
+  for (int e = threadIdx.x; e < k * cg; e += blockDim.x) sacc[e] = 0.0;
+  __syncthreads();
+  const double inv = 1.0 / sqrt((double)s);
+  const int64_t beg = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t end = min(n, beg + rows_per_cta);
+  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    int rows[16], sg[16];
+    sparse_sign_column((uint64_t)(row0 + i), seed, k, s, rows, sg);
+    for (int c = 0; c < cc; ++c) {
+      const double x = (double)X[i + (int64_t)(c0 + c) * ldx] * inv;
+      for (int q = 0; q < s; ++q) atomicAdd(&sacc[rows[q] + c * k], sg[q] > 0 ? x : -x);
+    }
+  }
+  __syncthreads();
+  double* dst = ws + (int64_t)blockIdx.x * k * ncols;
+  for (int e = threadIdx.x; e < k * cc; e += blockDim.x) {
+    const int r = e % k, c = e / k;
+    dst[r + (int64_t)(c0 + c) * k] = sacc[e];
+  }
+}
+
+template <typename TX>
+int sparse_sketch(int64_t n, int ncols, const TX* X, int64_t ldx, int64_t row0, uint64_t seed,
+                  int k, int nnz, double* out, int64_t ldo, int accumulate, void* ws,
+                  size_t ws_bytes, cudaStream_t st) {
+  const int s = std::min(nnz, k);
+  RB_REQUIRE(s >= 1 && s <= 16, "sparse_sign: nnz must be in [1, 16]");
+  int cg = std::max(1, std::min(ncols, (int)(96 * 1024 / (k * sizeof(double)))));
+  RB_REQUIRE((size_t)k * sizeof(double) <= 96 * 1024, "sparse_sign: k too large");
+  const int cgroups = ceil_div(ncols, cg);
+  const size_t per = (size_t)k * ncols * sizeof(double);
+  int ctas = std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, (4 * sm_count() + cgroups - 1) / cgroups));
+  if ((size_t)ctas * per > ws_bytes) ctas = (int)std::max<size_t>(1, ws_bytes / per);
+  RB_REQUIRE(ws && (size_t)ctas * per <= ws_bytes, "sparse_sign: workspace too small");
+  const int64_t rpc = (n + ctas - 1) / std::max(ctas, 1);
+  const size_t smem = (size_t)k * cg * sizeof(double);
+  cudaFuncSetAttribute(sparse_partial<TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  if (n > 0)
+    RB_KLAUNCH sparse_partial<TX><<<dim3(ctas, cgroups), kThreads, smem, st>>>(n, ncols, X, ldx, row0, seed, k, s, cg,
+                                                                    std::max<int64_t>(rpc, 1), (double*)ws);
+  const int64_t tot = (int64_t)k * ncols;
+  RB_KLAUNCH reduce_splits<<<ceil_div(tot, 256), 256, 0, st>>>((double*)ws, n > 0 ? ctas : 0, k, ncols, 1.0, out, ldo,
+                                                    accumulate);
+  return check_launch("sparse_sign sketch");
+}
+
+}  // namespace
+
+// ============================== entry points ================================
+int gaussian_fill(uint64_t seed, int k, int64_t row0, int64_t nrows, int16_t* theta, int64_t ldt,
+                  cudaStream_t st) {
+  RB_REQUIRE(k >= 1 && k <= 4 * 65535 && nrows >= 0 && ldt >= nrows && theta, "rb_gaussian_fill: bad args");
+  if (nrows == 0) return RB_OK;
+  dim3 grid(ceil_div(nrows, 256), (k + 3) / 4);
+  RB_KLAUNCH gaussian_fill_kernel<<<grid, 256, 0, st>>>(seed, k, row0, nrows, theta, ldt);
+  return check_launch("rb_gaussian_fill");
+}
+
+int sketch_dense_i16(int xd, int64_t n, int ncols, const void* X, int64_t ldx, const int16_t* theta,
+                     int64_t ldt, int k, double scale, double* out, int64_t ldo, int acc, void* ws,
+                     size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(ncols >= 1 && ncols <= 64 && k >= 1 && ldo >= k && out, "rb_sketch_dense_i16: bad args");
+  RB_REQUIRE(n == 0 || (X && ldx >= n && theta && ldt >= n), "rb_sketch_dense_i16: bad X/theta");
+  I16Src src{theta, ldt};
+  if (xd == RB_F32) return dense_sketch<float>(n, ncols, (const float*)X, ldx, src, k, scale, out, ldo, acc, ws, wsb, st);
+  return dense_sketch<double>(n, ncols, (const double*)X, ldx, src, k, scale, out, ldo, acc, ws, wsb, st);
+}
+
+int sketch_signs(int xd, int64_t n, int ncols, const void* X, int64_t ldx, const uint32_t* bits, int64_t ldb,
+                 int k, double scale, double* out, int64_t ldo, int acc, void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(ncols >= 1 && ncols <= 64 && k >= 1 && ldo >= k && out, "rb_sketch_signs: bad args");
+  RB_REQUIRE(n == 0 || (X && ldx >= n && bits && ldb * 32 >= n), "rb_sketch_signs: bad X/bits");
+  BitSrc src{bits, ldb};
+  if (xd == RB_F32) return dense_sketch<float>(n, ncols, (const float*)X, ldx, src, k, scale, out, ldo, acc, ws, wsb, st);
+  return dense_sketch<double>(n, ncols, (const double*)X, ldx, src, k, scale, out, ldo, acc, ws, wsb, st);
+}
+
+int sketch_srht(int xd, int64_t n, int ncols, const void* X, int64_t ldx, int64_t row0, int64_t n_pad,
+                const uint32_t* bits, const int64_t* sample, int k, double scale, double* out, int64_t ldo,
+                int acc, void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(ncols >= 1 && k >= 1 && ldo >= k && out && bits && sample, "rb_sketch_srht: bad args");
+  RB_REQUIRE(n == 0 || (X && ldx >= n), "rb_sketch_srht: bad X");
+  if (xd == RB_F32) return srht_sketch<float>(n, ncols, (const float*)X, ldx, row0, n_pad, bits, sample, k, scale, out, ldo, acc, ws, wsb, st);
+  return srht_sketch<double>(n, ncols, (const double*)X, ldx, row0, n_pad, bits, sample, k, scale, out, ldo, acc, ws, wsb, st);
+}
+
+int sketch_sparse_sign(int xd, int64_t n, int ncols, const void* X, int64_t ldx, int64_t row0, uint64_t seed,
+                       int k, int nnz, double* out, int64_t ldo, int acc, void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(ncols >= 1 && k >= 1 && ldo >= k && out, "rb_sketch_sparse_sign: bad args");
+  RB_REQUIRE(n == 0 || (X && ldx >= n), "rb_sketch_sparse_sign: bad X");
+  if (xd == RB_F32) return sparse_sketch<float>(n, ncols, (const float*)X, ldx, row0, seed, k, nnz, out, ldo, acc, ws, wsb, st);
+  return sparse_sketch<double>(n, ncols, (const double*)X, ldx, row0, seed, k, nnz, out, ldo, acc, ws, wsb, st);
+}
+
+}  // namespace rb

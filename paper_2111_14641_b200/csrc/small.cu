@@ -1,0 +1,455 @@
+// Small fp64 kernels for the k- and m-dimensional steps of the sweep:
+// Step 2 (rbgs.py:144-225), the sketched Cholesky-QR (rbgs.py:267-290),
+// certification (rbgs.py:428-443), the tall triangular scaling of Steps 4-5
+// (rbgs.py:284, kernels.py:250-270) and the Householder QR used by the
+// direct LS solver and the GMRES least-squares problem (kernels.py:216-231).
+#include "common.cuh"
+
+namespace rb {
+
+int sm_count();
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// ============================ generic GEMM ==================================
+// C = alpha op(A) op(B) + beta C; fp64 accumulation, split-K over a fixed
+// grid (deterministic).  A, B may be binary32 (promoted on load).
+constexpr int GBM = 64, GBN = 64, GBK = 16;
+
+template <typename TA, typename TB>
+__global__ void __launch_bounds__(kThreads)
+gemm_partial(int tA, int tB, int m, int n, int64_t k, const TA* __restrict__ A, int64_t lda,
+             const TB* __restrict__ B, int64_t ldb, int64_t chunk, double* __restrict__ ws) {
+  __shared__ __align__(16) double sA[GBK][GBM];
+  __shared__ __align__(16) double sB[GBK][GBN];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.x * GBM, n0 = blockIdx.y * GBN;
+  const int64_t kb = (int64_t)blockIdx.z * chunk, ke = min(k, kb + chunk);
+  double acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int64_t k0 = kb; k0 < ke; k0 += GBK) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < GBM * GBK; e += kThreads) {
+      int i, kk;
+      if (tA) { kk = e % GBK; i = e / GBK; } else { i = e % GBM; kk = e / GBM; }
+      const int64_t kg = k0 + kk;
+      double v = 0.0;
+      if (m0 + i < m && kg < ke) v = tA ? (double)A[kg + (int64_t)(m0 + i) * lda] : (double)A[(m0 + i) + kg * lda];
+      sA[kk][i] = v;
+    }
+    for (int e = threadIdx.x; e < GBN * GBK; e += kThreads) {
+      int j, kk;
+      if (tB) { j = e % GBN; kk = e / GBN; } else { kk = e % GBK; j = e / GBK; }
+      const int64_t kg = k0 + kk;
+      double v = 0.0;
+      if (n0 + j < n && kg < ke) v = tB ? (double)B[(n0 + j) + kg * ldb] : (double)B[kg + (int64_t)(n0 + j) * ldb];
+      sB[kk][j] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GBK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) a[q] = sA[kk][ty + 16 * q];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) b[q] = sB[kk][tx + 16 * q];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc[q][t] = fma(a[q], b[t], acc[q][t]);
+    }
+  }
+  double* dst = ws + (int64_t)blockIdx.z * m * n;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int i = m0 + ty + 16 * q, j = n0 + tx + 16 * t;
+      if (i < m && j < n) dst[i + (int64_t)j * m] = acc[q][t];
+    }
+}
+
+__global__ void gemm_epilogue(const double* __restrict__ ws, int splits, int m, int n, double alpha,
+                              double beta, double* __restrict__ C, int64_t ldc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tot = (int64_t)m * n;
+  if (e >= tot) return;
+  double s = 0.0;
+  for (int q = 0; q < splits; ++q) s += ws[(int64_t)q * tot + e];
+  const int i = (int)(e % m), j = (int)(e / m);
+  double* c = C + i + (int64_t)j * ldc;
+  *c = beta == 0.0 ? alpha * s : alpha * s + beta * *c;
+}
+
+template <typename TA, typename TB>
+int gemm_t(int tA, int tB, int m, int n, int64_t k, double alpha, const TA* A, int64_t lda,
+           const TB* B, int64_t ldb, double beta, double* C, int64_t ldc, void* ws,
+           size_t wsb, cudaStream_t st) {
+  if (m == 0 || n == 0) return RB_OK;
+  const int mt = ceil_div(m, GBM), nt = ceil_div(n, GBN);
+  const size_t per = (size_t)m * n * sizeof(double);
+  int64_t splits = std::max<int64_t>(1, std::min<int64_t>((k + 255) / 256, (4 * sm_count() + mt * nt - 1) / (mt * nt)));
+  if ((size_t)splits * per > wsb) splits = std::max<int64_t>(1, (int64_t)(wsb / per));
+  RB_REQUIRE(ws && (size_t)splits * per <= wsb, "gemm: workspace too small (%zu B for %d x %d)", per, m, n);
+  RB_REQUIRE(splits <= 65535, "gemm: too many splits");
+  int64_t chunk = k > 0 ? (k + splits - 1) / splits : 0;
+  chunk = (chunk + GBK - 1) / GBK * GBK;
+  splits = chunk > 0 ? (k + chunk - 1) / chunk : 0;
+  if (splits > 0)
+    RB_KLAUNCH gemm_partial<TA, TB><<<dim3(mt, nt, (unsigned)splits), kThreads, 0, st>>>(tA, tB, m, n, k, A, lda, B, ldb, chunk,
+                                                                                 (double*)ws);
+  RB_KLAUNCH gemm_epilogue<<<ceil_div((int64_t)m * n, 256), 256, 0, st>>>((double*)ws, (int)splits, m, n, alpha, beta, C, ldc);
+  return check_launch("gemm");
+}
+
+// ============================ Cholesky ======================================
+// Right-looking, upper, in shared memory (p <= 128) -- dpotrf semantics:
+// info = j (1-based) at the first pivot that is <= 0 or NaN.
+__global__ void potrf_kernel(int p, const double* __restrict__ G, int64_t ldg, double* __restrict__ R,
+                             int64_t ldr, int* __restrict__ info) {
+  extern __shared__ double S[];  // p x p column-major
+  __shared__ int bad;
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    const int i = e % p, j = e / p;
+    S[e] = (i <= j) ? G[i + (int64_t)j * ldg] : 0.0;
+  }
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int j = 0; j < p; ++j) {
+    const double d = S[j + j * p];
+    if (!(d > 0.0)) {  // catches NaN too
+      if (threadIdx.x == 0) bad = j + 1;
+      break;
+    }
+    const double r = sqrt(d);
+    __syncthreads();
+    // scale row j right of the diagonal
+    for (int c = j + 1 + threadIdx.x; c < p; c += blockDim.x) S[j + c * p] /= r;
+    __syncthreads();
+    if (threadIdx.x == 0) S[j + j * p] = r;
+    // trailing update of the upper part: S[a, b] -= S[j, a] S[j, b], j < a <= b
+    const int t = p - j - 1;
+    for (int e = threadIdx.x; e < t * t; e += blockDim.x) {
+      const int a = j + 1 + e % t, b = j + 1 + e / t;
+      if (a <= b) S[a + b * p] -= S[j + a * p] * S[j + b * p];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    const int i = e % p, j = e / p;
+    R[i + (int64_t)j * ldr] = (i <= j) ? S[e] : 0.0;
+  }
+  if (threadIdx.x == 0) *info = bad;
+}
+
+// ============================ triangular solves =============================
+// Tall right solve X = B R^{-1}, one row per thread, row in registers.
+template <typename TI, typename TO, int PB>
+__global__ void __launch_bounds__(kThreads)
+trsm_right_kernel(int64_t n, int p, const TI* __restrict__ B, int64_t ldb, const double* __restrict__ Rg,
+                  int64_t ldr, TO* __restrict__ Xo, int64_t ldx) {
+  __shared__ double sR[PB * PB];
+  __shared__ double sInv[PB];
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
+    const int i = e % p, j = e / p;
+    sR[i + j * PB] = Rg[i + (int64_t)j * ldr];
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < p; j += blockDim.x) sInv[j] = 1.0 / sR[j + j * PB];
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double x[PB];
+#pragma unroll
+  for (int j = 0; j < PB; ++j) x[j] = j < p ? (double)B[r + (int64_t)j * ldb] : 0.0;
+#pragma unroll
+  for (int j = 0; j < PB; ++j) {
+    if (j < p) {
+      double s = x[j];
+#pragma unroll
+      for (int l = 0; l < j; ++l) s = fma(-x[l], sR[l + j * PB], s);
+      x[j] = s * sInv[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < PB; ++j)
+    if (j < p) Xo[r + (int64_t)j * ldx] = (TO)x[j];
+}
+
+// Left solve R X = B in place, one warp per right-hand side.
+__global__ void trsm_left_upper_kernel(int m, int nrhs, const double* __restrict__ R, int64_t ldr,
+                                       double* __restrict__ B, int64_t ldb, int* __restrict__ info) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    int bad = 0;
+    for (int i = 0; i < m; ++i)
+      if (R[i + (int64_t)i * ldr] == 0.0) { bad = i + 1; break; }
+    *info = bad;
+  }
+  if (warp >= nrhs) return;
+  double* b = B + (int64_t)warp * ldb;
+  for (int i = m - 1; i >= 0; --i) {
+    double s = 0.0;
+    for (int l = i + 1 + lane; l < m; l += 32) s += R[i + (int64_t)l * ldr] * b[l];
+    s = warp_sum(s);
+    if (lane == 0) b[i] = (b[i] - s) / R[i + (int64_t)i * ldr];
+    __syncwarp();
+  }
+}
+
+// ============================ Householder QR (single CTA) ===================
+// A (m x q) -> explicit economic Q in A, R (q x q) with diag(R) >= 0.
+// Workspace: V (m x q) reflectors + tau (q).
+__global__ void __launch_bounds__(1024)
+geqrf_kernel(int m, int q, double* __restrict__ A, int64_t lda, double* __restrict__ R, int64_t ldr,
+             double* __restrict__ V, double* __restrict__ tau) {
+  __shared__ double red[32];
+  __shared__ double sh[4];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  auto bsum = [&](double v) -> double {
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    for (int i = 0; i < nw; ++i) s += red[i];
+    return s;
+  };
+  for (int j = 0; j < q; ++j) {
+    double s = 0.0;
+    for (int i = j + 1 + tid; i < m; i += nt) { const double a = A[i + (int64_t)j * lda]; s += a * a; }
+    const double tail2 = bsum(s);
+    const double alpha = A[j + (int64_t)j * lda];
+    const double nrm = sqrt(tail2 + alpha * alpha);
+    // v = x - beta e1 with beta = -sign(alpha) ||x||, unit-normalised; H = I - 2 v v^T
+    const double beta = alpha >= 0.0 ? -nrm : nrm;  // R_jj before the sign fix
+    const double v0 = alpha - beta;
+    const double vn2 = tail2 + v0 * v0;
+    const bool skip = !(nrm > 0.0) || !(vn2 > 0.0);
+    for (int i = tid; i < m; i += nt) {
+      double v = 0.0;
+      if (!skip && i >= j) v = (i == j ? v0 : A[i + (int64_t)j * lda]) / sqrt(vn2);
+      V[i + (int64_t)j * m] = v;
+    }
+    if (tid == 0) tau[j] = skip ? 0.0 : 2.0;
+    __syncthreads();
+    // apply H = I - tau v v^T to the trailing columns, one warp per column
+    if (!skip) {
+      for (int c = j + 1 + warp; c < q; c += nw) {
+        double d = 0.0;
+        for (int i = j + lane; i < m; i += 32) d += V[i + (int64_t)j * m] * A[i + (int64_t)c * lda];
+        d = warp_sum(d) * 2.0;
+        for (int i = j + lane; i < m; i += 32) A[i + (int64_t)c * lda] -= d * V[i + (int64_t)j * m];
+      }
+    }
+    __syncthreads();
+    if (tid == 0) sh[0] = skip ? alpha : beta;
+    __syncthreads();
+    // column j of R: rows < j already final in A, diagonal = beta
+    for (int i = tid; i < q; i += nt) {
+      double v = 0.0;
+      if (i < j) v = A[i + (int64_t)j * lda];
+      else if (i == j) v = sh[0];
+      R[i + (int64_t)j * ldr] = v;
+    }
+    __syncthreads();
+  }
+  // explicit Q: start from [I; 0], apply H_{q-1} .. H_0
+  for (int e = tid; e < m * q; e += nt) {
+    const int i = e % m, c = e / m;
+    A[i + (int64_t)c * lda] = (i == c) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  for (int j = q - 1; j >= 0; --j) {
+    if (tau[j] != 0.0) {
+      for (int c = j + warp; c < q; c += nw) {
+        double d = 0.0;
+        for (int i = j + lane; i < m; i += 32) d += V[i + (int64_t)j * m] * A[i + (int64_t)c * lda];
+        d = warp_sum(d) * 2.0;
+        for (int i = j + lane; i < m; i += 32) A[i + (int64_t)c * lda] -= d * V[i + (int64_t)j * m];
+      }
+    }
+    __syncthreads();
+  }
+  // sign fix: diag(R) >= 0 (zero stays zero)
+  __shared__ signed char neg[1024];
+  for (int c = tid; c < q; c += nt) neg[c] = R[c + (int64_t)c * ldr] < 0.0;
+  __syncthreads();
+  for (int e = tid; e < m * q; e += nt) {
+    const int c = e / m;
+    if (neg[c]) A[(e % m) + (int64_t)c * lda] = -A[(e % m) + (int64_t)c * lda];
+  }
+  for (int e = tid; e < q * q; e += nt) {
+    const int i = e % q, c = e / q;
+    if (i > c) R[i + (int64_t)c * ldr] = 0.0;
+    else if (neg[i]) R[i + (int64_t)c * ldr] = -R[i + (int64_t)c * ldr];
+  }
+}
+
+// ============================ sum of squares ================================
+template <typename T>
+__global__ void sumsq_partial(int64_t m, int n, const T* __restrict__ A, int64_t lda, int minus_id,
+                              double* __restrict__ part) {
+  __shared__ double red[kThreads / 32];
+  double s = 0.0;
+  const int64_t tot = m * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % m, j = e / m;
+    double v = (double)A[i + j * lda];
+    if (minus_id && i == j) v = 1.0 - v;
+    s += v * v;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void sum_vec(const double* __restrict__ part, int count, double* __restrict__ out) {
+  __shared__ double red[kThreads / 32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) s += part[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = s;
+}
+
+template <typename TI, typename TO>
+__global__ void convert_kernel(int64_t m, int n, const TI* __restrict__ X, int64_t ldx, TO* __restrict__ Y,
+                               int64_t ldy) {
+  const int64_t tot = m * n;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % m, j = e / m;
+    Y[i + j * ldy] = (TO)X[i + j * ldx];
+  }
+}
+
+__global__ void copy_f64(int m, int n, const double* __restrict__ A, int64_t lda, double* __restrict__ B,
+                         int64_t ldb) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)m * n) return;
+  const int i = (int)(e % m), j = (int)(e / m);
+  B[i + (int64_t)j * ldb] = A[i + (int64_t)j * lda];
+}
+
+template <typename TI, typename TO>
+void trsm_right_launch(int64_t n, int p, const void* B, int64_t ldb, const double* R, int64_t ldr, void* X,
+                       int64_t ldx, cudaStream_t st) {
+  const int grid = ceil_div(n, kThreads);
+#define RB_TR(V)                                                                                         \
+  if (p <= V) {                                                                                          \
+    RB_KLAUNCH trsm_right_kernel<TI, TO, V><<<grid, kThreads, 0, st>>>(n, p, (const TI*)B, ldb, R, ldr, (TO*)X, ldx); \
+    return;                                                                                              \
+  }
+  RB_TR(4) RB_TR(8) RB_TR(12) RB_TR(16) RB_TR(24) RB_TR(32) RB_TR(40) RB_TR(48) RB_TR(64)
+#undef RB_TR
+}
+
+}  // namespace
+
+// ============================== entry points ================================
+int gemm_f64(int tA, int tB, int m, int n, int k, double alpha, const double* A, int64_t lda, const double* B,
+             int64_t ldb, double beta, double* C, int64_t ldc, void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(m >= 0 && n >= 0 && k >= 0 && C && ldc >= std::max(m, 1), "rb_gemm_f64: bad args");
+  return gemm_t<double, double>(tA, tB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, ws, wsb, st);
+}
+
+int cross(int ad, int bd, int64_t n, int p, int q, const void* A, int64_t lda, const void* B, int64_t ldb,
+          double* out, int64_t ldo, int acc, void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(n >= 0 && p >= 1 && q >= 1 && out && ldo >= p, "rb_cross: bad args");
+  const double beta = acc ? 1.0 : 0.0;
+  if (ad == RB_F32 && bd == RB_F32)
+    return gemm_t<float, float>(1, 0, p, q, n, 1.0, (const float*)A, lda, (const float*)B, ldb, beta, out, ldo, ws, wsb, st);
+  if (ad == RB_F32)
+    return gemm_t<float, double>(1, 0, p, q, n, 1.0, (const float*)A, lda, (const double*)B, ldb, beta, out, ldo, ws, wsb, st);
+  if (bd == RB_F32)
+    return gemm_t<double, float>(1, 0, p, q, n, 1.0, (const double*)A, lda, (const float*)B, ldb, beta, out, ldo, ws, wsb, st);
+  return gemm_t<double, double>(1, 0, p, q, n, 1.0, (const double*)A, lda, (const double*)B, ldb, beta, out, ldo, ws, wsb, st);
+}
+
+int potrf_upper(int p, const double* G, int64_t ldg, double* R, int64_t ldr, int* info, cudaStream_t st) {
+  RB_REQUIRE(p >= 1 && p <= 128 && G && R && info && ldg >= p && ldr >= p, "rb_potrf_upper: bad args (p=%d)", p);
+  const size_t smem = (size_t)p * p * sizeof(double);
+  cudaFuncSetAttribute(potrf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 132 * 1024);
+  RB_KLAUNCH potrf_kernel<<<1, 256, smem, st>>>(p, G, ldg, R, ldr, info);
+  return check_launch("rb_potrf_upper");
+}
+
+int trsm_right(int ind, int outd, int64_t n, int p, const void* B, int64_t ldb, const double* R, int64_t ldr,
+               void* X, int64_t ldx, cudaStream_t st) {
+  RB_REQUIRE(n >= 0 && p >= 1 && p <= 64 && R && ldr >= p && ldb >= n && ldx >= n, "rb_trsm_right: bad args");
+  if (n == 0) return RB_OK;
+  if (ind == RB_F32 && outd == RB_F32) trsm_right_launch<float, float>(n, p, B, ldb, R, ldr, X, ldx, st);
+  else if (ind == RB_F32) trsm_right_launch<float, double>(n, p, B, ldb, R, ldr, X, ldx, st);
+  else if (outd == RB_F32) trsm_right_launch<double, float>(n, p, B, ldb, R, ldr, X, ldx, st);
+  else trsm_right_launch<double, double>(n, p, B, ldb, R, ldr, X, ldx, st);
+  return check_launch("rb_trsm_right");
+}
+
+int trsm_left_upper(int m, int nrhs, const double* R, int64_t ldr, double* B, int64_t ldb, int* info,
+                    cudaStream_t st) {
+  RB_REQUIRE(m >= 1 && nrhs >= 0 && R && B && info && ldr >= m && ldb >= m, "rb_trsm_left_upper: bad args");
+  const int warps = std::max(nrhs, 1);
+  RB_KLAUNCH trsm_left_upper_kernel<<<ceil_div(warps * 32, 128), 128, 0, st>>>(m, nrhs, R, ldr, B, ldb, info);
+  return check_launch("rb_trsm_left_upper");
+}
+
+int geqrf_small(int m, int q, double* A, int64_t lda, double* R, int64_t ldr, void* ws, size_t wsb,
+                cudaStream_t st) {
+  RB_REQUIRE(q >= 1 && q <= 1024 && m >= q && A && R && lda >= m && ldr >= q, "rb_geqrf_small: bad args (m=%d q=%d)", m, q);
+  RB_REQUIRE(ws && wsb >= ((size_t)m * q + q) * sizeof(double), "rb_geqrf_small: workspace");
+  double* V = (double*)ws;
+  RB_KLAUNCH geqrf_kernel<<<1, 1024, 0, st>>>(m, q, A, lda, R, ldr, V, V + (size_t)m * q);
+  return check_launch("rb_geqrf_small");
+}
+
+int sumsq(int dt, int64_t m, int n, const void* A, int64_t lda, int minus_id, double* out, void* ws, size_t wsb,
+          cudaStream_t st) {
+  RB_REQUIRE(m >= 0 && n >= 0 && out && (m * n == 0 || (A && lda >= m)), "rb_sumsq: bad args");
+  const int64_t tot = m * n;
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>((tot + 4095) / 4096, 2 * sm_count()));
+  RB_REQUIRE(ws && wsb >= (size_t)grid * sizeof(double), "rb_sumsq: workspace");
+  if (dt == RB_F32) RB_KLAUNCH sumsq_partial<float><<<grid, kThreads, 0, st>>>(m, n, (const float*)A, lda, minus_id, (double*)ws);
+  else RB_KLAUNCH sumsq_partial<double><<<grid, kThreads, 0, st>>>(m, n, (const double*)A, lda, minus_id, (double*)ws);
+  RB_KLAUNCH sum_vec<<<1, kThreads, 0, st>>>((double*)ws, grid, out);
+  return check_launch("rb_sumsq");
+}
+
+int convert(int ind, int outd, int64_t m, int n, const void* X, int64_t ldx, void* Y, int64_t ldy, cudaStream_t st) {
+  RB_REQUIRE(m >= 0 && n >= 0 && ldx >= m && ldy >= m, "rb_convert: bad args");
+  const int64_t tot = m * n;
+  if (tot == 0) return RB_OK;
+  const int grid = (int)std::min<int64_t>((tot + 255) / 256, 16 * sm_count());
+  if (ind == RB_F32 && outd == RB_F32) RB_KLAUNCH convert_kernel<float, float><<<grid, 256, 0, st>>>(m, n, (const float*)X, ldx, (float*)Y, ldy);
+  else if (ind == RB_F32) RB_KLAUNCH convert_kernel<float, double><<<grid, 256, 0, st>>>(m, n, (const float*)X, ldx, (double*)Y, ldy);
+  else if (outd == RB_F32) RB_KLAUNCH convert_kernel<double, float><<<grid, 256, 0, st>>>(m, n, (const double*)X, ldx, (float*)Y, ldy);
+  else RB_KLAUNCH convert_kernel<double, double><<<grid, 256, 0, st>>>(m, n, (const double*)X, ldx, (double*)Y, ldy);
+  return check_launch("rb_convert");
+}
+
+int ls_richardson(int k, int c, int p, const double* S, int64_t lds, const double* P, int64_t ldp, int l, double* X,
+                  int64_t ldx, double* T, int64_t ldt, void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(k >= 1 && c >= 1 && p >= 1 && l >= 1 && S && P && X && T, "rb_ls_richardson: bad args");
+  // sweep 1 from X = 0 is exactly S^T P (rbgs.py:153-155)
+  int rc = gemm_t<double, double>(1, 0, c, p, k, 1.0, S, lds, P, ldp, 0.0, X, ldx, ws, wsb, st);
+  for (int it = 1; it < l && rc == RB_OK; ++it) {
+    RB_KLAUNCH copy_f64<<<ceil_div((int64_t)k * p, 256), 256, 0, st>>>(k, p, P, ldp, T, ldt);
+    rc = gemm_t<double, double>(0, 0, k, p, c, -1.0, S, lds, X, ldx, 1.0, T, ldt, ws, wsb, st);  // T = P - S X
+    if (rc == RB_OK) rc = gemm_t<double, double>(1, 0, c, p, k, 1.0, S, lds, T, ldt, 1.0, X, ldx, ws, wsb, st);
+  }
+  return rc;
+}
+
+int sketched_cholqr_small(int k, int p, const double* Sp, int64_t lds, double* R, int64_t ldr, double* Sout,
+                          int64_t ldso, int* info, void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(k >= 1 && p >= 1 && p <= 64 && Sp && R && Sout && info, "rb_sketched_cholqr_small: bad args");
+  int rc = gemm_t<double, double>(1, 0, p, p, k, 1.0, Sp, lds, Sp, lds, 0.0, R, ldr, ws, wsb, st);  // G in R
+  if (rc == RB_OK) rc = potrf_upper(p, R, ldr, R, ldr, info, st);
+  if (rc == RB_OK) rc = trsm_right(RB_F64, RB_F64, k, p, Sp, lds, R, ldr, Sout, ldso, st);
+  return rc;
+}
+
+}  // namespace rb

@@ -1,0 +1,248 @@
+"""Block randomized Arnoldi and GMRES on the GPU sweep -- drop-in for
+`sketch_krylov.krylov.rbgs_arnoldi` / `block_gmres`
+(reference `pkg/src/sketch_krylov/krylov.py:49-281`).
+
+The operator products, the RBGS block steps, the n-dimensional basis
+combinations U_j = Q Z and the true-residual / basis-conditioning
+diagnostics all run on the device; the Hessenberg least-squares problems
+(at most (p mp) x ((p-1) mp)) use the single-CTA Householder kernel.
+Only the spectrum of the (rows x rows) basis Gram matrix used for the
+`basis_cond_history` diagnostic is taken on the host (a <= 244 x 244
+symmetric eigenproblem; the n-dimensional Gram itself is a device kernel).
+"""
+
+from __future__ import annotations
+
+import dataclasses
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _device as D
+from ._lib import require_cuda
+from .comm import Comm, RowShard
+from .errors import DependentBlockError, ShapeError
+from .kernels import FINE, BlockPartition, Matrix, PrecisionSpec, as_array
+from .operators import LinearOperator
+from .rbgs import DeviceConfig, RbgsConfig, RbgsSweep, certify
+
+__all__ = ["ArnoldiDecomposition", "KrylovSolveReport", "rbgs_arnoldi", "block_gmres"]
+
+
+@dataclass(eq=False)
+class ArnoldiDecomposition:
+    """Basis Q, Hessenberg data H = R[:, mp:], R_first = R[:, :mp]
+    (krylov.py:49-64)."""
+
+    Q: Matrix
+    H: Matrix
+    R_first: Matrix
+    S: Matrix
+    P: Matrix
+    cert: object
+    partition: BlockPartition
+
+
+@dataclass(eq=False)
+class KrylovSolveReport:
+    """Solution plus per-inner-iteration histories (krylov.py:67-95)."""
+
+    solution: Matrix
+    residual_history: list
+    basis_cond_history: list
+    restarts: int
+    breakdown: int = 0
+    cert_history: list = None
+
+    def __post_init__(self):
+        if not self.residual_history:
+            raise ValueError("residual history must be non-empty")
+        if len(self.residual_history) != len(self.basis_cond_history):
+            raise ValueError("history lengths must agree")
+        if self.cert_history is None:
+            self.cert_history = [(np.nan, np.nan)] * len(self.residual_history)
+        elif len(self.cert_history) != len(self.residual_history):
+            raise ValueError("history lengths must agree")
+
+
+def _partition(mp, p):
+    return BlockPartition(mp, p, p * mp)
+
+
+def _device_cfg(device_cfg, A):
+    dc = device_cfg or DeviceConfig(q_dtype=torch.float64)
+    if dc.q_dtype is None:
+        dc = dataclasses.replace(dc, q_dtype=torch.float64)
+    if dc.device is None and getattr(A, "device", None) is not None:
+        dc = dataclasses.replace(dc, device=A.device)
+    return dc
+
+
+def _to_dev(B, device):
+    if isinstance(B, Matrix):
+        B = B._dev if B._dev is not None else B.data
+    if isinstance(B, torch.Tensor):
+        return D.to_cm(B if B.dim() == 2 else B.reshape(-1, 1), torch.float64, device)
+    return D.to_cm(torch.from_numpy(np.asfortranarray(as_array(B))), torch.float64, device)
+
+
+def _matvec(A, X, prec):
+    Y = A._apply_dev(X, torch.float64)
+    if prec.format == "coarse":  # _round_to (rbgs.py:134-137)
+        Y = D.to_cm(Y, torch.float32)
+    return Y
+
+
+def rbgs_arnoldi(A: LinearOperator, B, theta, p: int, cfg: RbgsConfig = None,
+                 matvec_precision: PrecisionSpec = FINE, device_cfg: DeviceConfig = None) -> ArnoldiDecomposition:
+    """Block Arnoldi: W_1 = B, W_i = A Q_(i-1), orthogonalized by RBGS
+    (krylov.py:110-135).  Q is kept in binary64 by default because the
+    reference applies A to its binary64 Q."""
+    require_cuda()
+    dc = _device_cfg(device_cfg, A)
+    dev = D.cuda_device(dc.device)
+    with torch.cuda.device(dev):
+        Bd = _to_dev(B, dev)
+        n_local, mp = Bd.shape
+        if p < 2:
+            raise ShapeError("Arnoldi needs p >= 2 blocks")
+        n = A.n
+        cfg = dataclasses.replace(cfg or RbgsConfig(), partition=_partition(mp, p))
+        sweep = RbgsSweep(n, theta, cfg, dc)
+        sweep.push_block(Bd)
+        off = sweep.offsets
+        for i in range(2, p + 1):
+            sweep.push_block(_matvec(A, sweep.Q[:, off[i - 2]:off[i - 1]], matvec_precision))
+        f = sweep.finish()
+        R = sweep.R
+        return ArnoldiDecomposition(f.Q, Matrix(R[:, mp:]), Matrix(R[:, :mp]), f.S, f.P, f.cert,
+                                    cfg.partition)
+
+
+def _ls_qr_dev(M, T):
+    """min ||M Z - T||_F via Householder QR (krylov.py:164-167), device."""
+    rows, q = M.shape
+    A = D.empty_cm(rows, q, torch.float64, M.device)
+    A.copy_(M)
+    Rm = D.empty_cm(q, q, torch.float64, M.device)
+    D.geqrf(A, Rm)
+    Z = D.empty_cm(q, T.shape[1], torch.float64, M.device)
+    D.gemm(1, 0, 1.0, A, T, 0.0, Z)
+    info = torch.zeros(1, dtype=torch.int32, device=M.device)
+    D.trsm_left_upper(Rm, Z, info)
+    return Z
+
+
+def _cond2_dev(Q, comm):
+    """2-norm condition of the (row-sharded) basis from its Gram matrix."""
+    q = Q.shape[1]
+    G = D.empty_cm(q, q, torch.float64, Q.device)
+    D.cross(Q, Q, G)
+    comm.allreduce_(G)
+    ev = np.linalg.eigvalsh(G.cpu().numpy())
+    if ev.size == 0 or ev[0] <= 0.0:
+        return float("inf")
+    return float(math.sqrt(ev[-1] / ev[0]))
+
+
+def block_gmres(A: LinearOperator, B, theta, p: int, restarts: int = 1, cfg=None, tol: float = 0.0,
+                matvec_precision: PrecisionSpec = FINE, device_cfg: DeviceConfig = None) -> KrylovSolveReport:
+    """Restarted block GMRES over a sketch-orthonormal basis (krylov.py:170-281).
+
+    RBGS backend only (the reference's classical backend is a baseline,
+    out of scope).  With a sharded DeviceConfig, B, the solution and every
+    operator block hold this rank's rows; residual norms are global."""
+    require_cuda()
+    dc = _device_cfg(device_cfg, A)
+    dev = D.cuda_device(dc.device)
+    comm = dc.comm or Comm(None)
+    with torch.cuda.device(dev):
+        Bd = _to_dev(B, dev)
+        n_local, mp = Bd.shape
+        if p < 2:
+            raise ShapeError("GMRES needs p >= 2 blocks")
+        n = A.n
+        part = _partition(mp, p)
+
+        def colsq(M):
+            s = (M * M).sum(0)
+            comm.allreduce_(s)
+            return s
+
+        bn = colsq(Bd).sqrt()
+        bn = torch.where(bn == 0.0, torch.ones_like(bn), bn)
+        X = D.zeros_cm(n_local, mp, torch.float64, dev)
+        history, conds, certs = [], [], []
+        it = 0
+        breakdown = 0
+        cycles = 0
+
+        def rel_residual(Xc):
+            Rr = Bd - A._apply_dev(Xc, torch.float64)
+            return float((colsq(Rr).sqrt() / bn).max())
+
+        for cycle in range(max(restarts, 1)):
+            cycles += 1
+            Bres = D.to_cm(Bd - A._apply_dev(X, torch.float64)) if cycle else Bd.clone()
+            sweep = RbgsSweep(n, theta, dataclasses.replace(cfg or RbgsConfig(), partition=part), dc)
+            bk = 0
+            try:
+                sweep.push_block(Bres)
+                off = sweep.offsets
+                for i in range(2, p + 1):
+                    sweep.push_block(_matvec(A, sweep.Q[:, off[i - 2]:off[i - 1]], matvec_precision))
+            except DependentBlockError as e:
+                bk = e.block
+            q, c = sweep.blocks_done, sweep.cols_done
+            if q == 0:
+                it += 1
+                history.append((it, rel_residual(X)))
+                conds.append(1.0)
+                certs.append((np.nan, np.nan))
+                breakdown = bk
+                break
+            rep = certify(sweep.S[:, :c], sweep.P[:, :c], sweep.R[:c, :c])
+            pair = (rep.delta, rep.delta_tilde)
+            Hf = sweep.R[:c, mp:c]
+            Rf = sweep.R[:c, :mp]
+            U_best, rel_best = None, None
+            for j in range(1, q):
+                rows = (j + 1) * mp
+                Z = _ls_qr_dev(Hf[:rows, :j * mp], Rf[:rows, :])
+                Uj = D.empty_cm(n_local, mp, torch.float64, dev)
+                D.gemm(0, 0, 1.0, sweep.Q[:, :j * mp], Z, 0.0, Uj)
+                rel = rel_residual(X + Uj)
+                it += 1
+                history.append((it, rel))
+                conds.append(_cond2_dev(sweep.Q[:, :rows], comm))
+                certs.append(pair)
+                if rel_best is None or rel <= rel_best:
+                    U_best, rel_best = Uj, rel
+            if bk:
+                PA = D.empty_cm(theta.k, c - mp + mp, torch.float64, dev)
+                PA[:, :c - mp].copy_(sweep.P[:, mp:c])
+                PA[:, c - mp:].copy_(sweep.pending_P.tensor)
+                Z = _ls_qr_dev(PA, sweep.P[:, :mp])
+                Uj = D.empty_cm(n_local, mp, torch.float64, dev)
+                D.gemm(0, 0, 1.0, sweep.Q[:, :c], Z, 0.0, Uj)
+                rel = rel_residual(X + Uj)
+                it += 1
+                history.append((it, rel))
+                conds.append(_cond2_dev(sweep.Q[:, :c], comm))
+                certs.append(pair)
+                if rel_best is None or rel <= rel_best:
+                    U_best, rel_best = Uj, rel
+            if U_best is not None:
+                X = D.to_cm(X + U_best)
+            if bk:
+                breakdown = bk
+                break
+            if tol > 0.0 and rel_best is not None and rel_best <= tol:
+                break
+        if not history:
+            history.append((1, rel_residual(X)))
+            conds.append(1.0)
+            certs.append((np.nan, np.nan))
+        return KrylovSolveReport(Matrix(X), history, conds, cycles, breakdown, certs)

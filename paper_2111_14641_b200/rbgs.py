@@ -1,0 +1,748 @@
+"""Randomized block Gram-Schmidt on the GPU -- drop-in for
+`sketch_krylov.rbgs` (reference `pkg/src/sketch_krylov/rbgs.py`).
+
+Public names and signatures follow the reference: `RbgsConfig`, `CertReport`,
+`BlockQR`, `RbgsSweep(n, theta, cfg).push_block(W_i) / finish()`,
+`rbgs(W, theta, cfg)`, `certify(S, P, R)`, the Step-2 solvers `ls_*` and the
+Step-4/5 routines `interblock_*`.  Device-only knobs live in a separate
+`DeviceConfig` ("Config / flags"), so reference configs
+round-trip unchanged.
+
+Per block i (paper Alg. 2; rbgs.py:352-399), on one rank
+holding rows [row0, row0 + n_local):
+
+  Step 1   P_i = Theta W_i                  sketch kernel  (+ allreduce)
+  Step 2   X = argmin ||S X - P_i||          small fp64 kernels (replicated)
+  Step 3   Q' = W_i - Q_(1:i-1) X            rb_project, reference order,
+                                             fused sum-of-squares of W_i, Q'
+  Step 4-5 inter-block QR of Q'             sketch of Q' (+ allreduce),
+                                             fp64 Cholesky / TRSM, tall TRSM
+                                             writing Q_i into its slot
+  checks   one device->host read of the status words per block: the
+           dependence test (rbgs.py:373-376, GLOBAL n and norms), the
+           Cholesky info (-> InterblockError) and a finiteness flag
+           (the reference's Matrix() check, kernels.py:97-98).
+
+Storage: Q is n_local x m in the coarse format (binary32) when
+`cfg.coarse` is COARSE -- bit-identical to what the reference's coarse gemm
+reads (`Q.astype(float32)`, kernels.py:192) -- and binary64 otherwise;
+S, P (k x m) and R (m x m) are binary64 and replicated.
+"""
+
+from __future__ import annotations
+
+import math
+import re
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _device as D
+from . import sketching
+from ._lib import F32, F64, ORDER_FMA, ORDER_REFERENCE, require_cuda
+from .comm import Comm, RowShard
+from .errors import (
+    CertificationError,
+    DependentBlockError,
+    InterblockError,
+    NotPositiveDefiniteError,
+    RankDeficiencyError,
+    ShapeError,
+)
+from .kernels import COARSE, FINE, BlockPartition, Matrix, PrecisionSpec, as_array
+
+__all__ = ["RbgsConfig", "DeviceConfig", "BlockQR", "CertReport", "rbgs", "RbgsSweep", "certify",
+           "ls_richardson", "ls_bmgs_reorth", "ls_cg_normal", "ls_householder_direct",
+           "interblock_rgs", "interblock_sketched_cholqr", "interblock_l2_cholqr", "parse_method"]
+
+U_FINE = 2.0 ** -53
+
+_METHOD = re.compile(r"^([a-z0-9_]+)(?:[(:]\s*(\d+)\s*\)?)?$")
+_DEFAULTS = {"richardson": 5, "bmgs_reorth": 1, "cg_normal": 20, "sketched_cholqr": 1}
+
+
+def parse_method(spec: str):
+    """'name', 'name(3)' or 'name:3' -> (name, param) (rbgs.py:64-82)."""
+    m = _METHOD.match(spec.strip().lower())
+    if not m:
+        raise ValueError(f"cannot parse method spec {spec!r}")
+    name, param = m.group(1), m.group(2)
+    if param is None:
+        return name, _DEFAULTS.get(name)
+    param = int(param)
+    if param < 1:
+        raise ValueError(f"method parameter must be >= 1 in {spec!r}")
+    return name, param
+
+
+@dataclass
+class RbgsConfig:
+    """Reference knobs, same fields and validation (rbgs.py:85-107)."""
+
+    partition: BlockPartition = None
+    ls_solver: str = "richardson(5)"
+    interblock: str = "l2_plus_cholqr"
+    coarse: PrecisionSpec = COARSE
+    fine: PrecisionSpec = FINE
+    certify_blocks: bool = False
+    resketch: bool = False
+
+    def __post_init__(self):
+        if self.fine.u > self.coarse.u:
+            raise ValueError("fine precision must not be coarser than coarse")
+        name, param = parse_method(self.ls_solver)
+        if name not in ("richardson", "bmgs_reorth", "cg_normal", "householder_direct"):
+            raise ValueError(f"unknown ls solver {self.ls_solver!r}")
+        if name != "householder_direct" and (param is None or param < 1):
+            raise ValueError(f"solver {name} needs a positive iteration count")
+        if parse_method(self.interblock)[0] not in ("rgs_single", "sketched_cholqr", "l2_plus_cholqr"):
+            raise ValueError(f"unknown interblock method {self.interblock!r}")
+
+
+@dataclass
+class DeviceConfig:
+    """Device-side knobs (no reference counterpart).
+
+    device            CUDA device (default: current).
+    q_dtype           storage of Q (default binary32 when cfg.coarse is
+                      COARSE, else binary64); binary64 keeps the reference's
+                      fp64 Q (e.g. for Arnoldi, whose operator reads fp64 Q).
+    projection_order  "reference" (bit-identical Step 3) or "fma" (fused
+                      multiply-subtract, faster, not bit-identical).
+    comm / shard      row sharding: this rank's rows and the group that owns
+                      the other shards (comm.py).  Default: all rows here.
+    """
+
+    device: object = None
+    q_dtype: torch.dtype = None
+    projection_order: str = "reference"
+    comm: Comm = None
+    shard: RowShard = None
+
+
+@dataclass(frozen=True)
+class CertReport:
+    delta: float
+    delta_tilde: float
+    per_block_ortho: tuple = ()
+    per_block_resid: tuple = ()
+
+    def __post_init__(self):
+        vals = (self.delta, self.delta_tilde, *self.per_block_ortho, *self.per_block_resid)
+        if not all(np.isfinite(v) and v >= 0.0 for v in vals):
+            raise ValueError("certification quantities must be finite and nonnegative")
+
+
+@dataclass(eq=False)
+class BlockQR:
+    Q: Matrix
+    R: Matrix
+    S: Matrix
+    P: Matrix
+    partition: BlockPartition
+    cert: CertReport = None
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+def _dev_f64(A, device):
+    """fp64 column-major device copy of a host or device matrix."""
+    if isinstance(A, Matrix):
+        A = A._dev if A._dev is not None else A.data
+    if isinstance(A, torch.Tensor):
+        return D.to_cm(A if A.dim() == 2 else A.reshape(-1, 1), torch.float64, device)
+    return D.to_cm(torch.from_numpy(np.asfortranarray(as_array(A))), torch.float64, device)
+
+
+class _Scratch:
+    """Per-sweep device scratch, allocated once at the largest block width."""
+
+    def __init__(self, k, m, w, device):
+        f64 = torch.float64
+        self.Pi = D.empty_cm(k, w, f64, device)
+        self.Sp = D.empty_cm(k, w, f64, device)
+        self.Ss = D.empty_cm(k, w, f64, device)
+        self.Si = D.empty_cm(k, w, f64, device)
+        self.T = D.empty_cm(k, w, f64, device)
+        self.X = D.empty_cm(max(m, 1), w, f64, device)
+        self.G = D.empty_cm(w, w, f64, device)
+        self.R1 = D.empty_cm(w, w, f64, device)
+        self.R2 = D.empty_cm(w, w, f64, device)
+        self.Rt = D.empty_cm(w, w, f64, device)
+        self.norms = torch.zeros(8, dtype=f64, device=device)  # [w2, q2, fin, ...]
+        self.info = torch.zeros(8, dtype=torch.int32, device=device)
+        self.status_host = torch.zeros(8, dtype=f64).pin_memory()
+        self.info_host = torch.zeros(8, dtype=torch.int32).pin_memory()
+
+
+# ---------------------------------------------------------------------------
+# Step 2 solvers (rbgs.py:144-225) -- device, fp64
+# ---------------------------------------------------------------------------
+
+def _richardson_dev(S, P, l, X, T):
+    D.richardson(S, P, l, X, T)
+
+
+def _bmgs_dev(S, offsets, P, l, X, T):
+    c = S.shape[1]
+    T.copy_(P)
+    X.zero_()
+    blocks = [(offsets[j], min(offsets[j + 1], c)) for j in range(len(offsets) - 1) if offsets[j] < c]
+    for _ in range(l):
+        for a, b in blocks:
+            Sj = S[:, a:b]
+            inc = D.empty_cm(b - a, P.shape[1], torch.float64, S.device)
+            D.gemm(1, 0, 1.0, Sj, T, 0.0, inc)
+            X[a:b].add_(inc)
+            D.gemm(0, 0, -1.0, Sj, inc, 1.0, T)
+
+
+def _cg_dev(S, P, iters, X):
+    k, c = S.shape
+    p = P.shape[1]
+    dev = S.device
+    b = D.empty_cm(c, p, torch.float64, dev)
+    D.gemm(1, 0, 1.0, S, P, 0.0, b)
+    X.zero_()
+    r = b.clone()
+    d = r.clone()
+    rs = (r * r).sum(0)
+    SD = D.empty_cm(k, p, torch.float64, dev)
+    Ad = D.empty_cm(c, p, torch.float64, dev)
+    for _ in range(iters):
+        D.gemm(0, 0, 1.0, S, d, 0.0, SD)
+        D.gemm(1, 0, 1.0, S, SD, 0.0, Ad)
+        dAd = (d * Ad).sum(0)
+        alpha = torch.where(dAd > 0, rs / torch.where(dAd > 0, dAd, torch.ones_like(dAd)), torch.zeros_like(dAd))
+        X.add_(alpha * d)
+        r.sub_(alpha * Ad)
+        rs2 = (r * r).sum(0)
+        beta = torch.where(rs > 0, rs2 / torch.where(rs > 0, rs, torch.ones_like(rs)), torch.zeros_like(rs))
+        rs = rs2
+        d = r + beta * d
+
+
+def _householder_direct_dev(S, P, X, scr, sync=True):
+    k, c = S.shape
+    dev = S.device
+    A = D.empty_cm(k, c, torch.float64, dev)
+    A.copy_(S)
+    Rs = D.empty_cm(c, c, torch.float64, dev)
+    D.geqrf(A, Rs)
+    d = Rs.diagonal().abs()
+    if sync:
+        dmin, dmax = float(d.min()), float(d.max())
+        if dmin <= k * U_FINE * max(dmax, 1e-300):
+            raise RankDeficiencyError(f"least-squares matrix numerically rank deficient (min diag {dmin:.3e})")
+    D.gemm(1, 0, 1.0, A, P, 0.0, X)
+    D.trsm_left_upper(Rs, X, scr.info[6:7])
+
+
+# ---------------------------------------------------------------------------
+# the sweep
+# ---------------------------------------------------------------------------
+
+class RbgsSweep:
+    """Incremental RBGS on the GPU (rbgs.py:318-407).
+
+    Feed blocks left to right with `push_block`; `Q`, `S`, `P`, `R` are the
+    device buffers (torch, column-major; Q holds this rank's rows only)."""
+
+    def __init__(self, n: int, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None):
+        require_cuda()
+        if cfg.partition is None:
+            raise ShapeError("config needs a partition")
+        m = cfg.partition.total_cols
+        if theta.n != n:
+            raise ShapeError(f"sketch built for n={theta.n}, input has n={n}")
+        if not (m <= theta.k <= n):
+            raise ShapeError(f"need total cols m={m} <= sketch k={theta.k} <= n={n}")
+        if cfg.fine.format != "fine":
+            raise NotImplementedError("fine=COARSE (unique coarse precision) is not implemented on the "
+                                      "device path; the Step-2 solvers run in binary64")
+        dc = device_cfg or DeviceConfig()
+        self.device = D.cuda_device(dc.device)
+        self.comm = dc.comm or Comm(None)
+        self.shard = dc.shard or RowShard.whole(n)
+        if self.shard.n != n:
+            raise ShapeError("shard built for a different n")
+        self.n = n
+        self.n_local = self.shard.n_local
+        self.row0 = self.shard.row0
+        self.theta = theta
+        self.cfg = cfg
+        self.solver = parse_method(cfg.ls_solver)
+        self.inter = parse_method(cfg.interblock)
+        self.offsets = cfg.partition.offsets()
+        self.compute = F32 if cfg.coarse.format == "coarse" else F64
+        self.q_dtype = dc.q_dtype or (torch.float32 if self.compute == F32 else torch.float64)
+        if dc.projection_order not in ("reference", "fma"):
+            raise ValueError("projection_order must be 'reference' or 'fma'")
+        self.order = ORDER_FMA if dc.projection_order == "fma" else ORDER_REFERENCE
+        dev = self.device
+        k = theta.k
+        self.Q = D.zeros_cm(self.n_local, m, self.q_dtype, dev)
+        self.S = D.zeros_cm(k, m, torch.float64, dev)
+        self.P = D.zeros_cm(k, m, torch.float64, dev)
+        self.R = D.zeros_cm(m, m, torch.float64, dev)
+        wmax = max(cfg.partition.block_widths())
+        self._scr = _Scratch(k, m, wmax, dev)
+        self._tmp64 = None
+        self.blocks_done = 0
+        self.cols_done = 0
+        self.per_block_ortho = []
+        self.per_block_resid = []
+        self.pending_P = None
+
+    # -- small utilities ---------------------------------------------------
+    def _sketch(self, X, out):
+        sketching.sketch_into(self.theta, X, out, self.row0)
+
+    def _sketch_reduce(self, X, out):
+        self._sketch(X, out)
+        self.comm.allreduce_(out)
+
+    def _as_block(self, W_i, w):
+        """Device view of this rank's rows of block W_i (dtype kept: binary32
+        blocks are read as binary32, binary64 as binary64)."""
+        if isinstance(W_i, Matrix):
+            W_i = W_i._dev if W_i._dev is not None else W_i.data
+        if isinstance(W_i, torch.Tensor):
+            t = W_i if W_i.dim() == 2 else W_i.reshape(-1, 1)
+            if t.dtype not in (torch.float32, torch.float64):
+                t = t.to(torch.float64)
+            t = D.to_cm(t, t.dtype, self.device)
+        else:
+            A = np.asarray(W_i)
+            if A.dtype not in (np.float32, np.float64):
+                A = A.astype(np.float64)
+            if A.ndim == 1:
+                A = A.reshape(-1, 1)
+            t = D.to_cm(torch.from_numpy(np.asfortranarray(A)), None, self.device)
+        if t.shape != (self.n_local, w):
+            raise ShapeError(f"block {self.blocks_done + 1} has shape {tuple(t.shape)}, "
+                             f"expected {(self.n_local, w)}")
+        return t
+
+    def _tmp(self, w):
+        if self._tmp64 is None or self._tmp64.shape[1] < w:
+            self._tmp64 = D.empty_cm(self.n_local, w, torch.float64, self.device)
+        return self._tmp64[:, :w]
+
+    # -- Step 2 ------------------------------------------------------------
+    def _solve_ls(self, S, Pi, X):
+        name, param = self.solver
+        scr = self._scr
+        if name == "richardson":
+            _richardson_dev(S, Pi, param, X, scr.T[:, :Pi.shape[1]])
+        elif name == "bmgs_reorth":
+            _bmgs_dev(S, self.offsets, Pi, param, X, scr.T[:, :Pi.shape[1]])
+        elif name == "cg_normal":
+            _cg_dev(S, Pi, param, X)
+        else:
+            _householder_direct_dev(S, Pi, X, scr)
+
+    # -- Steps 4-5 -----------------------------------------------------------
+    def _interblock(self, Qp, Pi, slot, block1):
+        """Writes Q_i into `slot`; returns (R_ii, S_i, Sp_of_Qp or None)."""
+        name, param = self.inter
+        scr = self._scr
+        w = Qp.shape[1]
+        k = self.theta.k
+        Sp = scr.Sp[:, :w]
+        reuse = block1  # sketch(W_1) is P_1 bit for bit (same kernel, same data)
+        if name == "rgs_single":
+            return self._interblock_rgs(Qp, slot)
+        if name == "sketched_cholqr":
+            l = param or 1
+            Rt = scr.Rt[:w, :w]
+            Rt.zero_()
+            Rt.diagonal().fill_(1.0)
+            Qcur = Qp
+            RS = scr.R1[:w, :w]
+            for it in range(l):
+                if it == 0 and reuse:
+                    Sp.copy_(Pi)
+                else:
+                    self._sketch_reduce(Qcur, Sp)
+                if it == 0:
+                    sp_qp = Sp.clone() if self.cfg.certify_blocks else None
+                G = scr.G[:w, :w]
+                D.gemm(1, 0, 1.0, Sp, Sp, 0.0, G)
+                D.potrf(G, RS, scr.info[it % 4:it % 4 + 1])
+                last = it == l - 1
+                # resketch sketches the binary64 Q_i before it is rounded to
+                # the slot's format (rbgs.py:286-287 sketches fp64 Q)
+                out = slot if (last and not self.cfg.resketch) else self._tmp(w)
+                if not last and Qcur.data_ptr() == out.data_ptr():
+                    out = D.empty_cm(self.n_local, w, torch.float64, self.device)
+                D.trsm_right(Qcur, RS, out)
+                Rn = scr.R2[:w, :w]
+                D.gemm(0, 0, 1.0, RS, Rt, 0.0, Rn)
+                Rt.copy_(Rn)
+                Qcur = out
+            Si = scr.Si[:, :w]
+            if self.cfg.resketch:
+                self._sketch_reduce(Qcur, Si)
+                D.convert(Qcur, slot)
+            else:
+                D.trsm_right(Sp, RS, Si)
+            return Rt, Si, sp_qp
+        # l2_plus_cholqr -- Gram realisation of the l2 stage:
+        # R' = chol(Q'^T Q'), S* = (Theta Q') R'^{-1} = Theta Q*, then the
+        # sketched CholQR of Q*: R'' = chol(S*^T S*), R_ii = R'' R',
+        # Q_i = Q' R_ii^{-1}, S_i = S* R''^{-1}.
+        G = scr.G[:w, :w]
+        D.cross(Qp, Qp, G)
+        if reuse:
+            Sp.copy_(Pi)
+            self.comm.allreduce_(G)
+        else:
+            self._sketch(Qp, Sp)
+            self.comm.allreduce_(G, Sp)
+        sp_qp = Sp.clone() if self.cfg.certify_blocks else None
+        R1 = scr.R1[:w, :w]
+        D.potrf(G, R1, scr.info[0:1])
+        torch.cuda.current_stream(self.device).synchronize()
+        if int(scr.info[0]) != 0:
+            # Q' too ill-conditioned for the Gram stage: the sketched CholQR
+            # of Q' computes the same R_ii in exact arithmetic.
+            return self._one_pass_from_sketch(Qp, Sp, slot, sp_qp)
+        Ss = scr.Ss[:, :w]
+        D.trsm_right(Sp, R1, Ss)
+        G2 = scr.G[:w, :w]
+        D.gemm(1, 0, 1.0, Ss, Ss, 0.0, G2)
+        R2 = scr.R2[:w, :w]
+        D.potrf(G2, R2, scr.info[1:2])
+        Rt = scr.Rt[:w, :w]
+        D.gemm(0, 0, 1.0, R2, R1, 0.0, Rt)
+        Si = scr.Si[:, :w]
+        if self.cfg.resketch:
+            q64 = self._tmp(w)
+            D.trsm_right(Qp, Rt, q64)
+            self._sketch_reduce(q64, Si)
+            D.convert(q64, slot)
+        else:
+            D.trsm_right(Qp, Rt, slot)
+            D.trsm_right(Ss, R2, Si)
+        return Rt, Si, sp_qp
+
+    def _one_pass_from_sketch(self, Qp, Sp, slot, sp_qp):
+        scr = self._scr
+        w = Qp.shape[1]
+        G = scr.G[:w, :w]
+        D.gemm(1, 0, 1.0, Sp, Sp, 0.0, G)
+        Rt = scr.Rt[:w, :w]
+        scr.info[0:2].zero_()
+        D.potrf(G, Rt, scr.info[1:2])
+        Si = scr.Si[:, :w]
+        if self.cfg.resketch:
+            q64 = self._tmp(w)
+            D.trsm_right(Qp, Rt, q64)
+            self._sketch_reduce(q64, Si)
+            D.convert(q64, slot)
+        else:
+            D.trsm_right(Qp, Rt, slot)
+            D.trsm_right(Sp, Rt, Si)
+        return Rt, Si, sp_qp
+
+    def _interblock_rgs(self, Qp, slot):
+        """Column-wise randomized Gram-Schmidt (rbgs.py:232-264), fp64 block."""
+        scr = self._scr
+        dev = self.device
+        w = Qp.shape[1]
+        k = self.theta.k
+        Qi = self._tmp(w)
+        D.convert(Qp, Qi)
+        Rb = scr.Rt[:w, :w]
+        Rb.zero_()
+        Sb = scr.Si[:, :w]
+        pv = D.empty_cm(k, 1, torch.float64, dev)
+        s2 = D.empty_cm(k, 1, torch.float64, dev)
+        nrm = torch.zeros(w + 1, dtype=torch.float64, device=dev)
+        D.sumsq(Qp, nrm[w:w + 1])
+        self.comm.allreduce_(nrm[w:w + 1])
+        sp_qp = None
+        if self.cfg.certify_blocks:
+            sp_qp = D.empty_cm(k, w, torch.float64, dev)
+            self._sketch_reduce(Qp, sp_qp)
+        for t in range(w):
+            v = Qi[:, t:t + 1]
+            self._sketch_reduce(v, pv)
+            if t:
+                A = D.empty_cm(k, t, torch.float64, dev)
+                A.copy_(Sb[:, :t])
+                rf = D.empty_cm(t, t, torch.float64, dev)
+                D.geqrf(A, rf)
+                y = D.empty_cm(t, 1, torch.float64, dev)
+                D.gemm(1, 0, 1.0, A, pv, 0.0, y)
+                D.trsm_left_upper(rf, y, scr.info[7:8])
+                Rb[:t, t:t + 1].copy_(y)
+                D.project(Qi[:, :t], y, v, v, F64, ORDER_REFERENCE)
+            self._sketch_reduce(v, s2)
+            rtt = nrm[t:t + 1]
+            D.sumsq(s2, rtt)
+            rtt.sqrt_()
+            Rb[t, t:t + 1].copy_(rtt)
+            rr = rtt.reshape(1, 1)
+            D.trsm_right(v, rr, v)
+            D.trsm_right(s2, rr, Sb[:, t:t + 1])
+        D.convert(Qi, slot)
+        self._rgs_norms = nrm
+        return Rb, Sb, sp_qp
+
+    # -- one block -------------------------------------------------------------
+    def push_block(self, W_i) -> tuple:
+        """One RBGS iteration on block W_i (rbgs.py:352-399); returns (j0, j1)."""
+        self.pending_P = None
+        i = self.blocks_done + 1
+        if self.blocks_done >= len(self.offsets) - 1:
+            raise ShapeError(f"all {len(self.offsets) - 1} blocks already pushed")
+        j0, j1 = self.offsets[self.blocks_done], self.offsets[self.blocks_done + 1]
+        w = j1 - j0
+        with torch.cuda.device(self.device):
+            return self._push(i, j0, j1, w, self._as_block(W_i, w))
+
+    def _push(self, i, j0, j1, w, W):
+        scr = self._scr
+        cfg = self.cfg
+        c = self.cols_done
+        Pi = scr.Pi[:, :w]
+        # Step 1
+        self._sketch_reduce(W, Pi)
+        slot = self.Q[:, j0:j1]
+        norms = scr.norms
+        norms.zero_()
+        scr.info.zero_()
+        if c:
+            X = scr.X[:c, :w]
+            self._solve_ls(self.S[:, :c], Pi, X)
+            self.R[:c, j0:j1].copy_(X)
+            D.project(self.Q[:, :c], X, W, slot, self.compute, self.order, norms[0:2])
+            Qp = slot
+        else:
+            # Q' = W_1 itself (rbgs.py:371-372): read it in its own format
+            D.sumsq(W, norms[0:1])
+            Qp = W
+        self.comm.allreduce_(norms[0:2])
+        if not c:
+            norms[1:2].copy_(norms[0:1])
+        Rii, Si, sp_qp = self._interblock(Qp, Pi, slot, block1=(c == 0))
+        # finiteness of everything the block produced (Matrix() checks)
+        D.sumsq(Pi, norms[2:3])
+        D.sumsq(Si, norms[3:4])
+        D.sumsq(Rii, norms[4:5])
+        scr.status_host.copy_(norms, non_blocking=True)
+        scr.info_host.copy_(scr.info, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        st = scr.status_host.numpy()
+        info = scr.info_host.numpy()
+        w_norm = math.sqrt(st[0]) if st[0] >= 0 else float("nan")
+        q_norm = math.sqrt(st[1]) if st[1] >= 0 else float("nan")
+        if not (np.isfinite(st[0]) and np.isfinite(st[1]) and np.isfinite(st[2])):
+            raise ValueError("Matrix entries must be finite")
+        if q_norm <= self.n * U_FINE * w_norm:
+            self.pending_P = Matrix(Pi.clone())
+            if c:
+                slot.zero_()
+            raise DependentBlockError(i, "projected block vanished")
+        if self.inter[0] == "rgs_single":
+            self._check_rgs(i, q_norm, w)
+        for col in info[:4]:
+            if col:
+                if c:
+                    slot.zero_()
+                raise InterblockError(i, str(NotPositiveDefiniteError(int(col)))) from \
+                    NotPositiveDefiniteError(int(col))
+        if not (np.isfinite(st[3]) and np.isfinite(st[4])):
+            raise ValueError("Matrix entries must be finite")
+        self.S[:, j0:j1].copy_(Si)
+        self.P[:, j0:j1].copy_(Pi)
+        self.R[j0:j1, j0:j1].copy_(Rii)
+        if cfg.certify_blocks:
+            if sp_qp is None:
+                sp_qp = D.empty_cm(self.theta.k, w, torch.float64, self.device)
+                self._sketch_reduce(Qp, sp_qp)
+            self._certify_block(Si, Rii, sp_qp)
+        self.blocks_done += 1
+        self.cols_done = j1
+        return j0, j1
+
+    def _check_rgs(self, i, q_norm, w):
+        r = self._rgs_norms[:w].cpu().numpy()
+        thr = self.n * U_FINE * q_norm
+        for t in range(w):
+            if not r[t] > thr:
+                raise DependentBlockError(i, f"dependent column: block {t + 1} numerically "
+                                             f"dependent: sketched norm {r[t]:.3e} below dependence threshold")
+
+    def _certify_block(self, Si, Rii, Sp):
+        w = Si.shape[1]
+        dev = self.device
+        G = D.empty_cm(w, w, torch.float64, dev)
+        D.gemm(1, 0, 1.0, Si, Si, 0.0, G)
+        T = D.empty_cm(Sp.shape[0], w, torch.float64, dev)
+        T.copy_(Sp)
+        D.gemm(0, 0, -1.0, Si, Rii, 1.0, T)
+        out = torch.zeros(3, dtype=torch.float64, device=dev)
+        D.sumsq(G, out[0:1], minus_identity=True)
+        D.sumsq(T, out[1:2])
+        D.sumsq(Sp, out[2:3])
+        o = out.cpu().numpy()
+        self.per_block_ortho.append(float(math.sqrt(o[0])))
+        self.per_block_resid.append(float(math.sqrt(o[1]) / math.sqrt(o[2])))
+
+    def finish(self) -> BlockQR:
+        c = self.cols_done
+        with torch.cuda.device(self.device):
+            cert0 = certify(self.S[:, :c], self.P[:, :c], self.R[:c, :c])
+        cert = CertReport(cert0.delta, cert0.delta_tilde, tuple(self.per_block_ortho),
+                          tuple(self.per_block_resid))
+        return BlockQR(Matrix(self.Q, precision=self.cfg.coarse), Matrix(self.R), Matrix(self.S),
+                       Matrix(self.P), self.cfg.partition, cert)
+
+
+def rbgs(W, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None) -> BlockQR:
+    """Factor W = QR with Q orthonormal in the sketched inner product
+    (rbgs.py:410-421).  W: numpy / Matrix (uploaded once; binary32 arrays
+    stay binary32) or a CUDA tensor (used in place); with a sharded
+    DeviceConfig, W holds this rank's rows."""
+    require_cuda()
+    dc = device_cfg or DeviceConfig()
+    dev = D.cuda_device(dc.device)
+    if isinstance(W, Matrix):
+        W = W._dev if W._dev is not None else W.data
+    if isinstance(W, torch.Tensor):
+        Wd = D.to_cm(W, W.dtype if W.dtype in (torch.float32, torch.float64) else torch.float64, dev)
+    else:
+        A = np.asarray(W)
+        if A.dtype not in (np.float32, np.float64):
+            A = A.astype(np.float64)
+        if A.ndim != 2:
+            raise ShapeError(f"expected a 2-D array, got ndim={A.ndim}")
+        Wd = D.to_cm(torch.from_numpy(np.asfortranarray(A)), None, dev)
+    n_rows, m = Wd.shape
+    if cfg.partition.total_cols != m:
+        raise ShapeError(f"partition covers {cfg.partition.total_cols} cols, W has {m}")
+    n = theta.n if dc.shard is not None else n_rows
+    sweep = RbgsSweep(n, theta, cfg, dc)
+    off = cfg.partition.offsets()
+    for b in range(cfg.partition.num_blocks):
+        sweep.push_block(Wd[:, off[b]:off[b + 1]])
+    return sweep.finish()
+
+
+def certify(S, P, R, device=None) -> CertReport:
+    """Delta = ||I - S^T S||_F, Delta~ = ||P - S R||_F / ||P||_F on the GPU
+    (rbgs.py:428-443); k-dimensional data only."""
+    require_cuda()
+    dev = D.cuda_device(device if device is not None else
+                        (S.device if isinstance(S, torch.Tensor) and S.is_cuda else None))
+    with torch.cuda.device(dev):
+        Sd, Pd, Rd = _dev_f64(S, dev), _dev_f64(P, dev), _dev_f64(R, dev)
+        k, m = Sd.shape
+        out = torch.zeros(3, dtype=torch.float64, device=dev)
+        D.sumsq(Pd, out[2:3])
+        if m:
+            G = D.empty_cm(m, m, torch.float64, dev)
+            D.gemm(1, 0, 1.0, Sd, Sd, 0.0, G)
+            D.sumsq(G, out[0:1], minus_identity=True)
+            T = D.empty_cm(k, m, torch.float64, dev)
+            T.copy_(Pd)
+            D.gemm(0, 0, -1.0, Sd, Rd, 1.0, T)
+            D.sumsq(T, out[1:2])
+        o = out.cpu().numpy()
+    if not np.all(np.isfinite(o)):
+        raise ValueError("Matrix entries must be finite")
+    if o[2] == 0.0:
+        raise CertificationError("certification undefined for a zero sketch P")
+    return CertReport(float(math.sqrt(o[0])), float(math.sqrt(o[1]) / math.sqrt(o[2])))
+
+
+# ---------------------------------------------------------------------------
+# standalone Step-2 / Step-4-5 entry points (reference signatures)
+# ---------------------------------------------------------------------------
+
+def _ls_entry(fn, S, Pi, param, prec, device=None):
+    if prec.format != "fine":
+        raise NotImplementedError("coarse-precision LS solves are not implemented on the device path")
+    dev = D.cuda_device(device)
+    with torch.cuda.device(dev):
+        Sd, Pd = _dev_f64(S, dev), _dev_f64(Pi, dev)
+        X = D.empty_cm(Sd.shape[1], Pd.shape[1], torch.float64, dev)
+        fn(Sd, Pd, param, X)
+        return Matrix(X)
+
+
+def ls_richardson(S, Pi, l: int, prec: PrecisionSpec = FINE) -> Matrix:
+    def f(Sd, Pd, l, X):
+        T = D.empty_cm(Sd.shape[0], Pd.shape[1], torch.float64, Sd.device)
+        _richardson_dev(Sd, Pd, l, X, T)
+    return _ls_entry(f, S, Pi, l, prec)
+
+
+def ls_bmgs_reorth(S_blocks, Pi, l: int, prec: PrecisionSpec = FINE) -> Matrix:
+    blocks = [as_array(B) if not isinstance(B, torch.Tensor) else B for B in S_blocks]
+    widths = [B.shape[1] for B in blocks]
+    off = [0]
+    for w in widths:
+        off.append(off[-1] + w)
+    S = np.hstack([as_array(B) for B in blocks]) if blocks else np.zeros((as_array(Pi).shape[0], 0))
+
+    def f(Sd, Pd, l, X):
+        T = D.empty_cm(Sd.shape[0], Pd.shape[1], torch.float64, Sd.device)
+        _bmgs_dev(Sd, off, Pd, l, X, T)
+    return _ls_entry(f, S, Pi, l, prec)
+
+
+def ls_cg_normal(S, Pi, iters: int, prec: PrecisionSpec = FINE) -> Matrix:
+    return _ls_entry(lambda Sd, Pd, it, X: _cg_dev(Sd, Pd, it, X), S, Pi, iters, prec)
+
+
+def ls_householder_direct(S, Pi, prec: PrecisionSpec = FINE) -> Matrix:
+    class _S:
+        info = None
+
+    def f(Sd, Pd, _, X):
+        scr = _S()
+        scr.info = torch.zeros(8, dtype=torch.int32, device=Sd.device)
+        _householder_direct_dev(Sd, Pd, X, scr)
+    return _ls_entry(f, S, Pi, None, prec)
+
+
+def _standalone_interblock(Qprime, theta, cfg):
+    W = Qprime
+    if isinstance(W, Matrix):
+        W = W._dev if W._dev is not None else W.data
+    A = W if isinstance(W, torch.Tensor) else torch.from_numpy(np.asfortranarray(as_array(W)))
+    n, w = A.shape
+    if w > theta.k:
+        raise ShapeError(f"block width {w} exceeds sketch size {theta.k}")
+    sw = RbgsSweep(n, theta, RbgsConfig(partition=BlockPartition(w, 1, w), coarse=FINE, **cfg))
+    try:
+        sw.push_block(A.to(torch.float64) if isinstance(A, torch.Tensor) else A)
+    except InterblockError as e:
+        cause = e.__cause__
+        raise (cause if cause is not None else e)
+    except DependentBlockError as e:
+        cause = e.__cause__
+        raise (cause if cause is not None else e)
+    return Matrix(sw.Q), Matrix(sw.R), Matrix(sw.S)
+
+
+def interblock_sketched_cholqr(Qprime, theta, l: int = 1, resketch: bool = False):
+    """Sketched Cholesky QR of one block, l passes (rbgs.py:267-290)."""
+    return _standalone_interblock(Qprime, theta, dict(interblock=f"sketched_cholqr({l})", resketch=resketch))
+
+
+def interblock_l2_cholqr(Qprime, theta, resketch: bool = False):
+    """l2 stage then one sketched CholQR pass (rbgs.py:293-302)."""
+    return _standalone_interblock(Qprime, theta, dict(interblock="l2_plus_cholqr", resketch=resketch))
+
+
+def interblock_rgs(Qprime, theta):
+    """Column-wise randomized Gram-Schmidt (rbgs.py:232-264)."""
+    return _standalone_interblock(Qprime, theta, dict(interblock="rgs_single"))
