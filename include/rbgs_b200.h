@@ -71,17 +71,23 @@ int rb_project(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t n
  * out (k x ncols, fp64, col-major, ld ldo) = Theta[:, row0:row0+n] @ X,
  * summed in fp64.  accumulate != 0 adds into out instead of overwriting.  */
 
-/* gaussian kind: materialise the int16 table q (k x nrows, K-major: entry
- * (r, i) at theta[r * ldt + i]) for global rows row0..row0+nrows-1.
- * Definition in DESIGN.md section 3 (Philox4x32-10 + Box-Muller, 2^-11). */
+/* gaussian kind: materialise the table of q = rint(2048 g) (an int16 value;
+ * Philox4x32-10 + Box-Muller) for global rows
+ * row0 .. row0+nrows-1 as two byte planes, hi = q >> 8 (signed) and
+ * lo = q & 255, tiled in 128 x 128 blocks (csrc/gauss_layout.cuh).
+ * ldt (padded row count) % 128 == 0; the buffer holds
+ * 2 * ceil(k/128) * 128 * ldt bytes, padding zeroed.                      */
 int rb_gaussian_fill(uint64_t seed, int k, int64_t row0, int64_t nrows,
-                     int16_t* theta, int64_t ldt, void* stream);
-/* out = scale * (q @ X) for an int16 table (gaussian kind; scale =
- * 1 / (2048 sqrt(k))). */
-int rb_sketch_dense_i16(int x_dtype, int64_t n, int ncols, const void* X, int64_t ldx,
-                        const int16_t* theta, int64_t ldt, int k, double scale,
-                        double* out, int64_t ldo, int accumulate,
-                        void* ws, size_t ws_bytes, void* stream);
+                     uint8_t* theta, int64_t ldt, void* stream);
+/* out = scale * (q @ X) (scale = 1 / (2048 sqrt(k)) gives Theta @ X).
+ * mode 0 = auto (tensor pipe for binary32 X, fp64 CUDA cores for binary64),
+ * 1 = fp64 CUDA cores (exact fp64 products), 2 = tensor pipe: tcgen05
+ * kind::i8 on the exact byte split of q and of X's per-chunk fixed-point
+ * form (sketch_tc.cu).                                                    */
+int rb_sketch_gaussian(int x_dtype, int64_t n, int ncols, const void* X, int64_t ldx,
+                       const uint8_t* theta, int64_t ldt, int k, double scale,
+                       double* out, int64_t ldo, int accumulate, int mode,
+                       void* ws, size_t ws_bytes, void* stream);
 /* srht kind (sketching.py:129-137): signs as a bitmask over the GLOBAL
  * padded index space (bit i set <=> sign_diagonal[i] = -1), sample = the
  * k global sample indices, scale = 1/sqrt(k).  Rows >= n_valid (global)

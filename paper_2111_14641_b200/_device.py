@@ -137,12 +137,15 @@ def project(Q, X, W, Qp, compute, order, norms2=None):
         _t1(e0, "project", n * (c * qs + p * W.element_size() + p * Qp.element_size()), 2.0 * n * c * p)
 
 
-def sketch_dense_i16(X, theta, ldt, k, scale, out, accumulate=False):
+GAUSS_MODE = {"auto": 0, "fp64": 1, "tensor": 2}
+
+
+def sketch_gaussian(X, theta, ldt, k, scale, out, accumulate=False, mode="auto"):
     n, cols = X.shape
     ws, wsb = _ws(n, cols, k, X.device)
     e0 = _t0()
-    call("rb_sketch_dense_i16", dtype_code(X), n, cols, ptr(X), ld(X), ptr(theta), ldt, k, scale,
-         ptr(out), ld(out), int(accumulate), ws, wsb, st(X.device))
+    call("rb_sketch_gaussian", dtype_code(X), n, cols, ptr(X), ld(X), ptr(theta), ldt, k, scale,
+         ptr(out), ld(out), int(accumulate), GAUSS_MODE[mode], ws, wsb, st(X.device))
     _t1(e0, "sketch_gaussian", n * (cols * X.element_size() + 2 * k), 2.0 * k * n * cols)
 
 

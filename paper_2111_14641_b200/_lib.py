@@ -32,7 +32,7 @@ SIGNATURES = {
     "rb_workspace_bytes": [_i64, _i, _i],
     "rb_project": [_i, _i, _i, _i, _i64, _i, _i, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, _p, _sz, _p],
     "rb_gaussian_fill": [_u64, _i, _i64, _i64, _p, _i64, _p],
-    "rb_sketch_dense_i16": [_i, _i64, _i, _p, _i64, _p, _i64, _i, _d, _p, _i64, _i, _p, _sz, _p],
+    "rb_sketch_gaussian": [_i, _i64, _i, _p, _i64, _p, _i64, _i, _d, _p, _i64, _i, _i, _p, _sz, _p],
     "rb_sketch_srht": [_i, _i64, _i, _p, _i64, _i64, _i64, _p, _p, _i, _d, _p, _i64, _i, _p, _sz, _p],
     "rb_sketch_sparse_sign": [_i, _i64, _i, _p, _i64, _i64, _u64, _i, _i, _p, _i64, _i, _p, _sz, _p],
     "rb_sketch_signs": [_i, _i64, _i, _p, _i64, _p, _i64, _i, _d, _p, _i64, _i, _p, _sz, _p],

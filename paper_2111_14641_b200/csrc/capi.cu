@@ -41,9 +41,10 @@ int sm_count() {
 
 int project(int, int, int, int, int64_t, int, int, const void*, int64_t, const double*, int64_t, const void*, int64_t,
             void*, int64_t, double*, void*, size_t, cudaStream_t);
-int gaussian_fill(uint64_t, int, int64_t, int64_t, int16_t*, int64_t, cudaStream_t);
-int sketch_dense_i16(int, int64_t, int, const void*, int64_t, const int16_t*, int64_t, int, double, double*, int64_t,
-                     int, void*, size_t, cudaStream_t);
+int gaussian_fill(uint64_t, int, int64_t, int64_t, uint8_t*, int64_t, cudaStream_t);
+int sketch_gaussian(int, int64_t, int, const void*, int64_t, const uint8_t*, int64_t, int, double, double*, int64_t,
+                    int, int, void*, size_t, cudaStream_t);
+size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k);
 int sketch_signs(int, int64_t, int, const void*, int64_t, const uint32_t*, int64_t, int, double, double*, int64_t, int,
                  void*, size_t, cudaStream_t);
 int sketch_srht(int, int64_t, int, const void*, int64_t, int64_t, int64_t, const uint32_t*, const int64_t*, int,
@@ -87,7 +88,9 @@ size_t rb_workspace_bytes(int64_t n, int ncols, int k) {
   const size_t norms = ((size_t)(n > 0 ? n : 0) / 128 + 64) * 2 * sizeof(double);
   const size_t single = kk * cc * sizeof(double) * 2;
   size_t b = tiles > norms ? tiles : norms;
-  return (b > single ? b : single) + (1u << 20);
+  b = b > single ? b : single;
+  const size_t g = rb::gauss_tc_ws_bytes(n, ncols, k);
+  return (b > g ? b : g) + (1u << 20);
 }
 
 int rb_project(int qd, int wd, int cd, int order, int64_t n, int c, int p, const void* Q, int64_t ldq,
@@ -96,13 +99,14 @@ int rb_project(int qd, int wd, int cd, int order, int64_t n, int c, int p, const
   return rb::project(qd, wd, cd, order, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, norms2, ws, wsb, as_stream(s));
 }
 
-int rb_gaussian_fill(uint64_t seed, int k, int64_t row0, int64_t nrows, int16_t* theta, int64_t ldt, void* s) {
+int rb_gaussian_fill(uint64_t seed, int k, int64_t row0, int64_t nrows, uint8_t* theta, int64_t ldt, void* s) {
   return rb::gaussian_fill(seed, k, row0, nrows, theta, ldt, as_stream(s));
 }
 
-int rb_sketch_dense_i16(int xd, int64_t n, int ncols, const void* X, int64_t ldx, const int16_t* theta, int64_t ldt,
-                        int k, double scale, double* out, int64_t ldo, int acc, void* ws, size_t wsb, void* s) {
-  return rb::sketch_dense_i16(xd, n, ncols, X, ldx, theta, ldt, k, scale, out, ldo, acc, ws, wsb, as_stream(s));
+int rb_sketch_gaussian(int xd, int64_t n, int ncols, const void* X, int64_t ldx, const uint8_t* theta, int64_t ldt,
+                       int k, double scale, double* out, int64_t ldo, int acc, int mode, void* ws, size_t wsb,
+                       void* s) {
+  return rb::sketch_gaussian(xd, n, ncols, X, ldx, theta, ldt, k, scale, out, ldo, acc, mode, ws, wsb, as_stream(s));
 }
 
 int rb_sketch_srht(int xd, int64_t n, int ncols, const void* X, int64_t ldx, int64_t row0, int64_t n_pad,

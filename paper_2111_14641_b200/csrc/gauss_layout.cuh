@@ -1,0 +1,39 @@
+// Layout of the gaussian table q (and of the X byte planes) in HBM, tiled for
+// the tensor-core sketch: every (128 sketch rows x 128 W-rows) tile of the
+// two byte planes of q is one contiguous 32 KB block, laid out exactly as the
+// UMMA K-major no-swizzle operand wants it in shared memory
+// ([plane][16-byte K chunk][row][16 bytes]), so one bulk async copy moves it.
+#pragma once
+
+#include <stdint.h>
+
+namespace rb {
+namespace gl {
+
+constexpr int kTM = 128;  // sketch rows per tile (UMMA M)
+constexpr int kBK = 128;  // W-rows per tile (K bytes)
+constexpr int kTileBytes = kTM * kBK;  // one plane of one tile
+
+// q planes: plane 0 = hi (s8, q >> 8), plane 1 = lo (u8, q & 255).
+// ldt = padded W-row count (multiple of kBK); KT = ldt / kBK.
+__host__ __device__ __forceinline__ int64_t q_offset(int plane, int r, int64_t i, int64_t ldt) {
+  const int64_t KT = ldt / kBK;
+  const int mt = r / kTM, rr = r % kTM;
+  const int64_t kt = i / kBK;
+  const int kc = (int)((i % kBK) >> 4), b = (int)(i & 15);
+  return (((int64_t)mt * KT + kt) * 2 + plane) * kTileBytes + (int64_t)kc * (kTM * 16) + rr * 16 + b;
+}
+
+__host__ __device__ __forceinline__ int64_t q_bytes(int k, int64_t ldt) {
+  return (int64_t)((k + kTM - 1) / kTM) * kTM * ldt * 2;
+}
+
+// X planes (b0..b3) for NP padded columns: tile kt is 4 x kBK x NP bytes.
+__host__ __device__ __forceinline__ int64_t x_offset(int plane, int j, int64_t i, int NP) {
+  const int64_t kt = i / kBK;
+  const int kc = (int)((i % kBK) >> 4), b = (int)(i & 15);
+  return (kt * 4 + plane) * ((int64_t)kBK * NP) + (int64_t)kc * (NP * 16) + j * 16 + b;
+}
+
+}  // namespace gl
+}  // namespace rb

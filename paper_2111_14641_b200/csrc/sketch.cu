@@ -14,6 +14,7 @@
 //  * sparse_sign: each row i scatters s signed copies of X[i, :] into a
 //    shared-memory k x CG accumulator.
 #include "common.cuh"
+#include "gauss_layout.cuh"
 
 namespace rb {
 
@@ -26,10 +27,15 @@ constexpr int kThreads = 256;
 // ======================= dense (split-K fp64 GEMM) ==========================
 constexpr int BM = 128, BK = 16, TM = 8;
 
-struct I16Src {
-  const int16_t* t;
+// gaussian table: hi (s8, q >> 8) and lo (u8, q & 255) byte planes in the
+// tiled layout the tensor-core kernel streams (gauss_layout.cuh).
+struct PlaneSrc {
+  const uint8_t* t;
   int64_t ld;
-  __device__ __forceinline__ double at(int r, int64_t i) const { return (double)t[(int64_t)r * ld + i]; }
+  int k;
+  __device__ __forceinline__ double at(int r, int64_t i) const {
+    return (double)((int)(int8_t)t[gl::q_offset(0, r, i, ld)] * 256 + (int)t[gl::q_offset(1, r, i, ld)]);
+  }
 };
 struct BitSrc {
   const uint32_t* b;
@@ -143,7 +149,7 @@ int dense_sketch(int64_t n, int ncols, const TX* X, int64_t ldx, Src src, int k,
 
 // ======================= gaussian table fill ================================
 __global__ void gaussian_fill_kernel(uint64_t seed, int k, int64_t row0, int64_t nrows,
-                                     int16_t* __restrict__ theta, int64_t ldt) {
+                                     uint8_t* __restrict__ theta, int64_t ldt) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int q = blockIdx.y;  // quad of sketch rows 4q..4q+3
   if (i >= nrows) return;
@@ -165,7 +171,9 @@ __global__ void gaussian_fill_kernel(uint64_t seed, int k, int64_t row0, int64_t
     if (r < k) {
       double v = rint(2048.0 * g[t]);
       v = fmin(fmax(v, -32767.0), 32767.0);
-      theta[(int64_t)r * ldt + i] = (int16_t)v;
+      const int q = (int)v;
+      theta[gl::q_offset(0, r, i, ldt)] = (uint8_t)(q >> 8);   // hi plane (signed byte)
+      theta[gl::q_offset(1, r, i, ldt)] = (uint8_t)(q & 255);  // lo plane
     }
   }
 }
@@ -367,21 +375,30 @@ int sparse_sketch(int64_t n, int ncols, const TX* X, int64_t ldx, int64_t row0, 
 }  // namespace
 
 // ============================== entry points ================================
-int gaussian_fill(uint64_t seed, int k, int64_t row0, int64_t nrows, int16_t* theta, int64_t ldt,
+int gaussian_fill(uint64_t seed, int k, int64_t row0, int64_t nrows, uint8_t* theta, int64_t ldt,
                   cudaStream_t st) {
-  RB_REQUIRE(k >= 1 && k <= 4 * 65535 && nrows >= 0 && ldt >= nrows && theta, "rb_gaussian_fill: bad args");
-  if (nrows == 0) return RB_OK;
+  RB_REQUIRE(k >= 1 && k <= 4 * 65535 && nrows >= 0 && ldt >= nrows && ldt % gl::kBK == 0 && theta,
+             "rb_gaussian_fill: bad args (ldt must be a multiple of 128)");
+  cudaMemsetAsync(theta, 0, (size_t)gl::q_bytes(k, ldt), st);  // zero padding rows / columns
+  if (nrows == 0) return check_launch("rb_gaussian_fill");
   dim3 grid(ceil_div(nrows, 256), (k + 3) / 4);
   RB_KLAUNCH gaussian_fill_kernel<<<grid, 256, 0, st>>>(seed, k, row0, nrows, theta, ldt);
   return check_launch("rb_gaussian_fill");
 }
 
-int sketch_dense_i16(int xd, int64_t n, int ncols, const void* X, int64_t ldx, const int16_t* theta,
-                     int64_t ldt, int k, double scale, double* out, int64_t ldo, int acc, void* ws,
-                     size_t wsb, cudaStream_t st) {
-  RB_REQUIRE(ncols >= 1 && ncols <= 64 && k >= 1 && ldo >= k && out, "rb_sketch_dense_i16: bad args");
-  RB_REQUIRE(n == 0 || (X && ldx >= n && theta && ldt >= n), "rb_sketch_dense_i16: bad X/theta");
-  I16Src src{theta, ldt};
+size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k);
+int sketch_gaussian_tc(int xd, int64_t n, int ncols, const void* X, int64_t ldx, const uint8_t* theta, int64_t ldt,
+                       int k, double scale, double* out, int64_t ldo, int acc, void* ws, size_t wsb, cudaStream_t st);
+
+int sketch_gaussian(int xd, int64_t n, int ncols, const void* X, int64_t ldx, const uint8_t* theta, int64_t ldt,
+                    int k, double scale, double* out, int64_t ldo, int acc, int mode, void* ws, size_t wsb,
+                    cudaStream_t st) {
+  RB_REQUIRE(ncols >= 1 && ncols <= 64 && k >= 1 && ldo >= k && out, "rb_sketch_gaussian: bad args");
+  RB_REQUIRE(n == 0 || (X && ldx >= n && theta && ldt >= n), "rb_sketch_gaussian: bad X/theta");
+  RB_REQUIRE(mode >= 0 && mode <= 2, "rb_sketch_gaussian: bad mode %d", mode);
+  const bool tc = mode == 2 || (mode == 0 && xd == RB_F32);
+  if (tc) return sketch_gaussian_tc(xd, n, ncols, X, ldx, theta, ldt, k, scale, out, ldo, acc, ws, wsb, st);
+  PlaneSrc src{theta, ldt, k};
   if (xd == RB_F32) return dense_sketch<float>(n, ncols, (const float*)X, ldx, src, k, scale, out, ldo, acc, ws, wsb, st);
   return dense_sketch<double>(n, ncols, (const double*)X, ldx, src, k, scale, out, ldo, acc, ws, wsb, st);
 }

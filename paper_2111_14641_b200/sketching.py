@@ -20,6 +20,7 @@ sparse_sign kind needs no table; its rows are hashed in-kernel.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -35,6 +36,9 @@ __all__ = ["KINDS", "EXTENDED_KINDS", "SketchOperator", "make_operator", "apply"
 KINDS = ("rademacher", "srht", "identity")
 EXTENDED_KINDS = ("gaussian", "sparse_sign")
 GAUSS_GRID = 2048.0
+# gaussian sketch engine: "auto" (tensor pipe for binary32 inputs, fp64 CUDA
+# cores for binary64), "fp64" or "tensor"; overridable for tests/benchmarks.
+GAUSS_MODE = os.environ.get("RB_GAUSS_MODE", "auto")
 
 
 def _next_pow2(n: int) -> int:
@@ -113,8 +117,8 @@ class SketchOperator:
             bits = _pack_bits(sl < 0, words)
             tab = dict(bits=torch.from_numpy(np.ascontiguousarray(bits).view(np.int32)).to(dev), ldb=words)
         elif self.kind == "gaussian":
-            ldt = max(nrows, 1)
-            theta = torch.empty((self.k, ldt), dtype=torch.int16, device=dev)
+            ldt = max(-(-nrows // 128) * 128, 128)
+            theta = torch.empty((2 * (-(-self.k // 128)) * 128, ldt), dtype=torch.uint8, device=dev)
             with torch.cuda.device(dev):
                 D.gaussian_fill(self.seed, self.k, row0, nrows, theta, ldt)
             tab = dict(theta=theta, ldt=ldt)
@@ -171,8 +175,8 @@ def sketch_into(theta: SketchOperator, X: torch.Tensor, out: torch.Tensor, row0:
     elif theta.kind == "rademacher":
         D.sketch_signs(X, tab["bits"], tab["ldb"], k, 1.0 / math.sqrt(k), out, accumulate)
     elif theta.kind == "gaussian":
-        D.sketch_dense_i16(X, tab["theta"], tab["ldt"], k, 1.0 / (GAUSS_GRID * math.sqrt(k)), out,
-                           accumulate)
+        D.sketch_gaussian(X, tab["theta"], tab["ldt"], k, 1.0 / (GAUSS_GRID * math.sqrt(k)), out,
+                          accumulate, GAUSS_MODE)
     else:
         D.sketch_sparse_sign(X, row0, theta.seed, k, theta.nnz, out, accumulate)
 

@@ -106,7 +106,15 @@ def test_gaussian_table_matches_oracle(pkg):
     for k, n, seed, row0 in [(37, 50, 20240917, 0), (1600, 3000, 7, 0), (9, 5, 7, 2 ** 33), (81, 4096, 3, 1000)]:
         op = sketching.gaussian_operator(k, row0 + n, seed)
         tab = op.device_tables("cuda", row0, n)
-        got = tab["theta"][:, :n].cpu().numpy()
+        flat = tab["theta"].cpu().numpy().reshape(-1)
+        ldt = tab["ldt"]
+        r = np.arange(k)[:, None]
+        i = np.arange(n)[None, :]
+        KT = ldt // 128
+        base = (((r // 128) * KT + i // 128) * 2) * 16384 + ((i % 128) // 16) * 2048 + (r % 128) * 16 + i % 16
+        hi = flat[base].view(np.int8).astype(np.int32)
+        lo = flat[base + 16384].astype(np.int32)
+        got = (hi * 256 + lo).astype(np.int16)
         want = osk.gaussian_int16(seed, k, np.arange(row0, row0 + n))
         bad = np.sum(got != want)
         # CUDA and glibc log/sincos may differ by an ulp; a flip of the
@@ -134,7 +142,41 @@ def test_sketch_vs_oracle(pkg, kind, dtype):
     sketching.sketch_into(op, Xd, out)
     got = out.cpu().numpy()
     want = osk.apply(oop, X)
-    assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want), kind
+    # binary32 gaussian sketches run on the tensor pipe (exact byte-split
+    # products, inputs fixed-point at 2^-30 of each 8192-row chunk max)
+    tol = 1e-9 if (kind == "gaussian" and dtype == torch.float32) else 1e-13
+    assert np.linalg.norm(got - want) <= tol * np.linalg.norm(want), kind
+
+
+@pytest.mark.parametrize("n,k,cols", [(100, 37, 1), (8192, 128, 16), (20_001, 300, 40), (70_000, 1600, 64),
+                                      (9000, 129, 5)])
+def test_gaussian_tensor_pipe_vs_fp64(pkg, n, k, cols):
+    """tcgen05 kind::i8 gaussian sketch vs the fp64 CUDA-core kernel and the
+    oracle, on columns with 10 decades of dynamic range."""
+    rbgs, sketching, D = pkg
+    g = np.random.Generator(np.random.Philox(n + k))
+    X = g.standard_normal((n, cols)) * np.logspace(0, -10, cols)
+    X[::7] *= 1e-3  # rows far below their chunk max
+    X = X.astype(np.float32).astype(np.float64)
+    op = sketching.gaussian_operator(k, n, 99)
+    tab = op.device_tables("cuda", 0, n)
+    Xd = _dev(X, torch.float32)
+    res = {}
+    for mode in ("tensor", "fp64"):
+        out = D.empty_cm(k, cols, torch.float64, "cuda")
+        D.sketch_gaussian(Xd, tab["theta"], tab["ldt"], k, 1.0 / (2048 * math.sqrt(k)), out, False, mode)
+        res[mode] = out.cpu().numpy()
+    want = osk.apply(osk.OracleSketch("gaussian", k, n, 99), X)
+    for j in range(cols):
+        wn = np.linalg.norm(want[:, j])
+        assert np.linalg.norm(res["fp64"][:, j] - want[:, j]) <= 1e-13 * wn
+        assert np.linalg.norm(res["tensor"][:, j] - want[:, j]) <= 1e-8 * wn, (j, np.linalg.norm(
+            res["tensor"][:, j] - want[:, j]) / wn)
+    # accumulate flag adds
+    out = D.empty_cm(k, cols, torch.float64, "cuda")
+    out.copy_(torch.from_numpy(res["tensor"]))
+    D.sketch_gaussian(Xd, tab["theta"], tab["ldt"], k, 1.0 / (2048 * math.sqrt(k)), out, True, "tensor")
+    assert np.allclose(out.cpu().numpy(), 2 * res["tensor"], rtol=1e-15, atol=0)
 
 
 @pytest.mark.parametrize("kind", ["gaussian", "sparse_sign", "srht"])
@@ -213,8 +255,14 @@ def test_rbgs_vs_reference_golden(pkg, name):
     assert goldens.rel(f.Q.data, c["Q"]) <= qtol
     assert goldens.rel(f.P.data, c["P"]) <= 1e-12
     d, dt = c["cert"]
-    assert abs(f.cert.delta - d) <= 1e-2 * d + 1e-12, (f.cert.delta, d)
-    assert abs(f.cert.delta_tilde - dt) <= 1e-2 * dt + 1e-14, (f.cert.delta_tilde, dt)
+    if c["coarse"] == "fine":
+        assert abs(f.cert.delta - d) <= 1e-2 * d + 1e-12, (f.cert.delta, d)
+        assert abs(f.cert.delta_tilde - dt) <= 1e-2 * dt + 1e-14, (f.cert.delta_tilde, dt)
+    else:
+        # two-precision certificates sit at the binary32 rounding level:
+        # "same order" (north star), i.e. within a factor 1.5
+        assert d / 1.5 <= f.cert.delta <= 1.5 * d + 1e-12, (f.cert.delta, d)
+        assert dt / 1.5 <= f.cert.delta_tilde <= 1.5 * dt + 1e-14, (f.cert.delta_tilde, dt)
     if c["certify_blocks"]:
         assert np.allclose(f.cert.per_block_ortho, c["pbo"], rtol=1e-2, atol=1e-12)
         assert np.allclose(f.cert.per_block_resid, c["pbr"], rtol=1e-2, atol=1e-14)
