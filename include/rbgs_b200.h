@@ -88,6 +88,14 @@ int rb_sketch_gaussian(int x_dtype, int64_t n, int ncols, const void* X, int64_t
                        const uint8_t* theta, int64_t ldt, int k, double scale,
                        double* out, int64_t ldo, int accumulate, int mode,
                        void* ws, size_t ws_bytes, void* stream);
+/* Two-input form: [out1 | out2] = scale * (q @ [X1 | X2]) in ONE pass over
+ * the table (the sweep sketches [Q'_i | W_(i+1)] together, halving the q
+ * traffic).  c1, c2 <= 64; c2 may be 0.                                   */
+int rb_sketch_gaussian2(int x1_dtype, const void* X1, int64_t ldx1, int c1,
+                        int x2_dtype, const void* X2, int64_t ldx2, int c2, int64_t n,
+                        const uint8_t* theta, int64_t ldt, int k, double scale,
+                        double* out1, int64_t ldo1, double* out2, int64_t ldo2,
+                        int accumulate, int mode, void* ws, size_t ws_bytes, void* stream);
 /* srht kind (sketching.py:129-137): signs as a bitmask over the GLOBAL
  * padded index space (bit i set <=> sign_diagonal[i] = -1), sample = the
  * k global sample indices, scale = 1/sqrt(k).  Rows >= n_valid (global)

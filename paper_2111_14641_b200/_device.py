@@ -149,6 +149,18 @@ def sketch_gaussian(X, theta, ldt, k, scale, out, accumulate=False, mode="auto")
     _t1(e0, "sketch_gaussian", n * (cols * X.element_size() + 2 * k), 2.0 * k * n * cols)
 
 
+def sketch_gaussian2(X1, X2, theta, ldt, k, scale, out1, out2, accumulate=False, mode="auto"):
+    """[out1 | out2] = Theta [X1 | X2] in one pass over the gaussian table."""
+    n, c1 = X1.shape
+    c2 = X2.shape[1]
+    ws, wsb = _ws(n, c1 + c2, k, X1.device)
+    e0 = _t0()
+    call("rb_sketch_gaussian2", dtype_code(X1), ptr(X1), ld(X1), c1, dtype_code(X2), ptr(X2), ld(X2), c2, n,
+         ptr(theta), ldt, k, scale, ptr(out1), ld(out1), ptr(out2), ld(out2), int(accumulate), GAUSS_MODE[mode],
+         ws, wsb, st(X1.device))
+    _t1(e0, "sketch_gaussian", n * ((c1 + c2) * X1.element_size() + 2 * k), 2.0 * k * n * (c1 + c2))
+
+
 def gaussian_fill(seed, k, row0, nrows, theta, ldt):
     call("rb_gaussian_fill", ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), k, row0, nrows, ptr(theta), ldt,
          st(theta.device))

@@ -56,7 +56,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         raise RuntimeError(f"nvcc failed:\n{msg}")
     tmp = LIB + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
-           "-lcudart"]
+           "-lcudart", "-lcublas"]
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
     return LIB

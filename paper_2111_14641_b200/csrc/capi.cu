@@ -45,6 +45,8 @@ int gaussian_fill(uint64_t, int, int64_t, int64_t, uint8_t*, int64_t, cudaStream
 int sketch_gaussian(int, int64_t, int, const void*, int64_t, const uint8_t*, int64_t, int, double, double*, int64_t,
                     int, int, void*, size_t, cudaStream_t);
 size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k);
+int sketch_gaussian2(int, const void*, int64_t, int, int, const void*, int64_t, int, int64_t, const uint8_t*, int64_t,
+                     int, double, double*, int64_t, double*, int64_t, int, int, void*, size_t, cudaStream_t);
 int sketch_signs(int, int64_t, int, const void*, int64_t, const uint32_t*, int64_t, int, double, double*, int64_t, int,
                  void*, size_t, cudaStream_t);
 int sketch_srht(int, int64_t, int, const void*, int64_t, int64_t, int64_t, const uint32_t*, const int64_t*, int,
@@ -107,6 +109,13 @@ int rb_sketch_gaussian(int xd, int64_t n, int ncols, const void* X, int64_t ldx,
                        int k, double scale, double* out, int64_t ldo, int acc, int mode, void* ws, size_t wsb,
                        void* s) {
   return rb::sketch_gaussian(xd, n, ncols, X, ldx, theta, ldt, k, scale, out, ldo, acc, mode, ws, wsb, as_stream(s));
+}
+
+int rb_sketch_gaussian2(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2, int c2,
+                        int64_t n, const uint8_t* theta, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
+                        double* out2, int64_t ldo2, int acc, int mode, void* ws, size_t wsb, void* s) {
+  return rb::sketch_gaussian2(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, theta, ldt, k, scale, out1, ldo1, out2, ldo2, acc,
+                              mode, ws, wsb, as_stream(s));
 }
 
 int rb_sketch_srht(int xd, int64_t n, int ncols, const void* X, int64_t ldx, int64_t row0, int64_t n_pad,

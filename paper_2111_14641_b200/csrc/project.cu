@@ -16,6 +16,8 @@
 // Q is streamed once (column-major, each column contiguous): per l a warp
 // reads 256 contiguous bytes.  X (fp64 on entry) is rounded to the compute
 // format and staged, negated, in shared memory in chunks of kLC rows.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace rb {
@@ -30,75 +32,108 @@ __device__ __forceinline__ float to_f32(T v) {  // binary64 -> binary32 rounds t
 }
 
 // ---- coarse ---------------------------------------------------------------
-// RPT consecutive rows per thread, PB (multiple of 4) column accumulators per
-// row.  FAST = 0: reference order, acc = fl32(acc + fl32(q * (-x))) with
-// __fmul_rn / __fadd_rn (FMUL + FADD, never contracted: bit-identical to
-// kernels.gemm coarse).  FAST = 1: one packed FFMA2 per two columns,
-// acc = fl32(acc - q x) rounded once (the survey's "FMA" variant,
-// SURVEY.md section 0 finding 5; not bit-identical).
+// One row per thread, PB (multiple of 4) column accumulators.  FAST = 0:
+// reference order, acc = fl32(acc + fl32(q * (-x))) with __fmul_rn /
+// __fadd_rn (FMUL + FADD, never contracted: bit-identical to kernels.gemm
+// coarse).  FAST = 1: one packed FFMA2 per two columns, acc = fl32(acc - q x)
+// rounded once (the survey's "FMA" variant, SURVEY.md section 0 finding 5;
+// not bit-identical).  Q is streamed with a kPD-deep register prefetch ring
+// that runs across the X-chunk boundaries; X chunks are double-buffered.
+constexpr int kXC = 64;  // X rows per staged chunk
+constexpr int kPD = 8;   // Q prefetch depth (loads in flight per thread)
+
 template <typename TQ, typename TW, int PB, int RPT, bool FAST>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 2)
 project_coarse(int64_t n, int c, int p, const TQ* __restrict__ Q, int64_t ldq,
                const double* __restrict__ X, int64_t ldx, const TW* __restrict__ W, int64_t ldw,
                TQ* __restrict__ Qp, int64_t ldqp, double* __restrict__ partial) {
   static_assert(PB % 4 == 0, "PB multiple of 4");
-  __shared__ __align__(16) float sx[kLC][PB];  // -fl32(X[l0 + l, j])
+  __shared__ __align__(16) float sx[2][kXC][PB];  // -fl32(X[l, j]), double-buffered
   __shared__ double red[kThreads / 32];
 
+  // RPT consecutive rows per thread (each x broadcast from shared memory
+  // feeds RPT rows); rows beyond n compute on row 0 and are not stored
   const int64_t r0 = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * RPT;
   bool v[RPT];
+  const TQ* qrow[RPT];
 #pragma unroll
-  for (int r = 0; r < RPT; ++r) v[r] = r0 + r < n;
+  for (int t = 0; t < RPT; ++t) {
+    v[t] = r0 + t < n;
+    qrow[t] = Q + (v[t] ? r0 + t : 0);
+  }
 
   float acc[RPT][PB];
   double w2 = 0.0;
 #pragma unroll
-  for (int r = 0; r < RPT; ++r)
+  for (int t = 0; t < RPT; ++t)
 #pragma unroll
     for (int j = 0; j < PB; ++j) {
-      acc[r][j] = 0.f;
-      if (j < p && v[r]) {
-        const TW wv = W[r0 + r + (int64_t)j * ldw];
+      acc[t][j] = 0.f;
+      if (j < p && v[t]) {
+        const TW wv = W[r0 + t + (int64_t)j * ldw];
         w2 += (double)wv * (double)wv;
-        acc[r][j] = to_f32(wv);
+        acc[t][j] = to_f32(wv);
       }
     }
 
-  for (int l0 = 0; l0 < c; l0 += kLC) {
-    const int lc = min(kLC, c - l0);
-    __syncthreads();
-    for (int e = threadIdx.x; e < kLC * PB; e += kThreads) {
+  const int nch = (c + kXC - 1) / kXC;
+  auto stage = [&](int ch) {
+    const int l0 = ch * kXC, lc = min(kXC, c - l0);
+    float(*dst)[PB] = sx[ch & 1];
+    for (int e = threadIdx.x; e < kXC * PB; e += kThreads) {
       const int l = e / PB, j = e % PB;
-      sx[l][j] = (l < lc && j < p) ? -__double2float_rn(X[(l0 + l) + (int64_t)j * ldx]) : 0.f;
+      dst[l][j] = (l < lc && j < p) ? -__double2float_rn(X[(l0 + l) + (int64_t)j * ldx]) : 0.f;
     }
-    __syncthreads();
-    const TQ* qcol = Q + (int64_t)l0 * ldq + r0;
-#pragma unroll 2
-    for (int l = 0; l < lc; ++l) {
-      float q[RPT];
+  };
+  float qbuf[kPD][RPT];
 #pragma unroll
-      for (int r = 0; r < RPT; ++r) q[r] = v[r] ? to_f32(qcol[(int64_t)l * ldq + r]) : 0.f;
-      const float4* xr = reinterpret_cast<const float4*>(sx[l]);
+  for (int u = 0; u < kPD; ++u)
 #pragma unroll
-      for (int h = 0; h < PB / 4; ++h) {
-        const float4 xx = xr[h];
+    for (int t = 0; t < RPT; ++t) qbuf[u][t] = u < c ? to_f32(qrow[t][(int64_t)u * ldq]) : 0.f;
+  if (nch > 0) stage(0);
+  for (int ch = 0; ch < nch; ++ch) {
+    __syncthreads();  // chunk ch staged; buffer (ch + 1) & 1 no longer read
+    if (ch + 1 < nch) stage(ch + 1);
+    const int l0 = ch * kXC, lc = min(kXC, c - l0);
+    const float(*xs)[PB] = sx[ch & 1];
+    for (int lb = 0; lb < lc; lb += kPD) {
+      float qc[kPD][RPT];
 #pragma unroll
-        for (int r = 0; r < RPT; ++r) {
-          if (FAST) {
-            const float2 qq = make_float2(q[r], q[r]);
-            float2 a = make_float2(acc[r][4 * h], acc[r][4 * h + 1]);
-            float2 b = make_float2(acc[r][4 * h + 2], acc[r][4 * h + 3]);
-            a = __ffma2_rn(qq, make_float2(xx.x, xx.y), a);
-            b = __ffma2_rn(qq, make_float2(xx.z, xx.w), b);
-            acc[r][4 * h] = a.x;
-            acc[r][4 * h + 1] = a.y;
-            acc[r][4 * h + 2] = b.x;
-            acc[r][4 * h + 3] = b.y;
-          } else {
-            acc[r][4 * h] = __fadd_rn(acc[r][4 * h], __fmul_rn(q[r], xx.x));
-            acc[r][4 * h + 1] = __fadd_rn(acc[r][4 * h + 1], __fmul_rn(q[r], xx.y));
-            acc[r][4 * h + 2] = __fadd_rn(acc[r][4 * h + 2], __fmul_rn(q[r], xx.z));
-            acc[r][4 * h + 3] = __fadd_rn(acc[r][4 * h + 3], __fmul_rn(q[r], xx.w));
+      for (int u = 0; u < kPD; ++u)
+#pragma unroll
+        for (int t = 0; t < RPT; ++t) qc[u][t] = qbuf[u][t];
+#pragma unroll
+      for (int u = 0; u < kPD; ++u) {
+        const int ln = l0 + lb + kPD + u;
+#pragma unroll
+        for (int t = 0; t < RPT; ++t) qbuf[u][t] = ln < c ? to_f32(qrow[t][(int64_t)ln * ldq]) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < kPD; ++u) {
+        if (lb + u < lc) {
+          const float4* xr = reinterpret_cast<const float4*>(xs[lb + u]);
+#pragma unroll
+          for (int h = 0; h < PB / 4; ++h) {
+            const float4 xx = xr[h];
+#pragma unroll
+            for (int t = 0; t < RPT; ++t) {
+              const float q = qc[u][t];
+              float* a = &acc[t][4 * h];
+              if (FAST) {
+                const float2 qq = make_float2(q, q);
+                float2 lo = __ffma2_rn(qq, make_float2(xx.x, xx.y), make_float2(a[0], a[1]));
+                float2 hi = __ffma2_rn(qq, make_float2(xx.z, xx.w), make_float2(a[2], a[3]));
+                a[0] = lo.x;
+                a[1] = lo.y;
+                a[2] = hi.x;
+                a[3] = hi.y;
+              } else {
+                a[0] = __fadd_rn(a[0], __fmul_rn(q, xx.x));
+                a[1] = __fadd_rn(a[1], __fmul_rn(q, xx.y));
+                a[2] = __fadd_rn(a[2], __fmul_rn(q, xx.z));
+                a[3] = __fadd_rn(a[3], __fmul_rn(q, xx.w));
+              }
+            }
           }
         }
       }
@@ -107,12 +142,12 @@ project_coarse(int64_t n, int c, int p, const TQ* __restrict__ Q, int64_t ldq,
 
   double q2 = 0.0;
 #pragma unroll
-  for (int r = 0; r < RPT; ++r)
+  for (int t = 0; t < RPT; ++t)
 #pragma unroll
     for (int j = 0; j < PB; ++j)
-      if (j < p && v[r]) {
-        Qp[r0 + r + (int64_t)j * ldqp] = (TQ)acc[r][j];
-        q2 += (double)acc[r][j] * (double)acc[r][j];
+      if (j < p && v[t]) {
+        Qp[r0 + t + (int64_t)j * ldqp] = (TQ)acc[t][j];
+        q2 += (double)acc[t][j] * (double)acc[t][j];
       }
   if (partial) {
     const double sw = block_sum(w2, red);
@@ -193,26 +228,42 @@ __global__ void sum_pairs(const double* __restrict__ partial, int count, double*
   }
 }
 
+// rows per thread for the coarse kernel: two for narrow blocks (halves the
+// shared-memory broadcasts per FP instruction), one when the accumulators
+// would not fit two CTAs per SM.  Selectable at runtime via RB_PROJECT_RPT
+// for measurement.
 template <int PB>
-constexpr int rows_per_thread() { return PB <= 40 ? 2 : 1; }
+constexpr int default_rpt() { return PB <= 40 ? 2 : 1; }
+
+int rpt_override() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("RB_PROJECT_RPT");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
 
 template <typename TQ, typename TW, int PB>
 void launch_pb(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, const double* X, int64_t ldx,
                const void* W, int64_t ldw, void* Qp, int64_t ldqp, double* partial, cudaStream_t st) {
   if (mode == 2) {
     const int grid = ceil_div(n, kThreads);
-    RB_KLAUNCH project_fine<TQ, TW, PB><<<grid, kThreads, 0, st>>>(n, c, p, (const TQ*)Q, ldq, X, ldx, (const TW*)W, ldw,
-                                                       (TQ*)Qp, ldqp, partial);
+    RB_KLAUNCH project_fine<TQ, TW, PB><<<grid, kThreads, 0, st>>>(n, c, p, (const TQ*)Q, ldq, X, ldx, (const TW*)W,
+                                                                  ldw, (TQ*)Qp, ldqp, partial);
     return;
   }
-  constexpr int RPT = rows_per_thread<PB>();
-  const int grid = ceil_div(n, (int64_t)RPT * kThreads);
-  if (mode == 1)
-    RB_KLAUNCH project_coarse<TQ, TW, PB, RPT, true><<<grid, kThreads, 0, st>>>(n, c, p, (const TQ*)Q, ldq, X, ldx,
-                                                                    (const TW*)W, ldw, (TQ*)Qp, ldqp, partial);
-  else
-    RB_KLAUNCH project_coarse<TQ, TW, PB, RPT, false><<<grid, kThreads, 0, st>>>(n, c, p, (const TQ*)Q, ldq, X, ldx,
-                                                                     (const TW*)W, ldw, (TQ*)Qp, ldqp, partial);
+  const int rpt = rpt_override() > 0 ? rpt_override() : default_rpt<PB>();
+  const int grid = ceil_div(n, (int64_t)rpt * kThreads);
+#define RB_CO(R, F)                                                                                    \
+  RB_KLAUNCH project_coarse<TQ, TW, PB, R, F><<<grid, kThreads, 0, st>>>(n, c, p, (const TQ*)Q, ldq, X, ldx, \
+                                                                         (const TW*)W, ldw, (TQ*)Qp, ldqp, partial)
+  if (rpt == 2) {
+    if (mode == 1) RB_CO(2, true); else RB_CO(2, false);
+  } else {
+    if (mode == 1) RB_CO(1, true); else RB_CO(1, false);
+  }
+#undef RB_CO
 }
 
 template <typename TQ, typename TW>
@@ -228,9 +279,21 @@ int launch_tw(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, con
   return 0;
 }
 
+template <int PB>
+int rows_for() { return (rpt_override() > 0 ? rpt_override() : default_rpt<PB>()) * kThreads; }
+
 int grid_rows(int mode, int p) {
   if (mode == 2) return kThreads;
-  return (p <= 40 ? 2 : 1) * kThreads;
+  if (p <= 4) return rows_for<4>();
+  if (p <= 8) return rows_for<8>();
+  if (p <= 12) return rows_for<12>();
+  if (p <= 16) return rows_for<16>();
+  if (p <= 20) return rows_for<20>();
+  if (p <= 24) return rows_for<24>();
+  if (p <= 32) return rows_for<32>();
+  if (p <= 40) return rows_for<40>();
+  if (p <= 48) return rows_for<48>();
+  return rows_for<64>();
 }
 
 }  // namespace

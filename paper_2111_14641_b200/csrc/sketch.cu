@@ -387,20 +387,49 @@ int gaussian_fill(uint64_t seed, int k, int64_t row0, int64_t nrows, uint8_t* th
 }
 
 size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k);
-int sketch_gaussian_tc(int xd, int64_t n, int ncols, const void* X, int64_t ldx, const uint8_t* theta, int64_t ldt,
-                       int k, double scale, double* out, int64_t ldo, int acc, void* ws, size_t wsb, cudaStream_t st);
+int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2, int c2,
+                       int64_t n, const uint8_t* qt, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
+                       double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st);
+
+// [out1 | out2] = scale * (q @ [X1 | X2]).  mode 0 = auto (tensor pipe when
+// every input is binary32), 1 = fp64 CUDA cores, 2 = tensor pipe.
+int sketch_gaussian2(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2, int c2,
+                     int64_t n, const uint8_t* theta, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
+                     double* out2, int64_t ldo2, int acc, int mode, void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(c1 >= 1 && c2 >= 0 && c1 <= 64 && c2 <= 64 && k >= 1 && ldo1 >= k && out1 &&
+                 (c2 == 0 || (out2 && ldo2 >= k)),
+             "rb_sketch_gaussian: bad args");
+  RB_REQUIRE(n == 0 || (X1 && ld1 >= n && (c2 == 0 || (X2 && ld2 >= n)) && theta && ldt >= n),
+             "rb_sketch_gaussian: bad X/theta");
+  RB_REQUIRE(mode >= 0 && mode <= 2, "rb_sketch_gaussian: bad mode %d", mode);
+  const bool tc = mode == 2 || (mode == 0 && xd1 == RB_F32 && (c2 == 0 || xd2 == RB_F32));
+  if (tc && c1 + c2 <= 96)
+    return sketch_gaussian_tc(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, theta, ldt, k, scale, out1, ldo1, out2, ldo2,
+                              acc, ws, wsb, st);
+  if (tc) {
+    int rc = sketch_gaussian_tc(xd1, X1, ld1, c1, RB_F32, nullptr, 0, 0, n, theta, ldt, k, scale, out1, ldo1,
+                                nullptr, 0, acc, ws, wsb, st);
+    if (rc == RB_OK)
+      rc = sketch_gaussian_tc(xd2, X2, ld2, c2, RB_F32, nullptr, 0, 0, n, theta, ldt, k, scale, out2, ldo2, nullptr,
+                              0, acc, ws, wsb, st);
+    return rc;
+  }
+  PlaneSrc src{theta, ldt, k};
+  int rc = xd1 == RB_F32
+               ? dense_sketch<float>(n, c1, (const float*)X1, ld1, src, k, scale, out1, ldo1, acc, ws, wsb, st)
+               : dense_sketch<double>(n, c1, (const double*)X1, ld1, src, k, scale, out1, ldo1, acc, ws, wsb, st);
+  if (rc == RB_OK && c2 > 0)
+    rc = xd2 == RB_F32
+             ? dense_sketch<float>(n, c2, (const float*)X2, ld2, src, k, scale, out2, ldo2, acc, ws, wsb, st)
+             : dense_sketch<double>(n, c2, (const double*)X2, ld2, src, k, scale, out2, ldo2, acc, ws, wsb, st);
+  return rc;
+}
 
 int sketch_gaussian(int xd, int64_t n, int ncols, const void* X, int64_t ldx, const uint8_t* theta, int64_t ldt,
                     int k, double scale, double* out, int64_t ldo, int acc, int mode, void* ws, size_t wsb,
                     cudaStream_t st) {
-  RB_REQUIRE(ncols >= 1 && ncols <= 64 && k >= 1 && ldo >= k && out, "rb_sketch_gaussian: bad args");
-  RB_REQUIRE(n == 0 || (X && ldx >= n && theta && ldt >= n), "rb_sketch_gaussian: bad X/theta");
-  RB_REQUIRE(mode >= 0 && mode <= 2, "rb_sketch_gaussian: bad mode %d", mode);
-  const bool tc = mode == 2 || (mode == 0 && xd == RB_F32);
-  if (tc) return sketch_gaussian_tc(xd, n, ncols, X, ldx, theta, ldt, k, scale, out, ldo, acc, ws, wsb, st);
-  PlaneSrc src{theta, ldt, k};
-  if (xd == RB_F32) return dense_sketch<float>(n, ncols, (const float*)X, ldx, src, k, scale, out, ldo, acc, ws, wsb, st);
-  return dense_sketch<double>(n, ncols, (const double*)X, ldx, src, k, scale, out, ldo, acc, ws, wsb, st);
+  return sketch_gaussian2(xd, X, ldx, ncols, RB_F32, nullptr, 0, 0, n, theta, ldt, k, scale, out, ldo, nullptr, 0,
+                          acc, mode, ws, wsb, st);
 }
 
 int sketch_signs(int xd, int64_t n, int ncols, const void* X, int64_t ldx, const uint32_t* bits, int64_t ldb,

@@ -3,6 +3,10 @@
 // certification (rbgs.py:428-443), the tall triangular scaling of Steps 4-5
 // (rbgs.py:284, kernels.py:250-270) and the Householder QR used by the
 // direct LS solver and the GMRES least-squares problem (kernels.py:216-231).
+#include <cublas_v2.h>
+
+#include <mutex>
+
 #include "common.cuh"
 
 namespace rb {
@@ -350,11 +354,39 @@ void trsm_right_launch(int64_t n, int p, const void* B, int64_t ldb, const doubl
 
 }  // namespace
 
+// Plain fp64 GEMMs (Richardson sweeps, Gram matrices, certification) go to
+// cuBLAS DGEMM: they are library GEMMs in the sense of the build rules, and
+// cuBLAS' DMMA kernels beat a hand-rolled split-K fp64 kernel at these
+// small, latency-bound shapes.  One handle per device, stream set per call.
+static cublasHandle_t cublas_handle() {
+  static cublasHandle_t h[64] = {nullptr};
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  if (!h[dev]) cublasCreate(&h[dev]);
+  return h[dev];
+}
+
+int dgemm(int tA, int tB, int m, int n, int k, double alpha, const double* A, int64_t lda, const double* B,
+          int64_t ldb, double beta, double* C, int64_t ldc, cudaStream_t st) {
+  if (m == 0 || n == 0) return RB_OK;
+  cublasHandle_t h = cublas_handle();
+  RB_REQUIRE(h, "cuBLAS handle creation failed");
+  cublasSetStream(h, st);
+  const cublasStatus_t s = cublasDgemm(h, tA ? CUBLAS_OP_T : CUBLAS_OP_N, tB ? CUBLAS_OP_T : CUBLAS_OP_N, m, n, k,
+                                       &alpha, A, (int)std::max<int64_t>(lda, 1), B, (int)std::max<int64_t>(ldb, 1),
+                                       &beta, C, (int)ldc);
+  ++g_launches;
+  RB_REQUIRE(s == CUBLAS_STATUS_SUCCESS, "cublasDgemm failed (%d)", (int)s);
+  return check_launch("dgemm");
+}
+
 // ============================== entry points ================================
 int gemm_f64(int tA, int tB, int m, int n, int k, double alpha, const double* A, int64_t lda, const double* B,
              int64_t ldb, double beta, double* C, int64_t ldc, void* ws, size_t wsb, cudaStream_t st) {
   RB_REQUIRE(m >= 0 && n >= 0 && k >= 0 && C && ldc >= std::max(m, 1), "rb_gemm_f64: bad args");
-  return gemm_t<double, double>(tA, tB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, ws, wsb, st);
+  return dgemm(tA, tB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, st);
 }
 
 int cross(int ad, int bd, int64_t n, int p, int q, const void* A, int64_t lda, const void* B, int64_t ldb,
@@ -434,11 +466,11 @@ int ls_richardson(int k, int c, int p, const double* S, int64_t lds, const doubl
                   int64_t ldx, double* T, int64_t ldt, void* ws, size_t wsb, cudaStream_t st) {
   RB_REQUIRE(k >= 1 && c >= 1 && p >= 1 && l >= 1 && S && P && X && T, "rb_ls_richardson: bad args");
   // sweep 1 from X = 0 is exactly S^T P (rbgs.py:153-155)
-  int rc = gemm_t<double, double>(1, 0, c, p, k, 1.0, S, lds, P, ldp, 0.0, X, ldx, ws, wsb, st);
+  int rc = dgemm(1, 0, c, p, k, 1.0, S, lds, P, ldp, 0.0, X, ldx, st);
   for (int it = 1; it < l && rc == RB_OK; ++it) {
     RB_KLAUNCH copy_f64<<<ceil_div((int64_t)k * p, 256), 256, 0, st>>>(k, p, P, ldp, T, ldt);
-    rc = gemm_t<double, double>(0, 0, k, p, c, -1.0, S, lds, X, ldx, 1.0, T, ldt, ws, wsb, st);  // T = P - S X
-    if (rc == RB_OK) rc = gemm_t<double, double>(1, 0, c, p, k, 1.0, S, lds, T, ldt, 1.0, X, ldx, ws, wsb, st);
+    rc = dgemm(0, 0, k, p, c, -1.0, S, lds, X, ldx, 1.0, T, ldt, st);  // T = P - S X
+    if (rc == RB_OK) rc = dgemm(1, 0, c, p, k, 1.0, S, lds, T, ldt, 1.0, X, ldx, st);
   }
   return rc;
 }
@@ -446,7 +478,7 @@ int ls_richardson(int k, int c, int p, const double* S, int64_t lds, const doubl
 int sketched_cholqr_small(int k, int p, const double* Sp, int64_t lds, double* R, int64_t ldr, double* Sout,
                           int64_t ldso, int* info, void* ws, size_t wsb, cudaStream_t st) {
   RB_REQUIRE(k >= 1 && p >= 1 && p <= 64 && Sp && R && Sout && info, "rb_sketched_cholqr_small: bad args");
-  int rc = gemm_t<double, double>(1, 0, p, p, k, 1.0, Sp, lds, Sp, lds, 0.0, R, ldr, ws, wsb, st);  // G in R
+  int rc = dgemm(1, 0, p, p, k, 1.0, Sp, lds, Sp, lds, 0.0, R, ldr, st);  // G in R
   if (rc == RB_OK) rc = potrf_upper(p, R, ldr, R, ldr, info, st);
   if (rc == RB_OK) rc = trsm_right(RB_F64, RB_F64, k, p, Sp, lds, R, ldr, Sout, ldso, st);
   return rc;

@@ -163,6 +163,8 @@ class _Scratch:
     def __init__(self, k, m, w, device):
         f64 = torch.float64
         self.Pi = D.empty_cm(k, w, f64, device)
+        self.Pn = [D.empty_cm(k, w, f64, device), D.empty_cm(k, w, f64, device)]  # fused next-block sketches
+        self.pn_flip = 0
         self.Sp = D.empty_cm(k, w, f64, device)
         self.Ss = D.empty_cm(k, w, f64, device)
         self.Si = D.empty_cm(k, w, f64, device)
@@ -296,6 +298,7 @@ class RbgsSweep:
         self.per_block_ortho = []
         self.per_block_resid = []
         self.pending_P = None
+        self._next_P = None  # (key of the next block, its sketch) from a fused pass
 
     # -- small utilities ---------------------------------------------------
     def _sketch(self, X, out):
@@ -346,8 +349,10 @@ class RbgsSweep:
             _householder_direct_dev(S, Pi, X, scr)
 
     # -- Steps 4-5 -----------------------------------------------------------
-    def _interblock(self, Qp, Pi, slot, block1):
-        """Writes Q_i into `slot`; returns (R_ii, S_i, Sp_of_Qp or None)."""
+    def _interblock(self, Qp, Pi, slot, block1, sp_given=None):
+        """Writes Q_i into `slot`; returns (R_ii, S_i, Sp_of_Qp or None).
+        `sp_given`: Theta Q' already computed (fused pass) -- used for the
+        first sketch instead of recomputing it."""
         name, param = self.inter
         scr = self._scr
         w = Qp.shape[1]
@@ -359,13 +364,13 @@ class RbgsSweep:
         if name == "sketched_cholqr":
             l = param or 1
             Rt = scr.Rt[:w, :w]
-            Rt.zero_()
-            Rt.diagonal().fill_(1.0)
             Qcur = Qp
             RS = scr.R1[:w, :w]
             for it in range(l):
                 if it == 0 and reuse:
                     Sp.copy_(Pi)
+                elif it == 0 and sp_given is not None:
+                    Sp = sp_given
                 else:
                     self._sketch_reduce(Qcur, Sp)
                 if it == 0:
@@ -380,9 +385,12 @@ class RbgsSweep:
                 if not last and Qcur.data_ptr() == out.data_ptr():
                     out = D.empty_cm(self.n_local, w, torch.float64, self.device)
                 D.trsm_right(Qcur, RS, out)
-                Rn = scr.R2[:w, :w]
-                D.gemm(0, 0, 1.0, RS, Rt, 0.0, Rn)
-                Rt.copy_(Rn)
+                if it == 0:  # R_total = R_S I
+                    Rt.copy_(RS)
+                else:
+                    Rn = scr.R2[:w, :w]
+                    D.gemm(0, 0, 1.0, RS, Rt, 0.0, Rn)
+                    Rt.copy_(Rn)
                 Qcur = out
             Si = scr.Si[:, :w]
             if self.cfg.resketch:
@@ -397,8 +405,8 @@ class RbgsSweep:
         # Q_i = Q' R_ii^{-1}, S_i = S* R''^{-1}.
         G = scr.G[:w, :w]
         D.cross(Qp, Qp, G)
-        if reuse:
-            Sp.copy_(Pi)
+        if reuse or sp_given is not None:
+            Sp.copy_(Pi if reuse else sp_given)
             self.comm.allreduce_(G)
         else:
             self._sketch(Qp, Sp)
@@ -495,8 +503,15 @@ class RbgsSweep:
         return Rb, Sb, sp_qp
 
     # -- one block -------------------------------------------------------------
-    def push_block(self, W_i) -> tuple:
-        """One RBGS iteration on block W_i (rbgs.py:352-399); returns (j0, j1)."""
+    def push_block(self, W_i, lookahead=None) -> tuple:
+        """One RBGS iteration on block W_i (rbgs.py:352-399); returns (j0, j1).
+
+        `lookahead` (optional, device-path extension): the NEXT block, when
+        the caller already has it (one-shot `rbgs`).  Its Step-1 sketch is
+        then computed in the same pass over the gaussian table as this
+        block's Step-4 sketch of Q' (one table read and, when sharded, one
+        allreduce per block instead of two); the next push_block of that
+        same tensor reuses it."""
         self.pending_P = None
         i = self.blocks_done + 1
         if self.blocks_done >= len(self.offsets) - 1:
@@ -504,25 +519,65 @@ class RbgsSweep:
         j0, j1 = self.offsets[self.blocks_done], self.offsets[self.blocks_done + 1]
         w = j1 - j0
         with torch.cuda.device(self.device):
-            return self._push(i, j0, j1, w, self._as_block(W_i, w))
+            Wn = None
+            if lookahead is not None and self.blocks_done + 2 < len(self.offsets):
+                wn = self.offsets[self.blocks_done + 2] - j1
+                Wn = self._as_block(lookahead, wn)
+            return self._push(i, j0, j1, w, self._as_block(W_i, w), Wn)
 
-    def _push(self, i, j0, j1, w, W):
+    @staticmethod
+    def _key(t):
+        return (t.data_ptr(), tuple(t.shape), t.stride(), t.dtype)
+
+    def _fusable(self, A, B):
+        """Two sketches can share one table pass (gaussian kind, tensor pipe)."""
+        return (self.theta.kind == "gaussian" and self.inter[0] in ("sketched_cholqr", "l2_plus_cholqr")
+                and not self.cfg.certify_blocks and A.dtype == torch.float32 and B.dtype == torch.float32
+                and A.shape[1] + B.shape[1] <= 96 and sketching.GAUSS_MODE != "fp64")
+
+    def _sketch_pair(self, A, B, outA, outB):
+        tab = self.theta.device_tables(A.device, self.row0, A.shape[0])
+        D.sketch_gaussian2(A, B, tab["theta"], tab["ldt"], self.theta.k,
+                           1.0 / (sketching.GAUSS_GRID * math.sqrt(self.theta.k)), outA, outB,
+                           False, sketching.GAUSS_MODE)
+        self.comm.allreduce_(outA, outB)
+
+    def _push(self, i, j0, j1, w, W, Wn=None):
         scr = self._scr
         cfg = self.cfg
         c = self.cols_done
-        Pi = scr.Pi[:, :w]
-        # Step 1
-        self._sketch_reduce(W, Pi)
+        # Step 1 (possibly already done by the previous block's fused pass)
+        nxt = self._next_P
+        self._next_P = None
+        if nxt is not None and nxt[0] == self._key(W):
+            Pi = nxt[1]
+        else:
+            Pi = scr.Pi[:, :w]
+            if Wn is not None and c == 0 and self._fusable(W, Wn):
+                Pn = scr.Pn[scr.pn_flip][:, :Wn.shape[1]]
+                scr.pn_flip ^= 1
+                self._sketch_pair(W, Wn, Pi, Pn)
+                self._next_P = (self._key(Wn), Pn)
+                Wn = None
+            else:
+                self._sketch_reduce(W, Pi)
         slot = self.Q[:, j0:j1]
         norms = scr.norms
         norms.zero_()
         scr.info.zero_()
+        sp_given = None
         if c:
             X = scr.X[:c, :w]
             self._solve_ls(self.S[:, :c], Pi, X)
             self.R[:c, j0:j1].copy_(X)
             D.project(self.Q[:, :c], X, W, slot, self.compute, self.order, norms[0:2])
             Qp = slot
+            if Wn is not None and self._next_P is None and self._fusable(slot, Wn):
+                sp_given = scr.Sp[:, :w]
+                Pn = scr.Pn[scr.pn_flip][:, :Wn.shape[1]]
+                scr.pn_flip ^= 1
+                self._sketch_pair(slot, Wn, sp_given, Pn)
+                self._next_P = (self._key(Wn), Pn)
         else:
             # Q' = W_1 itself (rbgs.py:371-372): read it in its own format
             D.sumsq(W, norms[0:1])
@@ -530,7 +585,7 @@ class RbgsSweep:
         self.comm.allreduce_(norms[0:2])
         if not c:
             norms[1:2].copy_(norms[0:1])
-        Rii, Si, sp_qp = self._interblock(Qp, Pi, slot, block1=(c == 0))
+        Rii, Si, sp_qp = self._interblock(Qp, Pi, slot, block1=(c == 0), sp_given=sp_given)
         # finiteness of everything the block produced (Matrix() checks)
         D.sumsq(Pi, norms[2:3])
         D.sumsq(Si, norms[3:4])
@@ -631,7 +686,8 @@ def rbgs(W, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None) -> BlockQR:
     sweep = RbgsSweep(n, theta, cfg, dc)
     off = cfg.partition.offsets()
     for b in range(cfg.partition.num_blocks):
-        sweep.push_block(Wd[:, off[b]:off[b + 1]])
+        nxt = Wd[:, off[b + 1]:off[b + 2]] if b + 2 < len(off) else None
+        sweep.push_block(Wd[:, off[b]:off[b + 1]], lookahead=nxt)
     return sweep.finish()
 
 

@@ -302,3 +302,25 @@ def test_sweep_state_semantics(pkg):
     assert sw.blocks_done == 2 and sw.cols_done == 10
     assert sw.pending_P is not None and sw.pending_P.shape == (60, 5)
     assert np.allclose(sw.pending_P.data, 0.0)
+
+
+def test_fused_lookahead_sketch_is_bitwise_neutral(pkg):
+    """rbgs() fuses the next block's Step-1 sketch into this block's Step-4
+    pass; pushing blocks one by one (no lookahead) must give the same bits."""
+    rbgs, sketching, D = pkg
+    from paper_2111_14641_b200.kernels import BlockPartition
+    import goldens as G
+
+    n, m, p, k = 20_000, 60, 12, 200
+    W = G.trig_family(n, m, 5).astype(np.float32)
+    th = sketching.gaussian_operator(k, n, 3)
+    cfg = rbgs.RbgsConfig(partition=BlockPartition.uniform(m, p), interblock="sketched_cholqr(1)")
+    f = rbgs.rbgs(W, th, cfg)
+    sw = rbgs.RbgsSweep(n, th, cfg)
+    Wd = _dev(W.astype(np.float64), torch.float32)
+    for b in range(m // p):
+        sw.push_block(Wd[:, b * p:(b + 1) * p])
+    g = sw.finish()
+    assert np.array_equal(f.R.data, g.R.data)
+    assert np.array_equal(f.Q.data, g.Q.data)
+    assert np.array_equal(f.S.data, g.S.data)
