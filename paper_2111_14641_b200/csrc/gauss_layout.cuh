@@ -28,11 +28,19 @@ __host__ __device__ __forceinline__ int64_t q_bytes(int k, int64_t ldt) {
   return (int64_t)((k + kTM - 1) / kTM) * kTM * ldt * 2;
 }
 
-// X planes (b0..b3) for NP padded columns: tile kt is 4 x kBK x NP bytes.
+// X byte planes for NP padded columns, as ONE UMMA B operand per column
+// group: the NP columns are cut into groups of NG = np_group(NP) (so that
+// 4 NG <= 256, the largest MMA N), and within a K chunk the B rows are
+// ordered [group][plane][column], plane 0 = b3 (weight 2^24) .. plane 3 = b0.
+// A tile kt is 4 x kBK x NP bytes, [kc][group][plane][col][16 bytes].
+__host__ __device__ __forceinline__ int np_group(int NP) { return NP <= 64 ? NP : NP / 2; }
+
 __host__ __device__ __forceinline__ int64_t x_offset(int plane, int j, int64_t i, int NP) {
   const int64_t kt = i / kBK;
   const int kc = (int)((i % kBK) >> 4), b = (int)(i & 15);
-  return (kt * 4 + plane) * ((int64_t)kBK * NP) + (int64_t)kc * (NP * 16) + j * 16 + b;
+  const int NG = np_group(NP);
+  const int g = j / NG, jj = j % NG;
+  return kt * (4 * (int64_t)kBK * NP) + (int64_t)kc * (4 * NP * 16) + (int64_t)((g * 4 + plane) * NG + jj) * 16 + b;
 }
 
 }  // namespace gl

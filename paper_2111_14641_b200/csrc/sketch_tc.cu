@@ -3,15 +3,19 @@
 //
 // Exact integer split (Ozaki-style):
 //   q  = 256 qh + ql,            qh = q >> 8 (s8), ql = q & 255 (u8)
-//   x ~= xi 2^(E - 30)           per (column, 8192-row chunk); E: every |x| of
-//                                the chunk is < 2^E; xi a signed 31-bit integer
-//   xi = b3 2^24 + b2 2^16 + b1 2^8 + b0,   b3 s8, b2 b1 b0 u8
-// so q xi is a sum of 8 byte products grouped by weight 2^(8g), g = 0..4.
-// Each group accumulates exactly in an int32 TMEM accumulator over one chunk
-// (< 2^17 per row, < 2^30 per chunk), is drained to fp64 and scaled by
-// 2^(E - 30).  Relative to the fp64 reference Theta @ X the only errors are
-// fp64 accumulation and the fixed-point rounding of entries far below their
-// chunk's max (absolute 2^(E - 31)).
+//   x ~= xi 2^(E - 30)           per (column, 16384-row chunk); E: every |x|
+//                                of the chunk is < 2^E; xi a signed integer,
+//                                |xi| <= 2^30
+//   xi = b3 2^24 + b2 2^16 + b1 2^8 + b0,   balanced signed digits (all s8)
+// so q xi is a sum of 8 byte products grouped by weight 2^(8w), w = 0..4.
+// One MMA multiplies qh by the four digit planes side by side (N = 4 NG),
+// a second multiplies ql by the same operand into TMEM shifted by one block,
+// so each TMEM block accumulates one weight exactly in int32 over one chunk
+// (< 2^16 per row, < 2^30 per chunk).  Blocks are drained to fp64 (exact
+// int64 recombination) and scaled by 2^(E - 30).  Relative to the fp64
+// reference Theta @ X the only errors are fp64 accumulation and the
+// fixed-point rounding of entries far below their chunk's max (absolute
+// 2^(E - 31)).
 //
 // Two inputs: the sweep sketches [Q'_i | W_(i+1)] in ONE pass so the q stream
 // (2 bytes per entry, the dominant HBM traffic) is read once per block.
@@ -28,6 +32,10 @@
 //   warps 4..7     epilogue: tcgen05.ld of the 5 int32 groups of their 32
 //                  lanes, exact recombination, fp64 scale-and-add into the
 //                  CTA's own slice of the split-K partial buffer (L2-resident).
+#include <stdlib.h>
+
+#include <type_traits>
+
 #include "common.cuh"
 #include "gauss_layout.cuh"
 #include "tc.cuh"
@@ -40,45 +48,133 @@ namespace {
 
 using gl::kBK;
 using gl::kTM;
-constexpr int kChunk = 8192;  // rows per exact int32 accumulation
+constexpr int kChunk = 16384;  // rows per exact int32 accumulation (< 2^16 per row, balanced digits)
 constexpr int kTPC = kChunk / kBK;
 constexpr int kThreads = 256;
+constexpr int kSplitThreads = kChunk / 32;  // split pre-pass: 32 rows per thread, one chunk per CTA
 
+// pipeline depth: as many 128-row stages as fit next to each other in
+// shared memory (overridable with RB_TC_STAGES for measurement)
 template <int NP>
-constexpr int stages_for() { return NP <= 64 ? 3 : 2; }
+constexpr int max_stages() { return (227 * 1024 - 2048) / (2 * kTM * kBK + 4 * kBK * NP); }
 
 // ---- pre-pass: [X1 | X2] -> tiled byte planes + exponents --------------------------
 // grid (nchunks, NP / 2): one CTA per chunk x column pair; thread t owns 32
-// consecutive rows of both columns, so every plane store is a full 32-byte
-// sector (the two columns' 16-byte segments are adjacent in the layout).
-// Columns >= ncols are written as zeros (the UMMA N padding).
+// consecutive rows of both columns (vector loads when aligned), so every
+// plane store is a full 32-byte sector (the two columns' 16-byte segments
+// are adjacent in the layout).  Columns >= ncols are written as zeros (the
+// UMMA N padding).  binary32 inputs are converted in binary32: x 2^(30-E) is
+// an exact power-of-two scaling and |xi| <= 2^30 < 2^31, so the integer is
+// exact; binary64 inputs round once to nearest.
+template <typename T, typename TV>
+__device__ __forceinline__ void load32(const T* __restrict__ x, int64_t base, int64_t n, bool vec, TV (&v)[32]) {
+  if (vec && base + 32 <= n) {
+    if constexpr (sizeof(T) == 4) {
+      const float4* p4 = reinterpret_cast<const float4*>(x + base);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 f = __ldcs(p4 + q);
+        v[4 * q] = f.x;
+        v[4 * q + 1] = f.y;
+        v[4 * q + 2] = f.z;
+        v[4 * q + 3] = f.w;
+      }
+    } else {
+      const double2* p2 = reinterpret_cast<const double2*>(x + base);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const double2 f = __ldcs(p2 + q);
+        v[2 * q] = (TV)f.x;
+        v[2 * q + 1] = (TV)f.y;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 32; ++e) v[e] = base + e < n ? (TV)x[base + e] : TV(0);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t fixed_of(T v, T s) {
+  if constexpr (sizeof(T) == 4) return (uint32_t)__float2int_rn(v * s);
+  else return (uint32_t)__double2int_rn(v * s);
+}
+
+// Balanced signed byte digits: xi = b3 2^24 + b2 2^16 + b1 2^8 + b0 with
+// b0, b1, b2 in [-128, 127] and |b3| <= 65 (|xi| <= 2^30), so every plane is
+// s8 and ONE MMA can take all four planes as its B operand.  Plane order in
+// the layout: 0 = b3, 1 = b2, 2 = b1, 3 = b0 (descending weight).
+__device__ __forceinline__ void digits(int xi, uint32_t& d3, uint32_t& d2, uint32_t& d1, uint32_t& d0) {
+  const int b0 = (int)(int8_t)(xi & 255);
+  xi = (xi - b0) >> 8;
+  const int b1 = (int)(int8_t)(xi & 255);
+  xi = (xi - b1) >> 8;
+  const int b2 = (int)(int8_t)(xi & 255);
+  const int b3 = (xi - b2) >> 8;
+  d0 = (uint32_t)b0 & 255u;
+  d1 = (uint32_t)b1 & 255u;
+  d2 = (uint32_t)b2 & 255u;
+  d3 = (uint32_t)b3 & 255u;
+}
+
+template <typename T>
+__device__ __forceinline__ void split_column(const T (&v)[32], T s, uint32_t (&w)[2][4][4]) {
+  // w[seg][plane][word]
+#pragma unroll
+  for (int seg = 0; seg < 2; ++seg)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t p0 = 0, p1 = 0, p2 = 0, p3 = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        uint32_t d3, d2, d1, d0;
+        digits((int)fixed_of(v[16 * seg + 4 * q + e], s), d3, d2, d1, d0);
+        p0 |= d3 << (8 * e);
+        p1 |= d2 << (8 * e);
+        p2 |= d1 << (8 * e);
+        p3 |= d0 << (8 * e);
+      }
+      w[seg][0][q] = p0;
+      w[seg][1][q] = p1;
+      w[seg][2][q] = p2;
+      w[seg][3][q] = p3;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ float column_max(const T (&v)[32]) {
+  float m = 0.f;
+#pragma unroll
+  for (int e = 0; e < 32; ++e) m = fmaxf(m, (float)fabs((double)v[e]));
+  return m;
+}
+
 template <typename T1, typename T2>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kSplitThreads)
 split_planes(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, const T2* __restrict__ X2,
-             int64_t ld2, int NP, uint8_t* __restrict__ planes, int* __restrict__ exps) {
-  __shared__ float red[2][8];
+             int64_t ld2, int NP, bool vec1, bool vec2, uint8_t* __restrict__ planes, int* __restrict__ exps) {
+  __shared__ float red[2][kSplitThreads / 32];
   const int c = blockIdx.x;
   const int j0 = 2 * blockIdx.y;
   const int64_t base = (int64_t)c * kChunk + 32 * threadIdx.x;
-  double v[2][32];
-  float mx[2] = {0.f, 0.f};
+  // column h of the pair comes from X1, X2 or is padding (kind 0 / 1 / 2);
+  // values are held as binary32 when both inputs are binary32 (exact), else
+  // as binary64 (binary32 embeds exactly)
+  using TV = typename std::conditional<sizeof(T1) == 4 && sizeof(T2) == 4, float, double>::type;
+  int kind[2];
+  TV v[2][32];
+  float mx[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int j = j0 + h;
-    if (j < c1) {
-      const T1* x = X1 + (int64_t)j * ld1;
+    kind[h] = j < c1 ? 0 : (j < c1 + c2 ? 1 : 2);
+    if (kind[h] == 0) load32(X1 + (int64_t)j * ld1, base, n, vec1, v[h]);
+    else if (kind[h] == 1) load32(X2 + (int64_t)(j - c1) * ld2, base, n, vec2, v[h]);
+    else {
 #pragma unroll
-      for (int e = 0; e < 32; ++e) v[h][e] = base + e < n ? (double)x[base + e] : 0.0;
-    } else if (j < c1 + c2) {
-      const T2* x = X2 + (int64_t)(j - c1) * ld2;
-#pragma unroll
-      for (int e = 0; e < 32; ++e) v[h][e] = base + e < n ? (double)x[base + e] : 0.0;
-    } else {
-#pragma unroll
-      for (int e = 0; e < 32; ++e) v[h][e] = 0.0;
+      for (int e = 0; e < 32; ++e) v[h][e] = TV(0);
     }
-#pragma unroll
-    for (int e = 0; e < 32; ++e) mx[h] = fmaxf(mx[h], (float)fabs(v[h][e]));
+    mx[h] = column_max(v[h]);
     for (int o = 16; o; o >>= 1) mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], o));
   }
   if ((threadIdx.x & 31) == 0) {
@@ -86,66 +182,47 @@ split_planes(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, 
     red[1][threadIdx.x >> 5] = mx[1];
   }
   __syncthreads();
-  double s[2];
+  uint32_t w[2][2][4][4];  // [column][seg][plane][word]
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     float m = 0.f;
 #pragma unroll
-    for (int w = 0; w < 8; ++w) m = fmaxf(m, red[h][w]);
+    for (int q = 0; q < kSplitThreads / 32; ++q) m = fmaxf(m, red[h][q]);
     int E = 0;
     if (m > 0.f) frexpf(m, &E);  // m < 2^E; float rounding is monotone, so every |x| < 2^E
     if (threadIdx.x == 0) exps[(int64_t)c * NP + j0 + h] = E;
-    s[h] = ldexp(1.0, 30 - E);
+    split_column(v[h], (TV)ldexp(1.0, 30 - E), w[h]);  // padding columns are zeros
   }
 #pragma unroll
   for (int seg = 0; seg < 2; ++seg) {
-    uint32_t w[4][2][4];  // [plane][column][word]
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t b0 = 0, b1 = 0, b2 = 0, b3 = 0;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t xi = (uint32_t)(int)rint(v[h][16 * seg + 4 * q + e] * s[h]);
-          b0 |= (xi & 255u) << (8 * e);
-          b1 |= ((xi >> 8) & 255u) << (8 * e);
-          b2 |= ((xi >> 16) & 255u) << (8 * e);
-          b3 |= ((xi >> 24) & 255u) << (8 * e);
-        }
-        w[0][h][q] = b0;
-        w[1][h][q] = b1;
-        w[2][h][q] = b2;
-        w[3][h][q] = b3;
-      }
     const int64_t i0 = base + 16 * seg;
 #pragma unroll
     for (int pl = 0; pl < 4; ++pl) {
       uint4* dst = reinterpret_cast<uint4*>(planes + gl::x_offset(pl, j0, i0, NP));
-      dst[0] = make_uint4(w[pl][0][0], w[pl][0][1], w[pl][0][2], w[pl][0][3]);
-      dst[1] = make_uint4(w[pl][1][0], w[pl][1][1], w[pl][1][2], w[pl][1][3]);
+      dst[0] = make_uint4(w[0][seg][pl][0], w[0][seg][pl][1], w[0][seg][pl][2], w[0][seg][pl][3]);
+      dst[1] = make_uint4(w[1][seg][pl][0], w[1][seg][pl][1], w[1][seg][pl][2], w[1][seg][pl][3]);
     }
   }
 }
 
-template <int NP>
+template <int NP, int ST>
 struct Smem {
-  static constexpr int S = stages_for<NP>();
+  static constexpr int S = ST;
   uint8_t a[S][2][kBK / 16][kTM][16];  // one q tile
-  uint8_t b[S][4][kBK / 16][NP][16];   // one X-plane tile
+  uint8_t b[S][kBK / 16][4 * NP][16];  // one X-plane tile: [kc][group, plane, col][16]
   uint64_t full[S], empty[S];
   uint64_t tfull[2], tempty[2];
   uint32_t tbase;
 };
 
-template <int NP>
+template <int NP, int ST>
 __global__ void __launch_bounds__(kThreads, 1)
 gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt, int k,
                  const uint8_t* __restrict__ planes, const int* __restrict__ exps, int tiles_per_cta,
-                 double* __restrict__ ws) {
+                 double* __restrict__ ws, int dbg) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  Smem<NP>& S = *reinterpret_cast<Smem<NP>*>(smem_raw);
-  constexpr int kStages = Smem<NP>::S;
+  Smem<NP, ST>& S = *reinterpret_cast<Smem<NP, ST>*>(smem_raw);
+  constexpr int kStages = ST;
   constexpr int kGroupCols = 5 * NP;
   constexpr int kBufs = (2 * kGroupCols <= 512) ? 2 : 1;
   constexpr uint32_t kAlloc = kBufs * kGroupCols <= 64 ? 64 : kBufs * kGroupCols <= 128 ? 128
@@ -188,16 +265,21 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
         const int64_t kt = kt_beg + t;
         tc::mbar_arrive_expect_tx(&S.full[s], kABytes + kBBytes);
         tc::bulk_g2s(&S.a[s][0][0][0][0], qtile + kt * 2 * gl::kTileBytes, kABytes, &S.full[s]);
-        tc::bulk_g2s(&S.b[s][0][0][0][0], planes + kt * (int64_t)kBBytes, kBBytes, &S.full[s]);
+        tc::bulk_g2s(&S.b[s][0][0][0], planes + kt * (int64_t)kBBytes, kBBytes, &S.full[s]);
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
-      constexpr uint32_t ID_SS = tc::idesc_i8(kTM, NP, true, true);
-      constexpr uint32_t ID_SU = tc::idesc_i8(kTM, NP, true, false);
-      constexpr uint32_t ID_US = tc::idesc_i8(kTM, NP, false, true);
-      constexpr uint32_t ID_UU = tc::idesc_i8(kTM, NP, false, false);
+      // Per K step and column group g: two MMAs share the B operand
+      // [b3 | b2 | b1 | b0] (N = 4 NG, all s8).  qh x B lands on TMEM blocks
+      // 0..3 of the group, ql x B on blocks 1..4 (D shifted by NG columns), so
+      // block w accumulates exactly the products of weight 2^(32 - 8w).  The
+      // accumulators are zeroed by the epilogue, every MMA accumulates.
+      constexpr int NG = (NP <= 64) ? NP : NP / 2;
+      constexpr int NGRP = NP / NG;
+      constexpr uint32_t ID_HI = tc::idesc_i8(kTM, 4 * NG, true, true);
+      constexpr uint32_t ID_LO = tc::idesc_i8(kTM, 4 * NG, false, true);
       int seg_i = 0;
       for (int t = 0; t < T; ++t) {
         const int s = t % kStages;
@@ -205,27 +287,23 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
         const bool seg_first = (t == 0) || (kt % kTPC == 0);
         const bool seg_last = (t == T - 1) || ((kt + 1) % kTPC == 0);
         const int buf = seg_i % kBufs;
-        if (seg_first && seg_i >= kBufs) tc::mbar_wait(&S.tempty[buf], ((seg_i / kBufs) - 1) & 1);
+        if (seg_first) tc::mbar_wait(&S.tempty[buf], (seg_i / kBufs) & 1);
         tc::mbar_wait(&S.full[s], (t / kStages) & 1);
         tc::tc_fence_after();
         const uint32_t d = tbase + buf * kGroupCols;
+        if (!(dbg & 1)) {
 #pragma unroll
-        for (int ks = 0; ks < kBK / 32; ++ks) {
-          const uint32_t acc = (seg_first && ks == 0) ? 0u : 1u;
-          const uint64_t ah = tc::sdesc_kmajor(tc::smem_u32(&S.a[s][0][2 * ks][0][0]), kTM * 16, 128);
-          const uint64_t al = tc::sdesc_kmajor(tc::smem_u32(&S.a[s][1][2 * ks][0][0]), kTM * 16, 128);
-          uint64_t b[4];
+          for (int ks = 0; ks < kBK / 32; ++ks) {
+            const uint64_t ah = tc::sdesc_kmajor(tc::smem_u32(&S.a[s][0][2 * ks][0][0]), kTM * 16, 128);
+            const uint64_t al = tc::sdesc_kmajor(tc::smem_u32(&S.a[s][1][2 * ks][0][0]), kTM * 16, 128);
 #pragma unroll
-          for (int pl = 0; pl < 4; ++pl)
-            b[pl] = tc::sdesc_kmajor(tc::smem_u32(&S.b[s][pl][2 * ks][0][0]), NP * 16, 128);
-          tc::mma_i8(d + 4 * NP, ah, b[3], ID_SS, acc);  // 2^32
-          tc::mma_i8(d + 3 * NP, ah, b[2], ID_SU, acc);  // 2^24
-          tc::mma_i8(d + 3 * NP, al, b[3], ID_US, 1u);
-          tc::mma_i8(d + 2 * NP, ah, b[1], ID_SU, acc);  // 2^16
-          tc::mma_i8(d + 2 * NP, al, b[2], ID_UU, 1u);
-          tc::mma_i8(d + 1 * NP, ah, b[0], ID_SU, acc);  // 2^8
-          tc::mma_i8(d + 1 * NP, al, b[1], ID_UU, 1u);
-          tc::mma_i8(d + 0 * NP, al, b[0], ID_UU, acc);  // 2^0
+            for (int g = 0; g < NGRP; ++g) {
+              const uint64_t b = tc::sdesc_kmajor(tc::smem_u32(&S.b[s][2 * ks][0][0]) + g * (4 * NG * 16),
+                                                  4 * NP * 16, 128);
+              tc::mma_i8(d + g * 5 * NG, ah, b, ID_HI, 1u);
+              tc::mma_i8(d + g * 5 * NG + NG, al, b, ID_LO, 1u);
+            }
+          }
         }
         tc::mma_commit(&S.empty[s]);
         if (seg_last) {
@@ -236,9 +314,20 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
     }
   } else if (warp >= 4) {
     // ---------------- epilogue ----------------
+    constexpr int NG = (NP <= 64) ? NP : NP / 2;
     const int q = warp - 4;  // TMEM lane quadrant
     const int r = mt * kTM + q * 32 + lane;
-    double* dst = ws + (int64_t)blockIdx.y * k * ncols + r;
+    const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
+    double acc[NP];  // this row's fp64 partial sketch, all columns
+#pragma unroll
+    for (int j = 0; j < NP; ++j) acc[j] = 0.0;
+    // zero both accumulator buffers, then hand them to the MMA issuer
+    for (int b = 0; b < kBufs; ++b) {
+      for (int c0 = 0; c0 < kGroupCols; c0 += 8) tc::tmem_st8_zero(lane_base + b * kGroupCols + c0);
+      tc::tmem_st_wait();
+      tc::tc_fence_before();
+      tc::mbar_arrive(&S.tempty[b]);
+    }
     int ci = 0;
     for (int64_t ks = kt_beg; ks < kt_end; ++ci) {
       const int64_t chunk = ks / kTPC;
@@ -246,31 +335,35 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
       const int buf = ci % kBufs;
       tc::mbar_wait(&S.tfull[buf], (ci / kBufs) & 1);
       tc::tc_fence_after();
-      const uint32_t la = tbase + ((uint32_t)(q * 32) << 16) + buf * kGroupCols;
+      const uint32_t la = lane_base + buf * kGroupCols;
       const int* ex = exps + chunk * NP;
 #pragma unroll
-      for (int c0 = 0; c0 < NP; c0 += 16) {
-        uint32_t g[5][16];
+      for (int c0 = 0; c0 < NP; c0 += 8) {
+        const uint32_t gbase = la + (c0 / NG) * 5 * NG + (c0 % NG);
+        uint32_t g[5][8];
 #pragma unroll
-        for (int gi = 0; gi < 5; ++gi) tc::tmem_ld16(la + gi * NP + c0, g[gi]);
+        for (int w = 0; w < 5; ++w) tc::tmem_ld8(gbase + w * NG, g[w]);
         tc::tmem_ld_wait();
 #pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const int j = c0 + jj;
-          if (j < ncols && r < k) {
-            double v = (double)(int)g[4][jj];
-            v = v * 256.0 + (double)(int)g[3][jj];
-            v = v * 256.0 + (double)(int)g[2][jj];
-            v = v * 256.0 + (double)(int)g[1][jj];
-            v = v * 256.0 + (double)(int)g[0][jj];
-            v = ldexp(v, ex[j] - 30);
-            double* o = dst + (int64_t)j * k;
-            *o = ci ? *o + v : v;
-          }
+        for (int w = 0; w < 5; ++w) tc::tmem_st8_zero(gbase + w * NG);
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          // exact integer recombination of the weights 2^32, 2^24, .., 2^0
+          const long long v = ((long long)(int)g[0][jj] << 32) + ((long long)(int)g[1][jj] << 24) +
+                              ((long long)(int)g[2][jj] << 16) + ((long long)(int)g[3][jj] << 8) +
+                              (long long)(int)g[4][jj];
+          acc[c0 + jj] += ldexp((double)v, ex[c0 + jj] - 30);
         }
       }
+      tc::tmem_st_wait();
       tc::tc_fence_before();
       tc::mbar_arrive(&S.tempty[buf]);
+    }
+    if (r < k) {
+      double* dst = ws + (int64_t)blockIdx.y * k * ncols + r;
+#pragma unroll
+      for (int j = 0; j < NP; ++j)
+        if (j < ncols) dst[(int64_t)j * k] = acc[j];
     }
   }
   tc::tc_fence_before();
@@ -293,6 +386,15 @@ __global__ void reduce_splits_tc(const double* __restrict__ ws, int splits, int 
 
 int np_for(int ncols) { return ncols <= 16 ? 16 : ncols <= 32 ? 32 : ncols <= 48 ? 48 : ncols <= 64 ? 64 : ncols <= 80 ? 80 : 96; }
 
+int dbg_flag() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RB_TC_DEBUG");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 template <int NP>
 int launch_np(int64_t n, int ncols, const uint8_t* qt, int64_t ldt, int k, const uint8_t* planes, const int* exps,
               double* part, size_t part_bytes, int* splits_out, cudaStream_t st) {
@@ -305,23 +407,42 @@ int launch_np(int64_t n, int ncols, const uint8_t* qt, int64_t ldt, int k, const
   RB_REQUIRE((size_t)splits * per <= part_bytes, "gaussian tc: workspace too small");
   const int tpc = (int)((ktn + splits - 1) / splits);
   splits = (int)((ktn + tpc - 1) / tpc);
-  const size_t smem = sizeof(Smem<NP>) + 1024;
-  cudaFuncSetAttribute(gauss_tc_partial<NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  RB_KLAUNCH gauss_tc_partial<NP><<<dim3(mt, splits), kThreads, smem, st>>>(n, ncols, qt, ldt, k, planes, exps, tpc,
-                                                                           part);
+  static int env_st = -1;
+  if (env_st < 0) {
+    const char* e = getenv("RB_TC_STAGES");
+    env_st = e ? atoi(e) : 0;
+  }
+  constexpr int kMax = max_stages<NP>();
+  const int st_req = env_st > 0 ? std::min(env_st, kMax) : (NP <= 64 ? 3 : 2);
+#define RB_GL(STG)                                                                                               \
+  {                                                                                                              \
+    const size_t smem = sizeof(Smem<NP, STG>) + 1024;                                                            \
+    cudaFuncSetAttribute(gauss_tc_partial<NP, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+    RB_KLAUNCH gauss_tc_partial<NP, STG><<<dim3(mt, splits), kThreads, smem, st>>>(n, ncols, qt, ldt, k, planes, \
+                                                                                  exps, tpc, part, dbg_flag());   \
+  }
+  if (st_req >= 4 && kMax >= 4) RB_GL((kMax >= 4 ? 4 : 1))
+  else if (st_req >= 3 && kMax >= 3) RB_GL((kMax >= 3 ? 3 : 1))
+  else RB_GL(2)
+#undef RB_GL
   *splits_out = splits;
   return check_launch("gauss_tc_partial");
+}
+
+bool aligned16(const void* p, int64_t ld, int esz) {
+  return p && ((uintptr_t)p % 16 == 0) && ((ld * esz) % 16 == 0);
 }
 
 template <typename T1>
 void launch_split(int xd2, dim3 g, int64_t n, int c1, const void* X1, int64_t ld1, int c2, const void* X2, int64_t ld2,
                   int NP, uint8_t* planes, int* exps, cudaStream_t st) {
+  const bool v1 = aligned16(X1, ld1, sizeof(T1));
   if (xd2 == RB_F32)
-    RB_KLAUNCH split_planes<T1, float><<<g, 256, 0, st>>>(n, c1, (const T1*)X1, ld1, c2, (const float*)X2, ld2, NP,
-                                                         planes, exps);
+    RB_KLAUNCH split_planes<T1, float><<<g, kSplitThreads, 0, st>>>(n, c1, (const T1*)X1, ld1, c2, (const float*)X2, ld2, NP, v1,
+                                                         aligned16(X2, ld2, 4), planes, exps);
   else
-    RB_KLAUNCH split_planes<T1, double><<<g, 256, 0, st>>>(n, c1, (const T1*)X1, ld1, c2, (const double*)X2, ld2, NP,
-                                                          planes, exps);
+    RB_KLAUNCH split_planes<T1, double><<<g, kSplitThreads, 0, st>>>(n, c1, (const T1*)X1, ld1, c2, (const double*)X2, ld2, NP,
+                                                          v1, aligned16(X2, ld2, 8), planes, exps);
 }
 
 }  // namespace
