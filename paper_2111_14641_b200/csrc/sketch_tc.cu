@@ -413,7 +413,7 @@ int launch_np(int64_t n, int ncols, const uint8_t* qt, int64_t ldt, int k, const
     env_st = e ? atoi(e) : 0;
   }
   constexpr int kMax = max_stages<NP>();
-  const int st_req = env_st > 0 ? std::min(env_st, kMax) : (NP <= 64 ? 3 : 2);
+  const int st_req = env_st > 0 ? std::min(env_st, kMax) : (NP <= 80 ? 3 : 2);
 #define RB_GL(STG)                                                                                               \
   {                                                                                                              \
     const size_t smem = sizeof(Smem<NP, STG>) + 1024;                                                            \
