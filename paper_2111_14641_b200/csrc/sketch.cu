@@ -6,15 +6,18 @@
 //    per-split partials are reduced in a fixed order (deterministic).
 //  * srht: pruned subsampled Walsh-Hadamard.  Rows are cut in tiles of
 //    T = 2048; with global row i = (g, l), H[s, i] = (-1)^popc(g_s & g) *
-//    (-1)^popc(l_s & l), so each tile needs its own 2048-point FWHT (three
-//    register stages, five warp-shuffle stages, three stages after one
-//    shared-memory transpose) and then only a signed gather at the k sampled
-//    local indices.  This is the Kronecker split H_n = H_G (x) H_T of
-//    SURVEY.md 8(e), with CTAs playing the role of shards.
+//    (-1)^popc(l_s & l), so each tile needs its own 2048-point FWHT and then
+//    only a signed gather at the k sampled local indices.  This is the
+//    Kronecker split H_n = H_G (x) H_T of SURVEY.md 8(e), with CTAs playing
+//    the role of shards.  k <= 1024: one warp per (column, tile), six
+//    register stages + one padded smem transpose + five register stages,
+//    tiles streamed by per-warp bulk copies (srht_warp); larger k: one CTA
+//    per tile, shuffle stages (srht_partial).
 //  * sparse_sign: each row i scatters s signed copies of X[i, :] into a
 //    shared-memory k x CG accumulator.
 #include "common.cuh"
 #include "gauss_layout.cuh"
+#include "tc.cuh"
 
 namespace rb {
 
@@ -22,6 +25,7 @@ int sm_count();
 
 namespace {
 
+using namespace tc;
 constexpr int kThreads = 256;
 
 // ======================= dense (split-K fp64 GEMM) ==========================
@@ -288,18 +292,218 @@ srht_partial(int64_t n, int ncols, const TX* __restrict__ X, int64_t ldx, int64_
   }
 }
 
+// Warp-per-column SRHT (k <= 1024): warp w of the CTA owns column c0 + w for
+// every tile of the CTA's range.  Phase A: lane L holds rows e = L + 32 i
+// (i < 64, coalesced 128-byte loads) and runs the six stages on bits 5..10
+// in registers; a padded per-warp smem transpose (row stride 33, conflict
+// free both ways) hands lane L the rows (L + 32 h) * 32 + b (h < 2, b < 32)
+// for the five stages on bits 0..4.  The transformed tile goes back to smem
+// and each lane gathers its samples s = L + 32 m (accumulators in
+// registers).  11 * 2048 / 32 = 704 DADD per lane per tile column: the
+// kernel sits at the fp64 add rate ~ the HBM rate of the tile stream.
+constexpr int kSW = 8;                 // warps (columns) per CTA
+
+// lane L holds row L of a 32 x 32 bit matrix; returns column L (bit i = row
+// i's bit L).  Recursive block swap, one shuffle per level.
+__device__ __forceinline__ uint32_t warp_bit_transpose(uint32_t w, int lane) {
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int q = 0; q < 5; ++q) {
+    const int j = 16 >> q;
+    const uint32_t m = masks[q];
+    const uint32_t p = __shfl_xor_sync(0xffffffffu, w, j);
+    w = (lane & j) ? ((w & ~m) | ((p & ~m) >> j)) : ((w & m) | ((p & m) << j));
+  }
+  return w;
+}
+constexpr int kZS = kT / 32 * 33;      // padded per-warp tile (2112 doubles)
+
+// ST: interior tiles arrive by one bulk copy per (warp, tile) into a per-warp
+// staging buffer, issued a tile ahead, so the next tile streams in while the
+// current one is transformed (needs 16-B aligned tile starts).
+template <int MS, typename TX, bool ST>
+__global__ void __launch_bounds__(kSW * 32, 1)
+srht_warp(int64_t n, int ncols, const TX* __restrict__ X, int64_t ldx, int64_t row0,
+          const uint32_t* __restrict__ sign_bits, const int64_t* __restrict__ sample, int k,
+          int tiles_per_cta, int ntiles, double* __restrict__ ws) {
+  extern __shared__ __align__(128) double zsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.y * kSW + warp;
+  double* zs = zsm + warp * kZS;
+  TX* stage = reinterpret_cast<TX*>(zsm + kSW * kZS) + warp * kT;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(reinterpret_cast<TX*>(zsm + kSW * kZS) + (ST ? kSW * kT : 0)) + warp;
+  // sample s: padded smem slot (12 bits) | global tile index << 12, shared by
+  // the CTA's warps (kept out of registers)
+  uint32_t* stab = reinterpret_cast<uint32_t*>(bar - warp + kSW);
+  for (int s = threadIdx.x; s < 32 * MS; s += blockDim.x) {
+    const int64_t idx = s < k ? sample[s] : 0;
+    const int l = (int)(idx & (kT - 1));
+    stab[s] = (uint32_t)((l >> 5) * 33 + (l & 31)) | ((uint32_t)(idx >> 11) << 12);
+  }
+  __syncthreads();
+  if (c >= ncols) return;  // no CTA-wide barriers below
+  const TX* xc = X + (int64_t)c * ldx;
+  double acc[MS];
+#pragma unroll
+  for (int m = 0; m < MS; ++m) acc[m] = 0.0;
+  const int tbeg = blockIdx.x * tiles_per_cta;
+  const int tend = min(ntiles, tbeg + tiles_per_cta);
+  const int64_t gtile0 = row0 >> 11;
+  const int64_t off = row0 & (kT - 1);
+  const int64_t galign = row0 & ~(int64_t)(kT - 1);
+  auto interior = [&](int t) {
+    const int64_t lb = (int64_t)t * kT - off;
+    return lb >= 0 && lb + kT <= n;
+  };
+  auto prefetch = [&](int t) {  // lane 0 only
+    mbar_arrive_expect_tx(bar, kT * sizeof(TX));
+    bulk_g2s(stage, xc + ((int64_t)t * kT - off), kT * sizeof(TX), bar);
+  };
+  uint32_t phase = 0;
+  if (ST) {
+    if (lane == 0) {
+      mbar_init(bar, 1);
+      mbar_fence_init();
+      if (tbeg < tend && interior(tbeg)) prefetch(tbeg);
+    }
+    __syncwarp();
+  }
+  for (int t = tbeg; t < tend; ++t) {
+    const int64_t lbase = (int64_t)t * kT - off;  // local row of tile element 0
+    const int g = (int)(gtile0 + t);
+    const uint32_t* sb = sign_bits + ((galign + (int64_t)t * kT) >> 5);
+    double v[64];
+    if (ST && interior(t)) {
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = (double)stage[lane + 32 * i];
+      __syncwarp();
+      if (lane == 0 && t + 1 < tend && interior(t + 1)) {
+        fence_proxy_async_smem();
+        prefetch(t + 1);
+      }
+    } else if (lbase >= 0 && lbase + kT <= n) {
+      // interior tile: 64 unpredicated loads in flight before the first use
+      const TX* xt = xc + lbase + lane;
+      TX raw[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) raw[i] = __ldg(xt + 32 * i);
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = (double)raw[i];
+    } else {
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        const int64_t lr = lbase + lane + 32 * i;
+        v[i] = (lr >= 0 && lr < n) ? (double)xc[lr] : 0.0;
+      }
+      if (ST) {
+        __syncwarp();
+        if (lane == 0 && t + 1 < tend && interior(t + 1)) prefetch(t + 1);
+      }
+    }
+    // D: lane L needs bit L of sign words i = 0..63 -> transpose the two
+    // 32 x 32 bit blocks across the warp (5 shuffle rounds each)
+    const uint32_t t0 = warp_bit_transpose(__ldg(sb + lane), lane);
+    const uint32_t t1 = warp_bit_transpose(__ldg(sb + 32 + lane), lane);
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+      const uint32_t t = i < 32 ? t0 : t1;
+      const uint32_t flip = (t << (31 - (i & 31))) & 0x80000000u;
+      v[i] = __hiloint2double(__double2hiint(v[i]) ^ (int)flip, __double2loint(v[i]));
+    }
+#pragma unroll
+    for (int h = 1; h < 64; h <<= 1)
+#pragma unroll
+      for (int i = 0; i < 64; ++i)
+        if (!(i & h)) {
+          const double a = v[i], b = v[i + h];
+          v[i] = a + b;
+          v[i + h] = a - b;
+        }
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 64; ++i) zs[i * 33 + lane] = v[i];
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int b = 0; b < 32; ++b) v[h * 32 + b] = zs[(lane + 32 * h) * 33 + b];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+      for (int i = 0; i < 64; ++i)
+        if (!(i & o)) {
+          const double a = v[i], b = v[i + o];
+          v[i] = a + b;
+          v[i + o] = a - b;
+        }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int b = 0; b < 32; ++b) zs[(lane + 32 * h) * 33 + b] = v[h * 32 + b];
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < MS; ++m) {
+      const uint32_t e = stab[lane + 32 * m];
+      const double z = zs[e & 4095u];
+      acc[m] += (__popc((e >> 12) & (uint32_t)g) & 1) ? -z : z;
+    }
+  }
+  double* dst = ws + (int64_t)blockIdx.x * k * ncols + (int64_t)c * k;
+#pragma unroll
+  for (int m = 0; m < MS; ++m)
+    if (lane + 32 * m < k) dst[lane + 32 * m] = acc[m];
+}
+
 template <typename TX>
 int srht_sketch(int64_t n, int ncols, const TX* X, int64_t ldx, int64_t row0, int64_t n_pad,
                 const uint32_t* bits, const int64_t* sample, int k, double scale, double* out,
                 int64_t ldo, int accumulate, void* ws, size_t ws_bytes, cudaStream_t st) {
   RB_REQUIRE(k <= 8 * kThreads, "srht: k=%d > 2048 unsupported", k);
+  RB_REQUIRE(n_pad <= ((int64_t)1 << 31), "srht: n_pad > 2^31 unsupported");
   RB_REQUIRE(n_pad <= kT || (row0 % kT) == 0, "srht: row0 must be a multiple of 2048");
   const int64_t span = (row0 % kT) + n;  // rows covered from the first tile start
   const int ntiles = ceil_div(span, kT);
+  const size_t per = (size_t)k * ncols * sizeof(double);
+  if (k <= 1024 && !getenv("RB_SRHT_V1")) {
+    const int cgroups = ceil_div(ncols, kSW);
+    int ctas = std::max(1, std::min(ntiles, sm_count() / cgroups));
+    if ((size_t)ctas * per > ws_bytes) ctas = (int)std::max<size_t>(1, ws_bytes / per);
+    RB_REQUIRE(ws && (size_t)ctas * per <= ws_bytes, "srht: workspace too small");
+    const int tpc = ceil_div(ntiles, ctas);
+    ctas = ceil_div(ntiles, tpc);
+    const dim3 grid(ctas, cgroups);
+    const bool stage = sizeof(TX) == 4 && ((uintptr_t)X % 16) == 0 && ldx % 4 == 0 &&
+                       (row0 % kT) % 4 == 0 && !getenv("RB_SRHT_NOSTAGE");
+    const size_t smem = (size_t)kSW * kZS * sizeof(double) + (stage ? kSW * kT * sizeof(TX) : 0) + kSW * 8 +
+                        (size_t)32 * 32 * sizeof(uint32_t);
+    double* w = (double*)ws;
+#define RB_SRHTW(M)                                                                                    \
+  do {                                                                                                 \
+    if (stage) {                                                                                       \
+      cudaFuncSetAttribute(srht_warp<M, TX, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      RB_KLAUNCH srht_warp<M, TX, true><<<grid, kSW * 32, smem, st>>>(n, ncols, X, ldx, row0, bits, sample, k, \
+                                                                      tpc, ntiles, w);                 \
+    } else {                                                                                           \
+      cudaFuncSetAttribute(srht_warp<M, TX, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+      RB_KLAUNCH srht_warp<M, TX, false><<<grid, kSW * 32, smem, st>>>(n, ncols, X, ldx, row0, bits, sample, \
+                                                                       k, tpc, ntiles, w);             \
+    }                                                                                                  \
+  } while (0)
+    if (k <= 64) RB_SRHTW(2);
+    else if (k <= 128) RB_SRHTW(4);
+    else if (k <= 256) RB_SRHTW(8);
+    else if (k <= 512) RB_SRHTW(16);
+    else RB_SRHTW(32);
+#undef RB_SRHTW
+    const int64_t tot = (int64_t)k * ncols;
+    RB_KLAUNCH reduce_splits<<<ceil_div(tot, 256), 256, 0, st>>>(w, ctas, k, ncols, scale, out, ldo, accumulate);
+    return check_launch("srht sketch");
+  }
   const int MS = k <= 256 ? 1 : k <= 512 ? 2 : k <= 1024 ? 4 : 8;
   const int CG = MS >= 8 ? 4 : 8;
   const int cgroups = ceil_div(ncols, CG);
-  const size_t per = (size_t)k * ncols * sizeof(double);
   int ctas = std::max(1, std::min(ntiles, (2 * sm_count() + cgroups - 1) / cgroups));
   if ((size_t)ctas * per > ws_bytes) ctas = (int)std::max<size_t>(1, ws_bytes / per);
   RB_REQUIRE(ws && (size_t)ctas * per <= ws_bytes, "srht: workspace too small");

@@ -670,7 +670,23 @@ def rbgs(W, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None) -> BlockQR:
     dev = D.cuda_device(dc.device)
     if isinstance(W, Matrix):
         W = W._dev if W._dev is not None else W.data
-    if isinstance(W, torch.Tensor):
+    events = None
+    if isinstance(W, torch.Tensor) and not W.is_cuda and W.is_pinned() and W.dim() == 2 and D.is_cm(W) \
+            and W.dtype in (torch.float32, torch.float64):
+        # pinned column-major host W: upload block by block on a side stream,
+        # so block b's transfer overlaps the factorization of earlier blocks
+        Wd = D.empty_cm(W.shape[0], W.shape[1], W.dtype, dev)
+        off = cfg.partition.offsets()
+        copy_stream = torch.cuda.Stream(dev)
+        copy_stream.wait_stream(torch.cuda.current_stream(dev))
+        events = []
+        with torch.cuda.stream(copy_stream):
+            for b in range(cfg.partition.num_blocks):
+                Wd[:, off[b]:off[b + 1]].copy_(W[:, off[b]:off[b + 1]], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(copy_stream)
+                events.append(ev)
+    elif isinstance(W, torch.Tensor):
         Wd = D.to_cm(W, W.dtype if W.dtype in (torch.float32, torch.float64) else torch.float64, dev)
     else:
         A = np.asarray(W)
@@ -687,6 +703,11 @@ def rbgs(W, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None) -> BlockQR:
     off = cfg.partition.offsets()
     for b in range(cfg.partition.num_blocks):
         nxt = Wd[:, off[b + 1]:off[b + 2]] if b + 2 < len(off) else None
+        if events is not None:
+            stream = torch.cuda.current_stream(dev)
+            stream.wait_event(events[b])
+            if nxt is not None:
+                stream.wait_event(events[b + 1])
         sweep.push_block(Wd[:, off[b]:off[b + 1]], lookahead=nxt)
     return sweep.finish()
 
