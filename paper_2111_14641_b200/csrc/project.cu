@@ -19,6 +19,7 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "tc.cuh"
 
 namespace rb {
 namespace {
@@ -32,27 +33,45 @@ __device__ __forceinline__ float to_f32(T v) {  // binary64 -> binary32 rounds t
 }
 
 // ---- coarse ---------------------------------------------------------------
-// One row per thread, PB (multiple of 4) column accumulators.  FAST = 0:
-// reference order, acc = fl32(acc + fl32(q * (-x))) with __fmul_rn /
-// __fadd_rn (FMUL + FADD, never contracted: bit-identical to kernels.gemm
-// coarse).  FAST = 1: one packed FFMA2 per two columns, acc = fl32(acc - q x)
-// rounded once (the survey's "FMA" variant, SURVEY.md section 0 finding 5;
-// not bit-identical).  Q is streamed with a kPD-deep register prefetch ring
-// that runs across the X-chunk boundaries; X chunks are double-buffered.
+// RPT consecutive rows per thread, PB (multiple of 4) column accumulators
+// each.  FAST = 0: reference order, acc = fl32(acc + fl32(q * (-x))) with
+// __fmul_rn / __fadd_rn (FMUL + FADD, never contracted: bit-identical to
+// kernels.gemm coarse).  FAST = 1: one packed FFMA2 per two columns,
+// acc = fl32(acc - q x) rounded once (the survey's "FMA" variant, SURVEY.md
+// section 0 finding 5; not bit-identical).
+//
+// The FP32 pipe is the bound (2 instructions per element step in reference
+// order), so everything else is kept off the issue slots: X arrives
+// pre-rounded and negated (prep_x) and is staged by cp.async, double
+// buffered, in chunks of kXC rows padded with -0.0f (q = 0 there, so the
+// padded steps add -0.0f: acc unchanged, signed zeros included) -- the inner
+// loop has no bounds checks; Q is streamed through a two-bank register ring
+// of PD rows (loads for the next PD rows in flight while the current bank
+// is consumed); per l one LDS.128 broadcast feeds 8 * RPT FP instructions.
 constexpr int kXC = 64;  // X rows per staged chunk
-constexpr int kPD = 8;   // Q prefetch depth (loads in flight per thread)
 
+// Xs[l * PB + j] = -fl32(X[l, j]) for l < c, j < p; -0.0f elsewhere (l < cpad)
+__global__ void prep_x(int c, int cpad, int p, int pb, const double* __restrict__ X, int64_t ldx,
+                       float* __restrict__ Xs) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= cpad * pb) return;
+  const int l = e / pb, j = e % pb;
+  Xs[e] = (l < c && j < p) ? -__double2float_rn(X[l + (int64_t)j * ldx]) : -0.0f;
+}
+
+// RPT >= 4: one CTA per SM with up to 255 registers; otherwise two CTAs
+// per SM (<= 128 registers).  Ring depth PD rows of Q per bank.
 template <typename TQ, typename TW, int PB, int RPT, bool FAST>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, RPT >= 4 ? 1 : 2)
 project_coarse(int64_t n, int c, int p, const TQ* __restrict__ Q, int64_t ldq,
-               const double* __restrict__ X, int64_t ldx, const TW* __restrict__ W, int64_t ldw,
+               const float* __restrict__ Xs, const TW* __restrict__ W, int64_t ldw,
                TQ* __restrict__ Qp, int64_t ldqp, double* __restrict__ partial) {
-  static_assert(PB % 4 == 0, "PB multiple of 4");
-  __shared__ __align__(16) float sx[2][kXC][PB];  // -fl32(X[l, j]), double-buffered
+  constexpr int PD = RPT >= 2 ? 4 : 8;
+  static_assert(PB % 4 == 0 && kXC % (2 * PD) == 0, "tiling");
+  __shared__ __align__(16) float sx[2][kXC][PB];
   __shared__ double red[kThreads / 32];
 
-  // RPT consecutive rows per thread (each x broadcast from shared memory
-  // feeds RPT rows); rows beyond n compute on row 0 and are not stored
+  // rows beyond n compute on row 0 and are not stored
   const int64_t r0 = ((int64_t)blockIdx.x * kThreads + threadIdx.x) * RPT;
   bool v[RPT];
   const TQ* qrow[RPT];
@@ -78,65 +97,66 @@ project_coarse(int64_t n, int c, int p, const TQ* __restrict__ Q, int64_t ldq,
 
   const int nch = (c + kXC - 1) / kXC;
   auto stage = [&](int ch) {
-    const int l0 = ch * kXC, lc = min(kXC, c - l0);
-    float(*dst)[PB] = sx[ch & 1];
-    for (int e = threadIdx.x; e < kXC * PB; e += kThreads) {
-      const int l = e / PB, j = e % PB;
-      dst[l][j] = (l < lc && j < p) ? -__double2float_rn(X[(l0 + l) + (int64_t)j * ldx]) : 0.f;
-    }
+    const float4* src = reinterpret_cast<const float4*>(Xs + (int64_t)ch * kXC * PB);
+    float4* dst = reinterpret_cast<float4*>(&sx[ch & 1][0][0]);
+    for (int e = threadIdx.x; e < kXC * PB / 4; e += kThreads) tc::cp_async16(dst + e, src + e, 16);
+    tc::cp_async_commit();
   };
-  float qbuf[kPD][RPT];
+  auto loadq = [&](float (&dst)[PD][RPT], int l0) {
 #pragma unroll
-  for (int u = 0; u < kPD; ++u)
+    for (int u = 0; u < PD; ++u)
 #pragma unroll
-    for (int t = 0; t < RPT; ++t) qbuf[u][t] = u < c ? to_f32(qrow[t][(int64_t)u * ldq]) : 0.f;
-  if (nch > 0) stage(0);
-  for (int ch = 0; ch < nch; ++ch) {
-    __syncthreads();  // chunk ch staged; buffer (ch + 1) & 1 no longer read
-    if (ch + 1 < nch) stage(ch + 1);
-    const int l0 = ch * kXC, lc = min(kXC, c - l0);
-    const float(*xs)[PB] = sx[ch & 1];
-    for (int lb = 0; lb < lc; lb += kPD) {
-      float qc[kPD][RPT];
+      for (int t = 0; t < RPT; ++t) dst[u][t] = l0 + u < c ? to_f32(qrow[t][(int64_t)(l0 + u) * ldq]) : 0.f;
+  };
+  auto step = [&](const float (&q)[PD][RPT], const float (*xs)[PB], int lim) {
 #pragma unroll
-      for (int u = 0; u < kPD; ++u)
+    for (int u = 0; u < PD; ++u) {
+      // never taken (lim >= PD), but a block boundary per row of X keeps
+      // ptxas from hoisting later rows' LDS.128s into spills
+      if (u >= lim) break;
+      const float4* xr = reinterpret_cast<const float4*>(xs[u]);
 #pragma unroll
-        for (int t = 0; t < RPT; ++t) qc[u][t] = qbuf[u][t];
+      for (int h = 0; h < PB / 4; ++h) {
+        const float4 xx = xr[h];
 #pragma unroll
-      for (int u = 0; u < kPD; ++u) {
-        const int ln = l0 + lb + kPD + u;
-#pragma unroll
-        for (int t = 0; t < RPT; ++t) qbuf[u][t] = ln < c ? to_f32(qrow[t][(int64_t)ln * ldq]) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < kPD; ++u) {
-        if (lb + u < lc) {
-          const float4* xr = reinterpret_cast<const float4*>(xs[lb + u]);
-#pragma unroll
-          for (int h = 0; h < PB / 4; ++h) {
-            const float4 xx = xr[h];
-#pragma unroll
-            for (int t = 0; t < RPT; ++t) {
-              const float q = qc[u][t];
-              float* a = &acc[t][4 * h];
-              if (FAST) {
-                const float2 qq = make_float2(q, q);
-                float2 lo = __ffma2_rn(qq, make_float2(xx.x, xx.y), make_float2(a[0], a[1]));
-                float2 hi = __ffma2_rn(qq, make_float2(xx.z, xx.w), make_float2(a[2], a[3]));
-                a[0] = lo.x;
-                a[1] = lo.y;
-                a[2] = hi.x;
-                a[3] = hi.y;
-              } else {
-                a[0] = __fadd_rn(a[0], __fmul_rn(q, xx.x));
-                a[1] = __fadd_rn(a[1], __fmul_rn(q, xx.y));
-                a[2] = __fadd_rn(a[2], __fmul_rn(q, xx.z));
-                a[3] = __fadd_rn(a[3], __fmul_rn(q, xx.w));
-              }
-            }
+        for (int t = 0; t < RPT; ++t) {
+          const float qq = q[u][t];
+          float* a = &acc[t][4 * h];
+          if (FAST) {
+            const float2 q2 = make_float2(qq, qq);
+            float2 lo = __ffma2_rn(q2, make_float2(xx.x, xx.y), make_float2(a[0], a[1]));
+            float2 hi = __ffma2_rn(q2, make_float2(xx.z, xx.w), make_float2(a[2], a[3]));
+            a[0] = lo.x;
+            a[1] = lo.y;
+            a[2] = hi.x;
+            a[3] = hi.y;
+          } else {
+            a[0] = __fadd_rn(a[0], __fmul_rn(qq, xx.x));
+            a[1] = __fadd_rn(a[1], __fmul_rn(qq, xx.y));
+            a[2] = __fadd_rn(a[2], __fmul_rn(qq, xx.z));
+            a[3] = __fadd_rn(a[3], __fmul_rn(qq, xx.w));
           }
         }
       }
+    }
+  };
+
+  float qa[PD][RPT], qb[PD][RPT];
+  loadq(qa, 0);
+  if (nch > 0) stage(0);
+  for (int ch = 0; ch < nch; ++ch) {
+    tc::cp_async_wait<0>();
+    __syncthreads();  // chunk ch landed for all; buffer (ch + 1) & 1 no longer read
+    if (ch + 1 < nch) stage(ch + 1);
+    const float(*xs)[PB] = sx[ch & 1];
+    const int l0 = ch * kXC;
+    const int lim = (nch - ch) * kXC;  // >= kXC
+#pragma unroll 1
+    for (int lb = 0; lb < kXC; lb += 2 * PD) {
+      loadq(qb, l0 + lb + PD);
+      step(qa, xs + lb, lim - lb);
+      loadq(qa, l0 + lb + 2 * PD);
+      step(qb, xs + lb + PD, lim - lb - PD);
     }
   }
 
@@ -155,6 +175,185 @@ project_coarse(int64_t n, int c, int p, const TQ* __restrict__ Q, int64_t ldq,
     if (threadIdx.x == 0) {
       partial[2 * blockIdx.x] = sw;
       partial[2 * blockIdx.x + 1] = sq;
+    }
+  }
+}
+
+// ---- coarse, staged (binary32 Q, aligned) ---------------------------------
+// Same arithmetic as project_coarse, but Q never passes through registers
+// ahead of use: a CTA owns R = NT / CS * RPT consecutive rows, and each stage
+// (kKQ rows of X, i.e. kKQ columns of Q) arrives by bulk copies -- one per Q
+// column segment (R * 4 contiguous bytes) plus the stage's pre-negated X
+// rows -- completing on a per-buffer mbarrier; kQS buffers give two stages
+// of look-ahead and a buffer is released by the last warp to finish it (no
+// CTA barrier in the loop).  A thread owns RPT rows x PB / CS columns
+// (CS column slices per row group), so per l it issues one LDS for its RPT
+// q values and PB / CS / 4 LDS.128 for 2 * RPT * PB / CS FP instructions
+// (RPT = 4, CS = 2 at p = 40: 6 loads per 160 FP).  The CTA covering the
+// ragged end of the rows fills its stages with ordinary loads instead.
+constexpr int kKQ = 16;          // l rows per stage
+constexpr int kStagedRows = 512;  // rows per CTA
+constexpr int kQS = 3;   // stage buffers
+
+template <int PB, int RPT, int CS, int NT>
+constexpr size_t staged_smem() {
+  return (size_t)kQS * (kKQ * (NT / CS) * RPT + kKQ * PB) * sizeof(float) + kQS * (sizeof(uint64_t) + 4);
+}
+
+template <typename TW, int PB, int RPT, int CS, int NT, bool FAST>
+__global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2)
+project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq,
+               const float* __restrict__ Xs, const TW* __restrict__ W, int64_t ldw,
+               float* __restrict__ Qp, int64_t ldqp, double* __restrict__ partial) {
+  constexpr int PC = PB / CS;        // columns per thread
+  constexpr int R = NT / CS * RPT;   // rows per CTA
+  constexpr int QB = kKQ * R;        // Q floats per stage
+  constexpr int XB = kKQ * PB;       // X floats per stage
+  static_assert(PC % 4 == 0 && (RPT == 1 || RPT == 2 || RPT == 4) && (R * 4) % 16 == 0, "tiling");
+  extern __shared__ __align__(128) float smem[];
+  float* sq = smem;                                             // [kQS][kKQ][R]
+  float* sx = smem + kQS * QB;                                  // [kQS][kKQ][PB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sx + kQS * XB);  // [kQS]
+  uint32_t* done = reinterpret_cast<uint32_t*>(full + kQS);     // [kQS] warps done
+  __shared__ double red[NT / 32];
+
+  const int cg = threadIdx.x % CS, rt = threadIdx.x / CS;
+  const int jc = cg * PC;  // first column of this thread
+  const int64_t rc = (int64_t)blockIdx.x * R;
+  const bool bulk = rc + R <= n;
+  const int64_t r0 = rc + (int64_t)rt * RPT;
+  bool v[RPT];
+#pragma unroll
+  for (int t = 0; t < RPT; ++t) v[t] = r0 + t < n;
+
+  float acc[RPT][PC];
+  double w2 = 0.0;
+#pragma unroll
+  for (int t = 0; t < RPT; ++t)
+#pragma unroll
+    for (int j = 0; j < PC; ++j) {
+      acc[t][j] = 0.f;
+      if (jc + j < p && v[t]) {
+        const TW wv = W[r0 + t + (int64_t)(jc + j) * ldw];
+        w2 += (double)wv * (double)wv;
+        acc[t][j] = to_f32(wv);
+      }
+    }
+
+  const int nst = (c + kKQ - 1) / kKQ;
+  auto issue_bulk = [&](int s) {  // one thread
+    const int b = s % kQS, l0 = s * kKQ, lc = min(kKQ, c - l0);
+    float* dq = sq + b * QB;
+    tc::fence_proxy_async_smem();
+    tc::mbar_arrive_expect_tx(&full[b], (uint32_t)((lc * R + XB) * sizeof(float)));
+    for (int u = 0; u < lc; ++u)
+      tc::bulk_g2s(dq + u * R, Q + (int64_t)(l0 + u) * ldq + rc, R * sizeof(float), &full[b]);
+    tc::bulk_g2s(sx + b * XB, Xs + (int64_t)l0 * PB, XB * sizeof(float), &full[b]);
+  };
+  auto issue_tail = [&](int s) {  // all threads
+    const int b = s % kQS, l0 = s * kKQ, lc = min(kKQ, c - l0);
+    float* dq = sq + b * QB;
+    float* dx = sx + b * XB;
+    for (int e = threadIdx.x; e < lc * R; e += NT) {
+      const int u = e / R, r = e % R;
+      dq[e] = rc + r < n ? Q[(int64_t)(l0 + u) * ldq + rc + r] : 0.f;
+    }
+    for (int e = threadIdx.x; e < XB; e += NT) dx[e] = Xs[(int64_t)l0 * PB + e];
+  };
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < kQS; ++b) {
+      tc::mbar_init(&full[b], 1);
+      done[b] = 0;
+    }
+    tc::mbar_fence_init();
+  }
+  __syncthreads();
+  for (int s = 0; s < kQS && s < nst; ++s) {
+    if (!bulk) issue_tail(s);
+    else if (threadIdx.x == 0) issue_bulk(s);
+  }
+  __syncthreads();  // tail path: prologue stages written
+
+  for (int s = 0; s < nst; ++s) {
+    const int b = s % kQS, lc = min(kKQ, c - s * kKQ);
+    if (bulk) tc::mbar_wait(&full[b], (uint32_t)(s / kQS) & 1u);
+    const float* qs = sq + b * QB + rt * RPT;
+    const float* xs = sx + b * XB + jc;
+#pragma unroll 2
+    for (int u = 0; u < lc; ++u) {
+      float q[RPT];
+      if constexpr (RPT == 4) {
+        const float4 qq = *reinterpret_cast<const float4*>(qs + u * R);
+        q[0] = qq.x;
+        q[1] = qq.y;
+        q[2] = qq.z;
+        q[3] = qq.w;
+      } else if constexpr (RPT == 2) {
+        const float2 qq = *reinterpret_cast<const float2*>(qs + u * R);
+        q[0] = qq.x;
+        q[1] = qq.y;
+      } else {
+        q[0] = qs[u * R];
+      }
+      const float4* xr = reinterpret_cast<const float4*>(xs + u * PB);
+#pragma unroll
+      for (int h = 0; h < PC / 4; ++h) {
+        const float4 xx = xr[h];
+#pragma unroll
+        for (int t = 0; t < RPT; ++t) {
+          float* a = &acc[t][4 * h];
+          if (FAST) {
+            const float2 q2 = make_float2(q[t], q[t]);
+            float2 lo = __ffma2_rn(q2, make_float2(xx.x, xx.y), make_float2(a[0], a[1]));
+            float2 hi = __ffma2_rn(q2, make_float2(xx.z, xx.w), make_float2(a[2], a[3]));
+            a[0] = lo.x;
+            a[1] = lo.y;
+            a[2] = hi.x;
+            a[3] = hi.y;
+          } else {
+            a[0] = __fadd_rn(a[0], __fmul_rn(q[t], xx.x));
+            a[1] = __fadd_rn(a[1], __fmul_rn(q[t], xx.y));
+            a[2] = __fadd_rn(a[2], __fmul_rn(q[t], xx.z));
+            a[3] = __fadd_rn(a[3], __fmul_rn(q[t], xx.w));
+          }
+        }
+      }
+    }
+    if (bulk) {
+      // release buffer b without a CTA barrier: the last warp to finish
+      // stage s refills it with stage s + kQS
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) {
+        __threadfence_block();
+        if (atomicAdd(&done[b], 1u) == NT / 32 - 1) {
+          done[b] = 0;
+          if (s + kQS < nst) issue_bulk(s + kQS);
+        }
+      }
+    } else {
+      __syncthreads();  // buffer b consumed by every thread
+      if (s + kQS < nst) {
+        issue_tail(s + kQS);
+        __syncthreads();
+      }
+    }
+  }
+
+  double q2 = 0.0;
+#pragma unroll
+  for (int t = 0; t < RPT; ++t)
+#pragma unroll
+    for (int j = 0; j < PC; ++j)
+      if (jc + j < p && v[t]) {
+        Qp[r0 + t + (int64_t)(jc + j) * ldqp] = acc[t][j];
+        q2 += (double)acc[t][j] * (double)acc[t][j];
+      }
+  if (partial) {
+    const double sw = block_sum(w2, red);
+    const double sq2 = block_sum(q2, red);
+    if (threadIdx.x == 0) {
+      partial[2 * blockIdx.x] = sw;
+      partial[2 * blockIdx.x + 1] = sq2;
     }
   }
 }
@@ -244,20 +443,73 @@ int rpt_override() {
   return v;
 }
 
+// RB_PROJECT_STAGED=0 selects the register-ring kernel for binary32 Q
+bool staged_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RB_PROJECT_STAGED");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// rows per thread actually launched (RPT 4 is instantiated for f32/f32 only)
+template <int PB>
+int rpt_for(bool ff) {
+  const int o = rpt_override();
+  if (o == 4) return ff ? 4 : 2;
+  if (o == 1 || o == 2) return o;
+  return default_rpt<PB>();
+}
+
 template <typename TQ, typename TW, int PB>
 void launch_pb(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, const double* X, int64_t ldx,
-               const void* W, int64_t ldw, void* Qp, int64_t ldqp, double* partial, cudaStream_t st) {
+               const void* W, int64_t ldw, void* Qp, int64_t ldqp, double* partial, float* xs,
+               bool staged, cudaStream_t st) {
   if (mode == 2) {
     const int grid = ceil_div(n, kThreads);
     RB_KLAUNCH project_fine<TQ, TW, PB><<<grid, kThreads, 0, st>>>(n, c, p, (const TQ*)Q, ldq, X, ldx, (const TW*)W,
                                                                   ldw, (TQ*)Qp, ldqp, partial);
     return;
   }
-  const int rpt = rpt_override() > 0 ? rpt_override() : default_rpt<PB>();
+  const int cpad = ceil_div(c, kXC) * kXC;
+  if (cpad > 0) RB_KLAUNCH prep_x<<<ceil_div(cpad * PB, 256), 256, 0, st>>>(c, cpad, p, PB, X, ldx, xs);
+  if constexpr (sizeof(TQ) == 4) {
+    if (staged) {
+      // RPT x CS: rows per thread x column slices (PB / CS <= 20 columns each)
+      constexpr int RPT = PB <= 20 ? 2 : 4;
+      constexpr int CS = PB <= 20 ? 1 : PB <= 40 ? 2 : 4;
+      constexpr int NT = kStagedRows / RPT * CS;
+      constexpr size_t smem = staged_smem<PB, RPT, CS, NT>();
+      const int grid = ceil_div(n, (int64_t)kStagedRows);
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attr = true;
+      }
+      if (mode == 1)
+        RB_KLAUNCH project_staged<TW, PB, RPT, CS, NT, true><<<grid, NT, smem, st>>>(
+            n, c, p, (const float*)Q, ldq, xs, (const TW*)W, ldw, (float*)Qp, ldqp, partial);
+      else
+        RB_KLAUNCH project_staged<TW, PB, RPT, CS, NT, false><<<grid, NT, smem, st>>>(
+            n, c, p, (const float*)Q, ldq, xs, (const TW*)W, ldw, (float*)Qp, ldqp, partial);
+      return;
+    }
+  }
+  const int rpt = rpt_for<PB>(sizeof(TQ) == 4 && sizeof(TW) == 4);
   const int grid = ceil_div(n, (int64_t)rpt * kThreads);
-#define RB_CO(R, F)                                                                                    \
-  RB_KLAUNCH project_coarse<TQ, TW, PB, R, F><<<grid, kThreads, 0, st>>>(n, c, p, (const TQ*)Q, ldq, X, ldx, \
+#define RB_CO(R, F)                                                                                     \
+  RB_KLAUNCH project_coarse<TQ, TW, PB, R, F><<<grid, kThreads, 0, st>>>(n, c, p, (const TQ*)Q, ldq, xs, \
                                                                          (const TW*)W, ldw, (TQ*)Qp, ldqp, partial)
+  if constexpr (sizeof(TQ) == 4 && sizeof(TW) == 4) {
+    if (rpt == 4) {
+      if (mode == 1) RB_CO(4, true); else RB_CO(4, false);
+      return;
+    }
+  }
   if (rpt == 2) {
     if (mode == 1) RB_CO(2, true); else RB_CO(2, false);
   } else {
@@ -268,11 +520,12 @@ void launch_pb(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, co
 
 template <typename TQ, typename TW>
 int launch_tw(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, const double* X, int64_t ldx,
-              const void* W, int64_t ldw, void* Qp, int64_t ldqp, double* partial, cudaStream_t st) {
-#define RB_PB(V)                                                                              \
-  if (p <= V) {                                                                               \
-    launch_pb<TQ, TW, V>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, st);       \
-    return V;                                                                                 \
+              const void* W, int64_t ldw, void* Qp, int64_t ldqp, double* partial, float* xs, bool staged,
+              cudaStream_t st) {
+#define RB_PB(V)                                                                                \
+  if (p <= V) {                                                                                 \
+    launch_pb<TQ, TW, V>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st); \
+    return V;                                                                                   \
   }
   RB_PB(4) RB_PB(8) RB_PB(12) RB_PB(16) RB_PB(20) RB_PB(24) RB_PB(32) RB_PB(40) RB_PB(48) RB_PB(64)
 #undef RB_PB
@@ -280,20 +533,20 @@ int launch_tw(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, con
 }
 
 template <int PB>
-int rows_for() { return (rpt_override() > 0 ? rpt_override() : default_rpt<PB>()) * kThreads; }
+int rows_for(bool ff) { return rpt_for<PB>(ff) * kThreads; }
 
-int grid_rows(int mode, int p) {
+int grid_rows(int mode, int p, bool ff) {
   if (mode == 2) return kThreads;
-  if (p <= 4) return rows_for<4>();
-  if (p <= 8) return rows_for<8>();
-  if (p <= 12) return rows_for<12>();
-  if (p <= 16) return rows_for<16>();
-  if (p <= 20) return rows_for<20>();
-  if (p <= 24) return rows_for<24>();
-  if (p <= 32) return rows_for<32>();
-  if (p <= 40) return rows_for<40>();
-  if (p <= 48) return rows_for<48>();
-  return rows_for<64>();
+  if (p <= 4) return rows_for<4>(ff);
+  if (p <= 8) return rows_for<8>(ff);
+  if (p <= 12) return rows_for<12>(ff);
+  if (p <= 16) return rows_for<16>(ff);
+  if (p <= 20) return rows_for<20>(ff);
+  if (p <= 24) return rows_for<24>(ff);
+  if (p <= 32) return rows_for<32>(ff);
+  if (p <= 40) return rows_for<40>(ff);
+  if (p <= 48) return rows_for<48>(ff);
+  return rows_for<64>(ff);
 }
 
 }  // namespace
@@ -307,21 +560,26 @@ int project(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t n, i
   RB_REQUIRE(W && ldw >= n && Qp && ldqp >= n, "rb_project: bad W/Qp");
   RB_REQUIRE(order == RB_ORDER_REFERENCE || order == RB_ORDER_FMA, "rb_project: bad order %d", order);
   const int mode = compute_dtype == RB_F64 ? 2 : (order == RB_ORDER_FMA ? 1 : 0);
-  const int grid = ceil_div(n, grid_rows(mode, p));
-  double* partial = nullptr;
-  if (norms2) {
-    RB_REQUIRE(ws && ws_bytes >= (size_t)grid * 2 * sizeof(double), "rb_project: workspace");
-    partial = (double*)ws;
-  }
+  const bool q32 = q_dtype == RB_F32, w32 = w_dtype == RB_F32;
+  // binary32 Q with 16-B aligned columns streams through the staged kernel
+  const bool staged = mode != 2 && q32 && c > 0 && rpt_override() == 0 && (uintptr_t)Q % 16 == 0 &&
+                      ldq % 4 == 0 && staged_enabled();
+  const int grid = ceil_div(n, staged ? kStagedRows : grid_rows(mode, p, q32 && w32));
+  // workspace: [per-CTA norm pairs | staged -fl32(X), cpad x 64 floats]
+  const size_t part_bytes = norms2 ? ((size_t)grid * 2 * sizeof(double) + 255) / 256 * 256 : 0;
+  const size_t xs_bytes = mode == 2 ? 0 : (size_t)ceil_div(c, kXC) * kXC * 64 * sizeof(float);
+  RB_REQUIRE(part_bytes + xs_bytes == 0 || (ws && ws_bytes >= part_bytes + xs_bytes && (uintptr_t)ws % 16 == 0),
+             "rb_project: workspace too small (%zu < %zu)", ws_bytes, part_bytes + xs_bytes);
+  double* partial = norms2 ? (double*)ws : nullptr;
+  float* xs = xs_bytes ? (float*)((char*)ws + part_bytes) : nullptr;
   if (n == 0) {
     if (norms2) cudaMemsetAsync(norms2, 0, 2 * sizeof(double), st);
     return check_launch("rb_project");
   }
-  const bool q32 = q_dtype == RB_F32, w32 = w_dtype == RB_F32;
-  if (q32 && w32) launch_tw<float, float>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, st);
-  else if (q32) launch_tw<float, double>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, st);
-  else if (w32) launch_tw<double, float>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, st);
-  else launch_tw<double, double>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, st);
+  if (q32 && w32) launch_tw<float, float>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st);
+  else if (q32) launch_tw<float, double>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st);
+  else if (w32) launch_tw<double, float>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st);
+  else launch_tw<double, double>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st);
   if (norms2) RB_KLAUNCH sum_pairs<<<1, kThreads, 0, st>>>(partial, grid, norms2);
   return check_launch("rb_project");
 }
