@@ -51,7 +51,8 @@ using gl::kTM;
 constexpr int kChunk = 16384;  // rows per exact int32 accumulation (< 2^16 per row, balanced digits)
 constexpr int kTPC = kChunk / kBK;
 constexpr int kThreads = 256;
-constexpr int kSplitThreads = kChunk / 32;  // split pre-pass: 32 rows per thread, one chunk per CTA
+constexpr int kSplitThreads = 256;                    // split pre-pass: one chunk x column pair per CTA
+constexpr int kSplitSeg = kChunk / (16 * kSplitThreads);  // 16-row segments per thread
 
 // pipeline depth: as many 128-row stages as fit next to each other in
 // shared memory (overridable with RB_TC_STAGES for measurement)
@@ -66,14 +67,14 @@ constexpr int max_stages() { return (227 * 1024 - 2048) / (2 * kTM * kBK + 4 * k
 // UMMA N padding).  binary32 inputs are converted in binary32: x 2^(30-E) is
 // an exact power-of-two scaling and |xi| <= 2^30 < 2^31, so the integer is
 // exact; binary64 inputs round once to nearest.
-template <typename T, typename TV>
-__device__ __forceinline__ void load32(const T* __restrict__ x, int64_t base, int64_t n, bool vec, TV (&v)[32]) {
-  if (vec && base + 32 <= n) {
+template <int L, typename T, typename TV>
+__device__ __forceinline__ void loadL(const T* __restrict__ x, int64_t base, int64_t n, bool vec, TV (&v)[L]) {
+  if (vec && base + L <= n) {
     if constexpr (sizeof(T) == 4) {
       const float4* p4 = reinterpret_cast<const float4*>(x + base);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const float4 f = __ldcs(p4 + q);
+      for (int q = 0; q < L / 4; ++q) {
+        const float4 f = __ldg(p4 + q);
         v[4 * q] = f.x;
         v[4 * q + 1] = f.y;
         v[4 * q + 2] = f.z;
@@ -82,15 +83,15 @@ __device__ __forceinline__ void load32(const T* __restrict__ x, int64_t base, in
     } else {
       const double2* p2 = reinterpret_cast<const double2*>(x + base);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const double2 f = __ldcs(p2 + q);
+      for (int q = 0; q < L / 2; ++q) {
+        const double2 f = __ldg(p2 + q);
         v[2 * q] = (TV)f.x;
         v[2 * q + 1] = (TV)f.y;
       }
     }
   } else {
 #pragma unroll
-    for (int e = 0; e < 32; ++e) v[e] = base + e < n ? (TV)x[base + e] : TV(0);
+    for (int e = 0; e < L; ++e) v[e] = base + e < n ? (TV)x[base + e] : TV(0);
   }
 }
 
@@ -117,11 +118,11 @@ __device__ __forceinline__ void digits(int xi, uint32_t& d3, uint32_t& d2, uint3
   d3 = (uint32_t)b3 & 255u;
 }
 
-template <typename T>
-__device__ __forceinline__ void split_column(const T (&v)[32], T s, uint32_t (&w)[2][4][4]) {
+template <int L, typename T>
+__device__ __forceinline__ void split_column(const T (&v)[L], T s, uint32_t (&w)[L / 16][4][4]) {
   // w[seg][plane][word]
 #pragma unroll
-  for (int seg = 0; seg < 2; ++seg)
+  for (int seg = 0; seg < L / 16; ++seg)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       uint32_t p0 = 0, p1 = 0, p2 = 0, p3 = 0;
@@ -141,11 +142,11 @@ __device__ __forceinline__ void split_column(const T (&v)[32], T s, uint32_t (&w
     }
 }
 
-template <typename T>
-__device__ __forceinline__ float column_max(const T (&v)[32]) {
+template <int L, typename T>
+__device__ __forceinline__ float column_max(const T (&v)[L]) {
   float m = 0.f;
 #pragma unroll
-  for (int e = 0; e < 32; ++e) m = fmaxf(m, (float)fabs((double)v[e]));
+  for (int e = 0; e < L; ++e) m = fmaxf(m, (float)fabs((double)v[e]));
   return m;
 }
 
@@ -153,36 +154,45 @@ template <typename T1, typename T2>
 __global__ void __launch_bounds__(kSplitThreads)
 split_planes(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, const T2* __restrict__ X2,
              int64_t ld2, int NP, bool vec1, bool vec2, uint8_t* __restrict__ planes, int* __restrict__ exps) {
+  // Two passes over the CTA's chunk x column pair, kSplitSeg segments of 16
+  // rows per thread: the max pass reads with normal caching so that the
+  // encode pass re-reads from L2; the encode pass converts both columns of
+  // a segment together so each plane store fills a whole 32-byte sector.
+  // Few registers live per thread -> several CTAs per SM.
   __shared__ float red[2][kSplitThreads / 32];
   const int c = blockIdx.x;
   const int j0 = 2 * blockIdx.y;
-  const int64_t base = (int64_t)c * kChunk + 32 * threadIdx.x;
-  // column h of the pair comes from X1, X2 or is padding (kind 0 / 1 / 2);
   // values are held as binary32 when both inputs are binary32 (exact), else
   // as binary64 (binary32 embeds exactly)
   using TV = typename std::conditional<sizeof(T1) == 4 && sizeof(T2) == 4, float, double>::type;
-  int kind[2];
-  TV v[2][32];
-  float mx[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
+  auto load = [&](int h, int64_t base, TV (&v)[16]) {
     const int j = j0 + h;
-    kind[h] = j < c1 ? 0 : (j < c1 + c2 ? 1 : 2);
-    if (kind[h] == 0) load32(X1 + (int64_t)j * ld1, base, n, vec1, v[h]);
-    else if (kind[h] == 1) load32(X2 + (int64_t)(j - c1) * ld2, base, n, vec2, v[h]);
+    if (j < c1) loadL<16>(X1 + (int64_t)j * ld1, base, n, vec1, v);
+    else if (j < c1 + c2) loadL<16>(X2 + (int64_t)(j - c1) * ld2, base, n, vec2, v);
     else {
 #pragma unroll
-      for (int e = 0; e < 32; ++e) v[h][e] = TV(0);
+      for (int e = 0; e < 16; ++e) v[e] = TV(0);  // UMMA N padding
     }
-    mx[h] = column_max(v[h]);
-    for (int o = 16; o; o >>= 1) mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], o));
+  };
+  auto row0 = [&](int sg) { return (int64_t)c * kChunk + (int64_t)sg * (16 * kSplitThreads) + 16 * threadIdx.x; };
+  float mx[2] = {0.f, 0.f};
+#pragma unroll 2
+  for (int sg = 0; sg < kSplitSeg; ++sg) {
+    TV v[2][16];
+    load(0, row0(sg), v[0]);
+    load(1, row0(sg), v[1]);
+    mx[0] = fmaxf(mx[0], column_max(v[0]));
+    mx[1] = fmaxf(mx[1], column_max(v[1]));
   }
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+    for (int o = 16; o; o >>= 1) mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], o));
   if ((threadIdx.x & 31) == 0) {
     red[0][threadIdx.x >> 5] = mx[0];
     red[1][threadIdx.x >> 5] = mx[1];
   }
   __syncthreads();
-  uint32_t w[2][2][4][4];  // [column][seg][plane][word]
+  TV sc[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     float m = 0.f;
@@ -191,16 +201,22 @@ split_planes(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, 
     int E = 0;
     if (m > 0.f) frexpf(m, &E);  // m < 2^E; float rounding is monotone, so every |x| < 2^E
     if (threadIdx.x == 0) exps[(int64_t)c * NP + j0 + h] = E;
-    split_column(v[h], (TV)ldexp(1.0, 30 - E), w[h]);  // padding columns are zeros
+    sc[h] = (TV)ldexp(1.0, 30 - E);
   }
-#pragma unroll
-  for (int seg = 0; seg < 2; ++seg) {
-    const int64_t i0 = base + 16 * seg;
+#pragma unroll 1
+  for (int sg = 0; sg < kSplitSeg; ++sg) {
+    const int64_t base = row0(sg);
+    TV v[2][16];
+    load(0, base, v[0]);
+    load(1, base, v[1]);
+    uint32_t w[2][1][4][4];  // [column][seg][plane][word]
+    split_column(v[0], sc[0], w[0]);
+    split_column(v[1], sc[1], w[1]);
 #pragma unroll
     for (int pl = 0; pl < 4; ++pl) {
-      uint4* dst = reinterpret_cast<uint4*>(planes + gl::x_offset(pl, j0, i0, NP));
-      dst[0] = make_uint4(w[0][seg][pl][0], w[0][seg][pl][1], w[0][seg][pl][2], w[0][seg][pl][3]);
-      dst[1] = make_uint4(w[1][seg][pl][0], w[1][seg][pl][1], w[1][seg][pl][2], w[1][seg][pl][3]);
+      uint4* dst = reinterpret_cast<uint4*>(planes + gl::x_offset(pl, j0, base, NP));
+      __stcs(dst, make_uint4(w[0][0][pl][0], w[0][0][pl][1], w[0][0][pl][2], w[0][0][pl][3]));
+      __stcs(dst + 1, make_uint4(w[1][0][pl][0], w[1][0][pl][1], w[1][0][pl][2], w[1][0][pl][3]));
     }
   }
 }
