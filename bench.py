@@ -250,6 +250,8 @@ def gpu_arm(args, cfgd):
         del W
         torch.cuda.empty_cache()
         e2e_steps = max(1, min(args.steps, 3))
+        for _ in range(min(args.warmup, 2)):  # untimed: allocator / copy-stream first use
+            rbgs(Wh, theta, cfg, dc).R.data
         barrier()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
