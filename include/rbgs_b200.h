@@ -129,6 +129,12 @@ int rb_trsm_right(int in_dtype, int out_dtype, int64_t n, int p, const void* B, 
 int rb_gemm_f64(int transA, int transB, int m, int n, int k, double alpha,
                 const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
                 double* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
+/* binary32 C = alpha op(A) op(B) + beta C (cuBLAS SGEMM, default math mode:
+ * no TF32) -- the Step-2 solvers in unique-coarse mode (fine = COARSE),
+ * where the reference runs them in float32 (rbgs.py:144-212, prec.dtype). */
+int rb_gemm_f32(int transA, int transB, int m, int n, int k, float alpha,
+                const float* A, int64_t lda, const float* B, int64_t ldb, float beta,
+                float* C, int64_t ldc, void* stream);
 /* Tall Gram / cross product: out (p x q fp64) = A^T B for n-row A (n x p)
  * and B (n x q), inputs f32 or f64, fp64 accumulation (fused l2 stage).  */
 int rb_cross(int a_dtype, int b_dtype, int64_t n, int p, int q, const void* A, int64_t lda,

@@ -209,6 +209,14 @@ def gemm(tA, tB, alpha, A, B, beta, C):
          ws, wsb, st(C.device))
 
 
+def gemm32(tA, tB, alpha, A, B, beta, C):
+    """binary32 C = alpha op(A) op(B) + beta C (cuBLAS SGEMM, no TF32)."""
+    m, n = C.shape
+    k = A.shape[0] if tA else A.shape[1]
+    call("rb_gemm_f32", int(tA), int(tB), m, n, k, alpha, ptr(A), ld(A), ptr(B), ld(B), beta, ptr(C), ld(C),
+         st(C.device))
+
+
 def cross(A, B, out, accumulate=False):
     """out = A^T B for tall A (n x p), B (n x q)."""
     n, p = A.shape

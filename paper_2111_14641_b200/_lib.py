@@ -22,6 +22,7 @@ F32, F64 = 0, 1
 ORDER_REFERENCE, ORDER_FMA = 0, 1
 
 _i, _i64, _u64, _sz, _d = ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_double
+_f = ctypes.c_float
 _p = ctypes.c_void_p
 
 # name -> argtypes (all return int unless listed in _RESTYPE)
@@ -40,6 +41,7 @@ SIGNATURES = {
     "rb_sketch_signs": [_i, _i64, _i, _p, _i64, _p, _i64, _i, _d, _p, _i64, _i, _p, _sz, _p],
     "rb_trsm_right": [_i, _i, _i64, _i, _p, _i64, _p, _i64, _p, _i64, _p],
     "rb_gemm_f64": [_i, _i, _i, _i, _i, _d, _p, _i64, _p, _i64, _d, _p, _i64, _p, _sz, _p],
+    "rb_gemm_f32": [_i, _i, _i, _i, _i, _f, _p, _i64, _p, _i64, _f, _p, _i64, _p],
     "rb_cross": [_i, _i, _i64, _i, _i, _p, _i64, _p, _i64, _p, _i64, _i, _p, _sz, _p],
     "rb_potrf_upper": [_i, _p, _i64, _p, _i64, _p, _p],
     "rb_trsm_left_upper": [_i, _i, _p, _i64, _p, _i64, _p, _p],

@@ -58,6 +58,8 @@ int gemm_f64(int, int, int, int, int, double, const double*, int64_t, const doub
              int64_t, void*, size_t, cudaStream_t);
 int cross(int, int, int64_t, int, int, const void*, int64_t, const void*, int64_t, double*, int64_t, int, void*,
           size_t, cudaStream_t);
+int gemm_f32(int, int, int, int, int, float, const float*, int64_t, const float*, int64_t, float, float*, int64_t,
+             cudaStream_t);
 int potrf_upper(int, const double*, int64_t, double*, int64_t, int*, cudaStream_t);
 int trsm_left_upper(int, int, const double*, int64_t, double*, int64_t, int*, cudaStream_t);
 int geqrf_small(int, int, double*, int64_t, double*, int64_t, void*, size_t, cudaStream_t);
@@ -138,6 +140,11 @@ int rb_sketch_signs(int xd, int64_t n, int ncols, const void* X, int64_t ldx, co
 int rb_trsm_right(int ind, int outd, int64_t n, int p, const void* B, int64_t ldb, const double* R, int64_t ldr,
                   void* X, int64_t ldx, void* s) {
   return rb::trsm_right(ind, outd, n, p, B, ldb, R, ldr, X, ldx, as_stream(s));
+}
+
+int rb_gemm_f32(int tA, int tB, int m, int n, int k, float alpha, const float* A, int64_t lda, const float* B,
+                int64_t ldb, float beta, float* C, int64_t ldc, void* s) {
+  return rb::gemm_f32(tA, tB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, as_stream(s));
 }
 
 int rb_gemm_f64(int tA, int tB, int m, int n, int k, double alpha, const double* A, int64_t lda, const double* B,

@@ -407,6 +407,22 @@ int dgemm(int tA, int tB, int m, int n, int k, double alpha, const double* A, in
   return check_launch("dgemm");
 }
 
+int gemm_f32(int tA, int tB, int m, int n, int k, float alpha, const float* A, int64_t lda, const float* B,
+             int64_t ldb, float beta, float* C, int64_t ldc, cudaStream_t st) {
+  RB_REQUIRE(m >= 0 && n >= 0 && k >= 0 && C && ldc >= std::max(m, 1), "rb_gemm_f32: bad args");
+  if (m == 0 || n == 0) return RB_OK;
+  cublasHandle_t h = cublas_handle();
+  RB_REQUIRE(h, "cuBLAS handle creation failed");
+  cublasSetStream(h, st);
+  cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);
+  const cublasStatus_t s = cublasSgemm(h, tA ? CUBLAS_OP_T : CUBLAS_OP_N, tB ? CUBLAS_OP_T : CUBLAS_OP_N, m, n, k,
+                                       &alpha, A, (int)std::max<int64_t>(lda, 1), B, (int)std::max<int64_t>(ldb, 1),
+                                       &beta, C, (int)ldc);
+  ++g_launches;
+  RB_REQUIRE(s == CUBLAS_STATUS_SUCCESS, "cublasSgemm failed (%d)", (int)s);
+  return check_launch("sgemm");
+}
+
 // ============================== entry points ================================
 int gemm_f64(int tA, int tB, int m, int n, int k, double alpha, const double* A, int64_t lda, const double* B,
              int64_t ldb, double beta, double* C, int64_t ldc, void* ws, size_t wsb, cudaStream_t st) {

@@ -57,6 +57,7 @@ __all__ = ["RbgsConfig", "DeviceConfig", "BlockQR", "CertReport", "rbgs", "RbgsS
            "interblock_rgs", "interblock_sketched_cholqr", "interblock_l2_cholqr", "parse_method"]
 
 U_FINE = 2.0 ** -53
+U_COARSE = 2.0 ** -24
 
 _METHOD = re.compile(r"^([a-z0-9_]+)(?:[(:]\s*(\d+)\s*\)?)?$")
 _DEFAULTS = {"richardson": 5, "bmgs_reorth": 1, "cg_normal": 20, "sketched_cholqr": 1}
@@ -174,6 +175,8 @@ class _Scratch:
         self.R1 = D.empty_cm(w, w, f64, device)
         self.R2 = D.empty_cm(w, w, f64, device)
         self.Rt = D.empty_cm(w, w, f64, device)
+        self.Pr = D.empty_cm(k, w, f64, device)  # binary32-rounded P_i (fine = COARSE)
+        self.P32 = D.empty_cm(k, w, torch.float32, device)
         self.norms = torch.zeros(8, dtype=f64, device=device)  # [w2, q2, fin, ...]
         self.info = torch.zeros(8, dtype=torch.int32, device=device)
         self.status_host = torch.zeros(8, dtype=f64).pin_memory()
@@ -227,7 +230,7 @@ def _cg_dev(S, P, iters, X):
         d = r + beta * d
 
 
-def _householder_direct_dev(S, P, X, scr, sync=True):
+def _householder_direct_dev(S, P, X, scr, sync=True, u=None):
     k, c = S.shape
     dev = S.device
     A = D.empty_cm(k, c, torch.float64, dev)
@@ -237,10 +240,72 @@ def _householder_direct_dev(S, P, X, scr, sync=True):
     d = Rs.diagonal().abs()
     if sync:
         dmin, dmax = float(d.min()), float(d.max())
-        if dmin <= k * U_FINE * max(dmax, 1e-300):
+        if dmin <= k * (U_FINE if u is None else u) * max(dmax, 1e-300):
             raise RankDeficiencyError(f"least-squares matrix numerically rank deficient (min diag {dmin:.3e})")
     D.gemm(1, 0, 1.0, A, P, 0.0, X)
     D.trsm_left_upper(Rs, X, scr.info[6:7])
+
+
+def _solve_ls_f32(name, param, S, offsets, P, X, scr):
+    """Step 2 in binary32 (fine = COARSE): the reference casts S and P_i to
+    float32 and runs the solver in float32 BLAS (rbgs.py:144-212); here
+    cuBLAS SGEMM (no TF32) on the device.  X comes back as binary64 values
+    of the binary32 solution (`X.astype(np.float64)`)."""
+    k, c = S.shape
+    p = P.shape[1]
+    dev = S.device
+    f32 = torch.float32
+    S32 = D.empty_cm(k, c, f32, dev)
+    D.convert(S, S32)
+    P32 = D.empty_cm(k, p, f32, dev)
+    D.convert(P, P32)
+    X32 = D.zeros_cm(c, p, f32, dev)
+    if name == "richardson":
+        T = D.empty_cm(k, p, f32, dev)
+        for _ in range(param):
+            T.copy_(P32)
+            D.gemm32(0, 0, -1.0, S32, X32, 1.0, T)     # Pd - Sd X
+            D.gemm32(1, 0, 1.0, S32, T, 1.0, X32)      # X + Sd^T (...)
+    elif name == "bmgs_reorth":
+        T = P32.clone()
+        blocks = [(offsets[j], min(offsets[j + 1], c)) for j in range(len(offsets) - 1) if offsets[j] < c]
+        for _ in range(param):
+            for a, b in blocks:
+                inc = D.empty_cm(b - a, p, f32, dev)
+                D.gemm32(1, 0, 1.0, S32[:, a:b], T, 0.0, inc)
+                X32[a:b].add_(inc)
+                D.gemm32(0, 0, -1.0, S32[:, a:b], inc, 1.0, T)
+    elif name == "cg_normal":
+        b = D.empty_cm(c, p, f32, dev)
+        D.gemm32(1, 0, 1.0, S32, P32, 0.0, b)
+        r = b.clone()
+        d = r.clone()
+        rs = (r * r).sum(0)
+        SD = D.empty_cm(k, p, f32, dev)
+        Ad = D.empty_cm(c, p, f32, dev)
+        for _ in range(param):
+            D.gemm32(0, 0, 1.0, S32, d, 0.0, SD)
+            D.gemm32(1, 0, 1.0, S32, SD, 0.0, Ad)
+            dAd = (d * Ad).sum(0)
+            alpha = torch.where(dAd > 0, rs / torch.where(dAd > 0, dAd, torch.ones_like(dAd)),
+                                torch.zeros_like(dAd))
+            X32.add_(alpha * d)
+            r.sub_(alpha * Ad)
+            rs2 = (r * r).sum(0)
+            beta = torch.where(rs > 0, rs2 / torch.where(rs > 0, rs, torch.ones_like(rs)), torch.zeros_like(rs))
+            rs = rs2
+            d = r + beta * d
+    else:
+        # Householder on the binary32-rounded data, factorised in binary64,
+        # rank test at u = 2^-24 (rbgs.py:208 with prec = COARSE)
+        Sr = D.empty_cm(k, c, torch.float64, dev)
+        D.convert(S32, Sr)
+        Pr = D.empty_cm(k, p, torch.float64, dev)
+        D.convert(P32, Pr)
+        Xd = D.empty_cm(c, p, torch.float64, dev)
+        _householder_direct_dev(Sr, Pr, Xd, scr, u=U_COARSE)
+        D.convert(Xd, X32)
+    D.convert(X32, X)
 
 
 # ---------------------------------------------------------------------------
@@ -262,9 +327,10 @@ class RbgsSweep:
             raise ShapeError(f"sketch built for n={theta.n}, input has n={n}")
         if not (m <= theta.k <= n):
             raise ShapeError(f"need total cols m={m} <= sketch k={theta.k} <= n={n}")
-        if cfg.fine.format != "fine":
-            raise NotImplementedError("fine=COARSE (unique coarse precision) is not implemented on the "
-                                      "device path; the Step-2 solvers run in binary64")
+        # unique coarse precision (fine = COARSE): P_i is rounded to binary32
+        # values (rbgs.py:363 _round_to) and the Step-2 solvers run in
+        # binary32 (prec.dtype, rbgs.py:144-212); inter-block stays binary64
+        self.fine32 = cfg.fine.format != "fine"
         dc = device_cfg or DeviceConfig()
         self.device = D.cuda_device(dc.device)
         self.comm = dc.comm or Comm(None)
@@ -339,6 +405,9 @@ class RbgsSweep:
     def _solve_ls(self, S, Pi, X):
         name, param = self.solver
         scr = self._scr
+        if self.fine32:
+            _solve_ls_f32(name, param, S, self.offsets, Pi, X, scr)
+            return
         if name == "richardson":
             _richardson_dev(S, Pi, param, X, scr.T[:, :Pi.shape[1]])
         elif name == "bmgs_reorth":
@@ -561,6 +630,11 @@ class RbgsSweep:
                 Wn = None
             else:
                 self._sketch_reduce(W, Pi)
+        Pu = Pi  # as sketched (the inter-block step re-sketches Q' unrounded)
+        if self.fine32:
+            D.convert(Pi, scr.P32[:, :w])
+            Pi = scr.Pr[:, :w]
+            D.convert(scr.P32[:, :w], Pi)
         slot = self.Q[:, j0:j1]
         norms = scr.norms
         norms.zero_()
@@ -585,7 +659,7 @@ class RbgsSweep:
         self.comm.allreduce_(norms[0:2])
         if not c:
             norms[1:2].copy_(norms[0:1])
-        Rii, Si, sp_qp = self._interblock(Qp, Pi, slot, block1=(c == 0), sp_given=sp_given)
+        Rii, Si, sp_qp = self._interblock(Qp, Pu, slot, block1=(c == 0), sp_given=sp_given)
         # finiteness of everything the block produced (Matrix() checks)
         D.sumsq(Pi, norms[2:3])
         D.sumsq(Si, norms[3:4])
@@ -743,14 +817,17 @@ def certify(S, P, R, device=None) -> CertReport:
 # standalone Step-2 / Step-4-5 entry points (reference signatures)
 # ---------------------------------------------------------------------------
 
-def _ls_entry(fn, S, Pi, param, prec, device=None):
-    if prec.format != "fine":
-        raise NotImplementedError("coarse-precision LS solves are not implemented on the device path")
+def _ls_entry(fn, S, Pi, param, prec, device=None, name=None, offsets=None):
     dev = D.cuda_device(device)
     with torch.cuda.device(dev):
         Sd, Pd = _dev_f64(S, dev), _dev_f64(Pi, dev)
         X = D.empty_cm(Sd.shape[1], Pd.shape[1], torch.float64, dev)
-        fn(Sd, Pd, param, X)
+        if prec.format != "fine":  # binary32 solve (prec.dtype = float32)
+            class _S:
+                info = torch.zeros(8, dtype=torch.int32, device=dev)
+            _solve_ls_f32(name, param, Sd, offsets, Pd, X, _S())
+        else:
+            fn(Sd, Pd, param, X)
         return Matrix(X)
 
 
@@ -758,7 +835,7 @@ def ls_richardson(S, Pi, l: int, prec: PrecisionSpec = FINE) -> Matrix:
     def f(Sd, Pd, l, X):
         T = D.empty_cm(Sd.shape[0], Pd.shape[1], torch.float64, Sd.device)
         _richardson_dev(Sd, Pd, l, X, T)
-    return _ls_entry(f, S, Pi, l, prec)
+    return _ls_entry(f, S, Pi, l, prec, name="richardson")
 
 
 def ls_bmgs_reorth(S_blocks, Pi, l: int, prec: PrecisionSpec = FINE) -> Matrix:
@@ -772,11 +849,11 @@ def ls_bmgs_reorth(S_blocks, Pi, l: int, prec: PrecisionSpec = FINE) -> Matrix:
     def f(Sd, Pd, l, X):
         T = D.empty_cm(Sd.shape[0], Pd.shape[1], torch.float64, Sd.device)
         _bmgs_dev(Sd, off, Pd, l, X, T)
-    return _ls_entry(f, S, Pi, l, prec)
+    return _ls_entry(f, S, Pi, l, prec, name="bmgs_reorth", offsets=off)
 
 
 def ls_cg_normal(S, Pi, iters: int, prec: PrecisionSpec = FINE) -> Matrix:
-    return _ls_entry(lambda Sd, Pd, it, X: _cg_dev(Sd, Pd, it, X), S, Pi, iters, prec)
+    return _ls_entry(lambda Sd, Pd, it, X: _cg_dev(Sd, Pd, it, X), S, Pi, iters, prec, name="cg_normal")
 
 
 def ls_householder_direct(S, Pi, prec: PrecisionSpec = FINE) -> Matrix:
@@ -787,7 +864,7 @@ def ls_householder_direct(S, Pi, prec: PrecisionSpec = FINE) -> Matrix:
         scr = _S()
         scr.info = torch.zeros(8, dtype=torch.int32, device=Sd.device)
         _householder_direct_dev(Sd, Pd, X, scr)
-    return _ls_entry(f, S, Pi, None, prec)
+    return _ls_entry(f, S, Pi, None, prec, name="householder_direct")
 
 
 def _standalone_interblock(Qprime, theta, cfg):

@@ -220,7 +220,7 @@ def test_srht_large_pruned_fwht(pkg):
 # full sweep vs golden
 
 CASES = goldens.rbgs_cases()
-SKIP = {"coarse_all": "fine=COARSE not implemented on the device path"}
+SKIP = {}
 
 
 def _make_op(sketching, c):
@@ -324,3 +324,39 @@ def test_fused_lookahead_sketch_is_bitwise_neutral(pkg):
     assert np.array_equal(f.R.data, g.R.data)
     assert np.array_equal(f.Q.data, g.Q.data)
     assert np.array_equal(f.S.data, g.S.data)
+
+
+@pytest.mark.parametrize("solver", ["richardson", "bmgs_reorth", "cg_normal", "householder_direct"])
+def test_ls_solvers_coarse_precision_vs_oracle(pkg, solver):
+    """Step-2 solvers with prec = COARSE run in binary32 (rbgs.py:144-212,
+    prec.dtype); compared with the oracle's float32 numpy restatement."""
+    rbgs, sketching, D = pkg
+    from paper_2111_14641_b200.kernels import COARSE, FINE
+
+    g = np.random.Generator(np.random.Philox(31))
+    k, c, p = 300, 40, 8
+    S, _ = np.linalg.qr(g.standard_normal((k, c)))
+    S = S @ np.diag(1 + 0.01 * g.standard_normal(c))
+    P = g.standard_normal((k, p))
+    if solver == "richardson":
+        got = rbgs.ls_richardson(S, P, 5, COARSE).data
+        want = osw.ls_richardson(S, P, 5, "coarse")
+        ref64 = rbgs.ls_richardson(S, P, 5, FINE).data
+    elif solver == "bmgs_reorth":
+        blocks = [S[:, :20], S[:, 20:]]
+        got = rbgs.ls_bmgs_reorth(blocks, P, 2, COARSE).data
+        want = osw.ls_bmgs_reorth(blocks, P, 2, "coarse")
+        ref64 = rbgs.ls_bmgs_reorth(blocks, P, 2, FINE).data
+    elif solver == "cg_normal":
+        got = rbgs.ls_cg_normal(S, P, 10, COARSE).data
+        want = osw.ls_cg_normal(S, P, 10, "coarse")
+        ref64 = rbgs.ls_cg_normal(S, P, 10, FINE).data
+    else:
+        got = rbgs.ls_householder_direct(S, P, COARSE).data
+        want = osw.ls_householder_direct(S, P, "coarse")
+        ref64 = rbgs.ls_householder_direct(S, P, FINE).data
+    # binary32 values, same answer as the float32 restatement to binary32
+    # rounding, and visibly different from the binary64 solve
+    assert np.array_equal(got, got.astype(np.float32).astype(np.float64))
+    assert np.linalg.norm(got - want) <= 1e-5 * np.linalg.norm(want)
+    assert np.linalg.norm(got - ref64) > 0
