@@ -360,3 +360,65 @@ def test_ls_solvers_coarse_precision_vs_oracle(pkg, solver):
     assert np.array_equal(got, got.astype(np.float32).astype(np.float64))
     assert np.linalg.norm(got - want) <= 1e-5 * np.linalg.norm(want)
     assert np.linalg.norm(got - ref64) > 0
+
+
+# ---------------------------------------------------------------------------
+# Krylov drivers (krylov.py:110-281) vs the reference golden vectors
+
+def _lap1d(n):
+    import scipy.sparse as sp
+    return sp.diags([-np.ones(n - 1), 2 * np.ones(n), -np.ones(n - 1)], [-1, 0, 1], format="csr")
+
+
+def test_arnoldi_vs_reference_golden(pkg):
+    rbgs, sketching, D = pkg
+    from paper_2111_14641_b200 import krylov, operators
+
+    z = goldens.load("krylov")
+    n = 200
+    A = operators.CsrOperator(_lap1d(n))
+    arn = krylov.rbgs_arnoldi(A, z["arn/B"], sketching.SketchOperator("srht", 64, n, 1), 5)
+    # two-precision (reference default coarse = COARSE): binary32 rounding level
+    assert goldens.rel(arn.H.data, z["arn/H"]) <= 1e-5
+    assert goldens.rel(arn.Q.data, z["arn/Q"]) <= 5e-5
+    assert goldens.rel(arn.R_first.data, z["arn/Rf"]) <= 1e-5
+    assert goldens.rel(arn.P.data, z["arn/P"]) <= 1e-5
+
+
+def test_block_gmres_vs_reference_golden(pkg):
+    rbgs, sketching, D = pkg
+    from paper_2111_14641_b200 import krylov, operators
+
+    z = goldens.load("krylov")
+    d = np.arange(1.0, 101.0)
+    A = operators.DenseOperator(np.diag(d))
+    rep = krylov.block_gmres(A, z["gm/b"], sketching.SketchOperator("srht", 48, 100, 21), 12)
+    assert goldens.rel(rep.solution.data, z["gm/x"]) <= 1e-5
+    hist = np.array(rep.residual_history)
+    assert hist.shape == z["gm/hist"].shape
+    assert np.array_equal(hist[:, 0], z["gm/hist"][:, 0])
+    assert np.allclose(hist[:, 1], z["gm/hist"][:, 1], rtol=1e-3, atol=1e-7)
+    # happy breakdown: identity operator, block 2 vanishes
+    rep = krylov.block_gmres(operators.DenseOperator(np.eye(50)), z["gmid/B"],
+                             sketching.SketchOperator("identity", 50, 50, 0), 4)
+    assert rep.breakdown == int(z["gmid/breakdown"]) == 2
+    assert goldens.rel(rep.solution.data, z["gmid/x"]) <= 1e-6
+
+
+def test_block_gmres_poisson3d_vs_reference_golden(pkg):
+    """C4 shape family at a reduced grid: 7-point 3-D Poisson, sparse-sign
+    sketch, 2 restarts, sketched CholQR."""
+    rbgs, sketching, D = pkg
+    from paper_2111_14641_b200 import krylov, operators
+
+    z = goldens.load("krylov")
+    nx = int(z["p3/nx"])
+    A = operators.Poisson3D(nx, nx, nx)
+    op = sketching.sparse_sign_operator(72, nx ** 3, 11)
+    cfg = rbgs.RbgsConfig(interblock="sketched_cholqr(1)")
+    rep = krylov.block_gmres(A, z["p3/B"], op, 8, restarts=2, cfg=cfg)
+    assert goldens.rel(rep.solution.data, z["p3/x"]) <= 1e-4
+    hist = np.array(rep.residual_history)
+    assert hist.shape == z["p3/hist"].shape
+    assert np.allclose(hist[:, 1], z["p3/hist"][:, 1], rtol=1e-2)
+    assert np.allclose(np.array(rep.basis_cond_history), z["p3/conds"], rtol=1e-2)
