@@ -200,11 +200,19 @@ constexpr size_t staged_smem() {
   return (size_t)kQS * (kKQ * (NT / CS) * RPT + kKQ * PB) * sizeof(float) + kQS * (sizeof(uint64_t) + 4);
 }
 
-template <typename TW, int PB, int RPT, int CS, int NT, bool FAST>
+// MODE 0: scalar FMUL + FADD; MODE 2: the same two roundings as packed
+// instructions -- FFMA2(q, x, nz) with nz = -0.0f passed at run time (the
+// exactly rounded product, signed zeros included: p + (-0) = p) followed by
+// FADD2.  ptxas cannot see that nz is -0, so it cannot contract the pair
+// into one FFMA2 (which it does for mul.rn.f32x2 + add.rn.f32x2).  Both
+// packed instructions process two elements per issue slot at the scalar
+// element rate, halving the FP issue pressure.  MODE 1: one FFMA2 (FMA
+// order, not bit-identical).
+template <typename TW, int PB, int RPT, int CS, int NT, int MODE>
 __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2)
 project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq,
                const float* __restrict__ Xs, const TW* __restrict__ W, int64_t ldw,
-               float* __restrict__ Qp, int64_t ldqp, double* __restrict__ partial) {
+               float* __restrict__ Qp, int64_t ldqp, double* __restrict__ partial, float nz) {
   constexpr int PC = PB / CS;        // columns per thread
   constexpr int R = NT / CS * RPT;   // rows per CTA
   constexpr int QB = kKQ * R;        // Q floats per stage
@@ -302,10 +310,21 @@ project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq
 #pragma unroll
         for (int t = 0; t < RPT; ++t) {
           float* a = &acc[t][4 * h];
-          if (FAST) {
+          if constexpr (MODE == 1) {
             const float2 q2 = make_float2(q[t], q[t]);
             float2 lo = __ffma2_rn(q2, make_float2(xx.x, xx.y), make_float2(a[0], a[1]));
             float2 hi = __ffma2_rn(q2, make_float2(xx.z, xx.w), make_float2(a[2], a[3]));
+            a[0] = lo.x;
+            a[1] = lo.y;
+            a[2] = hi.x;
+            a[3] = hi.y;
+          } else if constexpr (MODE == 2) {
+            const float2 q2 = make_float2(q[t], q[t]);
+            const float2 z2 = make_float2(nz, nz);
+            const float2 plo = __ffma2_rn(q2, make_float2(xx.x, xx.y), z2);
+            const float2 phi = __ffma2_rn(q2, make_float2(xx.z, xx.w), z2);
+            const float2 lo = __fadd2_rn(make_float2(a[0], a[1]), plo);
+            const float2 hi = __fadd2_rn(make_float2(a[2], a[3]), phi);
             a[0] = lo.x;
             a[1] = lo.y;
             a[2] = hi.x;
@@ -453,6 +472,17 @@ bool staged_enabled() {
   return v == 1;
 }
 
+// RB_PROJECT_PACKED=0 selects the scalar FMUL + FADD form of the reference
+// order in the staged kernel (default: packed FFMA2(-0) + FADD2, same bits)
+bool packed_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RB_PROJECT_PACKED");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 // rows per thread actually launched (RPT 4 is instantiated for f32/f32 only)
 template <int PB>
 int rpt_for(bool ff) {
@@ -484,18 +514,21 @@ void launch_pb(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, co
       const int grid = ceil_div(n, (int64_t)kStagedRows);
       static bool attr = false;
       if (!attr) {
-        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attr = true;
       }
-      if (mode == 1)
-        RB_KLAUNCH project_staged<TW, PB, RPT, CS, NT, true><<<grid, NT, smem, st>>>(
-            n, c, p, (const float*)Q, ldq, xs, (const TW*)W, ldw, (float*)Qp, ldqp, partial);
-      else
-        RB_KLAUNCH project_staged<TW, PB, RPT, CS, NT, false><<<grid, NT, smem, st>>>(
-            n, c, p, (const float*)Q, ldq, xs, (const TW*)W, ldw, (float*)Qp, ldqp, partial);
+#define RB_ST(M)                                                                                  \
+  RB_KLAUNCH project_staged<TW, PB, RPT, CS, NT, M><<<grid, NT, smem, st>>>(                      \
+      n, c, p, (const float*)Q, ldq, xs, (const TW*)W, ldw, (float*)Qp, ldqp, partial, -0.0f)
+      if (mode == 1) RB_ST(1);
+      else if (packed_enabled()) RB_ST(2);
+      else RB_ST(0);
+#undef RB_ST
       return;
     }
   }
