@@ -174,6 +174,7 @@ def gpu_arm(args, cfgd):
     from paper_2111_14641_b200 import _lib, sketching, workloads
     from paper_2111_14641_b200.comm import Comm, RowShard
     from paper_2111_14641_b200.kernels import COARSE, FINE, BlockPartition
+    from paper_2111_14641_b200 import rbgs as rbgs_mod
     from paper_2111_14641_b200.rbgs import DeviceConfig, RbgsConfig, rbgs
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -315,6 +316,7 @@ def gpu_arm(args, cfgd):
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(),
             "cert": {"delta": cert.delta, "delta_tilde": cert.delta_tilde},
+            "status_replays": rbgs_mod.REPLAYS,
         }
         print(json.dumps(line), flush=True)
     if group is not None:

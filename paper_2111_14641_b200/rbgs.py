@@ -32,6 +32,7 @@ S, P (k x m) and R (m x m) are binary64 and replicated.
 from __future__ import annotations
 
 import math
+import os
 import re
 from dataclasses import dataclass, field
 
@@ -365,6 +366,7 @@ class RbgsSweep:
         self.per_block_resid = []
         self.pending_P = None
         self._next_P = None  # (key of the next block, its sketch) from a fused pass
+        self._deferred = None  # (status, info) per block when checks are deferred
 
     # -- small utilities ---------------------------------------------------
     def _sketch(self, X, out):
@@ -664,11 +666,37 @@ class RbgsSweep:
         D.sumsq(Pi, norms[2:3])
         D.sumsq(Si, norms[3:4])
         D.sumsq(Rii, norms[4:5])
+        if self._deferred is not None:
+            # one-shot rbgs(): record this block's status words on the device
+            # and carry on without a host round trip; rbgs() checks every
+            # block once at the end (and replays eagerly on a failure)
+            self._deferred[0][i - 1].copy_(norms)
+            self._deferred[1][i - 1].copy_(scr.info)
+            self._commit_block(j0, j1, Pi, Si, Rii)
+            return j0, j1
         scr.status_host.copy_(norms, non_blocking=True)
         scr.info_host.copy_(scr.info, non_blocking=True)
         torch.cuda.current_stream(self.device).synchronize()
-        st = scr.status_host.numpy()
-        info = scr.info_host.numpy()
+        self._check_status(i, scr.status_host.numpy(), scr.info_host.numpy(), Pi, slot, c, w)
+        if cfg.certify_blocks:
+            if sp_qp is None:
+                sp_qp = D.empty_cm(self.theta.k, w, torch.float64, self.device)
+                self._sketch_reduce(Qp, sp_qp)
+        self._commit_block(j0, j1, Pi, Si, Rii)
+        if cfg.certify_blocks:
+            self._certify_block(Si, Rii, sp_qp)
+        return j0, j1
+
+    def _commit_block(self, j0, j1, Pi, Si, Rii):
+        self.S[:, j0:j1].copy_(Si)
+        self.P[:, j0:j1].copy_(Pi)
+        self.R[j0:j1, j0:j1].copy_(Rii)
+        self.blocks_done += 1
+        self.cols_done = j1
+
+    def _check_status(self, i, st, info, Pi, slot, c, w):
+        """The reference's per-block failure tests (rbgs.py:373-399 and the
+        Matrix() finiteness checks) on the block's status words."""
         w_norm = math.sqrt(st[0]) if st[0] >= 0 else float("nan")
         q_norm = math.sqrt(st[1]) if st[1] >= 0 else float("nan")
         if not (np.isfinite(st[0]) and np.isfinite(st[1]) and np.isfinite(st[2])):
@@ -688,17 +716,26 @@ class RbgsSweep:
                     NotPositiveDefiniteError(int(col))
         if not (np.isfinite(st[3]) and np.isfinite(st[4])):
             raise ValueError("Matrix entries must be finite")
-        self.S[:, j0:j1].copy_(Si)
-        self.P[:, j0:j1].copy_(Pi)
-        self.R[j0:j1, j0:j1].copy_(Rii)
-        if cfg.certify_blocks:
-            if sp_qp is None:
-                sp_qp = D.empty_cm(self.theta.k, w, torch.float64, self.device)
-                self._sketch_reduce(Qp, sp_qp)
-            self._certify_block(Si, Rii, sp_qp)
-        self.blocks_done += 1
-        self.cols_done = j1
-        return j0, j1
+
+    def _defer_status(self):
+        """Switch to deferred status checks (one-shot rbgs() only, variants
+        without data-dependent host branches)."""
+        B = len(self.offsets) - 1
+        self._deferred = (torch.zeros(B, 8, dtype=torch.float64, device=self.device),
+                          torch.zeros(B, 8, dtype=torch.int32, device=self.device))
+
+    def _deferred_ok(self) -> bool:
+        """One host read of every block's status words; True when no block
+        would have raised in the eager sweep."""
+        st_all = self._deferred[0].cpu().numpy()
+        info_all = self._deferred[1].cpu().numpy()
+        for b in range(self.blocks_done):
+            st, info = st_all[b], info_all[b]
+            if not np.all(np.isfinite(st[:5])) or np.any(info[:4]):
+                return False
+            if math.sqrt(st[1]) <= self.n * U_FINE * math.sqrt(st[0]):
+                return False
+        return True
 
     def _check_rgs(self, i, q_norm, w):
         r = self._rgs_norms[:w].cpu().numpy()
@@ -734,12 +771,16 @@ class RbgsSweep:
                        Matrix(self.P), self.cfg.partition, cert)
 
 
-def rbgs(W, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None) -> BlockQR:
+REPLAYS = 0  # one-shot factorizations replayed eagerly after a deferred-status failure
+
+
+def rbgs(W, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None, *, _eager: bool = False) -> BlockQR:
     """Factor W = QR with Q orthonormal in the sketched inner product
     (rbgs.py:410-421).  W: numpy / Matrix (uploaded once; binary32 arrays
     stay binary32) or a CUDA tensor (used in place); with a sharded
     DeviceConfig, W holds this rank's rows."""
     require_cuda()
+    W_in = W
     dc = device_cfg or DeviceConfig()
     dev = D.cuda_device(dc.device)
     if isinstance(W, Matrix):
@@ -774,6 +815,14 @@ def rbgs(W, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None) -> BlockQR:
         raise ShapeError(f"partition covers {cfg.partition.total_cols} cols, W has {m}")
     n = theta.n if dc.shard is not None else n_rows
     sweep = RbgsSweep(n, theta, cfg, dc)
+    # Per-block host round trips are only needed to raise at the failing
+    # block; the one-shot driver defers them to one read at the end and, if
+    # any block failed, replays the factorization eagerly so the exception
+    # (type, message, block index) is exactly the reference's.
+    deferred = (not _eager and sweep.inter[0] == "sketched_cholqr" and not cfg.certify_blocks
+                and os.environ.get("RB_EAGER_STATUS", "0") != "1")
+    if deferred:
+        sweep._defer_status()
     off = cfg.partition.offsets()
     for b in range(cfg.partition.num_blocks):
         nxt = Wd[:, off[b + 1]:off[b + 2]] if b + 2 < len(off) else None
@@ -783,6 +832,11 @@ def rbgs(W, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None) -> BlockQR:
             if nxt is not None:
                 stream.wait_event(events[b + 1])
         sweep.push_block(Wd[:, off[b]:off[b + 1]], lookahead=nxt)
+    if deferred and not sweep._deferred_ok():
+        global REPLAYS
+        REPLAYS += 1
+        del sweep
+        return rbgs(W_in, theta, cfg, device_cfg, _eager=True)
     return sweep.finish()
 
 
