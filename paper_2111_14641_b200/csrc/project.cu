@@ -13,6 +13,10 @@
 // the opt-in RB_ORDER_FMA mode uses.
 // Fine (binary64) path: one row per thread, __dmul_rn / __dsub_rn.
 //
+// W and Qp may alias (Q' written over W_i: DeviceConfig.overwrite_w): every
+// thread reads its W entries before it writes the same entries of Qp, so
+// they carry no __restrict__.
+//
 // Q is streamed once (column-major, each column contiguous): per l a warp
 // reads 256 contiguous bytes.  X (fp64 on entry) is rounded to the compute
 // format and staged, negated, in shared memory in chunks of kLC rows.
@@ -64,8 +68,8 @@ __global__ void prep_x(int c, int cpad, int p, int pb, const double* __restrict_
 template <typename TQ, typename TW, int PB, int RPT, bool FAST>
 __global__ void __launch_bounds__(kThreads, RPT >= 4 ? 1 : 2)
 project_coarse(int64_t n, int c, int p, const TQ* __restrict__ Q, int64_t ldq,
-               const float* __restrict__ Xs, const TW* __restrict__ W, int64_t ldw,
-               TQ* __restrict__ Qp, int64_t ldqp, double* __restrict__ partial) {
+               const float* __restrict__ Xs, const TW* W, int64_t ldw,
+               TQ* Qp, int64_t ldqp, double* __restrict__ partial) {
   constexpr int PD = RPT >= 2 ? 4 : 8;
   static_assert(PB % 4 == 0 && kXC % (2 * PD) == 0, "tiling");
   __shared__ __align__(16) float sx[2][kXC][PB];
@@ -211,8 +215,8 @@ constexpr size_t staged_smem() {
 template <typename TW, int PB, int RPT, int CS, int NT, int MODE>
 __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2)
 project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq,
-               const float* __restrict__ Xs, const TW* __restrict__ W, int64_t ldw,
-               float* __restrict__ Qp, int64_t ldqp, double* __restrict__ partial, float nz) {
+               const float* __restrict__ Xs, const TW* W, int64_t ldw,
+               float* Qp, int64_t ldqp, double* __restrict__ partial, float nz) {
   constexpr int PC = PB / CS;        // columns per thread
   constexpr int R = NT / CS * RPT;   // rows per CTA
   constexpr int QB = kKQ * R;        // Q floats per stage
@@ -381,8 +385,8 @@ project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq
 template <typename TQ, typename TW, int PB>
 __global__ void __launch_bounds__(kThreads)
 project_fine(int64_t n, int c, int p, const TQ* __restrict__ Q, int64_t ldq,
-             const double* __restrict__ X, int64_t ldx, const TW* __restrict__ W, int64_t ldw,
-             TQ* __restrict__ Qp, int64_t ldqp, double* __restrict__ partial) {
+             const double* __restrict__ X, int64_t ldx, const TW* W, int64_t ldw,
+             TQ* Qp, int64_t ldqp, double* __restrict__ partial) {
   __shared__ double sx[kLC][PB];
   __shared__ double red[kThreads / 32];
   const int64_t r = (int64_t)blockIdx.x * kThreads + threadIdx.x;

@@ -126,7 +126,7 @@ int dense_sketch(int64_t n, int ncols, const TX* X, int64_t ldx, Src src, int k,
                  cudaStream_t st) {
   const int mt = ceil_div(k, BM);
   const int target = 4 * sm_count();
-  int splits = (int)std::max<int64_t>(1, std::min<int64_t>((n + 2047) / 2048, (target + mt - 1) / mt));
+  int splits = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (target + mt - 1) / mt));
   const size_t per = (size_t)k * ncols * sizeof(double);
   if ((size_t)splits * per > ws_bytes) splits = (int)std::max<size_t>(1, ws_bytes / per);
   RB_REQUIRE(ws && (size_t)splits * per <= ws_bytes, "sketch: workspace too small");

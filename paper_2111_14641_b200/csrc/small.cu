@@ -160,8 +160,8 @@ __global__ void potrf_kernel(int p, const double* __restrict__ G, int64_t ldg, d
 // 2 * RPT DFMAs; 1 / R_jj is a multiply.
 template <typename TI, typename TO, int PB, int RPT>
 __global__ void __launch_bounds__(kThreads, RPT > 1 ? 1 : 2)
-trsm_right_kernel(int64_t n, int p, const TI* __restrict__ B, int64_t ldb, const double* __restrict__ Rg,
-                  int64_t ldr, TO* __restrict__ Xo, int64_t ldx) {
+trsm_right_kernel(int64_t n, int p, const TI* B, int64_t ldb, const double* __restrict__ Rg,
+                  int64_t ldr, TO* Xo, int64_t ldx) {  // B and Xo may alias (in-place solve)
   constexpr int LD = (PB + 1) & ~1;
   __shared__ __align__(16) double sR[LD * PB];
   __shared__ double sInv[PB];

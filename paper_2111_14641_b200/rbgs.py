@@ -114,6 +114,12 @@ class DeviceConfig:
                       multiply-subtract, faster, not bit-identical).
     comm / shard      row sharding: this rank's rows and the group that owns
                       the other shards (comm.py).  Default: all rows here.
+    overwrite_w       one-shot rbgs() only: Q is written over W's own device
+                      storage (W must be a column-major CUDA tensor of Q's
+                      dtype), block by block as each W_i is consumed -- the
+                      n x m buffer that lets the C5 shard (2^24 x 1024 fp32
+                      plus its 2^24 x 2048 gaussian table) fit one GPU.  W
+                      is destroyed; failures raise at the failing block.
     """
 
     device: object = None
@@ -121,6 +127,7 @@ class DeviceConfig:
     projection_order: str = "reference"
     comm: Comm = None
     shard: RowShard = None
+    overwrite_w: bool = False
 
 
 @dataclass(frozen=True)
@@ -319,7 +326,7 @@ class RbgsSweep:
     Feed blocks left to right with `push_block`; `Q`, `S`, `P`, `R` are the
     device buffers (torch, column-major; Q holds this rank's rows only)."""
 
-    def __init__(self, n: int, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None):
+    def __init__(self, n: int, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None, *, _q_storage=None):
         require_cuda()
         if cfg.partition is None:
             raise ShapeError("config needs a partition")
@@ -353,7 +360,13 @@ class RbgsSweep:
         self.order = ORDER_FMA if dc.projection_order == "fma" else ORDER_REFERENCE
         dev = self.device
         k = theta.k
-        self.Q = D.zeros_cm(self.n_local, m, self.q_dtype, dev)
+        if _q_storage is not None:  # Q over W's storage (DeviceConfig.overwrite_w)
+            if (_q_storage.shape != (self.n_local, m) or _q_storage.dtype != self.q_dtype
+                    or not D.is_cm(_q_storage) or _q_storage.device != dev):
+                raise ShapeError("overwrite_w needs W as a column-major CUDA tensor of Q's dtype")
+            self.Q = _q_storage
+        else:
+            self.Q = D.zeros_cm(self.n_local, m, self.q_dtype, dev)
         self.S = D.zeros_cm(k, m, torch.float64, dev)
         self.P = D.zeros_cm(k, m, torch.float64, dev)
         self.R = D.zeros_cm(m, m, torch.float64, dev)
@@ -814,13 +827,25 @@ def rbgs(W, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None, *, _eager: 
     if cfg.partition.total_cols != m:
         raise ShapeError(f"partition covers {cfg.partition.total_cols} cols, W has {m}")
     n = theta.n if dc.shard is not None else n_rows
-    sweep = RbgsSweep(n, theta, cfg, dc)
+    # Q over W's storage: always for the private upload of a pinned host W
+    # (the slot of block i is written only after W_i has been consumed),
+    # on request (overwrite_w) for a caller's device W
+    q_storage = None
+    qd = dc.q_dtype or (torch.float32 if cfg.coarse.format == "coarse" else torch.float64)
+    if dc.overwrite_w or events is not None:
+        if Wd.dtype == qd and Wd.is_cuda and D.is_cm(Wd):
+            q_storage = Wd
+        elif dc.overwrite_w:
+            raise ShapeError("overwrite_w needs W as a column-major CUDA tensor of Q's dtype")
+    destroys_input = (q_storage is not None and isinstance(W_in, torch.Tensor) and W_in.is_cuda
+                      and Wd.data_ptr() == W_in.data_ptr())
+    sweep = RbgsSweep(n, theta, cfg, dc, _q_storage=q_storage)
     # Per-block host round trips are only needed to raise at the failing
     # block; the one-shot driver defers them to one read at the end and, if
     # any block failed, replays the factorization eagerly so the exception
     # (type, message, block index) is exactly the reference's.
-    deferred = (not _eager and sweep.inter[0] == "sketched_cholqr" and not cfg.certify_blocks
-                and os.environ.get("RB_EAGER_STATUS", "0") != "1")
+    deferred = (not _eager and not destroys_input and sweep.inter[0] == "sketched_cholqr"
+                and not cfg.certify_blocks and os.environ.get("RB_EAGER_STATUS", "0") != "1")
     if deferred:
         sweep._defer_status()
     off = cfg.partition.offsets()

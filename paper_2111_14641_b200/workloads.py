@@ -50,16 +50,19 @@ def trig_device(n: int, m: int, seed: int, row0: int = 0, n_local: int = None, d
 
 
 def colscaled_gaussian_device(n_local: int, m: int, seed: int, lo: float = 1e-6, dtype=torch.float32,
-                              device=None, rank: int = 0) -> torch.Tensor:
-    """C5: G diag(logspace(0, log10(lo), m)) for this rank's rows."""
+                              device=None, rank: int = 0, out: torch.Tensor = None) -> torch.Tensor:
+    """C5: G diag(logspace(0, log10(lo), m)) for this rank's rows (written
+    into `out` when given: the in-place bench regenerates W every step)."""
     dev = D.cuda_device(device)
     g = torch.Generator(device=dev).manual_seed(int(seed) * 1000003 + rank)
-    out = D.empty_cm(n_local, m, dtype, dev)
+    if out is None:
+        out = D.empty_cm(n_local, m, dtype, dev)
     scale = torch.logspace(0.0, math.log10(lo), m, dtype=torch.float64, device=dev)
-    for j0 in range(0, m, 64):
-        j1 = min(m, j0 + 64)
+    for j0 in range(0, m, 16):
+        j1 = min(m, j0 + 16)
         G = torch.randn(j1 - j0, n_local, generator=g, device=dev, dtype=torch.float32)
         out[:, j0:j1].copy_((G.t().double() * scale[None, j0:j1]))
+        del G
     return out
 
 

@@ -326,6 +326,56 @@ def test_fused_lookahead_sketch_is_bitwise_neutral(pkg):
     assert np.array_equal(f.S.data, g.S.data)
 
 
+def test_overwrite_w_and_pinned_upload_are_bitwise_neutral(pkg):
+    """Q written over W's storage (DeviceConfig.overwrite_w; always for the
+    private upload of a pinned host W) gives the same bits as a separate Q,
+    and the deferred-status one-shot path matches the eager per-block one."""
+    rbgs, sketching, D = pkg
+    from paper_2111_14641_b200.kernels import BlockPartition
+    import goldens as G
+
+    n, m, p, k = 20_000, 60, 12, 200
+    W = G.trig_family(n, m, 5).astype(np.float32)
+    th = sketching.gaussian_operator(k, n, 3)
+    cfg = rbgs.RbgsConfig(partition=BlockPartition.uniform(m, p), interblock="sketched_cholqr(1)")
+    f = rbgs.rbgs(W, th, cfg)
+    Wd = _dev(W.astype(np.float64), torch.float32)
+    g = rbgs.rbgs(Wd, th, cfg, rbgs.DeviceConfig(overwrite_w=True))
+    assert g.Q._dev.data_ptr() == Wd.data_ptr()
+    Wh = torch.empty((m, n), dtype=torch.float32).pin_memory().t()
+    Wh.copy_(torch.from_numpy(W))
+    h = rbgs.rbgs(Wh, th, cfg)
+    for other in (g, h):
+        assert np.array_equal(f.R.data, other.R.data)
+        assert np.array_equal(f.Q.data, other.Q.data)
+        assert np.array_equal(f.S.data, other.S.data)
+    import os
+    os.environ["RB_EAGER_STATUS"] = "1"
+    try:
+        e = rbgs.rbgs(W, th, cfg)
+    finally:
+        del os.environ["RB_EAGER_STATUS"]
+    assert np.array_equal(f.R.data, e.R.data) and np.array_equal(f.Q.data, e.Q.data)
+
+
+def test_deferred_status_replays_to_the_reference_exception(pkg):
+    """A failing block in the one-shot (deferred-status) path raises the same
+    exception, at the same block, as the eager sweep (rbgs.py:373-399)."""
+    rbgs, sketching, D = pkg
+    from paper_2111_14641_b200.errors import DependentBlockError
+    from paper_2111_14641_b200.kernels import BlockPartition
+
+    g = np.random.Generator(np.random.Philox(27))
+    W = np.hstack([g.standard_normal((3000, 10)), np.zeros((3000, 5)), g.standard_normal((3000, 5))])
+    th = sketching.gaussian_operator(200, 3000, 7)
+    cfg = rbgs.RbgsConfig(partition=BlockPartition.uniform(20, 5), interblock="sketched_cholqr(1)")
+    before = rbgs.REPLAYS
+    with pytest.raises(DependentBlockError) as ei:
+        rbgs.rbgs(W.astype(np.float32), th, cfg)
+    assert ei.value.block == 3
+    assert rbgs.REPLAYS == before + 1
+
+
 @pytest.mark.parametrize("solver", ["richardson", "bmgs_reorth", "cg_normal", "householder_direct"])
 def test_ls_solvers_coarse_precision_vs_oracle(pkg, solver):
     """Step-2 solvers with prec = COARSE run in binary32 (rbgs.py:144-212,
