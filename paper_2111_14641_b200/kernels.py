@@ -16,7 +16,7 @@ import torch
 
 from .errors import ShapeError
 
-__all__ = ["PrecisionSpec", "COARSE", "FINE", "Matrix", "BlockPartition", "as_array"]
+__all__ = ["PrecisionSpec", "COARSE", "FINE", "Matrix", "BlockPartition", "as_array", "cond_estimate"]
 
 
 @dataclass(frozen=True)
@@ -161,3 +161,11 @@ class BlockPartition:
         for w in self.block_widths():
             out.append(out[-1] + w)
         return tuple(out)
+
+
+def cond_estimate(A, device=None) -> float:
+    """sigma_max / sigma_min of a tall matrix on the GPU (kernels.py:552-566);
+    see post.cond_estimate."""
+    from .post import cond_estimate as _ce
+
+    return _ce(A, device)

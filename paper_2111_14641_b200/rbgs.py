@@ -55,7 +55,9 @@ from .kernels import COARSE, FINE, BlockPartition, Matrix, PrecisionSpec, as_arr
 
 __all__ = ["RbgsConfig", "DeviceConfig", "BlockQR", "CertReport", "rbgs", "RbgsSweep", "certify",
            "ls_richardson", "ls_bmgs_reorth", "ls_cg_normal", "ls_householder_direct",
-           "interblock_rgs", "interblock_sketched_cholqr", "interblock_l2_cholqr", "parse_method"]
+           "interblock_rgs", "interblock_sketched_cholqr", "interblock_l2_cholqr", "parse_method",
+           "cholesky_qr_postprocess", "certify_embedding", "save_blockqr", "load_blockqr",
+           "save_blockqr_binary", "load_blockqr_binary"]
 
 U_FINE = 2.0 ** -53
 U_COARSE = 2.0 ** -24
@@ -979,3 +981,18 @@ def interblock_l2_cholqr(Qprime, theta, resketch: bool = False):
 def interblock_rgs(Qprime, theta):
     """Column-wise randomized Gram-Schmidt (rbgs.py:232-264)."""
     return _standalone_interblock(Qprime, theta, dict(interblock="rgs_single"))
+
+
+# ---------------------------------------------------------------------------
+# post-processing, embedding certificate, serialization (rbgs.py:446-552;
+# device implementations in post.py)
+# ---------------------------------------------------------------------------
+
+from .post import (  # noqa: E402
+    certify_embedding,
+    cholesky_qr_postprocess,
+    load_blockqr,
+    load_blockqr_binary,
+    save_blockqr,
+    save_blockqr_binary,
+)

@@ -279,6 +279,53 @@ def gen_operators():
     save("operators", **out)
 
 
+def gen_post():
+    """Post-processing / embedding certificate / serialization:
+    cholesky_qr_postprocess, certify_embedding and save_blockqr on the
+    reference's own test shapes (test_rbgs.py:570-651)."""
+    out = {}
+    W = gen_oscillatory(2048, 100)
+    th = sketching.SketchOperator("srht", 1000, 2048, 3)
+    f = R.rbgs(W, th, R.RbgsConfig(partition=kernels.BlockPartition.uniform(100, 10)))
+    o = R.cholesky_qr_postprocess(f)
+    out.update({"p1/R_in": f.R.data, "p1/R": o.R.data, "p1/S": o.S.data,
+                "p1/cert": np.array([o.cert.delta, o.cert.delta_tilde])})
+    # fp64 hand-made factor: Q orthonormal times a column scaling
+    g = rng(131)
+    Q0, _ = np.linalg.qr(g.standard_normal((400, 6)))
+    Qs = Q0 * np.array([1.0, 2.0, 0.5, 3.0, 1.5, 0.25])
+    ident = sketching.SketchOperator("identity", 400, 400, 0)
+    S = sketching.apply(ident, Qs).data
+    f2 = R.BlockQR(kernels.Matrix(Qs), kernels.Matrix(np.eye(6)), kernels.Matrix(S), kernels.Matrix(S),
+                   kernels.BlockPartition.uniform(6, 3), None)
+    o2 = R.cholesky_qr_postprocess(f2)
+    out.update({"p2/Q_in": Qs, "p2/Q": o2.Q.data, "p2/R": o2.R.data, "p2/S": o2.S.data,
+                "p2/cert": np.array([o2.cert.delta, o2.cert.delta_tilde])})
+    # certify_embedding
+    n = 300
+    M = g.standard_normal((n, 6)) @ np.diag(np.logspace(0, -3, 6))
+    Wm = g.standard_normal((n, 6))
+    th7 = sketching.SketchOperator("srht", 60, n, 7)
+    phi = sketching.SketchOperator("rademacher", 80, n, 99)
+    eq, ew = R.certify_embedding(M, Wm, th7, phi)
+    out.update({"e1/M": M, "e1/W": Wm, "e1/eps": np.array([eq, ew])})
+    _, _, Vt = np.linalg.svd(sketching.materialize(th7) if hasattr(sketching, "materialize")
+                             else sketching.apply(th7, np.eye(n)).data)
+    Mb = Vt[60:].T[:, :6] + 1e-9 * g.standard_normal((n, 6))
+    eq2, ew2 = R.certify_embedding(Mb, Wm, th7, phi)
+    out.update({"e2/M": Mb, "e2/eps": np.array([eq2, ew2])})
+    save("post", **out)
+    # a reference-written BlockQR directory (Matrix Market text) for the
+    # load_blockqr interoperability test
+    Wc = conditioned(rng(30), 300, 12, 50.0)
+    th72 = sketching.SketchOperator("srht", 72, 300, 19)
+    fc = R.rbgs(Wc, th72, R.RbgsConfig(partition=kernels.BlockPartition.uniform(12, 4),
+                                       certify_blocks=True))
+    d = os.path.join(HERE, "blockqr_ref")
+    R.save_blockqr(fc, d)
+    print("blockqr_ref:", sorted(os.listdir(d)))
+
+
 if __name__ == "__main__":
     gen_gemm()
     gen_sketch()
@@ -286,3 +333,4 @@ if __name__ == "__main__":
     gen_errors()
     gen_rbgs()
     gen_krylov()
+    gen_post()

@@ -1,0 +1,108 @@
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <vector>
+#include <cstring>
+#include <cuda_runtime.h>
+// V0: dot form (current), 1 row/thread
+template <int PB>
+__global__ void __launch_bounds__(256, 2) v0(int64_t n, int p, const float* B, int64_t ldb, const double* __restrict__ Rg, int64_t ldr, float* Xo, int64_t ldx) {
+  constexpr int LD = (PB + 1) & ~1;
+  __shared__ __align__(16) double sR[LD * PB];
+  __shared__ double sInv[PB];
+  for (int e = threadIdx.x; e < LD * PB; e += blockDim.x) { const int i = e % LD, j = e / LD; sR[e] = (i < p && j < p) ? Rg[i + (int64_t)j * ldr] : 0.0; }
+  __syncthreads();
+  for (int j = threadIdx.x; j < p; j += blockDim.x) sInv[j] = 1.0 / sR[j + j * LD];
+  __syncthreads();
+  const int64_t r0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r0 >= n) return;
+  double x[PB];
+#pragma unroll
+  for (int j = 0; j < PB; ++j) x[j] = (j < p) ? (double)B[r0 + (int64_t)j * ldb] : 0.0;
+#pragma unroll
+  for (int j = 0; j < PB; ++j) {
+    if (j < p) {
+      double s = x[j];
+      const double2* col = reinterpret_cast<const double2*>(sR + j * LD);
+#pragma unroll
+      for (int l2 = 0; l2 < (j + 1) / 2; ++l2) {
+        const double2 rr = col[l2];
+        s = fma(-x[2 * l2], rr.x, s);
+        if (2 * l2 + 1 < j) s = fma(-x[2 * l2 + 1], rr.y, s);
+      }
+      x[j] = s * sInv[j];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < PB; ++j) if (j < p) Xo[r0 + (int64_t)j * ldx] = (float)x[j];
+}
+// V1: axpy form, LDS.128 row pairs, NaN-dependency against hoisting
+template <int PB, int MINB>
+__global__ void __launch_bounds__(256, MINB) v1(int64_t n, int p, const float* B, int64_t ldb, const double* __restrict__ Rg, int64_t ldr, float* Xo, int64_t ldx) {
+  constexpr int LD = (PB + 1) & ~1;
+  __shared__ __align__(16) double sR[PB * LD];
+  __shared__ double sInv[PB];
+  for (int e = threadIdx.x; e < LD * PB; e += blockDim.x) { const int j = e % LD, l = e / LD; sR[e] = (l < p && j < p && j >= l) ? Rg[l + (int64_t)j * ldr] : 0.0; }
+  __syncthreads();
+  for (int j = threadIdx.x; j < PB; j += blockDim.x) sInv[j] = j < p ? 1.0 / sR[j * LD + j] : 0.0;
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double x[PB];
+  const float* pb = B + r;
+#pragma unroll
+  for (int j = 0; j < PB; ++j) { x[j] = j < p ? (double)*pb : 0.0; pb += ldb; }
+  float* po = Xo + r;
+#pragma unroll
+  for (int l = 0; l < PB; ++l) {
+    const double xl = x[l] * sInv[l];
+    if (l < p) *po = (float)xl;
+    po += ldx;
+    const double2* row = reinterpret_cast<const double2*>(sR + l * LD + (xl != xl ? 2 : 0));
+#pragma unroll
+    for (int j2 = (l + 1) / 2; j2 < LD / 2; ++j2) {
+      const double2 rr = row[j2];
+      if (2 * j2 > l && 2 * j2 < PB) x[2 * j2] = fma(-xl, rr.x, x[2 * j2]);
+      if (2 * j2 + 1 > l && 2 * j2 + 1 < PB) x[2 * j2 + 1] = fma(-xl, rr.y, x[2 * j2 + 1]);
+    }
+  }
+}
+template <int PB>
+void run(int64_t n) {
+  const int p = PB;
+  float *B, *X0, *X1; double* R;
+  cudaMalloc(&B, n * p * 4); cudaMalloc(&X0, n * p * 4); cudaMalloc(&X1, n * p * 4); cudaMalloc(&R, p * p * 8);
+  std::vector<double> h(p * p, 0.0);
+  srand(3);
+  for (int j = 0; j < p; ++j) for (int i = 0; i <= j; ++i) h[i + j * p] = (i == j) ? 1.0 + rand() / (double)RAND_MAX : 0.1 * (rand() / (double)RAND_MAX - 0.5);
+  cudaMemcpy(R, h.data(), p * p * 8, cudaMemcpyHostToDevice);
+  std::vector<float> hb(n * p); for (auto& v : hb) v = rand() / (float)RAND_MAX - 0.5f;
+  cudaMemcpy(B, hb.data(), n * p * 4, cudaMemcpyHostToDevice);
+  int grid = (int)((n + 255) / 256);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  float ms[4];
+  for (int v = 0; v < 3; ++v) {
+    for (int rep = 0; rep < 2; ++rep) {
+      cudaEventRecord(a);
+      for (int i = 0; i < 5; ++i) {
+        if (v == 0) v0<PB><<<grid, 256>>>(n, p, B, n, R, p, X0, n);
+        else if (v == 1) v1<PB, 1><<<grid, 256>>>(n, p, B, n, R, p, X1, n);
+        else v1<PB, 2><<<grid, 256>>>(n, p, B, n, R, p, X1, n);
+      }
+      cudaEventRecord(b); cudaEventSynchronize(b);
+      cudaEventElapsedTime(&ms[v], a, b); ms[v] /= 5;
+    }
+  }
+  std::vector<float> o0(n * p), o1(n * p);
+  cudaMemcpy(o0.data(), X0, n * p * 4, cudaMemcpyDeviceToHost);
+  cudaMemcpy(o1.data(), X1, n * p * 4, cudaMemcpyDeviceToHost);
+  int64_t diff = 0; for (int64_t i = 0; i < n * p; ++i) diff += memcmp(&o0[i], &o1[i], 4) != 0;
+  printf("{\"p\": %d, \"n\": %lld, \"v0_ms\": %.4f, \"v1_minb1_ms\": %.4f, \"v1_minb2_ms\": %.4f, \"bitdiff\": %lld, \"hbm_ms\": %.4f}\n", p, (long long)n, ms[0], ms[1], ms[2], (long long)diff, 2.0 * n * p * 4 / 6.5e12 * 1e3);
+  cudaFree(B); cudaFree(X0); cudaFree(X1); cudaFree(R);
+}
+int main() {
+  run<40>(1000000);
+  run<64>(1 << 24);
+  run<32>(1 << 24);
+  return 0;
+}
