@@ -48,6 +48,10 @@ CONFIGS = {
                coarse="fine", desc="RBGS QR fp64 throughout, trig family 20000 x 200, p=10, gaussian k=400"),
     "c3": dict(name="C3", n=1 << 24, m=512, p=32, k=1024, kind="srht", gen="lowrank", dtype="f32",
                coarse="coarse", desc="RBGS QR two-precision, U diag(s) V^T 2^24 x 512, p=32, SRHT k=1024"),
+    "c4": dict(name="C4", n=256 ** 3, grid=256, m=244, p=61, mp=4, k=488, kind="sparse_sign", nnz=8,
+               gen="poisson", dtype="f64", coarse="coarse", krylov=True,
+               desc="block GMRES, 4 RHS, 7-point Poisson 256^3, 61 RBGS blocks (60 Arnoldi steps), "
+                    "sparse-sign k=488 (8 nnz/col), fp32 coarse / fp64 fine"),
     "c5shard": dict(name="C5-shard", n=1 << 24, m=1024, p=64, k=2048, kind="gaussian", gen="colscaled",
                     dtype="f32", coarse="coarse", inplace=True,
                     desc="RBGS QR two-precision, per-GPU shard of C5: 2^24 x 1024, p=64, gaussian k=2048"),
@@ -362,6 +366,90 @@ def gpu_arm(args, cfgd):
         dist.destroy_process_group()
 
 
+def gpu_arm_krylov(args, cfgd):
+    """C4: one restarted block GMRES solve (krylov.block_gmres, restarts=1)
+    per step on the 7-point Poisson operator; W = the 61 Arnoldi blocks
+    (binary64, n x 244).  Rows are z-slab sharded with a halo exchange per
+    operator apply when run under torchrun (strong scaling)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2111_14641_b200 import _lib, krylov, operators, sketching
+    from paper_2111_14641_b200.comm import Comm, RowShard
+    from paper_2111_14641_b200.rbgs import DeviceConfig, RbgsConfig
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        group = dist.group.WORLD
+    comm = Comm(group) if group else None
+    g = cfgd["grid"]
+    A = operators.Poisson3D(g, g, g, comm=comm, device=dev)
+    n, n_local, row0 = A.n, A.n_local, A.row0
+    mp, p, k = cfgd["mp"], cfgd["p"], cfgd["k"]
+    gen = torch.Generator(device=dev).manual_seed(SEED_W)
+    Bfull_cols = torch.randn(mp, n, generator=gen, device=dev, dtype=torch.float64)
+    B = Bfull_cols[:, row0:row0 + n_local].t()  # this rank's rows, column-major view
+    del gen
+    theta = sketching.sparse_sign_operator(k, n, SEED_THETA, cfgd["nnz"])
+    dc = DeviceConfig(device=dev, comm=comm, shard=RowShard(n, row0, n_local) if world > 1 else None)
+    cfg = RbgsConfig()
+
+    def step():
+        return krylov.block_gmres(A, B, theta, p, restarts=1, cfg=cfg, device_cfg=dc)
+
+    for _ in range(args.warmup):
+        rep = step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if group is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    n0 = _lib.launch_count()
+    with Clocks(local) as clk:
+        barrier()
+        t0 = time.perf_counter()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            rep = step()
+        e1.record()
+        barrier()
+        wall = (time.perf_counter() - t0) / args.steps
+    launches = _lib.launch_count() - n0
+    ms = e0.elapsed_time(e1) / args.steps
+    if group is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    wbytes = 8 * n * cfgd["m"]
+    value = wbytes / (ms * 1e-3) / 1e9
+    hbm, _, src = _peaks()
+    if rank == 0:
+        line = {
+            "metric": "RBGS QR GB/s of W processed", "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32-coarse/f64-fine", "data": "synthetic",
+            "config": {"workload": cfgd["desc"], "n": n, "m": cfgd["m"], "p_blocks": p, "block_width": mp,
+                       "k": k, "sketch": "sparse_sign(8)", "restarts": 1, "parallelism": f"zslab{world}",
+                       "l2": "inputs larger than L2 (basis = %.1f GB)" % (wbytes / 1e9)},
+            "rel_residual": rep.residual_history[-1][1], "iterations": len(rep.residual_history),
+            "basis_cond_last": rep.basis_cond_history[-1], "cert_last": list(rep.cert_history[-1]),
+            "host_wall_ms_per_step": wall * 1e3, "gpu_launches": launches, "clocks": clk.summary(),
+            "peak_hbm_GBps": hbm, "peak_source": src,
+        }
+        print(json.dumps(line), flush=True)
+    if group is not None:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -378,6 +466,8 @@ def main():
     cfgd = CONFIGS[args.config]
     if args.impl == "reference":
         reference_arm(args, cfgd)
+    elif cfgd.get("krylov"):
+        gpu_arm_krylov(args, cfgd)
     else:
         gpu_arm(args, cfgd)
 

@@ -204,9 +204,9 @@ def trsm_right(B, R, out):
 def gemm(tA, tB, alpha, A, B, beta, C):
     m, n = C.shape
     k = A.shape[0] if tA else A.shape[1]
-    ws, wsb = _ws(max(m, n), 64, max(m, n, 64), C.device)
+    # cuBLAS DGEMM: no workspace of ours
     call("rb_gemm_f64", int(tA), int(tB), m, n, k, alpha, ptr(A), ld(A), ptr(B), ld(B), beta, ptr(C), ld(C),
-         ws, wsb, st(C.device))
+         None, 0, st(C.device))
 
 
 def gemm32(tA, tB, alpha, A, B, beta, C):

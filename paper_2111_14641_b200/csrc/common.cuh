@@ -112,6 +112,33 @@ __device__ __forceinline__ int sparse_sign_column(uint64_t i, uint64_t seed, int
   return have;
 }
 
+// Register-resident variant (no local memory): the same rows, signs and
+// order as sparse_sign_column for s <= SMAX, every array index static.
+// tr[q] = (row << 1) | (negative sign).
+template <int SMAX>
+__device__ __forceinline__ void sparse_sign_targets(uint64_t i, uint64_t seed, int k, int s, int (&tr)[SMAX]) {
+  int have = 0;
+#pragma unroll
+  for (int q = 0; q < SMAX; ++q) tr[q] = 0;
+  for (uint32_t t = 0; have < s; ++t) {
+    const u32x4 w4 = philox4x32_10(u32x4{(uint32_t)i, (uint32_t)(i >> 32), t, kTagSparse},
+                                   (uint32_t)seed, (uint32_t)(seed >> 32));
+    const uint32_t ws[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int cand = (int)(((uint64_t)(ws[j] >> 1) * (uint64_t)k) >> 31);
+      bool dup = false;
+#pragma unroll
+      for (int q = 0; q < SMAX; ++q) dup |= (q < have) && ((tr[q] >> 1) == cand);
+      const bool take = !dup && have < s;
+#pragma unroll
+      for (int q = 0; q < SMAX; ++q)
+        if (take && q == have) tr[q] = (cand << 1) | (int)(ws[j] & 1u);
+      have += take ? 1 : 0;
+    }
+  }
+}
+
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
 }  // namespace rb

@@ -523,32 +523,126 @@ int srht_sketch(int64_t n, int ncols, const TX* X, int64_t ldx, int64_t row0, in
 }
 
 // ======================= sparse sign ========================================
-template <typename TX>
+// Bucketed accumulation: a CTA streams tiles of kST rows; for every row it
+// hashes the s target sketch rows (sparse_sign_column), stages x / sqrt(s)
+// in shared memory and counts the targets per sketch row (native 32-bit
+// shared atomics); a block scan turns the counts into bucket offsets, the
+// (row, sign) entries are scattered into their buckets, and the owner thread
+// of each sketch row sums its bucket for all columns of the pass.  This
+// replaces s * ncols binary64 shared-memory atomics per row (a CAS loop on
+// sm_100) by 2 s integer atomics per row.  Per-CTA partials are reduced in
+// CTA order by reduce_splits.
+constexpr int kST = 1024;            // rows per tile
+constexpr int kSRPT = kST / kThreads;  // rows per thread per tile
+
+template <typename TX, int CG, int SMAX>
 __global__ void __launch_bounds__(kThreads)
-sparse_partial(int64_t n, int ncols, const TX* __restrict__ X, int64_t ldx, int64_t row0,
-               uint64_t seed, int k, int s, int cg, int64_t rows_per_cta, double* __restrict__ ws) {
-  extern __shared__ double sacc[];  // k x cg
-  const int c0 = blockIdx.y * cg;
-  const int cc = min(cg, ncols - c0);
-  for (int e = threadIdx.x; e < k * cg; e += blockDim.x) sacc[e] = 0.0;
-  __syncthreads();
+sparse_bucket_partial(int64_t n, int ncols, const TX* __restrict__ X, int64_t ldx, int64_t row0, uint64_t seed,
+                      int k, int s, double* __restrict__ ws) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sx = reinterpret_cast<double*>(smem_raw);          // [kST][CG]
+  double* sacc = sx + kST * CG;                               // [k][CG]
+  int* cnt = reinterpret_cast<int*>(sacc + (size_t)k * CG);   // [k]
+  int* cur = cnt + k;                                         // [k]
+  uint32_t* list = reinterpret_cast<uint32_t*>(cur + k);      // [kST * s]
+  __shared__ int wsum[kThreads / 32];
+  const int c0 = blockIdx.y * CG;
+  const int cc = min(CG, ncols - c0);
   const double inv = 1.0 / sqrt((double)s);
-  const int64_t beg = (int64_t)blockIdx.x * rows_per_cta;
-  const int64_t end = min(n, beg + rows_per_cta);
-  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
-    int rows[16], sg[16];
-    sparse_sign_column((uint64_t)(row0 + i), seed, k, s, rows, sg);
-    for (int c = 0; c < cc; ++c) {
-      const double x = (double)X[i + (int64_t)(c0 + c) * ldx] * inv;
-      for (int q = 0; q < s; ++q) atomicAdd(&sacc[rows[q] + c * k], sg[q] > 0 ? x : -x);
+  for (int e = threadIdx.x; e < k * CG; e += kThreads) sacc[e] = 0.0;
+  const int64_t ntiles = (n + kST - 1) / kST;
+  const int per = (k + kThreads - 1) / kThreads;  // scan segment per thread
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t base = tile * kST;
+    for (int e = threadIdx.x; e < k; e += kThreads) cnt[e] = 0;
+    __syncthreads();
+    int tr[kSRPT][SMAX];
+    bool live[kSRPT];
+#pragma unroll
+    for (int u = 0; u < kSRPT; ++u) {
+      const int il = threadIdx.x + u * kThreads;
+      const int64_t i = base + il;
+      live[u] = i < n;
+      if (live[u]) {
+        sparse_sign_targets<SMAX>((uint64_t)(row0 + i), seed, k, s, tr[u]);
+#pragma unroll
+        for (int q = 0; q < SMAX; ++q)
+          if (q < s) atomicAdd(&cnt[tr[u][q] >> 1], 1);
+#pragma unroll
+        for (int c = 0; c < CG; ++c) sx[il * CG + c] = c < cc ? (double)X[i + (int64_t)(c0 + c) * ldx] * inv : 0.0;
+      }
     }
+    __syncthreads();
+    // exclusive scan of cnt -> cur (thread t owns bins [t per, (t+1) per))
+    int loc = 0;
+    for (int j = 0; j < per; ++j) {
+      const int r = threadIdx.x * per + j;
+      if (r < k) loc += cnt[r];
+    }
+    int incl = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if ((threadIdx.x & 31) >= o) incl += v;
+    }
+    if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    int off = incl - loc;
+    for (int w = 0; w < (threadIdx.x >> 5); ++w) off += wsum[w];
+    for (int j = 0; j < per; ++j) {
+      const int r = threadIdx.x * per + j;
+      if (r < k) {
+        cur[r] = off;
+        off += cnt[r];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < kSRPT; ++u) {
+      if (!live[u]) continue;
+      const int il = threadIdx.x + u * kThreads;
+#pragma unroll
+      for (int q = 0; q < SMAX; ++q) {
+        if (q < s) {
+          const int pos = atomicAdd(&cur[tr[u][q] >> 1], 1);
+          list[pos] = ((uint32_t)il << 1) | (uint32_t)(tr[u][q] & 1);
+        }
+      }
+    }
+    __syncthreads();
+    // owners: cur[r] now holds the END of bucket r
+    for (int r = threadIdx.x; r < k; r += kThreads) {
+      const int e1 = cur[r], e0 = e1 - cnt[r];
+      double acc[CG];
+#pragma unroll
+      for (int c = 0; c < CG; ++c) acc[c] = sacc[r * CG + c];
+      for (int e = e0; e < e1; ++e) {
+        const uint32_t v = list[e];
+        const double* xr = sx + (v >> 1) * CG;
+        if (v & 1u) {
+#pragma unroll
+          for (int c = 0; c < CG; ++c) acc[c] -= xr[c];
+        } else {
+#pragma unroll
+          for (int c = 0; c < CG; ++c) acc[c] += xr[c];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < CG; ++c) sacc[r * CG + c] = acc[c];
+    }
+    __syncthreads();
   }
-  __syncthreads();
   double* dst = ws + (int64_t)blockIdx.x * k * ncols;
-  for (int e = threadIdx.x; e < k * cc; e += blockDim.x) {
+  for (int e = threadIdx.x; e < k * cc; e += kThreads) {
     const int r = e % k, c = e / k;
-    dst[r + (int64_t)(c0 + c) * k] = sacc[e];
+    dst[r + (int64_t)(c0 + c) * k] = sacc[r * CG + c];
   }
+}
+
+template <typename TX, int CG>
+size_t sparse_smem(int k, int s) {
+  return (size_t)kST * CG * sizeof(double) + (size_t)k * CG * sizeof(double) + 2 * (size_t)k * sizeof(int) +
+         (size_t)kST * s * sizeof(uint32_t);
 }
 
 template <typename TX>
@@ -557,19 +651,28 @@ int sparse_sketch(int64_t n, int ncols, const TX* X, int64_t ldx, int64_t row0, 
                   size_t ws_bytes, cudaStream_t st) {
   const int s = std::min(nnz, k);
   RB_REQUIRE(s >= 1 && s <= 16, "sparse_sign: nnz must be in [1, 16]");
-  int cg = std::max(1, std::min(ncols, (int)(96 * 1024 / (k * sizeof(double)))));
-  RB_REQUIRE((size_t)k * sizeof(double) <= 96 * 1024, "sparse_sign: k too large");
-  const int cgroups = ceil_div(ncols, cg);
+  constexpr int CG = 4;
+  const size_t smem = sparse_smem<TX, CG>(k, s);
+  RB_REQUIRE(smem <= 200 * 1024, "sparse_sign: k too large (%d)", k);
+  const int cgroups = ceil_div(ncols, CG);
   const size_t per = (size_t)k * ncols * sizeof(double);
-  int ctas = std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, (4 * sm_count() + cgroups - 1) / cgroups));
+  const int64_t ntiles = (n + kST - 1) / kST;
+  int ctas = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (2 * sm_count() + cgroups - 1) / cgroups));
   if ((size_t)ctas * per > ws_bytes) ctas = (int)std::max<size_t>(1, ws_bytes / per);
   RB_REQUIRE(ws && (size_t)ctas * per <= ws_bytes, "sparse_sign: workspace too small");
-  const int64_t rpc = (n + ctas - 1) / std::max(ctas, 1);
-  const size_t smem = (size_t)k * cg * sizeof(double);
-  cudaFuncSetAttribute(sparse_partial<TX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  if (n > 0)
-    RB_KLAUNCH sparse_partial<TX><<<dim3(ctas, cgroups), kThreads, smem, st>>>(n, ncols, X, ldx, row0, seed, k, s, cg,
-                                                                    std::max<int64_t>(rpc, 1), (double*)ws);
+#define RB_SB(SM)                                                                                             \
+  do {                                                                                                        \
+    cudaFuncSetAttribute(sparse_bucket_partial<TX, CG, SM>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+                         (int)smem);                                                                          \
+    RB_KLAUNCH sparse_bucket_partial<TX, CG, SM><<<dim3(ctas, cgroups), kThreads, smem, st>>>(                \
+        n, ncols, X, ldx, row0, seed, k, s, (double*)ws);                                                     \
+  } while (0)
+  if (n > 0) {
+    if (s <= 4) RB_SB(4);
+    else if (s <= 8) RB_SB(8);
+    else RB_SB(16);
+  }
+#undef RB_SB
   const int64_t tot = (int64_t)k * ncols;
   RB_KLAUNCH reduce_splits<<<ceil_div(tot, 256), 256, 0, st>>>((double*)ws, n > 0 ? ctas : 0, k, ncols, 1.0, out, ldo,
                                                     accumulate);

@@ -430,10 +430,84 @@ int gemm_f64(int tA, int tB, int m, int n, int k, double alpha, const double* A,
   return dgemm(tA, tB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, st);
 }
 
+// Tall-skinny cross product out = A^T B for p, q <= 8 (the l2 stage's
+// Q'^T Q' at block width 4 / 8): the split-K tile kernel
+// would multiply a 128 x 16 register tile of mostly padding per row.  Here
+// a thread keeps the p x q products of its rows in registers, a CTA reduces
+// them in a fixed order and writes one partial; the partials are summed in
+// CTA order (deterministic).  HBM-bound: (p + q) s bytes per row.
+template <typename TA, typename TB, int PB>
+__global__ void __launch_bounds__(kThreads)
+cross_small_partial(int64_t n, int p, int q, const TA* __restrict__ A, int64_t lda, const TB* __restrict__ B,
+                    int64_t ldb, int64_t rows_per_cta, double* __restrict__ ws) {
+  __shared__ double red[kThreads / 32][PB * PB];
+  double acc[PB][PB];
+#pragma unroll
+  for (int a = 0; a < PB; ++a)
+#pragma unroll
+    for (int b = 0; b < PB; ++b) acc[a][b] = 0.0;
+  const int64_t beg = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t end = min(n, beg + rows_per_cta);
+  for (int64_t i = beg + threadIdx.x; i < end; i += kThreads) {
+    double x[PB], y[PB];
+#pragma unroll
+    for (int a = 0; a < PB; ++a) x[a] = a < p ? (double)A[i + (int64_t)a * lda] : 0.0;
+#pragma unroll
+    for (int b = 0; b < PB; ++b) y[b] = b < q ? (double)B[i + (int64_t)b * ldb] : 0.0;
+#pragma unroll
+    for (int a = 0; a < PB; ++a)
+#pragma unroll
+      for (int b = 0; b < PB; ++b) acc[a][b] = fma(x[a], y[b], acc[a][b]);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int a = 0; a < PB; ++a)
+#pragma unroll
+    for (int b = 0; b < PB; ++b) {
+      const double v = warp_sum(acc[a][b]);
+      if (lane == 0) red[warp][a * PB + b] = v;
+    }
+  __syncthreads();
+  for (int e = threadIdx.x; e < p * q; e += kThreads) {
+    const int a = e % p, b = e / p;
+    double v = 0.0;
+    for (int w = 0; w < kThreads / 32; ++w) v += red[w][a * PB + b];
+    ws[(int64_t)blockIdx.x * p * q + e] = v;  // column-major p x q partial
+  }
+}
+
+template <typename TA, typename TB>
+int cross_small(int64_t n, int p, int q, const TA* A, int64_t lda, const TB* B, int64_t ldb, double beta,
+                double* out, int64_t ldo, void* ws, size_t wsb, cudaStream_t st) {
+  const size_t per = (size_t)p * q * sizeof(double);
+  int ctas = (int)std::max<int64_t>(1, std::min<int64_t>((n + 4095) / 4096, 4 * sm_count()));
+  if ((size_t)ctas * per > wsb) ctas = (int)std::max<size_t>(1, wsb / per);
+  RB_REQUIRE(ws && (size_t)ctas * per <= wsb, "rb_cross: workspace too small");
+  const int64_t rpc = (n + ctas - 1) / ctas;
+  if (n > 0) {
+    if (p <= 4 && q <= 4)
+      RB_KLAUNCH cross_small_partial<TA, TB, 4><<<ctas, kThreads, 0, st>>>(n, p, q, A, lda, B, ldb, rpc, (double*)ws);
+    else
+      RB_KLAUNCH cross_small_partial<TA, TB, 8><<<ctas, kThreads, 0, st>>>(n, p, q, A, lda, B, ldb, rpc, (double*)ws);
+  }
+  RB_KLAUNCH gemm_epilogue<<<ceil_div((int64_t)p * q, 256), 256, 0, st>>>((double*)ws, n > 0 ? ctas : 0, p, q, 1.0,
+                                                                       beta, out, ldo);
+  return check_launch("rb_cross (small)");
+}
+
 int cross(int ad, int bd, int64_t n, int p, int q, const void* A, int64_t lda, const void* B, int64_t ldb,
           double* out, int64_t ldo, int acc, void* ws, size_t wsb, cudaStream_t st) {
   RB_REQUIRE(n >= 0 && p >= 1 && q >= 1 && out && ldo >= p, "rb_cross: bad args");
   const double beta = acc ? 1.0 : 0.0;
+  if (p <= 8 && q <= 8) {
+    if (ad == RB_F32 && bd == RB_F32)
+      return cross_small<float, float>(n, p, q, (const float*)A, lda, (const float*)B, ldb, beta, out, ldo, ws, wsb, st);
+    if (ad == RB_F32)
+      return cross_small<float, double>(n, p, q, (const float*)A, lda, (const double*)B, ldb, beta, out, ldo, ws, wsb, st);
+    if (bd == RB_F32)
+      return cross_small<double, float>(n, p, q, (const double*)A, lda, (const float*)B, ldb, beta, out, ldo, ws, wsb, st);
+    return cross_small<double, double>(n, p, q, (const double*)A, lda, (const double*)B, ldb, beta, out, ldo, ws, wsb, st);
+  }
   if (ad == RB_F32 && bd == RB_F32)
     return gemm_t<float, float>(1, 0, p, q, n, 1.0, (const float*)A, lda, (const float*)B, ldb, beta, out, ldo, ws, wsb, st);
   if (ad == RB_F32)

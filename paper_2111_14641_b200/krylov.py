@@ -207,33 +207,53 @@ def block_gmres(A: LinearOperator, B, theta, p: int, restarts: int = 1, cfg=None
             pair = (rep.delta, rep.delta_tilde)
             Hf = sweep.R[:c, mp:c]
             Rf = sweep.R[:c, :mp]
-            U_best, rel_best = None, None
+            # Every inner iterate j = 1 .. q-1 (plus the breakdown candidate)
+            # of krylov.py:229-262, evaluated in batches: the small LS
+            # solves first, then ONE pass over the basis for all corrections
+            # U_j = Q[:, :j mp] Z_j (a block upper-triangular right factor),
+            # one operator apply per candidate for the true residual, and one
+            # basis Gram for the cond(Q[:, :rows]) history -- one host read
+            # for all of them.
+            cands = []  # (width of Q used, Z, rows of the cond basis)
             for j in range(1, q):
                 rows = (j + 1) * mp
-                Z = _ls_qr_dev(Hf[:rows, :j * mp], Rf[:rows, :])
-                Uj = D.empty_cm(n_local, mp, torch.float64, dev)
-                D.gemm(0, 0, 1.0, sweep.Q[:, :j * mp], Z, 0.0, Uj)
-                rel = rel_residual(X + Uj)
-                it += 1
-                history.append((it, rel))
-                conds.append(_cond2_dev(sweep.Q[:, :rows], comm))
-                certs.append(pair)
-                if rel_best is None or rel <= rel_best:
-                    U_best, rel_best = Uj, rel
+                cands.append((j * mp, _ls_qr_dev(Hf[:rows, :j * mp], Rf[:rows, :]), rows))
             if bk:
                 PA = D.empty_cm(theta.k, c - mp + mp, torch.float64, dev)
                 PA[:, :c - mp].copy_(sweep.P[:, mp:c])
                 PA[:, c - mp:].copy_(sweep.pending_P.tensor)
-                Z = _ls_qr_dev(PA, sweep.P[:, :mp])
-                Uj = D.empty_cm(n_local, mp, torch.float64, dev)
-                D.gemm(0, 0, 1.0, sweep.Q[:, :c], Z, 0.0, Uj)
-                rel = rel_residual(X + Uj)
-                it += 1
-                history.append((it, rel))
-                conds.append(_cond2_dev(sweep.Q[:, :c], comm))
-                certs.append(pair)
-                if rel_best is None or rel <= rel_best:
-                    U_best, rel_best = Uj, rel
+                cands.append((c, _ls_qr_dev(PA, sweep.P[:, :mp]), c))
+            U_best, rel_best = None, None
+            if cands:
+                wmax = max(w for w, _, _ in cands)
+                Zb = D.zeros_cm(wmax, mp * len(cands), torch.float64, dev)
+                for t, (w, Z, _) in enumerate(cands):
+                    Zb[:w, t * mp:(t + 1) * mp].copy_(Z)
+                U = D.empty_cm(n_local, mp * len(cands), torch.float64, dev)
+                D.gemm(0, 0, 1.0, sweep.Q[:, :wmax], Zb, 0.0, U)
+                res2 = torch.empty(len(cands), mp, dtype=torch.float64, device=dev)
+                for t in range(len(cands)):
+                    Rr = Bd - A._apply_dev(D.to_cm(X + U[:, t * mp:(t + 1) * mp]), torch.float64)
+                    res2[t] = (Rr * Rr).sum(0)
+                comm.allreduce_(res2)
+                rels = (res2.sqrt() / bn).amax(1).cpu().tolist()
+                # ONE Gram of the widest basis (a single pass over Q): every
+                # cond(Q[:, :rows]) is that of a leading principal block
+                rmax = max(r for _, _, r in cands)
+                G = D.empty_cm(rmax, rmax, torch.float64, dev)
+                D.gemm(1, 0, 1.0, sweep.Q[:, :rmax], sweep.Q[:, :rmax], 0.0, G)
+                comm.allreduce_(G)
+                Gh = G.cpu().numpy()
+                Gh = np.triu(Gh) + np.triu(Gh, 1).T
+                for t, (w, Z, r) in enumerate(cands):
+                    it += 1
+                    history.append((it, rels[t]))
+                    ev = np.linalg.eigvalsh(Gh[:r, :r])
+                    conds.append(float("inf") if ev.size == 0 or ev[0] <= 0.0
+                                 else float(math.sqrt(ev[-1] / ev[0])))
+                    certs.append(pair)
+                    if rel_best is None or rels[t] <= rel_best:
+                        U_best, rel_best = U[:, t * mp:(t + 1) * mp], rels[t]
             if U_best is not None:
                 X = D.to_cm(X + U_best)
             if bk:

@@ -122,6 +122,8 @@ class DeviceConfig:
                       n x m buffer that lets the C5 shard (2^24 x 1024 fp32
                       plus its 2^24 x 2048 gaussian table) fit one GPU.  W
                       is destroyed; failures raise at the failing block.
+    coarse_shadow     binary64 Q with binary32 Step 3: keep a binary32 copy
+                      of Q for the projection (same bits, half the bytes).
     """
 
     device: object = None
@@ -130,6 +132,7 @@ class DeviceConfig:
     comm: Comm = None
     shard: RowShard = None
     overwrite_w: bool = False
+    coarse_shadow: bool = True
 
 
 @dataclass(frozen=True)
@@ -369,6 +372,13 @@ class RbgsSweep:
             self.Q = _q_storage
         else:
             self.Q = D.zeros_cm(self.n_local, m, self.q_dtype, dev)
+        # binary64 Q with binary32 projections (Arnoldi: the operator reads
+        # the binary64 basis): keep a binary32 shadow -- exactly the
+        # Q.astype(float32) the reference's coarse gemm reads (kernels.py:192)
+        # -- so Step 3 streams half the bytes through the staged kernel
+        self.Q32 = None
+        if self.q_dtype == torch.float64 and self.compute == F32 and dc.coarse_shadow:
+            self.Q32 = D.zeros_cm(self.n_local, m, torch.float32, dev)
         self.S = D.zeros_cm(k, m, torch.float64, dev)
         self.P = D.zeros_cm(k, m, torch.float64, dev)
         self.R = D.zeros_cm(m, m, torch.float64, dev)
@@ -661,7 +671,13 @@ class RbgsSweep:
             X = scr.X[:c, :w]
             self._solve_ls(self.S[:, :c], Pi, X)
             self.R[:c, j0:j1].copy_(X)
-            D.project(self.Q[:, :c], X, W, slot, self.compute, self.order, norms[0:2])
+            if self.Q32 is not None:
+                # Q' in binary32 into the (not yet committed) shadow slot,
+                # then widened exactly into the binary64 slot
+                D.project(self.Q32[:, :c], X, W, self.Q32[:, j0:j1], self.compute, self.order, norms[0:2])
+                D.convert(self.Q32[:, j0:j1], slot)
+            else:
+                D.project(self.Q[:, :c], X, W, slot, self.compute, self.order, norms[0:2])
             Qp = slot
             if Wn is not None and self._next_P is None and self._fusable(slot, Wn):
                 sp_given = scr.Sp[:, :w]
@@ -703,6 +719,8 @@ class RbgsSweep:
         return j0, j1
 
     def _commit_block(self, j0, j1, Pi, Si, Rii):
+        if self.Q32 is not None:
+            D.convert(self.Q[:, j0:j1], self.Q32[:, j0:j1])
         self.S[:, j0:j1].copy_(Si)
         self.P[:, j0:j1].copy_(Pi)
         self.R[j0:j1, j0:j1].copy_(Rii)
