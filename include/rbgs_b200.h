@@ -111,6 +111,18 @@ int rb_sketch_sparse_sign(int x_dtype, int64_t n, int ncols, const void* X, int6
                           int64_t row0, uint64_t seed, int k, int nnz,
                           double* out, int64_t ldo, int accumulate,
                           void* ws, size_t ws_bytes, void* stream);
+/* sparse_sign kind, table path: pre-bucketed per 1024-row tile (built once
+ * per operator shard by rb_sparse_sign_table: offs int32[ntiles][k+1],
+ * lists uint16[ntiles][1024 * min(nnz, k)], ntiles = ceil(nrows / 1024));
+ * the per-call sketch streams X and the table with a fixed summation
+ * order.  Same operator as rb_sketch_sparse_sign (no reference
+ * counterpart: the kind is a north-star addition). */
+int rb_sparse_sign_table(uint64_t seed, int k, int nnz, int64_t row0, int64_t nrows,
+                         int32_t* offs, uint16_t* lists, void* stream);
+int rb_sketch_sparse_sign_tab(int x_dtype, int64_t n, int ncols, const void* X, int64_t ldx,
+                              const int32_t* offs, const uint16_t* lists, int k, int nnz,
+                              double* out, int64_t ldo, int accumulate,
+                              void* ws, size_t ws_bytes, void* stream);
 /* rademacher kind (sketching.py:151-155): k x n sign bits (row r at
  * bits + r * ldb words, bit i set <=> sign -1), out = scale * S @ X. */
 int rb_sketch_signs(int x_dtype, int64_t n, int ncols, const void* X, int64_t ldx,

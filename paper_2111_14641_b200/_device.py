@@ -175,14 +175,32 @@ def sketch_srht(X, row0, n_pad, bits, sample, k, scale, out, accumulate=False):
     _t1(e0, "sketch_srht", n * cols * X.element_size())
 
 
-def sketch_sparse_sign(X, row0, seed, k, nnz, out, accumulate=False):
+def sketch_sparse_sign(X, row0, seed, k, nnz, out, accumulate=False, table=None):
+    """table: (offs, lists) from sparse_sign_table for THIS row range (the
+    per-call path then streams X and the table; else rows are hashed)."""
     n, cols = X.shape
     ws, wsb = _ws(n, cols, k, X.device)
     e0 = _t0()
-    call("rb_sketch_sparse_sign", dtype_code(X), n, cols, ptr(X), ld(X), row0,
-         ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), k, nnz, ptr(out), ld(out), int(accumulate), ws, wsb,
-         st(X.device))
+    if table is not None:
+        offs, lists = table
+        call("rb_sketch_sparse_sign_tab", dtype_code(X), n, cols, ptr(X), ld(X), ptr(offs), ptr(lists), k, nnz,
+             ptr(out), ld(out), int(accumulate), ws, wsb, st(X.device))
+    else:
+        call("rb_sketch_sparse_sign", dtype_code(X), n, cols, ptr(X), ld(X), row0,
+             ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), k, nnz, ptr(out), ld(out), int(accumulate), ws, wsb,
+             st(X.device))
     _t1(e0, "sketch_sparse_sign", n * cols * X.element_size())
+
+
+def sparse_sign_table(seed, k, nnz, row0, nrows, device):
+    """Pre-bucketed sparse-sign table of rows row0 .. row0 + nrows - 1."""
+    s = min(nnz, k)
+    ntiles = -(-nrows // 1024)
+    offs = torch.empty(max(ntiles, 1) * (k + 1), dtype=torch.int32, device=device)
+    lists = torch.empty(max(ntiles, 1) * 1024 * s, dtype=torch.int16, device=device)
+    call("rb_sparse_sign_table", ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), k, nnz, row0, nrows, ptr(offs),
+         ptr(lists), st(device))
+    return offs, lists
 
 
 def sketch_signs(X, bits, ldb, k, scale, out, accumulate=False):

@@ -38,6 +38,8 @@ SIGNATURES = {
                             _p, _sz, _p],
     "rb_sketch_srht": [_i, _i64, _i, _p, _i64, _i64, _i64, _p, _p, _i, _d, _p, _i64, _i, _p, _sz, _p],
     "rb_sketch_sparse_sign": [_i, _i64, _i, _p, _i64, _i64, _u64, _i, _i, _p, _i64, _i, _p, _sz, _p],
+    "rb_sparse_sign_table": [_u64, _i, _i, _i64, _i64, _p, _p, _p],
+    "rb_sketch_sparse_sign_tab": [_i, _i64, _i, _p, _i64, _p, _p, _i, _i, _p, _i64, _i, _p, _sz, _p],
     "rb_sketch_signs": [_i, _i64, _i, _p, _i64, _p, _i64, _i, _d, _p, _i64, _i, _p, _sz, _p],
     "rb_trsm_right": [_i, _i, _i64, _i, _p, _i64, _p, _i64, _p, _i64, _p],
     "rb_gemm_f64": [_i, _i, _i, _i, _i, _d, _p, _i64, _p, _i64, _d, _p, _i64, _p, _sz, _p],

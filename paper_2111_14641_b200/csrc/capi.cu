@@ -53,6 +53,9 @@ int sketch_srht(int, int64_t, int, const void*, int64_t, int64_t, int64_t, const
                 double, double*, int64_t, int, void*, size_t, cudaStream_t);
 int sketch_sparse_sign(int, int64_t, int, const void*, int64_t, int64_t, uint64_t, int, int, double*, int64_t, int,
                        void*, size_t, cudaStream_t);
+int sparse_sign_table(uint64_t, int, int, int64_t, int64_t, int32_t*, uint16_t*, cudaStream_t);
+int sketch_sparse_sign_tab(int, int64_t, int, const void*, int64_t, const int32_t*, const uint16_t*, int, int, double*,
+                           int64_t, int, void*, size_t, cudaStream_t);
 int trsm_right(int, int, int64_t, int, const void*, int64_t, const double*, int64_t, void*, int64_t, cudaStream_t);
 int gemm_f64(int, int, int, int, int, double, const double*, int64_t, const double*, int64_t, double, double*,
              int64_t, void*, size_t, cudaStream_t);
@@ -130,6 +133,17 @@ int rb_sketch_srht(int xd, int64_t n, int ncols, const void* X, int64_t ldx, int
 int rb_sketch_sparse_sign(int xd, int64_t n, int ncols, const void* X, int64_t ldx, int64_t row0, uint64_t seed,
                           int k, int nnz, double* out, int64_t ldo, int acc, void* ws, size_t wsb, void* s) {
   return rb::sketch_sparse_sign(xd, n, ncols, X, ldx, row0, seed, k, nnz, out, ldo, acc, ws, wsb, as_stream(s));
+}
+
+int rb_sparse_sign_table(uint64_t seed, int k, int nnz, int64_t row0, int64_t nrows, int32_t* offs, uint16_t* lists,
+                         void* s) {
+  return rb::sparse_sign_table(seed, k, nnz, row0, nrows, offs, lists, as_stream(s));
+}
+
+int rb_sketch_sparse_sign_tab(int xd, int64_t n, int ncols, const void* X, int64_t ldx, const int32_t* offs,
+                              const uint16_t* lists, int k, int nnz, double* out, int64_t ldo, int acc, void* ws,
+                              size_t wsb, void* s) {
+  return rb::sketch_sparse_sign_tab(xd, n, ncols, X, ldx, offs, lists, k, nnz, out, ldo, acc, ws, wsb, as_stream(s));
 }
 
 int rb_sketch_signs(int xd, int64_t n, int ncols, const void* X, int64_t ldx, const uint32_t* bits, int64_t ldb,

@@ -645,6 +645,197 @@ size_t sparse_smem(int k, int s) {
          (size_t)kST * s * sizeof(uint32_t);
 }
 
+// ---- pre-bucketed table (built once per operator shard) --------------------
+// Per tile of kST local rows: offs[k + 1] (int32 bucket starts) and the
+// tile's s * rows entries (uint16: local row << 1 | negative sign) sorted by
+// sketch row, then by local row -- the summation order of every sketch is
+// fixed (deterministic) and no hashing or atomics remain on the per-call
+// path, which just streams X, the lists and the offsets.
+template <int SMAX>
+__global__ void __launch_bounds__(kThreads)
+sparse_table_build(int64_t nrows, int64_t row0, uint64_t seed, int k, int s, int32_t* __restrict__ offs,
+                   uint16_t* __restrict__ lists) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int* cnt = reinterpret_cast<int*>(smem_raw);  // [k]
+  int* cur = cnt + k;                           // [k]
+  uint16_t* lst = reinterpret_cast<uint16_t*>(cur + k);  // [kST * s]
+  __shared__ int wsum[kThreads / 32];
+  const int64_t tile = blockIdx.x;
+  const int64_t base = tile * kST;
+  for (int e = threadIdx.x; e < k; e += kThreads) cnt[e] = 0;
+  __syncthreads();
+  int tr[kSRPT][SMAX];
+  bool live[kSRPT];
+#pragma unroll
+  for (int u = 0; u < kSRPT; ++u) {
+    const int64_t i = base + threadIdx.x + u * kThreads;
+    live[u] = i < nrows;
+    if (live[u]) {
+      sparse_sign_targets<SMAX>((uint64_t)(row0 + i), seed, k, s, tr[u]);
+#pragma unroll
+      for (int q = 0; q < SMAX; ++q)
+        if (q < s) atomicAdd(&cnt[tr[u][q] >> 1], 1);
+    }
+  }
+  __syncthreads();
+  const int per = (k + kThreads - 1) / kThreads;
+  int loc = 0;
+  for (int j = 0; j < per; ++j) {
+    const int r = threadIdx.x * per + j;
+    if (r < k) loc += cnt[r];
+  }
+  int incl = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((threadIdx.x & 31) >= o) incl += v;
+  }
+  if ((threadIdx.x & 31) == 31) wsum[threadIdx.x >> 5] = incl;
+  __syncthreads();
+  int off = incl - loc;
+  for (int w = 0; w < (threadIdx.x >> 5); ++w) off += wsum[w];
+  int32_t* to = offs + tile * (int64_t)(k + 1);
+  for (int j = 0; j < per; ++j) {
+    const int r = threadIdx.x * per + j;
+    if (r < k) {
+      cur[r] = off;
+      to[r] = off;
+      off += cnt[r];
+    }
+  }
+  if (threadIdx.x == kThreads - 1) to[k] = off;  // last thread's running end = total
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kSRPT; ++u) {
+    if (!live[u]) continue;
+    const int il = threadIdx.x + u * kThreads;
+#pragma unroll
+    for (int q = 0; q < SMAX; ++q)
+      if (q < s) lst[atomicAdd(&cur[tr[u][q] >> 1], 1)] = (uint16_t)((il << 1) | (tr[u][q] & 1));
+  }
+  __syncthreads();
+  // deterministic order inside each bucket: insertion sort by local row
+  for (int r = threadIdx.x; r < k; r += kThreads) {
+    const int e1 = cur[r], e0 = e1 - cnt[r];
+    for (int a = e0 + 1; a < e1; ++a) {
+      const uint16_t v = lst[a];
+      int b = a - 1;
+      while (b >= e0 && lst[b] > v) {
+        lst[b + 1] = lst[b];
+        --b;
+      }
+      lst[b + 1] = v;
+    }
+  }
+  __syncthreads();
+  uint16_t* tl = lists + tile * (int64_t)kST * s;
+  const int tot = (int)min((int64_t)kST, nrows - base) * s;
+  for (int e = threadIdx.x; e < tot; e += kThreads) tl[e] = lst[e];
+}
+
+template <typename TX, int CG>
+__global__ void __launch_bounds__(kThreads)
+sparse_tab_partial(int64_t n, int ncols, const TX* __restrict__ X, int64_t ldx, const int32_t* __restrict__ offs,
+                   const uint16_t* __restrict__ lists, int k, int s, double* __restrict__ ws) {
+  // x staged column-major (sx[c][il]): random-row reads of one column hit
+  // ~distinct banks; the next tile's X, list and offsets are prefetched
+  // into registers while the current tile is summed
+  constexpr int XPT = kST / kThreads;  // rows per thread per column
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* sx = reinterpret_cast<double*>(smem_raw);          // [CG][kST]
+  double* sacc = sx + kST * CG;                               // [k][CG]
+  int* so = reinterpret_cast<int*>(sacc + (size_t)k * CG);    // [k + 1]
+  uint16_t* sl = reinterpret_cast<uint16_t*>(so + ((k + 1 + 7) & ~7));  // [kST * s], 16-B aligned
+  const int c0 = blockIdx.y * CG;
+  const int cc = min(CG, ncols - c0);
+  const double inv = 1.0 / sqrt((double)s);
+  for (int e = threadIdx.x; e < k * CG; e += kThreads) sacc[e] = 0.0;
+  const int64_t ntiles = (n + kST - 1) / kST;
+  const int LV = (kST * s / 8 + kThreads - 1) / kThreads;  // uint4 of list per thread (<= 8)
+  TX px[CG][XPT];  // raw loads: consumed (scaled) only at the smem store
+  uint4 pl[8];
+  auto fetch = [&](int64_t tile) {
+    const int64_t base = tile * kST;
+#pragma unroll
+    for (int c = 0; c < CG; ++c)
+#pragma unroll
+      for (int u = 0; u < XPT; ++u) {
+        const int64_t i = base + threadIdx.x + u * kThreads;
+        px[c][u] = (c < cc && i < n) ? X[i + (int64_t)(c0 + c) * ldx] : TX(0);
+      }
+    const uint4* tl = reinterpret_cast<const uint4*>(lists + tile * (int64_t)kST * s);
+    const int rows = (int)min((int64_t)kST, n - base);
+    const int vec = (rows * s + 7) / 8;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u < LV) {
+        const int e = threadIdx.x + u * kThreads;
+        pl[u] = e < vec ? tl[e] : make_uint4(0, 0, 0, 0);
+      }
+  };
+  int64_t tile = blockIdx.x;
+  if (tile < ntiles) fetch(tile);
+  for (; tile < ntiles; tile += gridDim.x) {
+    __syncthreads();  // previous tile consumed
+#pragma unroll
+    for (int c = 0; c < CG; ++c)
+#pragma unroll
+      for (int u = 0; u < XPT; ++u) sx[c * kST + threadIdx.x + u * kThreads] = (double)px[c][u] * inv;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (u < LV && threadIdx.x + u * kThreads < kST * s / 8)
+        reinterpret_cast<uint4*>(sl)[threadIdx.x + u * kThreads] = pl[u];
+    for (int e = threadIdx.x; e <= k; e += kThreads) so[e] = offs[tile * (int64_t)(k + 1) + e];
+    __syncthreads();
+    if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);  // in flight during the sums
+    for (int r = threadIdx.x; r < k; r += kThreads) {
+      const int e0 = so[r], e1 = so[r + 1];
+      double acc[CG];
+#pragma unroll
+      for (int c = 0; c < CG; ++c) acc[c] = sacc[r * CG + c];
+      for (int e = e0; e < e1; ++e) {
+        const uint32_t v = sl[e];
+        const int il = (int)(v >> 1);
+        const double sg = (v & 1u) ? -1.0 : 1.0;
+#pragma unroll
+        for (int c = 0; c < CG; ++c) acc[c] = fma(sg, sx[c * kST + il], acc[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < CG; ++c) sacc[r * CG + c] = acc[c];
+    }
+  }
+  __syncthreads();
+  double* dst = ws + (int64_t)blockIdx.x * k * ncols;
+  for (int e = threadIdx.x; e < k * cc; e += kThreads) {
+    const int r = e % k, c = e / k;
+    dst[r + (int64_t)(c0 + c) * k] = sacc[r * CG + c];
+  }
+}
+
+template <typename TX>
+int sparse_sketch_tab(int64_t n, int ncols, const TX* X, int64_t ldx, const int32_t* offs, const uint16_t* lists,
+                      int k, int s, double* out, int64_t ldo, int accumulate, void* ws, size_t ws_bytes,
+                      cudaStream_t st) {
+  constexpr int CG = 4;
+  const size_t smem = (size_t)kST * CG * sizeof(double) + (size_t)k * CG * sizeof(double) +
+                      (size_t)((k + 1 + 7) & ~7) * sizeof(int) + (size_t)kST * s * sizeof(uint16_t) + 16;
+  RB_REQUIRE(smem <= 200 * 1024, "sparse_sign: k too large (%d)", k);
+  const int cgroups = ceil_div(ncols, CG);
+  const size_t per = (size_t)k * ncols * sizeof(double);
+  const int64_t ntiles = (n + kST - 1) / kST;
+  int ctas = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (2 * sm_count() + cgroups - 1) / cgroups));
+  if ((size_t)ctas * per > ws_bytes) ctas = (int)std::max<size_t>(1, ws_bytes / per);
+  RB_REQUIRE(ws && (size_t)ctas * per <= ws_bytes, "sparse_sign: workspace too small");
+  cudaFuncSetAttribute(sparse_tab_partial<TX, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (n > 0)
+    RB_KLAUNCH sparse_tab_partial<TX, CG><<<dim3(ctas, cgroups), kThreads, smem, st>>>(n, ncols, X, ldx, offs, lists,
+                                                                                     k, s, (double*)ws);
+  const int64_t tot = (int64_t)k * ncols;
+  RB_KLAUNCH reduce_splits<<<ceil_div(tot, 256), 256, 0, st>>>((double*)ws, n > 0 ? ctas : 0, k, ncols, 1.0, out, ldo,
+                                                    accumulate);
+  return check_launch("sparse_sign sketch (table)");
+}
+
 template <typename TX>
 int sparse_sketch(int64_t n, int ncols, const TX* X, int64_t ldx, int64_t row0, uint64_t seed,
                   int k, int nnz, double* out, int64_t ldo, int accumulate, void* ws,
@@ -691,6 +882,43 @@ int gaussian_fill(uint64_t seed, int k, int64_t row0, int64_t nrows, uint8_t* th
   dim3 grid(ceil_div(nrows, 256), (k + 3) / 4);
   RB_KLAUNCH gaussian_fill_kernel<<<grid, 256, 0, st>>>(seed, k, row0, nrows, theta, ldt);
   return check_launch("rb_gaussian_fill");
+}
+
+// Pre-bucketed sparse-sign table for local rows [0, nrows) of a shard that
+// starts at global row row0: offs int32[ntiles][k + 1], lists
+// uint16[ntiles][1024 s], ntiles = ceil(nrows / 1024).
+int sparse_sign_table(uint64_t seed, int k, int nnz, int64_t row0, int64_t nrows, int32_t* offs, uint16_t* lists,
+                      cudaStream_t st) {
+  const int s = std::min(nnz, k);
+  RB_REQUIRE(s >= 1 && s <= 16 && k >= 1 && k < 32768 && nrows >= 0 && (nrows == 0 || (offs && lists)),
+             "rb_sparse_sign_table: bad args");
+  const int64_t ntiles = (nrows + kST - 1) / kST;
+  const size_t smem = 2 * (size_t)k * sizeof(int) + (size_t)kST * s * sizeof(uint16_t) + 16;
+  RB_REQUIRE(smem <= 200 * 1024, "rb_sparse_sign_table: k too large");
+  if (ntiles == 0) return check_launch("rb_sparse_sign_table");
+#define RB_TB(SM)                                                                                         \
+  do {                                                                                                    \
+    cudaFuncSetAttribute(sparse_table_build<SM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    RB_KLAUNCH sparse_table_build<SM><<<(unsigned)ntiles, kThreads, smem, st>>>(nrows, row0, seed, k, s, offs, lists); \
+  } while (0)
+  if (s <= 4) RB_TB(4);
+  else if (s <= 8) RB_TB(8);
+  else RB_TB(16);
+#undef RB_TB
+  return check_launch("rb_sparse_sign_table");
+}
+
+int sketch_sparse_sign_tab(int xd, int64_t n, int ncols, const void* X, int64_t ldx, const int32_t* offs,
+                           const uint16_t* lists, int k, int nnz, double* out, int64_t ldo, int acc, void* ws,
+                           size_t wsb, cudaStream_t st) {
+  const int s = std::min(nnz, k);
+  RB_REQUIRE(n >= 0 && ncols >= 1 && k >= 1 && s >= 1 && s <= 16 && out && ldo >= k &&
+                 (n == 0 || (X && ldx >= n && offs && lists)),
+             "rb_sketch_sparse_sign_tab: bad args");
+  return xd == RB_F32 ? sparse_sketch_tab<float>(n, ncols, (const float*)X, ldx, offs, lists, k, s, out, ldo, acc, ws,
+                                                 wsb, st)
+                      : sparse_sketch_tab<double>(n, ncols, (const double*)X, ldx, offs, lists, k, s, out, ldo, acc,
+                                                  ws, wsb, st);
 }
 
 size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k);

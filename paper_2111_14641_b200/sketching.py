@@ -122,6 +122,9 @@ class SketchOperator:
             with torch.cuda.device(dev):
                 D.gaussian_fill(self.seed, self.k, row0, nrows, theta, ldt)
             tab = dict(theta=theta, ldt=ldt)
+        elif self.kind == "sparse_sign":
+            with torch.cuda.device(dev):
+                tab = dict(table=D.sparse_sign_table(self.seed, self.k, self.nnz, row0, nrows, dev))
         else:
             tab = {}
         cache[key] = tab
@@ -178,7 +181,9 @@ def sketch_into(theta: SketchOperator, X: torch.Tensor, out: torch.Tensor, row0:
         D.sketch_gaussian(X, tab["theta"], tab["ldt"], k, 1.0 / (GAUSS_GRID * math.sqrt(k)), out,
                           accumulate, GAUSS_MODE)
     else:
-        D.sketch_sparse_sign(X, row0, theta.seed, k, theta.nnz, out, accumulate)
+        # the pre-bucketed table of exactly this row range (cached on the
+        # operator; shards and whole-matrix calls each get their own)
+        D.sketch_sparse_sign(X, row0, theta.seed, k, theta.nnz, out, accumulate, table=tab["table"])
 
 
 def apply(theta: SketchOperator, X, device=None) -> Matrix:
