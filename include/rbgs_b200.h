@@ -147,6 +147,11 @@ int rb_gemm_f64(int transA, int transB, int m, int n, int k, double alpha,
 int rb_gemm_f32(int transA, int transB, int m, int n, int k, float alpha,
                 const float* A, int64_t lda, const float* B, int64_t ldb, float beta,
                 float* C, int64_t ldc, void* stream);
+/* Symmetric rank-k update, upper triangle: C = alpha A^T A + beta C for a
+ * tall binary64 A (k x n, C n x n; cuBLAS DSYRK) -- the basis Gram of the
+ * GMRES conditioning history (krylov.py:98-103, 247-257). */
+int rb_syrk_f64(int n, int64_t k, double alpha, const double* A, int64_t lda, double beta,
+                double* C, int64_t ldc, void* stream);
 /* Tall Gram / cross product: out (p x q fp64) = A^T B for n-row A (n x p)
  * and B (n x q), inputs f32 or f64, fp64 accumulation (fused l2 stage).  */
 int rb_cross(int a_dtype, int b_dtype, int64_t n, int p, int q, const void* A, int64_t lda,

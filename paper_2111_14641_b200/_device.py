@@ -235,6 +235,12 @@ def gemm32(tA, tB, alpha, A, B, beta, C):
          st(C.device))
 
 
+def syrk(A, C):
+    """Upper triangle of C = A^T A (binary64, cuBLAS DSYRK)."""
+    k, n = A.shape
+    call("rb_syrk_f64", n, k, 1.0, ptr(A), ld(A), 0.0, ptr(C), ld(C), st(C.device))
+
+
 def cross(A, B, out, accumulate=False):
     """out = A^T B for tall A (n x p), B (n x q)."""
     n, p = A.shape

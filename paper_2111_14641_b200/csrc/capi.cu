@@ -61,6 +61,7 @@ int gemm_f64(int, int, int, int, int, double, const double*, int64_t, const doub
              int64_t, void*, size_t, cudaStream_t);
 int cross(int, int, int64_t, int, int, const void*, int64_t, const void*, int64_t, double*, int64_t, int, void*,
           size_t, cudaStream_t);
+int syrk_f64(int, int64_t, double, const double*, int64_t, double, double*, int64_t, cudaStream_t);
 int gemm_f32(int, int, int, int, int, float, const float*, int64_t, const float*, int64_t, float, float*, int64_t,
              cudaStream_t);
 int potrf_upper(int, const double*, int64_t, double*, int64_t, int*, cudaStream_t);
@@ -164,6 +165,11 @@ int rb_gemm_f32(int tA, int tB, int m, int n, int k, float alpha, const float* A
 int rb_gemm_f64(int tA, int tB, int m, int n, int k, double alpha, const double* A, int64_t lda, const double* B,
                 int64_t ldb, double beta, double* C, int64_t ldc, void* ws, size_t wsb, void* s) {
   return rb::gemm_f64(tA, tB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, ws, wsb, as_stream(s));
+}
+
+int rb_syrk_f64(int n, int64_t k, double alpha, const double* A, int64_t lda, double beta, double* C, int64_t ldc,
+                void* s) {
+  return rb::syrk_f64(n, k, alpha, A, lda, beta, C, ldc, as_stream(s));
 }
 
 int rb_cross(int ad, int bd, int64_t n, int p, int q, const void* A, int64_t lda, const void* B, int64_t ldb,

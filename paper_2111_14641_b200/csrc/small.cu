@@ -407,6 +407,21 @@ int dgemm(int tA, int tB, int m, int n, int k, double alpha, const double* A, in
   return check_launch("dgemm");
 }
 
+int syrk_f64(int n, int64_t k, double alpha, const double* A, int64_t lda, double beta, double* C, int64_t ldc,
+             cudaStream_t st) {
+  RB_REQUIRE(n >= 0 && k >= 0 && k <= INT32_MAX && C && ldc >= std::max(n, 1) && (k == 0 || (A && lda >= k)),
+             "rb_syrk_f64: bad args");
+  if (n == 0) return RB_OK;
+  cublasHandle_t h = cublas_handle();
+  RB_REQUIRE(h, "cuBLAS handle creation failed");
+  cublasSetStream(h, st);
+  const cublasStatus_t s = cublasDsyrk(h, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, n, (int)k, &alpha, A,
+                                       (int)std::max<int64_t>(lda, 1), &beta, C, (int)ldc);
+  ++g_launches;
+  RB_REQUIRE(s == CUBLAS_STATUS_SUCCESS, "cublasDsyrk failed (%d)", (int)s);
+  return check_launch("syrk");
+}
+
 int gemm_f32(int tA, int tB, int m, int n, int k, float alpha, const float* A, int64_t lda, const float* B,
              int64_t ldb, float beta, float* C, int64_t ldc, cudaStream_t st) {
   RB_REQUIRE(m >= 0 && n >= 0 && k >= 0 && C && ldc >= std::max(m, 1), "rb_gemm_f32: bad args");

@@ -135,6 +135,33 @@ def _ls_qr_dev(M, T):
     return Z
 
 
+def _ls_nested_dev(Hf, Rf, q, mp):
+    """Z_j = argmin ||H[:(j+1)mp, :j mp] Z - R_first[:(j+1)mp]|| for every
+    j = 1 .. q-1 from ONE Householder QR of the widest block Hessenberg
+    matrix (krylov.py:229-233 solves each j separately): column l of H is
+    zero below row (l // mp + 2) mp, so the reflectors of the first j mp
+    columns -- hence the thin Q and R of the truncated problem -- are the
+    leading parts of the full factorization; Z_j = R[:j mp, :j mp]^{-1}
+    (Q^T R_first)[:j mp]."""
+    if q < 2:
+        return []
+    rows, w = q * mp, (q - 1) * mp
+    A = D.empty_cm(rows, w, torch.float64, Hf.device)
+    A.copy_(Hf[:rows, :w])
+    Rm = D.empty_cm(w, w, torch.float64, Hf.device)
+    D.geqrf(A, Rm)
+    QtT = D.empty_cm(w, mp, torch.float64, Hf.device)
+    D.gemm(1, 0, 1.0, A, Rf[:rows, :], 0.0, QtT)
+    info = torch.zeros(1, dtype=torch.int32, device=Hf.device)
+    out = []
+    for j in range(1, q):
+        Z = D.empty_cm(j * mp, mp, torch.float64, Hf.device)
+        Z.copy_(QtT[:j * mp])
+        D.trsm_left_upper(Rm[:j * mp, :j * mp], Z, info)
+        out.append(Z)
+    return out
+
+
 def _cond2_dev(Q, comm):
     """2-norm condition of the (row-sharded) basis from its Gram matrix."""
     q = Q.shape[1]
@@ -215,9 +242,8 @@ def block_gmres(A: LinearOperator, B, theta, p: int, restarts: int = 1, cfg=None
             # basis Gram for the cond(Q[:, :rows]) history -- one host read
             # for all of them.
             cands = []  # (width of Q used, Z, rows of the cond basis)
-            for j in range(1, q):
-                rows = (j + 1) * mp
-                cands.append((j * mp, _ls_qr_dev(Hf[:rows, :j * mp], Rf[:rows, :]), rows))
+            for j, Z in enumerate(_ls_nested_dev(Hf, Rf, q, mp), start=1):
+                cands.append((j * mp, Z, (j + 1) * mp))
             if bk:
                 PA = D.empty_cm(theta.k, c - mp + mp, torch.float64, dev)
                 PA[:, :c - mp].copy_(sweep.P[:, mp:c])
@@ -241,6 +267,8 @@ def block_gmres(A: LinearOperator, B, theta, p: int, restarts: int = 1, cfg=None
                 # cond(Q[:, :rows]) is that of a leading principal block
                 rmax = max(r for _, _, r in cands)
                 G = D.empty_cm(rmax, rmax, torch.float64, dev)
+                # full DGEMM: cuBLAS' DSYRK picks a 3x slower kernel for
+                # K = n_local ~ 1.7e7 (measured)
                 D.gemm(1, 0, 1.0, sweep.Q[:, :rmax], sweep.Q[:, :rmax], 0.0, G)
                 comm.allreduce_(G)
                 Gh = G.cpu().numpy()
