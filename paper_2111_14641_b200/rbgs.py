@@ -53,7 +53,7 @@ from .errors import (
 )
 from .kernels import COARSE, FINE, BlockPartition, Matrix, PrecisionSpec, as_array
 
-__all__ = ["RbgsConfig", "DeviceConfig", "BlockQR", "CertReport", "rbgs", "RbgsSweep", "certify",
+__all__ = ["RbgsConfig", "DeviceConfig", "BlockQR", "CertReport", "rbgs", "RbgsSweep", "RbgsPlan", "certify",
            "ls_richardson", "ls_bmgs_reorth", "ls_cg_normal", "ls_householder_direct",
            "interblock_rgs", "interblock_sketched_cholqr", "interblock_l2_cholqr", "parse_method",
            "cholesky_qr_postprocess", "certify_embedding", "save_blockqr", "load_blockqr",
@@ -807,6 +807,80 @@ class RbgsSweep:
 REPLAYS = 0  # one-shot factorizations replayed eagerly after a deferred-status failure
 
 
+def _deferrable(cfg) -> bool:
+    """Inter-block variants whose block step has no data-dependent host
+    branch (the l2 stage falls back on a Cholesky failure; RGS reads its
+    column norms), and no per-block certificate read."""
+    return parse_method(cfg.interblock)[0] == "sketched_cholqr" and not cfg.certify_blocks
+
+
+def _sweep_blocks(Wd, n, theta, cfg, dc, q_storage, deferred, events=None):
+    """The block loop of rbgs() (rbgs.py:417-421) on a device W."""
+    dev = Wd.device
+    sweep = RbgsSweep(n, theta, cfg, dc, _q_storage=q_storage)
+    if deferred:
+        sweep._defer_status()
+    off = cfg.partition.offsets()
+    for b in range(cfg.partition.num_blocks):
+        nxt = Wd[:, off[b + 1]:off[b + 2]] if b + 2 < len(off) else None
+        if events is not None:
+            stream = torch.cuda.current_stream(dev)
+            stream.wait_event(events[b])
+            if nxt is not None:
+                stream.wait_event(events[b + 1])
+        sweep.push_block(Wd[:, off[b]:off[b + 1]], lookahead=nxt)
+    return sweep
+
+
+class RbgsPlan:
+    """One-shot factorization of a FIXED device W, captured once as a CUDA
+    graph and replayed (device-path extension, no reference counterpart --
+    SURVEY.md 8(e): with the per-block stream time down to ~0.5 ms at 8
+    GPUs, launch latency and the host's launch rate bound the sweep).
+
+    W must be a column-major CUDA tensor; its CONTENTS may change between
+    replays, its storage may not.  The capture runs after one eager
+    factorization (tables, workspaces and library handles are created
+    outside the capture).  Each replay is the complete factorization --
+    every kernel of every block -- followed by the one host read of the
+    deferred block statuses and the final certification; if a block
+    failed, the factorization is re-run eagerly so the exception is the
+    reference's.  The returned BlockQR ALIASES the plan's buffers: the next
+    replay overwrites it (copy what must survive)."""
+
+    def __init__(self, W, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None):
+        require_cuda()
+        dc = device_cfg or DeviceConfig()
+        if not (isinstance(W, torch.Tensor) and W.is_cuda and W.dim() == 2 and D.is_cm(W)
+                and W.dtype in (torch.float32, torch.float64)):
+            raise ShapeError("RbgsPlan needs W as a column-major binary32/binary64 CUDA tensor")
+        if not _deferrable(cfg):
+            raise ValueError("RbgsPlan needs a sketched_cholqr inter-block variant without certify_blocks")
+        if dc.overwrite_w:
+            raise ValueError("RbgsPlan cannot overwrite its own input")
+        if cfg.partition.total_cols != W.shape[1]:
+            raise ShapeError(f"partition covers {cfg.partition.total_cols} cols, W has {W.shape[1]}")
+        self.W, self.theta, self.cfg, self.dc = W, theta, cfg, dc
+        self.n = theta.n if dc.shard is not None else W.shape[0]
+        dev = W.device
+        with torch.cuda.device(dev):
+            rbgs(W, theta, cfg, dc)  # warm-up outside the capture
+            torch.cuda.synchronize(dev)
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                self._sweep = _sweep_blocks(W, self.n, theta, cfg, dc, None, True)
+            torch.cuda.synchronize(dev)
+
+    def replay(self) -> BlockQR:
+        """Run the captured factorization on the current contents of W."""
+        self.graph.replay()
+        if not self._sweep._deferred_ok():
+            global REPLAYS
+            REPLAYS += 1
+            return rbgs(self.W, self.theta, self.cfg, self.dc, _eager=True)
+        return self._sweep.finish()
+
+
 def rbgs(W, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None, *, _eager: bool = False) -> BlockQR:
     """Factor W = QR with Q orthonormal in the sketched inner product
     (rbgs.py:410-421).  W: numpy / Matrix (uploaded once; binary32 arrays
@@ -859,24 +933,13 @@ def rbgs(W, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None, *, _eager: 
             raise ShapeError("overwrite_w needs W as a column-major CUDA tensor of Q's dtype")
     destroys_input = (q_storage is not None and isinstance(W_in, torch.Tensor) and W_in.is_cuda
                       and Wd.data_ptr() == W_in.data_ptr())
-    sweep = RbgsSweep(n, theta, cfg, dc, _q_storage=q_storage)
     # Per-block host round trips are only needed to raise at the failing
     # block; the one-shot driver defers them to one read at the end and, if
     # any block failed, replays the factorization eagerly so the exception
     # (type, message, block index) is exactly the reference's.
-    deferred = (not _eager and not destroys_input and sweep.inter[0] == "sketched_cholqr"
-                and not cfg.certify_blocks and os.environ.get("RB_EAGER_STATUS", "0") != "1")
-    if deferred:
-        sweep._defer_status()
-    off = cfg.partition.offsets()
-    for b in range(cfg.partition.num_blocks):
-        nxt = Wd[:, off[b + 1]:off[b + 2]] if b + 2 < len(off) else None
-        if events is not None:
-            stream = torch.cuda.current_stream(dev)
-            stream.wait_event(events[b])
-            if nxt is not None:
-                stream.wait_event(events[b + 1])
-        sweep.push_block(Wd[:, off[b]:off[b + 1]], lookahead=nxt)
+    deferred = (not _eager and not destroys_input and _deferrable(cfg)
+                and os.environ.get("RB_EAGER_STATUS", "0") != "1")
+    sweep = _sweep_blocks(Wd, n, theta, cfg, dc, q_storage, deferred, events)
     if deferred and not sweep._deferred_ok():
         global REPLAYS
         REPLAYS += 1

@@ -495,3 +495,34 @@ def test_sparse_sign_table_path_matches_hashed_path(pkg):
         c = torch.zeros_like(a)
         D.sketch_sparse_sign(X, row0, 11, k, nnz, c, table=tab)
         assert torch.equal(c * 2, b)
+
+
+def test_rbgs_plan_graph_replay_matches_eager(pkg):
+    """RbgsPlan (captured CUDA graph) == eager rbgs() bit for bit, follows
+    new contents of W, and raises the reference exception on a failing
+    block (eager re-run)."""
+    rbgs, sketching, D = pkg
+    from paper_2111_14641_b200.errors import DependentBlockError
+    from paper_2111_14641_b200.kernels import BlockPartition
+    import goldens as G
+
+    n, m, p, k = 20_000, 60, 12, 200
+    th = sketching.gaussian_operator(k, n, 3)
+    cfg = rbgs.RbgsConfig(partition=BlockPartition.uniform(m, p), interblock="sketched_cholqr(1)")
+    W1 = G.trig_family(n, m, 5).astype(np.float32)
+    W2 = (np.random.Generator(np.random.Philox(8)).standard_normal((n, m)) @ np.diag(np.logspace(0, -5, m)))
+    Wd = _dev(W1.astype(np.float64), torch.float32)
+    plan = rbgs.RbgsPlan(Wd, th, cfg)
+    for Wh in (W1, W2.astype(np.float32), W1):
+        Wd.copy_(torch.from_numpy(Wh.astype(np.float32)))
+        got = plan.replay()
+        want = rbgs.rbgs(Wh.astype(np.float32), th, cfg)
+        assert np.array_equal(got.R.data, want.R.data)
+        assert np.array_equal(got.Q.data, want.Q.data)
+        assert got.cert == want.cert
+    Wbad = W1.copy()
+    Wbad[:, 24:36] = 0.0
+    Wd.copy_(torch.from_numpy(Wbad))
+    with pytest.raises(DependentBlockError) as ei:
+        plan.replay()
+    assert ei.value.block == 3
