@@ -67,6 +67,44 @@ __global__ void __launch_bounds__(256, MINB) v1(int64_t n, int p, const float* B
     }
   }
 }
+
+// V2: dot form, G columns' chains interleaved (same per-column order, ILP G)
+template <int PB, int G, int MINB>
+__global__ void __launch_bounds__(256, MINB) v2(int64_t n, int p, const float* B, int64_t ldb, const double* __restrict__ Rg, int64_t ldr, float* Xo, int64_t ldx) {
+  constexpr int LD = ((PB + G - 1) / G) * G;  // row-major R, rows padded to a multiple of G
+  __shared__ __align__(16) double sR[PB * LD];
+  __shared__ double sInv[PB];
+  for (int e = threadIdx.x; e < LD * PB; e += blockDim.x) { const int j = e % LD, l = e / LD; sR[e] = (l < p && j < p && j >= l) ? Rg[l + (int64_t)j * ldr] : 0.0; }
+  __syncthreads();
+  for (int j = threadIdx.x; j < PB; j += blockDim.x) sInv[j] = j < p ? 1.0 / sR[j * LD + j] : 0.0;
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double x[PB];
+#pragma unroll
+  for (int j = 0; j < PB; ++j) x[j] = j < p ? (double)B[r + (int64_t)j * ldb] : 0.0;
+#pragma unroll
+  for (int j0 = 0; j0 < PB; j0 += G) {
+    // chains of columns j0 .. j0+G-1 over the finished x_l, l < j0
+#pragma unroll
+    for (int l = 0; l < j0; ++l) {
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        if (j0 + g < PB) x[j0 + g] = fma(-x[l], sR[l * LD + j0 + g], x[j0 + g]);
+    }
+    // finish the panel in order
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if (j0 + g < PB) {
+#pragma unroll
+        for (int h = 0; h < g; ++h) x[j0 + g] = fma(-x[j0 + h], sR[(j0 + h) * LD + j0 + g], x[j0 + g]);
+        x[j0 + g] = x[j0 + g] * sInv[j0 + g];
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < PB; ++j) if (j < p) Xo[r + (int64_t)j * ldx] = (float)x[j];
+}
 template <int PB>
 void run(int64_t n) {
   const int p = PB;
@@ -80,14 +118,17 @@ void run(int64_t n) {
   cudaMemcpy(B, hb.data(), n * p * 4, cudaMemcpyHostToDevice);
   int grid = (int)((n + 255) / 256);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  float ms[4];
-  for (int v = 0; v < 3; ++v) {
+  float ms[6];
+  for (int v = 0; v < 6; ++v) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(a);
       for (int i = 0; i < 5; ++i) {
         if (v == 0) v0<PB><<<grid, 256>>>(n, p, B, n, R, p, X0, n);
         else if (v == 1) v1<PB, 1><<<grid, 256>>>(n, p, B, n, R, p, X1, n);
-        else v1<PB, 2><<<grid, 256>>>(n, p, B, n, R, p, X1, n);
+        else if (v == 2) v1<PB, 2><<<grid, 256>>>(n, p, B, n, R, p, X1, n);
+        else if (v == 3) v2<PB, 4, 2><<<grid, 256>>>(n, p, B, n, R, p, X1, n);
+        else if (v == 4) v2<PB, 8, 2><<<grid, 256>>>(n, p, B, n, R, p, X1, n);
+        else v2<PB, 4, 1><<<grid, 256>>>(n, p, B, n, R, p, X1, n);
       }
       cudaEventRecord(b); cudaEventSynchronize(b);
       cudaEventElapsedTime(&ms[v], a, b); ms[v] /= 5;
@@ -97,7 +138,7 @@ void run(int64_t n) {
   cudaMemcpy(o0.data(), X0, n * p * 4, cudaMemcpyDeviceToHost);
   cudaMemcpy(o1.data(), X1, n * p * 4, cudaMemcpyDeviceToHost);
   int64_t diff = 0; for (int64_t i = 0; i < n * p; ++i) diff += memcmp(&o0[i], &o1[i], 4) != 0;
-  printf("{\"p\": %d, \"n\": %lld, \"v0_ms\": %.4f, \"v1_minb1_ms\": %.4f, \"v1_minb2_ms\": %.4f, \"bitdiff\": %lld, \"hbm_ms\": %.4f}\n", p, (long long)n, ms[0], ms[1], ms[2], (long long)diff, 2.0 * n * p * 4 / 6.5e12 * 1e3);
+  printf("{\"p\": %d, \"n\": %lld, \"v0_ms\": %.4f, \"v1_minb1_ms\": %.4f, \"v1_minb2_ms\": %.4f, \"v2_g4_ms\": %.4f, \"v2_g8_ms\": %.4f, \"v2_g4_minb1_ms\": %.4f, \"bitdiff_last\": %lld, \"hbm_ms\": %.4f}\n", p, (long long)n, ms[0], ms[1], ms[2], ms[3], ms[4], ms[5], (long long)diff, 2.0 * n * p * 4 / 6.5e12 * 1e3);
   cudaFree(B); cudaFree(X0); cudaFree(X1); cudaFree(R);
 }
 int main() {
