@@ -67,6 +67,17 @@ int rb_project(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t n
                const void* W, int64_t ldw, void* Qp, int64_t ldqp, double* norms2,
                void* ws, size_t ws_bytes, void* stream);
 
+/* Step 3 of block i with Step 5 of block i-1 fused in front (one-shot
+ * sweeps): Qf, the last pf columns of Q[:, :c] (= Q'_(i-1), in place),
+ * first becomes fl(Q'_(i-1) Rf^{-1}) (rbgs.py:281-283 -> kernels.py:250-270,
+ * right solve with the pf x pf upper Rf), then the projection runs on the
+ * updated Q.  Bitwise equal to rb_trsm_right(Qf -> Qf) + rb_project.     */
+int rb_project_trsm(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t n, int c, int p,
+                    const void* Q, int64_t ldq, const double* X, int64_t ldx,
+                    const void* W, int64_t ldw, void* Qp, int64_t ldqp, double* norms2,
+                    void* Qf, int64_t ldqf, const double* Rf, int64_t ldrf, int pf,
+                    void* ws, size_t ws_bytes, void* stream);
+
 /* ---- K1/K2  sketches (sketching.py:140-155 and the north-star kinds) -----
  * out (k x ncols, fp64, col-major, ld ldo) = Theta[:, row0:row0+n] @ X,
  * summed in fp64.  accumulate != 0 adds into out instead of overwriting.  */

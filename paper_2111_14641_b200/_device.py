@@ -137,6 +137,21 @@ def project(Q, X, W, Qp, compute, order, norms2=None):
         _t1(e0, "project", n * (c * qs + p * W.element_size() + p * Qp.element_size()), 2.0 * n * c * p)
 
 
+def project_trsm(Q, X, W, Qp, compute, order, norms2, Qf, Rf):
+    """Qf <- Qf Rf^{-1} (the previous block's Step-5 scaling, in place; Qf
+    must be the last columns of Q) fused in front of Qp = W - Q X."""
+    n, p = W.shape
+    c, pf = Q.shape[1], Qf.shape[1]
+    ws, wsb = _ws(n, p, 64, W.device)
+    e0 = _t0()
+    call("rb_project_trsm", dtype_code(Qp), dtype_code(W), compute, order, n, c, p, ptr(Q), ld(Q), ptr(X), ld(X),
+         ptr(W), ld(W), ptr(Qp), ld(Qp), ptr(norms2), ptr(Qf), ld(Qf), ptr(Rf), ld(Rf), pf, ws, wsb, st(W.device))
+    if e0 is not None:
+        qs = Q.element_size()
+        _t1(e0, "project", n * (c * qs + p * W.element_size() + p * Qp.element_size() + 2 * pf * qs),
+            2.0 * n * c * p)
+
+
 GAUSS_MODE = {"auto": 0, "fp64": 1, "tensor": 2}
 
 

@@ -32,6 +32,8 @@ SIGNATURES = {
     "rb_launch_count": [],
     "rb_workspace_bytes": [_i64, _i, _i],
     "rb_project": [_i, _i, _i, _i, _i64, _i, _i, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, _p, _sz, _p],
+    "rb_project_trsm": [_i, _i, _i, _i, _i64, _i, _i, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p,
+                        _p, _i64, _p, _i64, _i, _p, _sz, _p],
     "rb_gaussian_fill": [_u64, _i, _i64, _i64, _p, _i64, _p],
     "rb_sketch_gaussian": [_i, _i64, _i, _p, _i64, _p, _i64, _i, _d, _p, _i64, _i, _i, _p, _sz, _p],
     "rb_sketch_gaussian2": [_i, _p, _i64, _i, _i, _p, _i64, _i, _i64, _p, _i64, _i, _d, _p, _i64, _p, _i64, _i, _i,

@@ -41,6 +41,9 @@ int sm_count() {
 
 int project(int, int, int, int, int64_t, int, int, const void*, int64_t, const double*, int64_t, const void*, int64_t,
             void*, int64_t, double*, void*, size_t, cudaStream_t);
+int project_trsm(int, int, int, int, int64_t, int, int, const void*, int64_t, const double*, int64_t, const void*,
+                 int64_t, void*, int64_t, double*, void*, int64_t, const double*, int64_t, int, void*, size_t,
+                 cudaStream_t);
 int gaussian_fill(uint64_t, int, int64_t, int64_t, uint8_t*, int64_t, cudaStream_t);
 int sketch_gaussian(int, int64_t, int, const void*, int64_t, const uint8_t*, int64_t, int, double, double*, int64_t,
                     int, int, void*, size_t, cudaStream_t);
@@ -105,6 +108,13 @@ int rb_project(int qd, int wd, int cd, int order, int64_t n, int c, int p, const
                const double* X, int64_t ldx, const void* W, int64_t ldw, void* Qp, int64_t ldqp, double* norms2,
                void* ws, size_t wsb, void* s) {
   return rb::project(qd, wd, cd, order, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, norms2, ws, wsb, as_stream(s));
+}
+
+int rb_project_trsm(int qd, int wd, int cd, int order, int64_t n, int c, int p, const void* Q, int64_t ldq,
+                    const double* X, int64_t ldx, const void* W, int64_t ldw, void* Qp, int64_t ldqp, double* norms2,
+                    void* Qf, int64_t ldqf, const double* Rf, int64_t ldrf, int pf, void* ws, size_t wsb, void* s) {
+  return rb::project_trsm(qd, wd, cd, order, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, norms2, Qf, ldqf, Rf, ldrf,
+                          pf, ws, wsb, as_stream(s));
 }
 
 int rb_gaussian_fill(uint64_t seed, int k, int64_t row0, int64_t nrows, uint8_t* theta, int64_t ldt, void* s) {

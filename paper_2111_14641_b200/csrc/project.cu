@@ -216,7 +216,8 @@ template <typename TW, int PB, int RPT, int CS, int NT, int MODE>
 __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2)
 project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq,
                const float* __restrict__ Xs, const TW* W, int64_t ldw,
-               float* Qp, int64_t ldqp, double* __restrict__ partial, float nz) {
+               float* Qp, int64_t ldqp, double* __restrict__ partial, float nz, float* Qf, int64_t ldqf,
+               const double* __restrict__ Rf, int64_t ldrf, int pf) {
   constexpr int PC = PB / CS;        // columns per thread
   constexpr int R = NT / CS * RPT;   // rows per CTA
   constexpr int QB = kKQ * R;        // Q floats per stage
@@ -233,6 +234,52 @@ project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq
   const int jc = cg * PC;  // first column of this thread
   const int64_t rc = (int64_t)blockIdx.x * R;
   const bool bulk = rc + R <= n;
+
+  if constexpr (PB <= 40) if (pf > 0) {
+    // Fused Step-5 scaling of the PREVIOUS block (pf <= PB columns, the last
+    // pf of Q[:, :c]): Q_(i-1) = fl32(Q'_(i-1) R^{-1}) for this CTA's rows,
+    // in place, with exactly trsm_right_kernel's arithmetic (row solve in
+    // binary64 registers, l ascending, 1/R_jj as a multiply).  Only this
+    // CTA reads these rows afterwards, so no grid-wide ordering is needed;
+    // R is staged in the (not yet used) Q stage buffers.
+    constexpr int LDR = (PB + 1) & ~1;
+    double* sR = reinterpret_cast<double*>(smem);
+    double* sInv = sR + LDR * PB;
+    for (int e = threadIdx.x; e < LDR * PB; e += NT) {
+      const int i = e % LDR, j = e / LDR;
+      sR[e] = (i < pf && j < pf) ? Rf[i + (int64_t)j * ldrf] : 0.0;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < pf; j += NT) sInv[j] = 1.0 / sR[j + j * LDR];
+    __syncthreads();
+    for (int rr = threadIdx.x; rr < R; rr += NT) {
+      const int64_t row = rc + rr;
+      if (row >= n) break;
+      double x[PB];
+#pragma unroll
+      for (int j = 0; j < PB; ++j) x[j] = j < pf ? (double)Qf[row + (int64_t)j * ldqf] : 0.0;
+#pragma unroll
+      for (int j = 0; j < PB; ++j) {
+        if (j < pf) {
+          double sacc = x[j];
+          const double2* col = reinterpret_cast<const double2*>(sR + j * LDR);
+#pragma unroll
+          for (int l2 = 0; l2 < (j + 1) / 2; ++l2) {
+            const double2 r2 = col[l2];
+            sacc = fma(-x[2 * l2], r2.x, sacc);
+            if (2 * l2 + 1 < j) sacc = fma(-x[2 * l2 + 1], r2.y, sacc);
+          }
+          x[j] = sacc * sInv[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < PB; ++j)
+        if (j < pf) Qf[row + (int64_t)j * ldqf] = (float)x[j];
+    }
+    // these generic-proxy stores are read back by bulk (async-proxy) copies
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    __syncthreads();
+  }
   const int64_t r0 = rc + (int64_t)rt * RPT;
   bool v[RPT];
 #pragma unroll
@@ -496,10 +543,18 @@ int rpt_for(bool ff) {
   return default_rpt<PB>();
 }
 
+struct FusedTrsm {
+  void* Qf = nullptr;
+  int64_t ldqf = 0;
+  const double* Rf = nullptr;
+  int64_t ldrf = 0;
+  int pf = 0;
+};
+
 template <typename TQ, typename TW, int PB>
 void launch_pb(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, const double* X, int64_t ldx,
                const void* W, int64_t ldw, void* Qp, int64_t ldqp, double* partial, float* xs,
-               bool staged, cudaStream_t st) {
+               bool staged, cudaStream_t st, const FusedTrsm& fz) {
   if (mode == 2) {
     const int grid = ceil_div(n, kThreads);
     RB_KLAUNCH project_fine<TQ, TW, PB><<<grid, kThreads, 0, st>>>(n, c, p, (const TQ*)Q, ldq, X, ldx, (const TW*)W,
@@ -528,7 +583,8 @@ void launch_pb(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, co
       }
 #define RB_ST(M)                                                                                  \
   RB_KLAUNCH project_staged<TW, PB, RPT, CS, NT, M><<<grid, NT, smem, st>>>(                      \
-      n, c, p, (const float*)Q, ldq, xs, (const TW*)W, ldw, (float*)Qp, ldqp, partial, -0.0f)
+      n, c, p, (const float*)Q, ldq, xs, (const TW*)W, ldw, (float*)Qp, ldqp, partial, -0.0f,     \
+      (float*)fz.Qf, fz.ldqf, fz.Rf, fz.ldrf, fz.pf)
       if (mode == 1) RB_ST(1);
       else if (packed_enabled()) RB_ST(2);
       else RB_ST(0);
@@ -558,11 +614,11 @@ void launch_pb(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, co
 template <typename TQ, typename TW>
 int launch_tw(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, const double* X, int64_t ldx,
               const void* W, int64_t ldw, void* Qp, int64_t ldqp, double* partial, float* xs, bool staged,
-              cudaStream_t st) {
-#define RB_PB(V)                                                                                \
-  if (p <= V) {                                                                                 \
-    launch_pb<TQ, TW, V>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st); \
-    return V;                                                                                   \
+              cudaStream_t st, const FusedTrsm& fz = FusedTrsm()) {
+#define RB_PB(V)                                                                                    \
+  if (p <= V) {                                                                                     \
+    launch_pb<TQ, TW, V>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st, fz); \
+    return V;                                                                                       \
   }
   RB_PB(4) RB_PB(8) RB_PB(12) RB_PB(16) RB_PB(20) RB_PB(24) RB_PB(32) RB_PB(40) RB_PB(48) RB_PB(64)
 #undef RB_PB
@@ -588,9 +644,58 @@ int grid_rows(int mode, int p, bool ff) {
 
 }  // namespace
 
+int trsm_right(int, int, int64_t, int, const void*, int64_t, const double*, int64_t, void*, int64_t, cudaStream_t);
+
+namespace {
+int project_impl(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t n, int c, int p, const void* Q,
+                 int64_t ldq, const double* X, int64_t ldx, const void* W, int64_t ldw, void* Qp, int64_t ldqp,
+                 double* norms2, void* ws, size_t ws_bytes, cudaStream_t st, const FusedTrsm& fz);
+}  // namespace
+
 int project(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t n, int c, int p, const void* Q,
             int64_t ldq, const double* X, int64_t ldx, const void* W, int64_t ldw, void* Qp, int64_t ldqp,
             double* norms2, void* ws, size_t ws_bytes, cudaStream_t st) {
+  return project_impl(q_dtype, w_dtype, compute_dtype, order, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, norms2,
+                      ws, ws_bytes, st, FusedTrsm());
+}
+
+// Step 3 of block i with the Step-5 scaling of block i-1 fused in front:
+// Qf (the last pf columns of Q[:, :c], i.e. Q'_(i-1) in place) becomes
+// fl32(Q'_(i-1) Rf^{-1}) row by row inside the staged projection's CTAs, so
+// the scaled block is written and re-read while L2-hot and its DFMA /
+// shared-load work overlaps the other resident CTA's FP32 work.  Bitwise
+// the same as rb_trsm_right followed by rb_project.  Falls back to exactly
+// that pair when the staged kernel does not apply.
+int project_trsm(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t n, int c, int p, const void* Q,
+                 int64_t ldq, const double* X, int64_t ldx, const void* W, int64_t ldw, void* Qp, int64_t ldqp,
+                 double* norms2, void* Qf, int64_t ldqf, const double* Rf, int64_t ldrf, int pf, void* ws,
+                 size_t ws_bytes, cudaStream_t st) {
+  RB_REQUIRE(pf >= 1 && pf <= 64 && pf <= c && Qf && Rf && ldrf >= pf && ldqf >= n,
+             "rb_project_trsm: bad previous block (pf=%d c=%d)", pf, c);
+  const bool aligned = (uintptr_t)Q % 16 == 0 && ldq % 4 == 0;
+  const bool fusable = q_dtype == RB_F32 && compute_dtype == RB_F32 && aligned && rpt_override() == 0 &&
+                       staged_enabled() && p <= 40 && pf <= p && ldqf == ldq &&
+                       (const char*)Qf == (const char*)Q + (size_t)(c - pf) * ldq * sizeof(float);
+  if (!fusable) {
+    const int rc = trsm_right(q_dtype, q_dtype, n, pf, Qf, ldqf, Rf, ldrf, Qf, ldqf, st);
+    if (rc != RB_OK) return rc;
+    return project(q_dtype, w_dtype, compute_dtype, order, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, norms2, ws,
+                   ws_bytes, st);
+  }
+  FusedTrsm fz;
+  fz.Qf = Qf;
+  fz.ldqf = ldqf;
+  fz.Rf = Rf;
+  fz.ldrf = ldrf;
+  fz.pf = pf;
+  return project_impl(q_dtype, w_dtype, compute_dtype, order, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, norms2,
+                      ws, ws_bytes, st, fz);
+}
+
+namespace {
+int project_impl(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t n, int c, int p, const void* Q,
+                 int64_t ldq, const double* X, int64_t ldx, const void* W, int64_t ldw, void* Qp, int64_t ldqp,
+                 double* norms2, void* ws, size_t ws_bytes, cudaStream_t st, const FusedTrsm& fz) {
   RB_REQUIRE(n >= 0 && c >= 0 && p >= 1 && p <= 64, "rb_project: bad sizes n=%lld c=%d p=%d",
              (long long)n, c, p);
   RB_REQUIRE(c == 0 || (Q && ldq >= n && X && ldx >= c), "rb_project: bad Q/X");
@@ -613,12 +718,14 @@ int project(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t n, i
     if (norms2) cudaMemsetAsync(norms2, 0, 2 * sizeof(double), st);
     return check_launch("rb_project");
   }
-  if (q32 && w32) launch_tw<float, float>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st);
-  else if (q32) launch_tw<float, double>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st);
+  RB_REQUIRE(fz.pf == 0 || staged, "rb_project: fused scaling needs the staged kernel");
+  if (q32 && w32) launch_tw<float, float>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st, fz);
+  else if (q32) launch_tw<float, double>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st, fz);
   else if (w32) launch_tw<double, float>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st);
   else launch_tw<double, double>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st);
   if (norms2) RB_KLAUNCH sum_pairs<<<1, kThreads, 0, st>>>(partial, grid, norms2);
   return check_launch("rb_project");
 }
+}  // namespace
 
 }  // namespace rb

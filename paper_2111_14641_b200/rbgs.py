@@ -392,6 +392,10 @@ class RbgsSweep:
         self.pending_P = None
         self._next_P = None  # (key of the next block, its sketch) from a fused pass
         self._deferred = None  # (status, info) per block when checks are deferred
+        # one-shot sweeps: the Step-5 scaling of the previous block, deferred
+        # into the next projection (rb_project_trsm): (slot, R_S) or None
+        self._fuse_scaling = False
+        self._pending_scale = None
 
     # -- small utilities ---------------------------------------------------
     def _sketch(self, X, out):
@@ -480,7 +484,13 @@ class RbgsSweep:
                 out = slot if (last and not self.cfg.resketch) else self._tmp(w)
                 if not last and Qcur.data_ptr() == out.data_ptr():
                     out = D.empty_cm(self.n_local, w, torch.float64, self.device)
-                D.trsm_right(Qcur, RS, out)
+                if (last and l == 1 and self._fuse_scaling and out.data_ptr() == Qcur.data_ptr()
+                        and self.cols_done + w < self.Q.shape[1]):
+                    # in-place scaling of this block: done by the next block's
+                    # projection (rb_project_trsm), which alone reads it next
+                    self._pending_scale = (out, RS)
+                else:
+                    D.trsm_right(Qcur, RS, out)
                 if it == 0:  # R_total = R_S I
                     Rt.copy_(RS)
                 else:
@@ -676,6 +686,10 @@ class RbgsSweep:
                 # then widened exactly into the binary64 slot
                 D.project(self.Q32[:, :c], X, W, self.Q32[:, j0:j1], self.compute, self.order, norms[0:2])
                 D.convert(self.Q32[:, j0:j1], slot)
+            elif self._pending_scale is not None:
+                Qf, RSf = self._pending_scale
+                self._pending_scale = None
+                D.project_trsm(self.Q[:, :c], X, W, slot, self.compute, self.order, norms[0:2], Qf, RSf)
             else:
                 D.project(self.Q[:, :c], X, W, slot, self.compute, self.order, norms[0:2])
             Qp = slot
@@ -717,6 +731,12 @@ class RbgsSweep:
         if cfg.certify_blocks:
             self._certify_block(Si, Rii, sp_qp)
         return j0, j1
+
+    def _flush_scaling(self):
+        if self._pending_scale is not None:
+            Qf, RSf = self._pending_scale
+            self._pending_scale = None
+            D.trsm_right(Qf, RSf, Qf)
 
     def _commit_block(self, j0, j1, Pi, Si, Rii):
         if self.Q32 is not None:
@@ -820,6 +840,11 @@ def _sweep_blocks(Wd, n, theta, cfg, dc, q_storage, deferred, events=None):
     sweep = RbgsSweep(n, theta, cfg, dc, _q_storage=q_storage)
     if deferred:
         sweep._defer_status()
+        # nothing observes a block's Q_i before the next projection: fuse
+        # the scaling into it (binary32 Q only; rb_project_trsm checks the
+        # rest and falls back to the separate kernels)
+        sweep._fuse_scaling = (sweep.q_dtype == torch.float32 and sweep.compute == F32
+                               and os.environ.get("RB_FUSE_SCALING", "1") != "0")
     off = cfg.partition.offsets()
     for b in range(cfg.partition.num_blocks):
         nxt = Wd[:, off[b + 1]:off[b + 2]] if b + 2 < len(off) else None
@@ -829,6 +854,7 @@ def _sweep_blocks(Wd, n, theta, cfg, dc, q_storage, deferred, events=None):
             if nxt is not None:
                 stream.wait_event(events[b + 1])
         sweep.push_block(Wd[:, off[b]:off[b + 1]], lookahead=nxt)
+    sweep._flush_scaling()
     return sweep
 
 

@@ -526,3 +526,28 @@ def test_rbgs_plan_graph_replay_matches_eager(pkg):
     with pytest.raises(DependentBlockError) as ei:
         plan.replay()
     assert ei.value.block == 3
+
+
+def test_fused_scaling_is_bitwise_neutral(pkg):
+    """One-shot sweeps fold block i-1's Step-5 scaling into block i's
+    projection (rb_project_trsm); bits equal the separate kernels, for a
+    ragged partition too (widths 40, 40, 24, 40 -> fallback where pf > p)."""
+    import os
+    rbgs, sketching, D = pkg
+    from paper_2111_14641_b200.kernels import BlockPartition
+    import goldens as G
+
+    n, k = 30_000, 300
+    W = G.trig_family(n, 144, 6).astype(np.float32)
+    th = sketching.gaussian_operator(k, n, 4)
+    for part in (BlockPartition.uniform(144, 36), BlockPartition(40, 4, 144, widths=(40, 40, 24, 40))):
+        cfg = rbgs.RbgsConfig(partition=part, interblock="sketched_cholqr(1)")
+        a = rbgs.rbgs(W, th, cfg)
+        os.environ["RB_FUSE_SCALING"] = "0"
+        try:
+            b = rbgs.rbgs(W, th, cfg)
+        finally:
+            del os.environ["RB_FUSE_SCALING"]
+        assert np.array_equal(a.Q.data, b.Q.data)
+        assert np.array_equal(a.R.data, b.R.data)
+        assert np.array_equal(a.S.data, b.S.data)

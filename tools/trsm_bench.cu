@@ -105,6 +105,54 @@ __global__ void __launch_bounds__(256, MINB) v2(int64_t n, int p, const float* B
 #pragma unroll
   for (int j = 0; j < PB; ++j) if (j < p) Xo[r + (int64_t)j * ldx] = (float)x[j];
 }
+
+// V3: each row split over L = 4 lanes (columns j = t + 4 i), axpy order,
+// x_l broadcast in the lane group by shuffle; same FMA order per column.
+template <int PB, int MINB>
+__global__ void __launch_bounds__(256, MINB) v3(int64_t n, int p, const float* B, int64_t ldb, const double* __restrict__ Rg, int64_t ldr, float* Xo, int64_t ldx) {
+  constexpr int L = 4, NI = PB / L, TS = NI + 2;  // per-lane columns, padded lane stride
+  __shared__ __align__(16) double sR[PB * L * TS];  // sR[(l * L + t) * TS + i] = R[l][t + 4 i] (j > l)
+  __shared__ double sInv[PB];
+  for (int e = threadIdx.x; e < PB * L * TS; e += blockDim.x) {
+    const int i = e % TS, t = (e / TS) % L, l = e / (TS * L);
+    const int j = t + L * i;
+    sR[e] = (i < NI && l < p && j < p && j > l) ? Rg[l + (int64_t)j * ldr] : 0.0;
+  }
+  for (int j = threadIdx.x; j < PB; j += blockDim.x) sInv[j] = j < p ? 1.0 / Rg[j + (int64_t)j * ldr] : 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, t = lane & (L - 1);
+  const int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / L;
+  const bool live = r < n;
+  double x[NI];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int j = t + L * i;
+    x[i] = (live && j < p) ? (double)B[r + (int64_t)j * ldb] : 0.0;
+  }
+  const double* Rt = sR + t * TS;
+#pragma unroll
+  for (int l = 0; l < PB; ++l) {
+    constexpr int dummy = 0; (void)dummy;
+    const int io = l / L, o = l % L;
+    double xl = 0.0;
+    if (t == o) {
+      xl = x[io] * sInv[l];
+      x[io] = xl;
+    }
+    xl = __shfl_sync(0xffffffffu, xl, (lane & ~(L - 1)) | o);
+    const double* Rl = Rt + l * L * TS;
+    if (t > o) x[io] = fma(-xl, Rl[io], x[io]);
+#pragma unroll
+    for (int i = io + 1; i < NI; ++i) x[i] = fma(-xl, Rl[i], x[i]);
+  }
+  if (live) {
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const int j = t + L * i;
+      if (j < p) Xo[r + (int64_t)j * ldx] = (float)x[i];
+    }
+  }
+}
 template <int PB>
 void run(int64_t n) {
   const int p = PB;
@@ -118,8 +166,8 @@ void run(int64_t n) {
   cudaMemcpy(B, hb.data(), n * p * 4, cudaMemcpyHostToDevice);
   int grid = (int)((n + 255) / 256);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  float ms[6];
-  for (int v = 0; v < 6; ++v) {
+  float ms[8];
+  for (int v = 0; v < 8; ++v) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(a);
       for (int i = 0; i < 5; ++i) {
@@ -128,7 +176,9 @@ void run(int64_t n) {
         else if (v == 2) v1<PB, 2><<<grid, 256>>>(n, p, B, n, R, p, X1, n);
         else if (v == 3) v2<PB, 4, 2><<<grid, 256>>>(n, p, B, n, R, p, X1, n);
         else if (v == 4) v2<PB, 8, 2><<<grid, 256>>>(n, p, B, n, R, p, X1, n);
-        else v2<PB, 4, 1><<<grid, 256>>>(n, p, B, n, R, p, X1, n);
+        else if (v == 5) v2<PB, 4, 1><<<grid, 256>>>(n, p, B, n, R, p, X1, n);
+        else if (v == 6) v3<PB, 2><<<grid * 4, 256>>>(n, p, B, n, R, p, X1, n);
+        else v3<PB, 4><<<grid * 4, 256>>>(n, p, B, n, R, p, X1, n);
       }
       cudaEventRecord(b); cudaEventSynchronize(b);
       cudaEventElapsedTime(&ms[v], a, b); ms[v] /= 5;
@@ -138,7 +188,7 @@ void run(int64_t n) {
   cudaMemcpy(o0.data(), X0, n * p * 4, cudaMemcpyDeviceToHost);
   cudaMemcpy(o1.data(), X1, n * p * 4, cudaMemcpyDeviceToHost);
   int64_t diff = 0; for (int64_t i = 0; i < n * p; ++i) diff += memcmp(&o0[i], &o1[i], 4) != 0;
-  printf("{\"p\": %d, \"n\": %lld, \"v0_ms\": %.4f, \"v1_minb1_ms\": %.4f, \"v1_minb2_ms\": %.4f, \"v2_g4_ms\": %.4f, \"v2_g8_ms\": %.4f, \"v2_g4_minb1_ms\": %.4f, \"bitdiff_last\": %lld, \"hbm_ms\": %.4f}\n", p, (long long)n, ms[0], ms[1], ms[2], ms[3], ms[4], ms[5], (long long)diff, 2.0 * n * p * 4 / 6.5e12 * 1e3);
+  printf("{\"p\": %d, \"n\": %lld, \"v0_ms\": %.4f, \"v1_minb1_ms\": %.4f, \"v1_minb2_ms\": %.4f, \"v2_g4_ms\": %.4f, \"v2_g8_ms\": %.4f, \"v2_g4_minb1_ms\": %.4f, \"v3_minb2_ms\": %.4f, \"v3_minb4_ms\": %.4f, \"bitdiff_last\": %lld, \"hbm_ms\": %.4f}\n", p, (long long)n, ms[0], ms[1], ms[2], ms[3], ms[4], ms[5], ms[6], ms[7], (long long)diff, 2.0 * n * p * 4 / 6.5e12 * 1e3);
   cudaFree(B); cudaFree(X0); cudaFree(X1); cudaFree(R);
 }
 int main() {
