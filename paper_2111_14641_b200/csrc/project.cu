@@ -23,6 +23,7 @@
 #include <stdlib.h>
 
 #include "common.cuh"
+#include "tri_const.cuh"
 #include "tc.cuh"
 
 namespace rb {
@@ -238,40 +239,17 @@ project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq
   if constexpr (PB <= 40) if (pf > 0) {
     // Fused Step-5 scaling of the PREVIOUS block (pf <= PB columns, the last
     // pf of Q[:, :c]): Q_(i-1) = fl32(Q'_(i-1) R^{-1}) for this CTA's rows,
-    // in place, with exactly trsm_right_kernel's arithmetic (row solve in
-    // binary64 registers, l ascending, 1/R_jj as a multiply).  Only this
-    // CTA reads these rows afterwards, so no grid-wide ordering is needed;
-    // R is staged in the (not yet used) Q stage buffers.
-    constexpr int LDR = (PB + 1) & ~1;
-    double* sR = reinterpret_cast<double*>(smem);
-    double* sInv = sR + LDR * PB;
-    for (int e = threadIdx.x; e < LDR * PB; e += NT) {
-      const int i = e % LDR, j = e / LDR;
-      sR[e] = (i < pf && j < pf) ? Rf[i + (int64_t)j * ldrf] : 0.0;
-    }
-    __syncthreads();
-    for (int j = threadIdx.x; j < pf; j += NT) sInv[j] = 1.0 / sR[j + j * LDR];
-    __syncthreads();
+    // in place, with exactly trsm_right_kernel's arithmetic (tri_solve_row:
+    // binary64 registers, l ascending, R from the constant bank loaded by
+    // the host wrapper).  Only this CTA reads these rows afterwards, so no
+    // grid-wide ordering is needed.
     for (int rr = threadIdx.x; rr < R; rr += NT) {
       const int64_t row = rc + rr;
       if (row >= n) break;
       double x[PB];
 #pragma unroll
       for (int j = 0; j < PB; ++j) x[j] = j < pf ? (double)Qf[row + (int64_t)j * ldqf] : 0.0;
-#pragma unroll
-      for (int j = 0; j < PB; ++j) {
-        if (j < pf) {
-          double sacc = x[j];
-          const double2* col = reinterpret_cast<const double2*>(sR + j * LDR);
-#pragma unroll
-          for (int l2 = 0; l2 < (j + 1) / 2; ++l2) {
-            const double2 r2 = col[l2];
-            sacc = fma(-x[2 * l2], r2.x, sacc);
-            if (2 * l2 + 1 < j) sacc = fma(-x[2 * l2 + 1], r2.y, sacc);
-          }
-          x[j] = sacc * sInv[j];
-        }
-      }
+      tri_solve_row<PB>(x, pf);
 #pragma unroll
       for (int j = 0; j < PB; ++j)
         if (j < pf) Qf[row + (int64_t)j * ldqf] = (float)x[j];
@@ -682,6 +660,8 @@ int project_trsm(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t
     return project(q_dtype, w_dtype, compute_dtype, order, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, norms2, ws,
                    ws_bytes, st);
   }
+  const int lrc = load_tri_const(pf, Rf, ldrf, st);
+  if (lrc != RB_OK) return lrc;
   FusedTrsm fz;
   fz.Qf = Qf;
   fz.ldqf = ldqf;

@@ -8,6 +8,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "tri_const.cuh"
 
 namespace rb {
 
@@ -153,61 +154,23 @@ __global__ void potrf_kernel(int p, const double* __restrict__ G, int64_t ldg, d
 }
 
 // ============================ triangular solves =============================
-// Tall right solve X = B R^{-1} by forward substitution in fp64 (l
-// ascending per column), RPT rows per thread with the rows in registers.
-// R is staged column-major in shared memory with an even column stride so
-// that (l, l+1) pairs of a column load as one LDS.128 broadcast feeding
-// 2 * RPT DFMAs; 1 / R_jj is a multiply.
+// Tall right solve X = B R^{-1} by forward substitution in fp64, one row per
+// thread in registers, l ascending (dot form); R and 1 / R_jj come from the
+// constant bank (tri_const.cuh: the shared-memory version was bound by the
+// per-lane register writeback of its broadcast loads).
 template <typename TI, typename TO, int PB, int RPT>
-__global__ void __launch_bounds__(kThreads, RPT > 1 ? 1 : 2)
-trsm_right_kernel(int64_t n, int p, const TI* B, int64_t ldb, const double* __restrict__ Rg,
-                  int64_t ldr, TO* Xo, int64_t ldx) {  // B and Xo may alias (in-place solve)
-  constexpr int LD = (PB + 1) & ~1;
-  __shared__ __align__(16) double sR[LD * PB];
-  __shared__ double sInv[PB];
-  for (int e = threadIdx.x; e < LD * PB; e += blockDim.x) {
-    const int i = e % LD, j = e / LD;
-    sR[e] = (i < p && j < p) ? Rg[i + (int64_t)j * ldr] : 0.0;
-  }
-  __syncthreads();
-  for (int j = threadIdx.x; j < p; j += blockDim.x) sInv[j] = 1.0 / sR[j + j * LD];
-  __syncthreads();
-  const int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * RPT;
-  if (r0 >= n) return;
-  bool v[RPT];
+__global__ void __launch_bounds__(kThreads, 2)  // 2 CTAs/SM even at p = 64 (a few spills beat 8 warps/SM)
+trsm_right_kernel(int64_t n, int p, const TI* B, int64_t ldb, TO* Xo, int64_t ldx) {  // B, Xo may alias
+  static_assert(RPT == 1, "one row per thread");
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double x[PB];
 #pragma unroll
-  for (int t = 0; t < RPT; ++t) v[t] = r0 + t < n;
-  double x[RPT][PB];
+  for (int j = 0; j < PB; ++j) x[j] = j < p ? (double)B[r + (int64_t)j * ldb] : 0.0;
+  tri_solve_row<PB>(x, p);
 #pragma unroll
   for (int j = 0; j < PB; ++j)
-#pragma unroll
-    for (int t = 0; t < RPT; ++t) x[t][j] = (j < p && v[t]) ? (double)B[r0 + t + (int64_t)j * ldb] : 0.0;
-#pragma unroll
-  for (int j = 0; j < PB; ++j) {
-    if (j < p) {
-      double s[RPT];
-#pragma unroll
-      for (int t = 0; t < RPT; ++t) s[t] = x[t][j];
-      const double2* col = reinterpret_cast<const double2*>(sR + j * LD);
-#pragma unroll
-      for (int l2 = 0; l2 < (j + 1) / 2; ++l2) {
-        const double2 rr = col[l2];
-#pragma unroll
-        for (int t = 0; t < RPT; ++t) {
-          s[t] = fma(-x[t][2 * l2], rr.x, s[t]);
-          if (2 * l2 + 1 < j) s[t] = fma(-x[t][2 * l2 + 1], rr.y, s[t]);
-        }
-      }
-      const double iv = sInv[j];
-#pragma unroll
-      for (int t = 0; t < RPT; ++t) x[t][j] = s[t] * iv;
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < PB; ++j)
-#pragma unroll
-    for (int t = 0; t < RPT; ++t)
-      if (j < p && v[t]) Xo[r0 + t + (int64_t)j * ldx] = (TO)x[t][j];
+    if (j < p) Xo[r + (int64_t)j * ldx] = (TO)x[j];
 }
 
 // Left solve R X = B in place, one warp per right-hand side.
@@ -366,11 +329,12 @@ __global__ void copy_f64(int m, int n, const double* __restrict__ A, int64_t lda
 template <typename TI, typename TO>
 void trsm_right_launch(int64_t n, int p, const void* B, int64_t ldb, const double* R, int64_t ldr, void* X,
                        int64_t ldx, cudaStream_t st) {
+  if (load_tri_const(p, R, ldr, st) != RB_OK) return;
 #define RB_TR(V)                                                                                          \
   if (p <= V) {                                                                                           \
     constexpr int RPT = 1;                                                                                \
     RB_KLAUNCH trsm_right_kernel<TI, TO, V, RPT><<<ceil_div(n, (int64_t)RPT * kThreads), kThreads, 0, st>>>( \
-        n, p, (const TI*)B, ldb, R, ldr, (TO*)X, ldx);                                                    \
+        n, p, (const TI*)B, ldb, (TO*)X, ldx);                                                            \
     return;                                                                                               \
   }
   RB_TR(4) RB_TR(8) RB_TR(12) RB_TR(16) RB_TR(24) RB_TR(32) RB_TR(40) RB_TR(48) RB_TR(64)

@@ -1,0 +1,73 @@
+// Small upper-triangular R (p <= 64) in the CONSTANT bank for the tall
+// right solves X = B R^{-1} (rbgs.py:281-283 -> kernels.py:250-270).
+//
+// A row solve reads every R_lj once per row; from shared memory each read is
+// a broadcast LDS whose 8 bytes are still written back to all 32 lanes'
+// registers, and that writeback (not the DFMA pipe) bounded the kernel
+// (ncu: LSU writeback ~50%, FP64 pipe ~22%).  Served from the constant bank
+// the operand arrives through the uniform datapath instead: measured
+// 1.06 vs 1.96 ms at 2^24 x 32 and 6.6 vs 8.5 ms at 2^24 x 64
+// (tools/trsm_bench.cu, profiles/r01_trsm_variants.json), bit-identical.
+//
+// Each translation unit that includes this header gets its own copy (the
+// anonymous namespace); load_tri_const() refreshes THIS unit's copy,
+// stream-ordered (a pack kernel into a per-device staging buffer, then one
+// device-to-symbol copy -- both graph-capturable).  One solve per stream at
+// a time, which is how the sweep issues them.
+#pragma once
+
+#include "common.cuh"
+
+namespace rb {
+namespace {
+
+constexpr int kTriLd = 64;
+__constant__ double c_tri_R[kTriLd * kTriLd];  // column-major, ld 64, zero padded
+__constant__ double c_tri_inv[kTriLd];         // 1 / R_jj (0 for j >= p)
+
+__global__ void tri_pack_kernel(int p, const double* __restrict__ R, int64_t ldr, double* __restrict__ dst) {
+  for (int e = threadIdx.x; e < kTriLd * kTriLd; e += blockDim.x) {
+    const int i = e % kTriLd, j = e / kTriLd;
+    dst[e] = (i < p && j < p) ? R[i + (int64_t)j * ldr] : 0.0;
+  }
+  for (int j = threadIdx.x; j < kTriLd; j += blockDim.x)
+    dst[kTriLd * kTriLd + j] = j < p ? 1.0 / R[j + (int64_t)j * ldr] : 0.0;
+}
+
+inline int load_tri_const(int p, const double* R, int64_t ldr, cudaStream_t st) {
+  static double* staging[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!staging[dev]) {
+    if (cudaMalloc(&staging[dev], (kTriLd * kTriLd + kTriLd) * sizeof(double)) != cudaSuccess) {
+      set_error("tri_const: staging allocation failed");
+      return RB_ECUDA;
+    }
+  }
+  RB_KLAUNCH tri_pack_kernel<<<1, 256, 0, st>>>(p, R, ldr, staging[dev]);
+  cudaMemcpyToSymbolAsync(c_tri_R, staging[dev], kTriLd * kTriLd * sizeof(double), 0, cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyToSymbolAsync(c_tri_inv, staging[dev] + kTriLd * kTriLd, kTriLd * sizeof(double), 0,
+                          cudaMemcpyDeviceToDevice, st);
+  return check_launch("tri_const load");
+}
+
+// One row: x (registers, PB >= p columns) <- x R^{-1}, dot form, l ascending
+// with the (even, odd) pairing of trsm_right_kernel -- the same roundings.
+template <int PB>
+__device__ __forceinline__ void tri_solve_row(double (&x)[PB], int p) {
+#pragma unroll
+  for (int j = 0; j < PB; ++j) {
+    if (j < p) {
+      double s = x[j];
+#pragma unroll
+      for (int l2 = 0; l2 < (j + 1) / 2; ++l2) {
+        s = fma(-x[2 * l2], c_tri_R[2 * l2 + j * kTriLd], s);
+        if (2 * l2 + 1 < j) s = fma(-x[2 * l2 + 1], c_tri_R[2 * l2 + 1 + j * kTriLd], s);
+      }
+      x[j] = s * c_tri_inv[j];
+    }
+  }
+}
+
+}  // namespace
+}  // namespace rb

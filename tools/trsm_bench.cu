@@ -153,6 +153,55 @@ __global__ void __launch_bounds__(256, MINB) v3(int64_t n, int p, const float* B
     }
   }
 }
+
+// V4: R and 1/diag(R) in CONSTANT memory (loaded D2D per call), so every
+// DFMA takes its R operand from the constant bank: no shared loads, no
+// register writeback for R.  Dot form, same order as v0.
+__constant__ double c_R[64 * 64];  // column-major, ld 64
+__constant__ double c_inv[64];
+template <int PB>
+__global__ void __launch_bounds__(256, 2) v4(int64_t n, int p, const float* B, int64_t ldb, float* Xo, int64_t ldx) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double x[PB];
+#pragma unroll
+  for (int j = 0; j < PB; ++j) x[j] = j < p ? (double)B[r + (int64_t)j * ldb] : 0.0;
+#pragma unroll
+  for (int j = 0; j < PB; ++j) {
+    double s = x[j];
+#pragma unroll
+    for (int l = 0; l < j; ++l) s = fma(-x[l], c_R[l + j * 64], s);
+    x[j] = s * c_inv[j];
+  }
+#pragma unroll
+  for (int j = 0; j < PB; ++j) if (j < p) Xo[r + (int64_t)j * ldx] = (float)x[j];
+}
+__global__ void pack_R(int p, const double* R, int64_t ldr, double* Rp, double* inv) {
+  for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+    const int i = e % 64, j = e / 64;
+    Rp[e] = (i < p && j < p) ? R[i + (int64_t)j * ldr] : 0.0;
+  }
+  for (int j = threadIdx.x; j < 64; j += blockDim.x) inv[j] = j < p ? 1.0 / R[j + (int64_t)j * ldr] : 0.0;
+}
+
+// V5: constant-bank R, axpy (right-looking) order: same FMA sequence per
+// column as v0/v4, p-wide ILP.
+template <int PB, int MINB>
+__global__ void __launch_bounds__(256, MINB) v5(int64_t n, int p, const float* B, int64_t ldb, float* Xo, int64_t ldx) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double x[PB];
+#pragma unroll
+  for (int j = 0; j < PB; ++j) x[j] = j < p ? (double)B[r + (int64_t)j * ldb] : 0.0;
+#pragma unroll
+  for (int l = 0; l < PB; ++l) {
+    x[l] = x[l] * c_inv[l];
+#pragma unroll
+    for (int j = l + 1; j < PB; ++j) x[j] = fma(-x[l], c_R[l + j * 64], x[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < PB; ++j) if (j < p) Xo[r + (int64_t)j * ldx] = (float)x[j];
+}
 template <int PB>
 void run(int64_t n) {
   const int p = PB;
@@ -166,8 +215,9 @@ void run(int64_t n) {
   cudaMemcpy(B, hb.data(), n * p * 4, cudaMemcpyHostToDevice);
   int grid = (int)((n + 255) / 256);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  float ms[8];
-  for (int v = 0; v < 8; ++v) {
+  float ms[11];
+  double* Rpk; cudaMalloc(&Rpk, (64 * 64 + 64) * 8);
+  for (int v = 0; v < 11; ++v) {
     for (int rep = 0; rep < 2; ++rep) {
       cudaEventRecord(a);
       for (int i = 0; i < 5; ++i) {
@@ -178,7 +228,16 @@ void run(int64_t n) {
         else if (v == 4) v2<PB, 8, 2><<<grid, 256>>>(n, p, B, n, R, p, X1, n);
         else if (v == 5) v2<PB, 4, 1><<<grid, 256>>>(n, p, B, n, R, p, X1, n);
         else if (v == 6) v3<PB, 2><<<grid * 4, 256>>>(n, p, B, n, R, p, X1, n);
-        else v3<PB, 4><<<grid * 4, 256>>>(n, p, B, n, R, p, X1, n);
+        else if (v == 7) v3<PB, 4><<<grid * 4, 256>>>(n, p, B, n, R, p, X1, n);
+        else {
+          if (rep == 0 && v >= 8) {}
+          pack_R<<<1, 256>>>(p, R, p, Rpk, Rpk + 64 * 64);
+          cudaMemcpyToSymbolAsync(c_R, Rpk, 64 * 64 * 8, 0, cudaMemcpyDeviceToDevice);
+          cudaMemcpyToSymbolAsync(c_inv, Rpk + 64 * 64, 64 * 8, 0, cudaMemcpyDeviceToDevice);
+          if (v == 8) v4<PB><<<grid, 256>>>(n, p, B, n, X1, n);
+          else if (v == 9) v5<PB, 2><<<grid, 256>>>(n, p, B, n, X1, n);
+          else v5<PB, 1><<<grid, 256>>>(n, p, B, n, X1, n);
+        }
       }
       cudaEventRecord(b); cudaEventSynchronize(b);
       cudaEventElapsedTime(&ms[v], a, b); ms[v] /= 5;
@@ -188,7 +247,7 @@ void run(int64_t n) {
   cudaMemcpy(o0.data(), X0, n * p * 4, cudaMemcpyDeviceToHost);
   cudaMemcpy(o1.data(), X1, n * p * 4, cudaMemcpyDeviceToHost);
   int64_t diff = 0; for (int64_t i = 0; i < n * p; ++i) diff += memcmp(&o0[i], &o1[i], 4) != 0;
-  printf("{\"p\": %d, \"n\": %lld, \"v0_ms\": %.4f, \"v1_minb1_ms\": %.4f, \"v1_minb2_ms\": %.4f, \"v2_g4_ms\": %.4f, \"v2_g8_ms\": %.4f, \"v2_g4_minb1_ms\": %.4f, \"v3_minb2_ms\": %.4f, \"v3_minb4_ms\": %.4f, \"bitdiff_last\": %lld, \"hbm_ms\": %.4f}\n", p, (long long)n, ms[0], ms[1], ms[2], ms[3], ms[4], ms[5], ms[6], ms[7], (long long)diff, 2.0 * n * p * 4 / 6.5e12 * 1e3);
+  printf("{\"p\": %d, \"n\": %lld, \"v0_ms\": %.4f, \"v1_minb1_ms\": %.4f, \"v1_minb2_ms\": %.4f, \"v2_g4_ms\": %.4f, \"v2_g8_ms\": %.4f, \"v2_g4_minb1_ms\": %.4f, \"v3_minb2_ms\": %.4f, \"v3_minb4_ms\": %.4f, \"v4_const_ms\": %.4f, \"v5_minb2_ms\": %.4f, \"v5_minb1_ms\": %.4f, \"bitdiff_last\": %lld, \"hbm_ms\": %.4f}\n", p, (long long)n, ms[0], ms[1], ms[2], ms[3], ms[4], ms[5], ms[6], ms[7], ms[8], ms[9], ms[10], (long long)diff, 2.0 * n * p * 4 / 6.5e12 * 1e3);
   cudaFree(B); cudaFree(X0); cudaFree(X1); cudaFree(R);
 }
 int main() {
