@@ -200,6 +200,16 @@ constexpr int kKQ = 16;          // l rows per stage
 constexpr int kStagedRows = 512;  // rows per CTA
 constexpr int kQS = 3;   // stage buffers
 
+// Rows per CTA: the grid is cut into whole waves of resident CTAs (2 per SM
+// at <= 256 threads, else 1), each CTA <= kStagedRows rows, a multiple of 4.
+int staged_rows_per_cta(int64_t n, int nt) {
+  const int64_t slots = (int64_t)sm_count() * (nt >= 512 ? 1 : 2);
+  const int64_t waves = std::max<int64_t>(1, (n + slots * kStagedRows - 1) / (slots * kStagedRows));
+  int64_t rows = (n + slots * waves - 1) / (slots * waves);
+  rows = (rows + 3) / 4 * 4;
+  return (int)std::min<int64_t>(std::max<int64_t>(rows, 4), kStagedRows);
+}
+
 template <int PB, int RPT, int CS, int NT>
 constexpr size_t staged_smem() {
   return (size_t)kQS * (kKQ * (NT / CS) * RPT + kKQ * PB) * sizeof(float) + kQS * (sizeof(uint64_t) + 4);
@@ -218,7 +228,7 @@ __global__ void __launch_bounds__(NT, NT >= 512 ? 1 : 2)
 project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq,
                const float* __restrict__ Xs, const TW* W, int64_t ldw,
                float* Qp, int64_t ldqp, double* __restrict__ partial, float nz, float* Qf, int64_t ldqf,
-               const double* __restrict__ Rf, int64_t ldrf, int pf) {
+               const double* __restrict__ Rf, int64_t ldrf, int pf, int rows_per_cta) {
   constexpr int PC = PB / CS;        // columns per thread
   constexpr int R = NT / CS * RPT;   // rows per CTA
   constexpr int QB = kKQ * R;        // Q floats per stage
@@ -233,8 +243,12 @@ project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq
 
   const int cg = threadIdx.x % CS, rt = threadIdx.x / CS;
   const int jc = cg * PC;  // first column of this thread
-  const int64_t rc = (int64_t)blockIdx.x * R;
-  const bool bulk = rc + R <= n;
+  // Rt <= R rows per CTA (a multiple of 4 chosen by the host so the grid is
+  // a whole number of waves: no partial last wave on the FP32 pipe)
+  const int64_t rc = (int64_t)blockIdx.x * rows_per_cta;
+  const int Rt = (int)min((int64_t)rows_per_cta, n - rc);
+  const bool bulk = (Rt & 3) == 0;  // 16-byte column segments
+  const int64_t rend = rc + Rt;
 
   if constexpr (PB <= 40) if (pf > 0) {
     // Fused Step-5 scaling of the PREVIOUS block (pf <= PB columns, the last
@@ -243,9 +257,8 @@ project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq
     // binary64 registers, l ascending, R from the constant bank loaded by
     // the host wrapper).  Only this CTA reads these rows afterwards, so no
     // grid-wide ordering is needed.
-    for (int rr = threadIdx.x; rr < R; rr += NT) {
+    for (int rr = threadIdx.x; rr < Rt; rr += NT) {
       const int64_t row = rc + rr;
-      if (row >= n) break;
       double x[PB];
 #pragma unroll
       for (int j = 0; j < PB; ++j) x[j] = j < pf ? (double)Qf[row + (int64_t)j * ldqf] : 0.0;
@@ -261,7 +274,7 @@ project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq
   const int64_t r0 = rc + (int64_t)rt * RPT;
   bool v[RPT];
 #pragma unroll
-  for (int t = 0; t < RPT; ++t) v[t] = r0 + t < n;
+  for (int t = 0; t < RPT; ++t) v[t] = r0 + t < rend;
 
   float acc[RPT][PC];
   double w2 = 0.0;
@@ -282,9 +295,9 @@ project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq
     const int b = s % kQS, l0 = s * kKQ, lc = min(kKQ, c - l0);
     float* dq = sq + b * QB;
     tc::fence_proxy_async_smem();
-    tc::mbar_arrive_expect_tx(&full[b], (uint32_t)((lc * R + XB) * sizeof(float)));
+    tc::mbar_arrive_expect_tx(&full[b], (uint32_t)((lc * Rt + XB) * sizeof(float)));
     for (int u = 0; u < lc; ++u)
-      tc::bulk_g2s(dq + u * R, Q + (int64_t)(l0 + u) * ldq + rc, R * sizeof(float), &full[b]);
+      tc::bulk_g2s(dq + u * R, Q + (int64_t)(l0 + u) * ldq + rc, Rt * sizeof(float), &full[b]);
     tc::bulk_g2s(sx + b * XB, Xs + (int64_t)l0 * PB, XB * sizeof(float), &full[b]);
   };
   auto issue_tail = [&](int s) {  // all threads
@@ -293,7 +306,7 @@ project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq
     float* dx = sx + b * XB;
     for (int e = threadIdx.x; e < lc * R; e += NT) {
       const int u = e / R, r = e % R;
-      dq[e] = rc + r < n ? Q[(int64_t)(l0 + u) * ldq + rc + r] : 0.f;
+      dq[e] = r < Rt ? Q[(int64_t)(l0 + u) * ldq + rc + r] : 0.f;
     }
     for (int e = threadIdx.x; e < XB; e += NT) dx[e] = Xs[(int64_t)l0 * PB + e];
   };
@@ -548,7 +561,8 @@ void launch_pb(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, co
       constexpr int CS = PB <= 20 ? 1 : PB <= 40 ? 2 : 4;
       constexpr int NT = kStagedRows / RPT * CS;
       constexpr size_t smem = staged_smem<PB, RPT, CS, NT>();
-      const int grid = ceil_div(n, (int64_t)kStagedRows);
+      const int rows = staged_rows_per_cta(n, NT);
+      const int grid = ceil_div(n, (int64_t)rows);
       static bool attr = false;
       if (!attr) {
         cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -562,7 +576,7 @@ void launch_pb(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, co
 #define RB_ST(M)                                                                                  \
   RB_KLAUNCH project_staged<TW, PB, RPT, CS, NT, M><<<grid, NT, smem, st>>>(                      \
       n, c, p, (const float*)Q, ldq, xs, (const TW*)W, ldw, (float*)Qp, ldqp, partial, -0.0f,     \
-      (float*)fz.Qf, fz.ldqf, fz.Rf, fz.ldrf, fz.pf)
+      (float*)fz.Qf, fz.ldqf, fz.Rf, fz.ldrf, fz.pf, rows)
       if (mode == 1) RB_ST(1);
       else if (packed_enabled()) RB_ST(2);
       else RB_ST(0);
@@ -686,7 +700,8 @@ int project_impl(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t
   // binary32 Q with 16-B aligned columns streams through the staged kernel
   const bool staged = mode != 2 && q32 && c > 0 && rpt_override() == 0 && (uintptr_t)Q % 16 == 0 &&
                       ldq % 4 == 0 && staged_enabled();
-  const int grid = ceil_div(n, staged ? kStagedRows : grid_rows(mode, p, q32 && w32));
+  const int grid = staged ? ceil_div(n, (int64_t)staged_rows_per_cta(n, p > 40 ? 512 : 256))
+                          : ceil_div(n, grid_rows(mode, p, q32 && w32));
   // workspace: [per-CTA norm pairs | staged -fl32(X), cpad x 64 floats]
   const size_t part_bytes = norms2 ? ((size_t)grid * 2 * sizeof(double) + 255) / 256 * 256 : 0;
   const size_t xs_bytes = mode == 2 ? 0 : (size_t)ceil_div(c, kXC) * kXC * 64 * sizeof(float);
