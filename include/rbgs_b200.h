@@ -158,6 +158,12 @@ int rb_gemm_f64(int transA, int transB, int m, int n, int k, double alpha,
 int rb_gemm_f32(int transA, int transB, int m, int n, int k, float alpha,
                 const float* A, int64_t lda, const float* B, int64_t ldb, float beta,
                 float* C, int64_t ldc, void* stream);
+/* out[0..2] = sums of squares of three binary64 matrices (one launch; the
+ * per-block finiteness words of P_i, S_i, R_ii -- rbgs.py:380-388 through
+ * the reference's Matrix() checks). */
+int rb_sumsq3(int64_t m1, int n1, const double* A1, int64_t lda1,
+              int64_t m2, int n2, const double* A2, int64_t lda2,
+              int64_t m3, int n3, const double* A3, int64_t lda3, double* out, void* stream);
 /* Symmetric rank-k update, upper triangle: C = alpha A^T A + beta C for a
  * tall binary64 A (k x n, C n x n; cuBLAS DSYRK) -- the basis Gram of the
  * GMRES conditioning history (krylov.py:98-103, 247-257). */

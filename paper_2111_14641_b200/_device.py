@@ -287,6 +287,14 @@ def sumsq(A, out, minus_identity=False):
     call("rb_sumsq", dtype_code(A), m, n, ptr(A), ld(A), int(minus_identity), ptr(out), ws, wsb, st(A.device))
 
 
+def sumsq3(A1, A2, A3, out):
+    """out[0:3] = sums of squares of three binary64 matrices (one launch)."""
+    args = []
+    for A in (A1, A2, A3):
+        args += [A.shape[0], A.shape[1], ptr(A), ld(A)]
+    call("rb_sumsq3", *args, ptr(out), st(out.device))
+
+
 def richardson(S, P, l, X, T):
     k, c = S.shape
     p = P.shape[1]

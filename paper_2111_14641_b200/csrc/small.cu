@@ -132,16 +132,17 @@ __global__ void potrf_kernel(int p, const double* __restrict__ G, int64_t ldg, d
       break;
     }
     const double r = sqrt(d);
-    __syncthreads();
-    // scale row j right of the diagonal
+    // scale row j right of the diagonal (every thread has read d: the
+    // diagonal is only rewritten after the next barrier)
     for (int c = j + 1 + threadIdx.x; c < p; c += blockDim.x) S[j + c * p] /= r;
     __syncthreads();
     if (threadIdx.x == 0) S[j + j * p] = r;
-    // trailing update of the upper part: S[a, b] -= S[j, a] S[j, b], j < a <= b
-    const int t = p - j - 1;
-    for (int e = threadIdx.x; e < t * t; e += blockDim.x) {
-      const int a = j + 1 + e % t, b = j + 1 + e / t;
-      if (a <= b) S[a + b * p] -= S[j + a * p] * S[j + b * p];
+    // trailing update of the upper part: S[a, b] -= S[j, a] S[j, b],
+    // j < a <= b; lanes along a (column-contiguous), warps along b
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
+    for (int b = j + 1 + ty; b < p; b += ny) {
+      const double sjb = S[j + b * p];
+      for (int a = j + 1 + tx; a <= b; a += 32) S[a + b * p] -= S[j + a * p] * sjb;
     }
     __syncthreads();
   }
@@ -542,6 +543,45 @@ int sumsq(int dt, int64_t m, int n, const void* A, int64_t lda, int minus_id, do
   else RB_KLAUNCH sumsq_partial<double><<<grid, kThreads, 0, st>>>(m, n, (const double*)A, lda, minus_id, (double*)ws);
   RB_KLAUNCH sum_vec<<<1, kThreads, 0, st>>>((double*)ws, grid, out);
   return check_launch("rb_sumsq");
+}
+
+// Three binary64 sums of squares in ONE launch (the per-block finiteness
+// words of P_i, S_i and R_ii, rbgs.py:380-388 via Matrix() checks): one
+// CTA per matrix, column loops without integer division.
+struct Mat3 {
+  const double* a[3];
+  int64_t lda[3];
+  int64_t m[3];
+  int n[3];
+};
+
+__global__ void __launch_bounds__(512) sumsq3_kernel(Mat3 M, double* __restrict__ out) {
+  __shared__ double red[16];
+  const int b = blockIdx.x;
+  const double* A = M.a[b];
+  double s = 0.0;
+  for (int j = 0; j < M.n[b]; ++j)
+    for (int64_t i = threadIdx.x; i < M.m[b]; i += blockDim.x) {
+      const double v = A[i + (int64_t)j * M.lda[b]];
+      s += v * v;
+    }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) out[b] = s;
+}
+
+int sumsq3(int64_t m1, int n1, const double* A1, int64_t lda1, int64_t m2, int n2, const double* A2, int64_t lda2,
+           int64_t m3, int n3, const double* A3, int64_t lda3, double* out, cudaStream_t st) {
+  RB_REQUIRE(out && m1 >= 0 && m2 >= 0 && m3 >= 0 && n1 >= 0 && n2 >= 0 && n3 >= 0 &&
+                 (m1 * n1 == 0 || (A1 && lda1 >= m1)) && (m2 * n2 == 0 || (A2 && lda2 >= m2)) &&
+                 (m3 * n3 == 0 || (A3 && lda3 >= m3)),
+             "rb_sumsq3: bad args");
+  Mat3 M;
+  M.a[0] = A1; M.a[1] = A2; M.a[2] = A3;
+  M.lda[0] = lda1; M.lda[1] = lda2; M.lda[2] = lda3;
+  M.m[0] = m1; M.m[1] = m2; M.m[2] = m3;
+  M.n[0] = n1; M.n[1] = n2; M.n[2] = n3;
+  RB_KLAUNCH sumsq3_kernel<<<3, 512, 0, st>>>(M, out);
+  return check_launch("rb_sumsq3");
 }
 
 int convert(int ind, int outd, int64_t m, int n, const void* X, int64_t ldx, void* Y, int64_t ldy, cudaStream_t st) {

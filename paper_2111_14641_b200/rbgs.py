@@ -708,9 +708,12 @@ class RbgsSweep:
             norms[1:2].copy_(norms[0:1])
         Rii, Si, sp_qp = self._interblock(Qp, Pu, slot, block1=(c == 0), sp_given=sp_given)
         # finiteness of everything the block produced (Matrix() checks)
-        D.sumsq(Pi, norms[2:3])
-        D.sumsq(Si, norms[3:4])
-        D.sumsq(Rii, norms[4:5])
+        if Pi.dtype == torch.float64 and Si.dtype == torch.float64 and Rii.dtype == torch.float64:
+            D.sumsq3(Pi, Si, Rii, norms[2:5])
+        else:
+            D.sumsq(Pi, norms[2:3])
+            D.sumsq(Si, norms[3:4])
+            D.sumsq(Rii, norms[4:5])
         if self._deferred is not None:
             # one-shot rbgs(): record this block's status words on the device
             # and carry on without a host round trip; rbgs() checks every
