@@ -15,6 +15,8 @@
 //    per tile, shuffle stages (srht_partial).
 //  * sparse_sign: each row i scatters s signed copies of X[i, :] into a
 //    shared-memory k x CG accumulator.
+#include <type_traits>
+
 #include "common.cuh"
 #include "gauss_layout.cuh"
 #include "tc.cuh"
@@ -70,10 +72,29 @@ dense_partial(int64_t n, int ncols, const TX* __restrict__ X, int64_t ldx, Src s
   for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
     __syncthreads();
     // A tile: BM sketch rows x BK W-rows (K-major source: contiguous in i)
-    for (int e = threadIdx.x; e < BM * BK; e += kThreads) {
-      const int r = e / BK, kk = e % BK;
-      const int64_t i = k0 + kk;
-      sA[kk][r] = (m0 + r < k && i < kend) ? src.at(m0 + r, i) : 0.0;
+    if constexpr (std::is_same<Src, PlaneSrc>::value) {
+      // the gaussian table's 16-row K chunk of a 128-row M tile is one
+      // contiguous 2 KB run per plane (gauss_layout.cuh): one 16-byte load
+      // of each plane per sketch row instead of 32 scalar byte loads
+      static_assert(BK == 16 && BM == 128 && kThreads >= BM, "plane tile loader");
+      if (threadIdx.x < BM) {
+        const int r = threadIdx.x;
+        const uint4 hv = *reinterpret_cast<const uint4*>(src.t + gl::q_offset(0, m0 + r, k0, src.ld));
+        const uint4 lv = *reinterpret_cast<const uint4*>(src.t + gl::q_offset(1, m0 + r, k0, src.ld));
+        const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+          const int hb = (int)(int8_t)((hw[kk >> 2] >> (8 * (kk & 3))) & 255u);
+          const int lb = (int)((lw[kk >> 2] >> (8 * (kk & 3))) & 255u);
+          sA[kk][r] = (m0 + r < k && k0 + kk < kend) ? (double)(hb * 256 + lb) : 0.0;
+        }
+      }
+    } else {
+      for (int e = threadIdx.x; e < BM * BK; e += kThreads) {
+        const int r = e / BK, kk = e % BK;
+        const int64_t i = k0 + kk;
+        sA[kk][r] = (m0 + r < k && i < kend) ? src.at(m0 + r, i) : 0.0;
+      }
     }
     for (int e = threadIdx.x; e < BN * BK; e += kThreads) {
       const int j = e / BK, kk = e % BK;

@@ -22,8 +22,10 @@ namespace rb {
 namespace {
 
 constexpr int kTriLd = 64;
-__constant__ double c_tri_R[kTriLd * kTriLd];  // column-major, ld 64, zero padded
-__constant__ double c_tri_inv[kTriLd];         // 1 / R_jj (0 for j >= p)
+// [0, 64 * 64): R column-major, ld 64, zero padded; then 1 / R_jj (0 for j >= p)
+__constant__ double c_tri[kTriLd * kTriLd + kTriLd];
+#define c_tri_R c_tri
+#define c_tri_inv (c_tri + kTriLd * kTriLd)
 
 __global__ void tri_pack_kernel(int p, const double* __restrict__ R, int64_t ldr, double* __restrict__ dst) {
   for (int e = threadIdx.x; e < kTriLd * kTriLd; e += blockDim.x) {
@@ -45,8 +47,7 @@ inline int load_tri_const(int p, const double* R, int64_t ldr, cudaStream_t st) 
     }
   }
   RB_KLAUNCH tri_pack_kernel<<<1, 256, 0, st>>>(p, R, ldr, staging[dev]);
-  cudaMemcpyToSymbolAsync(c_tri_R, staging[dev], kTriLd * kTriLd * sizeof(double), 0, cudaMemcpyDeviceToDevice, st);
-  cudaMemcpyToSymbolAsync(c_tri_inv, staging[dev] + kTriLd * kTriLd, kTriLd * sizeof(double), 0,
+  cudaMemcpyToSymbolAsync(c_tri, staging[dev], (kTriLd * kTriLd + kTriLd) * sizeof(double), 0,
                           cudaMemcpyDeviceToDevice, st);
   return check_launch("tri_const load");
 }
