@@ -396,6 +396,7 @@ class RbgsSweep:
         # into the next projection (rb_project_trsm): (slot, R_S) or None
         self._fuse_scaling = False
         self._pending_scale = None
+        self._lookahead_event = None  # upload event of the lookahead block (pinned host W)
 
     # -- small utilities ---------------------------------------------------
     def _sketch(self, X, out):
@@ -662,6 +663,7 @@ class RbgsSweep:
             if Wn is not None and c == 0 and self._fusable(W, Wn):
                 Pn = scr.Pn[scr.pn_flip][:, :Wn.shape[1]]
                 scr.pn_flip ^= 1
+                self._wait_lookahead()
                 self._sketch_pair(W, Wn, Pi, Pn)
                 self._next_P = (self._key(Wn), Pn)
                 Wn = None
@@ -697,6 +699,7 @@ class RbgsSweep:
                 sp_given = scr.Sp[:, :w]
                 Pn = scr.Pn[scr.pn_flip][:, :Wn.shape[1]]
                 scr.pn_flip ^= 1
+                self._wait_lookahead()
                 self._sketch_pair(slot, Wn, sp_given, Pn)
                 self._next_P = (self._key(Wn), Pn)
         else:
@@ -734,6 +737,14 @@ class RbgsSweep:
         if cfg.certify_blocks:
             self._certify_block(Si, Rii, sp_qp)
         return j0, j1
+
+    def _wait_lookahead(self):
+        """The stream waits for the upload of the lookahead block (pinned
+        host W in one-shot rbgs()) only where that block is first read."""
+        ev = self._lookahead_event
+        self._lookahead_event = None
+        if ev is not None:
+            torch.cuda.current_stream(self.device).wait_event(ev)
 
     def _flush_scaling(self):
         if self._pending_scale is not None:
@@ -852,10 +863,11 @@ def _sweep_blocks(Wd, n, theta, cfg, dc, q_storage, deferred, events=None):
     for b in range(cfg.partition.num_blocks):
         nxt = Wd[:, off[b + 1]:off[b + 2]] if b + 2 < len(off) else None
         if events is not None:
-            stream = torch.cuda.current_stream(dev)
-            stream.wait_event(events[b])
-            if nxt is not None:
-                stream.wait_event(events[b + 1])
+            # block b needs W_b now; W_(b+1) only for the fused sketch at the
+            # end of block b (waited for there), so the projection of block b
+            # overlaps the upload of W_(b+1)
+            torch.cuda.current_stream(dev).wait_event(events[b])
+            sweep._lookahead_event = events[b + 1] if nxt is not None else None
         sweep.push_block(Wd[:, off[b]:off[b + 1]], lookahead=nxt)
     sweep._flush_scaling()
     return sweep
