@@ -276,20 +276,6 @@ project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq
 #pragma unroll
   for (int t = 0; t < RPT; ++t) v[t] = r0 + t < rend;
 
-  float acc[RPT][PC];
-  double w2 = 0.0;
-#pragma unroll
-  for (int t = 0; t < RPT; ++t)
-#pragma unroll
-    for (int j = 0; j < PC; ++j) {
-      acc[t][j] = 0.f;
-      if (jc + j < p && v[t]) {
-        const TW wv = W[r0 + t + (int64_t)(jc + j) * ldw];
-        w2 += (double)wv * (double)wv;
-        acc[t][j] = to_f32(wv);
-      }
-    }
-
   const int nst = (c + kKQ - 1) / kKQ;
   auto issue_bulk = [&](int s) {  // one thread
     const int b = s % kQS, l0 = s * kKQ, lc = min(kKQ, c - l0);
@@ -323,6 +309,21 @@ project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq
     else if (threadIdx.x == 0) issue_bulk(s);
   }
   __syncthreads();  // tail path: prologue stages written
+
+  // W_i into the accumulators while the first stages are in flight
+  float acc[RPT][PC];
+  double w2 = 0.0;
+#pragma unroll
+  for (int t = 0; t < RPT; ++t)
+#pragma unroll
+    for (int j = 0; j < PC; ++j) {
+      acc[t][j] = 0.f;
+      if (jc + j < p && v[t]) {
+        const TW wv = W[r0 + t + (int64_t)(jc + j) * ldw];
+        w2 += (double)wv * (double)wv;
+        acc[t][j] = to_f32(wv);
+      }
+    }
 
   for (int s = 0; s < nst; ++s) {
     const int b = s % kQS, lc = min(kKQ, c - s * kKQ);
