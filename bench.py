@@ -235,7 +235,9 @@ def gpu_arm(args, cfgd):
     # and replayed -- every kernel of every block per step, plus the host
     # read of the block statuses and the certification.  In-place runs
     # (C5 shard) and --no-graph use the eager one-shot rbgs().
-    use_graph = not inplace and not args.no_graph
+    # (single rank only: NCCL collectives inside a captured graph are not
+    # exercised on this one-GPU pod, so sharded runs stay eager)
+    use_graph = not inplace and not args.no_graph and world == 1
     plan = RbgsPlan(W, theta, cfg, dc) if use_graph else None
 
     def step():
