@@ -959,7 +959,9 @@ int sketch_gaussian2(int xd1, const void* X1, int64_t ld1, int c1, int xd2, cons
              "rb_sketch_gaussian: bad X/theta");
   RB_REQUIRE(mode >= 0 && mode <= 2, "rb_sketch_gaussian: bad mode %d", mode);
   const bool tc = mode == 2 || (mode == 0 && xd1 == RB_F32 && (c2 == 0 || xd2 == RB_F32));
-  if (tc && c1 + c2 <= 96)
+  // > 96 columns: CTA pairs sharing the table stream (RB_TC_PAIR=0: two passes)
+  static const int pair = getenv("RB_TC_PAIR") ? atoi(getenv("RB_TC_PAIR")) : 1;
+  if (tc && (c1 + c2 <= 96 || (pair && c2 > 0)))
     return sketch_gaussian_tc(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, theta, ldt, k, scale, out1, ldo1, out2, ldo2,
                               acc, ws, wsb, st);
   if (tc) {

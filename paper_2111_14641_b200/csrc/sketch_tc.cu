@@ -257,8 +257,18 @@ struct Smem {
 template <int NP, int ST>
 __global__ void __launch_bounds__(kThreads, 1)
 gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt, int k,
-                 const uint8_t* __restrict__ planes, const int* __restrict__ exps, int tiles_per_cta,
-                 double* __restrict__ ws, int dbg) {
+                 const uint8_t* __restrict__ planes1, const int* __restrict__ exps1, int tiles_per_cta,
+                 double* __restrict__ ws1, int dbg, int pairs, int ncols2, const uint8_t* __restrict__ planes2,
+                 const int* __restrict__ exps2, double* __restrict__ ws2) {
+  // pairs == 2: CTAs 2 mt and 2 mt + 1 own the same 128 sketch rows and K
+  // range for two inputs (two column halves of > 96 columns that do not fit
+  // one CTA's TMEM); launched side by side they read each q tile once from
+  // HBM and once from L2.
+  const int half = pairs == 2 ? (int)(blockIdx.x & 1) : 0;
+  const uint8_t* __restrict__ planes = half ? planes2 : planes1;
+  const int* __restrict__ exps = half ? exps2 : exps1;
+  double* __restrict__ ws = half ? ws2 : ws1;
+  if (half) ncols = ncols2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem<NP, ST>& S = *reinterpret_cast<Smem<NP, ST>*>(smem_raw);
   constexpr int kStages = ST;
@@ -269,7 +279,7 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
   static_assert(kGroupCols <= 512, "TMEM: 5 groups x NP columns must fit 512");
   constexpr uint32_t kABytes = 2 * kTM * kBK, kBBytes = 4 * kBK * NP;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int mt = blockIdx.x;
+  const int mt = blockIdx.x / pairs;
   const int64_t KT = ldt / kBK;
   // this CTA's K tiles [kt_beg, kt_end); accumulators drain at every global
   // 8192-row chunk boundary and at kt_end (segments)
@@ -434,14 +444,24 @@ int dbg_flag() {
   return v;
 }
 
+struct Half2 {  // the second input of a paired launch (pairs == 2)
+  int pairs = 1, ncols = 0;
+  const uint8_t* planes = nullptr;
+  const int* exps = nullptr;
+};
+
 template <int NP>
 int launch_np(int64_t n, int ncols, const uint8_t* qt, int64_t ldt, int k, const uint8_t* planes, const int* exps,
-              double* part, size_t part_bytes, int* splits_out, cudaStream_t st) {
+              double* part, size_t part_bytes, int* splits_out, cudaStream_t st, const Half2& h2 = Half2()) {
   const int mt = ceil_div(k, kTM);
-  // one wave: floor(SMs / m-tiles) K ranges of equal tile counts
+  // one wave: floor(SMs / m-tiles) K ranges of equal tile counts.  A paired
+  // launch keeps the same K ranges (two waves of CTA pairs), so each input's
+  // partials -- and the result bits -- equal those of its own launch.
   const int64_t ktn = (n + kBK - 1) / kBK;
   int splits = (int)std::max<int64_t>(1, std::min<int64_t>(ktn, sm_count() / mt));
-  const size_t per = (size_t)k * ncols * sizeof(double);
+  // a paired launch keeps each half's partials in its own half of `part`
+  if (h2.pairs == 2) part_bytes = (part_bytes / 2) & ~(size_t)255;
+  const size_t per = (size_t)k * std::max(ncols, h2.ncols) * sizeof(double);
   if ((size_t)splits * per > part_bytes) splits = (int)std::max<size_t>(1, part_bytes / per);
   RB_REQUIRE((size_t)splits * per <= part_bytes, "gaussian tc: workspace too small");
   const int tpc = (int)((ktn + splits - 1) / splits);
@@ -457,8 +477,9 @@ int launch_np(int64_t n, int ncols, const uint8_t* qt, int64_t ldt, int k, const
   {                                                                                                              \
     const size_t smem = sizeof(Smem<NP, STG>) + 1024;                                                            \
     cudaFuncSetAttribute(gauss_tc_partial<NP, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-    RB_KLAUNCH gauss_tc_partial<NP, STG><<<dim3(mt, splits), kThreads, smem, st>>>(n, ncols, qt, ldt, k, planes, \
-                                                                                  exps, tpc, part, dbg_flag());   \
+    RB_KLAUNCH gauss_tc_partial<NP, STG><<<dim3(mt * h2.pairs, splits), kThreads, smem, st>>>(                              \
+        n, ncols, qt, ldt, k, planes, exps, tpc, part, dbg_flag(), h2.pairs, h2.ncols, h2.planes, h2.exps,       \
+        part + part_bytes / sizeof(double));                                                                     \
   }
   if (st_req >= 4 && kMax >= 4) RB_GL((kMax >= 4 ? 4 : 1))
   else if (st_req >= 3 && kMax >= 3) RB_GL((kMax >= 3 ? 3 : 1))
@@ -484,11 +505,71 @@ void launch_split(int xd2, dim3 g, int64_t n, int c1, const void* X1, int64_t ld
                                                           v1, aligned16(X2, ld2, 8), planes, exps);
 }
 
+template <int NP>
+int launch_pair(int64_t n, int c1, int c2, const uint8_t* qt, int64_t ldt, int k, const uint8_t* pl1, const int* ex1,
+                const uint8_t* pl2, const int* ex2, double* part, size_t part_b, int* splits, cudaStream_t st) {
+  Half2 h2;
+  h2.pairs = 2;
+  h2.ncols = c2;
+  h2.planes = pl2;
+  h2.exps = ex2;
+  return launch_np<NP>(n, c1, qt, ldt, k, pl1, ex1, part, part_b, splits, st, h2);
+}
+
+// [out1 | out2] for c1 + c2 > 96 (each <= 64): the two inputs are split into
+// their own plane sets and sketched by CTA pairs of one launch that share
+// every q tile (one HBM read of the table per pair instead of per input).
+int sketch_gaussian_tc_pair(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2,
+                            int c2, int64_t n, const uint8_t* qt, int64_t ldt, int k, double scale, double* out1,
+                            int64_t ldo1, double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(c1 >= 1 && c2 >= 1 && c1 <= 64 && c2 <= 64 && k >= 1 && out1 && out2 && ldo1 >= k && ldo2 >= k,
+             "rb_sketch_gaussian (tensor pair): bad args (c1 %d, c2 %d)", c1, c2);
+  RB_REQUIRE(n == 0 || (X1 && ld1 >= n && X2 && ld2 >= n && qt && ldt >= n && ldt % kBK == 0),
+             "rb_sketch_gaussian (tensor pair): bad X/theta (ldt %% 128 required)");
+  const int NP = std::max(np_for(c1), np_for(c2));
+  const int nchunks = (int)((n + kChunk - 1) / kChunk);
+  const int64_t ktiles = (int64_t)nchunks * kTPC;
+  const size_t planes_b = (size_t)ktiles * 4 * kBK * NP;
+  const size_t exps_b = ((size_t)NP * nchunks * sizeof(int) + 255) / 256 * 256;
+  RB_REQUIRE(ws && wsb > 2 * (planes_b + exps_b) + 2048, "rb_sketch_gaussian (tensor pair): workspace too small");
+  uint8_t* pl1 = (uint8_t*)ws;
+  int* ex1 = (int*)(pl1 + planes_b);
+  uint8_t* pl2 = pl1 + planes_b + exps_b;
+  int* ex2 = (int*)(pl2 + planes_b);
+  double* part = (double*)(pl2 + planes_b + exps_b);
+  const size_t part_b = wsb - 2 * (planes_b + exps_b);
+  int splits = 0;
+  if (n > 0) {
+    dim3 g(nchunks, NP / 2);
+    if (xd1 == RB_F32) launch_split<float>(RB_F32, g, n, c1, X1, ld1, 0, nullptr, 0, NP, pl1, ex1, st);
+    else launch_split<double>(RB_F32, g, n, c1, X1, ld1, 0, nullptr, 0, NP, pl1, ex1, st);
+    if (xd2 == RB_F32) launch_split<float>(RB_F32, g, n, c2, X2, ld2, 0, nullptr, 0, NP, pl2, ex2, st);
+    else launch_split<double>(RB_F32, g, n, c2, X2, ld2, 0, nullptr, 0, NP, pl2, ex2, st);
+    int rc;
+    switch (NP) {
+      case 16: rc = launch_pair<16>(n, c1, c2, qt, ldt, k, pl1, ex1, pl2, ex2, part, part_b, &splits, st); break;
+      case 32: rc = launch_pair<32>(n, c1, c2, qt, ldt, k, pl1, ex1, pl2, ex2, part, part_b, &splits, st); break;
+      case 48: rc = launch_pair<48>(n, c1, c2, qt, ldt, k, pl1, ex1, pl2, ex2, part, part_b, &splits, st); break;
+      default: rc = launch_pair<64>(n, c1, c2, qt, ldt, k, pl1, ex1, pl2, ex2, part, part_b, &splits, st); break;
+    }
+    if (rc != RB_OK) return rc;
+  }
+  const size_t half_b = (part_b / 2) & ~(size_t)255;
+  double* part2 = part + half_b / sizeof(double);
+  RB_KLAUNCH reduce_splits_tc<<<ceil_div((int64_t)k * c1, 256), 256, 0, st>>>(part, splits, k, c1, c1, scale, out1,
+                                                                             ldo1, nullptr, 0, acc);
+  RB_KLAUNCH reduce_splits_tc<<<ceil_div((int64_t)k * c2, 256), 256, 0, st>>>(part2, splits, k, c2, c2, scale, out2,
+                                                                             ldo2, nullptr, 0, acc);
+  return check_launch("rb_sketch_gaussian (tensor pair)");
+}
+
 }  // namespace
 
 size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k) {
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
-  const int cols = std::max(ncols, 1) <= 48 ? 96 : 96;  // room for a fused two-input call
+  // room for a fused two-input call: <= 96 columns in one CTA, else two
+  // paired halves of <= 64 columns each
+  const int cols = ncols <= 96 ? 96 : 128;
   const size_t planes = (size_t)4 * cols * nchunks * kChunk;
   const size_t exps = ((size_t)cols * nchunks * sizeof(int) + 255) / 256 * 256;
   const size_t part = (size_t)(sm_count() + 1) * std::max(k, 64) * cols * sizeof(double);
@@ -501,6 +582,9 @@ int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, co
                        int64_t n, const uint8_t* qt, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
                        double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st) {
   const int ncols = c1 + c2;
+  if (ncols > 96)
+    return sketch_gaussian_tc_pair(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, qt, ldt, k, scale, out1, ldo1, out2, ldo2,
+                                   acc, ws, wsb, st);
   RB_REQUIRE(c1 >= 1 && c2 >= 0 && ncols <= 96 && k >= 1 && ldo1 >= k && out1 && (c2 == 0 || (out2 && ldo2 >= k)),
              "rb_sketch_gaussian (tensor): bad args (c1 %d, c2 %d)", c1, c2);
   RB_REQUIRE(n == 0 || (X1 && ld1 >= n && (c2 == 0 || (X2 && ld2 >= n)) && qt && ldt >= n && ldt % kBK == 0),

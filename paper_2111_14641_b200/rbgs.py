@@ -640,7 +640,7 @@ class RbgsSweep:
         """Two sketches can share one table pass (gaussian kind, tensor pipe)."""
         return (self.theta.kind == "gaussian" and self.inter[0] in ("sketched_cholqr", "l2_plus_cholqr")
                 and not self.cfg.certify_blocks and A.dtype == torch.float32 and B.dtype == torch.float32
-                and A.shape[1] + B.shape[1] <= 96 and sketching.GAUSS_MODE != "fp64")
+                and A.shape[1] <= 64 and B.shape[1] <= 64 and sketching.GAUSS_MODE != "fp64")
 
     def _sketch_pair(self, A, B, outA, outB):
         tab = self.theta.device_tables(A.device, self.row0, A.shape[0])

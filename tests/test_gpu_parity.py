@@ -179,6 +179,52 @@ def test_gaussian_tensor_pipe_vs_fp64(pkg, n, k, cols):
     assert np.allclose(out.cpu().numpy(), 2 * res["tensor"], rtol=1e-15, atol=0)
 
 
+@pytest.mark.parametrize("c1,c2", [(64, 64), (64, 50), (49, 64)])
+def test_gaussian_tensor_pair_matches_separate_calls(pkg, c1, c2):
+    """More than 96 columns: one launch of CTA pairs sharing the table stream
+    gives, per input, the bits of that input's own launch."""
+    rbgs, sketching, D = pkg
+    n, k = 70_001, 300
+    g = np.random.Generator(np.random.Philox(c1 + c2))
+    X = (g.standard_normal((n, c1 + c2)) * np.logspace(0, -6, c1 + c2)).astype(np.float32)
+    op = sketching.gaussian_operator(k, n, 5)
+    tab = op.device_tables("cuda", 0, n)
+    Xd = _dev(X.astype(np.float64), torch.float32)
+    A, B = Xd[:, :c1], Xd[:, c1:]
+    sc = 1.0 / (2048 * math.sqrt(k))
+    oa, ob = D.empty_cm(k, c1, torch.float64, "cuda"), D.empty_cm(k, c2, torch.float64, "cuda")
+    D.sketch_gaussian2(A, B, tab["theta"], tab["ldt"], k, sc, oa, ob, False, "tensor")
+    sa, sb = D.empty_cm(k, c1, torch.float64, "cuda"), D.empty_cm(k, c2, torch.float64, "cuda")
+    D.sketch_gaussian(A, tab["theta"], tab["ldt"], k, sc, sa, False, "tensor")
+    D.sketch_gaussian(B, tab["theta"], tab["ldt"], k, sc, sb, False, "tensor")
+    assert torch.equal(oa, sa) and torch.equal(ob, sb)
+    want = osk.apply(osk.OracleSketch("gaussian", k, n, 5), X.astype(np.float64))
+    got = np.concatenate([oa.cpu().numpy(), ob.cpu().numpy()], axis=1)
+    for j in range(c1 + c2):
+        wn = np.linalg.norm(want[:, j])
+        assert np.linalg.norm(got[:, j] - want[:, j]) <= 1e-8 * wn, j
+
+
+def test_fused_lookahead_pair_sketch_is_bitwise_neutral(pkg):
+    """p = 64: [Q'_i | W_(i+1)] (128 columns) runs as one paired launch."""
+    rbgs, sketching, D = pkg
+    from paper_2111_14641_b200.kernels import BlockPartition
+    import goldens as G
+
+    n, m, p, k = 20_000, 192, 64, 400
+    W = G.trig_family(n, m, 9).astype(np.float32)
+    th = sketching.gaussian_operator(k, n, 4)
+    cfg = rbgs.RbgsConfig(partition=BlockPartition.uniform(m, p), interblock="sketched_cholqr(1)")
+    f = rbgs.rbgs(W, th, cfg)
+    sw = rbgs.RbgsSweep(n, th, cfg)
+    Wd = _dev(W.astype(np.float64), torch.float32)
+    for b in range(m // p):
+        sw.push_block(Wd[:, b * p:(b + 1) * p])
+    g = sw.finish()
+    assert np.array_equal(f.R.data, g.R.data)
+    assert np.array_equal(f.Q.data, g.Q.data)
+
+
 @pytest.mark.parametrize("kind", ["gaussian", "sparse_sign", "srht"])
 def test_sharded_sketch_sums_to_whole(pkg, kind):
     """Virtual shards on one GPU: per-shard partial sketches (global row
