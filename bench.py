@@ -59,6 +59,30 @@ CONFIGS = {
 SEED_W, SEED_THETA = 7, 11
 
 
+def _dist_setup():
+    """One process per GPU (torchrun env), NCCL.  RB_BENCH_BACKEND=gloo with
+    RB_BENCH_ONE_DEVICE=1 runs every rank on cuda:0 with host-side gloo
+    collectives -- a functional check of the multi-rank path on a one-GPU
+    box (the ranks' kernels never wait on one another); never a timing."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = 0 if os.environ.get("RB_BENCH_ONE_DEVICE") == "1" else int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        backend = os.environ.get("RB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+        group = dist.group.WORLD
+    return world, rank, local, dev, group
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -117,10 +141,12 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # CPU restatement (oracle) -- the reference arm and the cpu_baseline leg
 
-def _oracle_sample(cfgd, n_s):
+def _oracle_sample(cfgd, n_s, parity=False, order="reference"):
     """One RBGS QR of an n_s-row sample of the workload with the CPU oracle;
     the gaussian table is materialised beforehand (operator construction),
-    like the reference's SRHT tables.  Returns seconds."""
+    like the reference's SRHT tables.  Returns seconds -- and with `parity`
+    also the device factorization of the SAME sample checked against it
+    (the oracle as the checker: R drift and both certificates)."""
     from oracle import sketches as osk
     from oracle import sweep as osw
     from paper_2111_14641_b200 import workloads as WL
@@ -137,8 +163,32 @@ def _oracle_sample(cfgd, n_s):
     cfg = osw.OracleConfig(osw.uniform_widths(m, p), interblock="sketched_cholqr(1)",
                            coarse=cfgd["coarse"])
     t0 = time.perf_counter()
-    osw.rbgs(W, op, cfg)
-    return time.perf_counter() - t0
+    sw, cert = osw.rbgs(W, op, cfg)
+    sec = time.perf_counter() - t0
+    if not parity:
+        return sec
+    import torch
+
+    from paper_2111_14641_b200 import sketching
+    from paper_2111_14641_b200.kernels import COARSE, FINE, BlockPartition
+    from paper_2111_14641_b200.rbgs import DeviceConfig, RbgsConfig, rbgs
+
+    theta = (sketching.gaussian_operator(k, n_s, SEED_THETA) if cfgd["kind"] == "gaussian"
+             else sketching.make_operator(cfgd["kind"], k, n_s, SEED_THETA))
+    gcfg = RbgsConfig(partition=BlockPartition.uniform(m, p), interblock="sketched_cholqr(1)",
+                      coarse=COARSE if cfgd["coarse"] == "coarse" else FINE)
+    Wg = W.astype(np.float32) if cfgd["dtype"] == "f32" else W
+    f = rbgs(Wg, theta, gcfg, DeviceConfig(projection_order=order))
+    torch.cuda.synchronize()
+    R, Rref = f.R.data, sw.R
+    par = {"rows": n_s, "oracle": "oracle/ restatement, same W, same seeded operator",
+           "rel_R_diff": float(np.linalg.norm(R - Rref) / np.linalg.norm(Rref)),
+           "max_rel_diag_diff": float(np.max(np.abs(np.diag(R) - np.diag(Rref)) / np.abs(np.diag(Rref)))),
+           "delta": [float(f.cert.delta), float(cert[0])],
+           "delta_tilde": [float(f.cert.delta_tilde), float(cert[1])],
+           "pairs": "[device, oracle]",
+           "tolerance": "R within 1e-5 relative (two-precision) / 1e-10 (fp64), BASELINE north_star"}
+    return sec, par
 
 
 def reference_arm(args, cfgd):
@@ -189,15 +239,7 @@ def gpu_arm(args, cfgd):
     from paper_2111_14641_b200 import rbgs as rbgs_mod
     from paper_2111_14641_b200.rbgs import DeviceConfig, RbgsConfig, RbgsPlan, rbgs
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    group = None
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        group = dist.group.WORLD
+    world, rank, local, dev, group = _dist_setup()
     n_per, m, p, k = cfgd["n"], cfgd["m"], cfgd["p"], cfgd["k"]
     n = n_per * world
     shard = RowShard(n, rank * n_per, n_per)
@@ -370,10 +412,10 @@ def gpu_arm(args, cfgd):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_s = args.sample_rows or 8192
-        sec = _oracle_sample(cfgd, n_s)
+        sec, parity = _oracle_sample(cfgd, n_s, parity=True, order=args.order)
         cpu = {"value": esz * n_s * m / sec / 1e9, "unit": "GB/s", "cores": _CORES, "kind": "port",
                "sample": f"{n_s} x {m} rows of {cfgd['name']}, one factorization, oracle/ restatement "
-                         f"(numpy + OpenBLAS)"}
+                         f"(numpy + OpenBLAS)", "parity": parity}
     if rank == 0:
         line = {
             "metric": "RBGS QR GB/s of W processed", "value": value, "unit": "GB/s", "n_gpus": world,
@@ -413,15 +455,7 @@ def gpu_arm_krylov(args, cfgd):
     from paper_2111_14641_b200.comm import Comm, RowShard
     from paper_2111_14641_b200.rbgs import DeviceConfig, RbgsConfig
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    group = None
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        group = dist.group.WORLD
+    world, rank, local, dev, group = _dist_setup()
     comm = Comm(group) if group else None
     g = cfgd["grid"]
     A = operators.Poisson3D(g, g, g, comm=comm, device=dev)

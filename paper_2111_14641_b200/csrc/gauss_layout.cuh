@@ -30,17 +30,20 @@ __host__ __device__ __forceinline__ int64_t q_bytes(int k, int64_t ldt) {
 
 // X byte planes for NP padded columns, as ONE UMMA B operand per column
 // group: the NP columns are cut into groups of NG = np_group(NP) (so that
-// 4 NG <= 256, the largest MMA N), and within a K chunk the B rows are
-// ordered [group][plane][column], plane 0 = b3 (weight 2^24) .. plane 3 = b0.
-// A tile kt is 4 x kBK x NP bytes, [kc][group][plane][col][16 bytes].
-__host__ __device__ __forceinline__ int np_group(int NP) { return NP <= 64 ? NP : NP / 2; }
+// kXDig NG <= 256, the largest MMA N, and is a multiple of 16 as M = 128
+// requires), and within a K chunk the B rows are ordered
+// [group][plane][column], plane 0 = b5 (weight 2^40) .. plane 5 = b0.
+// A tile kt is kXDig x kBK x NP bytes, [kc][group][plane][col][16 bytes].
+constexpr int kXDig = 6;  // signed byte digits per X entry (46-bit fixed point)
+__host__ __device__ constexpr int np_group(int NP) { return NP <= 40 ? NP : NP == 48 ? 24 : 32; }
 
 __host__ __device__ __forceinline__ int64_t x_offset(int plane, int j, int64_t i, int NP) {
   const int64_t kt = i / kBK;
   const int kc = (int)((i % kBK) >> 4), b = (int)(i & 15);
   const int NG = np_group(NP);
   const int g = j / NG, jj = j % NG;
-  return kt * (4 * (int64_t)kBK * NP) + (int64_t)kc * (4 * NP * 16) + (int64_t)((g * 4 + plane) * NG + jj) * 16 + b;
+  return kt * (kXDig * (int64_t)kBK * NP) + (int64_t)kc * (kXDig * NP * 16) +
+         (int64_t)((g * kXDig + plane) * NG + jj) * 16 + b;
 }
 
 }  // namespace gl

@@ -56,9 +56,17 @@ template <typename TX, typename Src, int TN>
 __global__ void __launch_bounds__(kThreads)
 dense_partial(int64_t n, int ncols, const TX* __restrict__ X, int64_t ldx, Src src, int k,
               int64_t chunk, double* __restrict__ ws) {
+  // Two shared-memory buffers: the global loads of K step t + 1 are issued
+  // into registers before the FMAs of step t and stored to the other buffer
+  // after them (one barrier per step) -- at the small all-fp64 shapes (C1)
+  // the kernel was bound by exposed load latency, not by the FP64 pipe.
+  // Per accumulator the FMA order (kk ascending) is unchanged.
   constexpr int BN = 16 * TN;
-  __shared__ __align__(16) double sA[BK][BM];
-  __shared__ __align__(16) double sB[BK][BN];
+  constexpr int kBE = (BN * BK + kThreads - 1) / kThreads;  // B elements per thread
+  constexpr bool kPlanes = std::is_same<Src, PlaneSrc>::value;
+  constexpr int kAE = kPlanes ? 1 : (BM * BK + kThreads - 1) / kThreads;
+  __shared__ __align__(16) double sA[2][BK][BM];
+  __shared__ __align__(16) double sB[2][BK][BN];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   const int m0 = blockIdx.x * BM;
   const int64_t kbeg = (int64_t)blockIdx.y * chunk;
@@ -69,51 +77,83 @@ dense_partial(int64_t n, int ncols, const TX* __restrict__ X, int64_t ldx, Src s
 #pragma unroll
     for (int b = 0; b < TN; ++b) acc[a][b] = 0.0;
 
-  for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
-    __syncthreads();
-    // A tile: BM sketch rows x BK W-rows (K-major source: contiguous in i)
-    if constexpr (std::is_same<Src, PlaneSrc>::value) {
+  uint4 hv = make_uint4(0, 0, 0, 0), lv = make_uint4(0, 0, 0, 0);
+  double ra[kAE], rb[kBE];
+  auto load = [&](int64_t k0) {
+    if constexpr (kPlanes) {
       // the gaussian table's 16-row K chunk of a 128-row M tile is one
       // contiguous 2 KB run per plane (gauss_layout.cuh): one 16-byte load
-      // of each plane per sketch row instead of 32 scalar byte loads
+      // of each plane per sketch row
       static_assert(BK == 16 && BM == 128 && kThreads >= BM, "plane tile loader");
       if (threadIdx.x < BM) {
+        hv = *reinterpret_cast<const uint4*>(src.t + gl::q_offset(0, m0 + threadIdx.x, k0, src.ld));
+        lv = *reinterpret_cast<const uint4*>(src.t + gl::q_offset(1, m0 + threadIdx.x, k0, src.ld));
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < kAE; ++q) {
+        const int e = threadIdx.x + q * kThreads;
+        const int r = e / BK, kk = e % BK;
+        ra[q] = (e < BM * BK && m0 + r < k && k0 + kk < kend) ? src.at(m0 + r, k0 + kk) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kBE; ++q) {
+      const int e = threadIdx.x + q * kThreads;
+      const int j = e / BK, kk = e % BK;
+      rb[q] = (e < BN * BK && j < ncols && k0 + kk < kend) ? (double)X[k0 + kk + (int64_t)j * ldx] : 0.0;
+    }
+  };
+  auto store = [&](int buf, int64_t k0) {
+    if constexpr (kPlanes) {
+      if (threadIdx.x < BM) {
         const int r = threadIdx.x;
-        const uint4 hv = *reinterpret_cast<const uint4*>(src.t + gl::q_offset(0, m0 + r, k0, src.ld));
-        const uint4 lv = *reinterpret_cast<const uint4*>(src.t + gl::q_offset(1, m0 + r, k0, src.ld));
         const uint32_t hw[4] = {hv.x, hv.y, hv.z, hv.w}, lw[4] = {lv.x, lv.y, lv.z, lv.w};
 #pragma unroll
         for (int kk = 0; kk < BK; ++kk) {
           const int hb = (int)(int8_t)((hw[kk >> 2] >> (8 * (kk & 3))) & 255u);
           const int lb = (int)((lw[kk >> 2] >> (8 * (kk & 3))) & 255u);
-          sA[kk][r] = (m0 + r < k && k0 + kk < kend) ? (double)(hb * 256 + lb) : 0.0;
+          sA[buf][kk][r] = (m0 + r < k && k0 + kk < kend) ? (double)(hb * 256 + lb) : 0.0;
         }
       }
     } else {
-      for (int e = threadIdx.x; e < BM * BK; e += kThreads) {
-        const int r = e / BK, kk = e % BK;
-        const int64_t i = k0 + kk;
-        sA[kk][r] = (m0 + r < k && i < kend) ? src.at(m0 + r, i) : 0.0;
+#pragma unroll
+      for (int q = 0; q < kAE; ++q) {
+        const int e = threadIdx.x + q * kThreads;
+        if (e < BM * BK) sA[buf][e % BK][e / BK] = ra[q];
       }
     }
-    for (int e = threadIdx.x; e < BN * BK; e += kThreads) {
-      const int j = e / BK, kk = e % BK;
-      const int64_t i = k0 + kk;
-      sB[kk][j] = (j < ncols && i < kend) ? (double)X[i + (int64_t)j * ldx] : 0.0;
+#pragma unroll
+    for (int q = 0; q < kBE; ++q) {
+      const int e = threadIdx.x + q * kThreads;
+      if (e < BN * BK) sB[buf][e % BK][e / BK] = rb[q];
     }
-    __syncthreads();
+  };
+
+  int buf = 0;
+  if (kbeg < kend) {
+    load(kbeg);
+    store(0, kbeg);
+  }
+  __syncthreads();
+  for (int64_t k0 = kbeg; k0 < kend; k0 += BK) {
+    const bool more = k0 + BK < kend;
+    if (more) load(k0 + BK);
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
       double a[TM], b[TN];
 #pragma unroll
-      for (int q = 0; q < TM; ++q) a[q] = sA[kk][ty * TM + q];
+      for (int q = 0; q < TM; ++q) a[q] = sA[buf][kk][ty * TM + q];
 #pragma unroll
-      for (int q = 0; q < TN; ++q) b[q] = sB[kk][tx * TN + q];
+      for (int q = 0; q < TN; ++q) b[q] = sB[buf][kk][tx * TN + q];
 #pragma unroll
       for (int q = 0; q < TM; ++q)
 #pragma unroll
         for (int t = 0; t < TN; ++t) acc[q][t] = fma(a[q], b[t], acc[q][t]);
     }
+    if (more) store(buf ^ 1, k0 + BK);
+    __syncthreads();
+    buf ^= 1;
   }
   // partial layout: ws[split][j][r] (column-major k x ncols per split)
   double* dst = ws + (int64_t)blockIdx.y * k * ncols;
@@ -959,9 +999,9 @@ int sketch_gaussian2(int xd1, const void* X1, int64_t ld1, int c1, int xd2, cons
              "rb_sketch_gaussian: bad X/theta");
   RB_REQUIRE(mode >= 0 && mode <= 2, "rb_sketch_gaussian: bad mode %d", mode);
   const bool tc = mode == 2 || (mode == 0 && xd1 == RB_F32 && (c2 == 0 || xd2 == RB_F32));
-  // > 96 columns: CTA pairs sharing the table stream (RB_TC_PAIR=0: two passes)
+  // > 64 columns: CTA pairs sharing the table stream (RB_TC_PAIR=0: two passes)
   static const int pair = getenv("RB_TC_PAIR") ? atoi(getenv("RB_TC_PAIR")) : 1;
-  if (tc && (c1 + c2 <= 96 || (pair && c2 > 0)))
+  if (tc && (c1 + c2 <= 64 || (pair && c2 > 0)))
     return sketch_gaussian_tc(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, theta, ldt, k, scale, out1, ldo1, out2, ldo2,
                               acc, ws, wsb, st);
   if (tc) {

@@ -3,19 +3,25 @@
 //
 // Exact integer split (Ozaki-style):
 //   q  = 256 qh + ql,            qh = q >> 8 (s8), ql = q & 255 (u8)
-//   x ~= xi 2^(E - 30)           per (column, 16384-row chunk); E: every |x|
+//   x ~= xi 2^(E - 46)           per (column, 16384-row chunk); E: every |x|
 //                                of the chunk is < 2^E; xi a signed integer,
-//                                |xi| <= 2^30
-//   xi = b3 2^24 + b2 2^16 + b1 2^8 + b0,   balanced signed digits (all s8)
-// so q xi is a sum of 8 byte products grouped by weight 2^(8w), w = 0..4.
-// One MMA multiplies qh by the four digit planes side by side (N = 4 NG),
+//                                |xi| <= 2^46
+//   xi = b5 2^40 + b4 2^32 + .. + b1 2^8 + b0,  balanced signed digits (s8)
+// so q xi is a sum of 12 byte products grouped by weight 2^(8w), w = 0..6.
+// One MMA multiplies qh by the six digit planes side by side (N = 6 NG),
 // a second multiplies ql by the same operand into TMEM shifted by one block,
 // so each TMEM block accumulates one weight exactly in int32 over one chunk
-// (< 2^16 per row, < 2^30 per chunk).  Blocks are drained to fp64 (exact
-// int64 recombination) and scaled by 2^(E - 30).  Relative to the fp64
-// reference Theta @ X the only errors are fp64 accumulation and the
-// fixed-point rounding of entries far below their chunk's max (absolute
-// 2^(E - 31)).
+// (< 2^16 per row, < 2^30 per chunk).  Blocks are drained to fp64 (int64
+// partial sums, two roundings) and scaled by 2^(E - 46).  Relative to the
+// fp64 reference Theta @ X the only errors are fp64 accumulation and the
+// fixed-point rounding of entries more than 2^22 below their chunk's max
+// (absolute 2^(E - 47)): a binary32 entry within 22 binades of the max is
+// exact, so the sketch carries binary64 accuracy like the CUDA-core path.
+// Why six digits: Step 3 rounds X to binary32 (kernels.py:192-199), so an
+// error of the sketch far below binary32 resolution still flips roundings
+// of X and moves R through the cancellation of the trig family: four digits
+// (2^(E-31)) drifted 4e-5 and five (2^(E-39)) 1.4e-5 / 3.1e-5 from the
+// oracle on C2 samples, the binary64 path 7e-7 / 1.6e-7.
 //
 // Two inputs: the sweep sketches [Q'_i | W_(i+1)] in ONE pass so the q stream
 // (2 bytes per entry, the dominant HBM traffic) is read once per block.
@@ -57,16 +63,16 @@ constexpr int kSplitSeg = kChunk / (16 * kSplitThreads);  // 16-row segments per
 // pipeline depth: as many 128-row stages as fit next to each other in
 // shared memory (overridable with RB_TC_STAGES for measurement)
 template <int NP>
-constexpr int max_stages() { return (227 * 1024 - 2048) / (2 * kTM * kBK + 4 * kBK * NP); }
+constexpr int max_stages() { return (227 * 1024 - 2048) / (2 * kTM * kBK + gl::kXDig * kBK * NP); }
 
 // ---- pre-pass: [X1 | X2] -> tiled byte planes + exponents --------------------------
 // grid (nchunks, NP / 2): one CTA per chunk x column pair; thread t owns 32
 // consecutive rows of both columns (vector loads when aligned), so every
 // plane store is a full 32-byte sector (the two columns' 16-byte segments
 // are adjacent in the layout).  Columns >= ncols are written as zeros (the
-// UMMA N padding).  binary32 inputs are converted in binary32: x 2^(30-E) is
-// an exact power-of-two scaling and |xi| <= 2^30 < 2^31, so the integer is
-// exact; binary64 inputs round once to nearest.
+// UMMA N padding).  The scaling x 2^(46-E) is exact in binary64 and
+// |xi| <= 2^46: binary32 entries within 22 binades of the chunk max convert
+// exactly, the rest (and binary64 inputs) round once to nearest.
 // L2 policy of the binary32 vector loads: the max pass keeps the chunk in L2
 // (evict_last) for the encode pass, which reads it for the last time
 // (evict_first) -- without the hint ncu saw 60% of the re-read miss L2.
@@ -115,50 +121,46 @@ __device__ __forceinline__ void loadL(const T* __restrict__ x, int64_t base, int
   }
 }
 
+// x 2^(46 - E) rounded to an integer (|xi| <= 2^46): the scaling is exact in
+// binary64 (binary32 embeds exactly), so this is the one rounding.
 template <typename T>
-__device__ __forceinline__ uint32_t fixed_of(T v, T s) {
-  if constexpr (sizeof(T) == 4) return (uint32_t)__float2int_rn(v * s);
-  else return (uint32_t)__double2int_rn(v * s);
+__device__ __forceinline__ long long fixed_of(T v, double s) {
+  return __double2ll_rn((double)v * s);
 }
 
-// Balanced signed byte digits: xi = b3 2^24 + b2 2^16 + b1 2^8 + b0 with
-// b0, b1, b2 in [-128, 127] and |b3| <= 65 (|xi| <= 2^30), so every plane is
-// s8 and ONE MMA can take all four planes as its B operand.  Plane order in
-// the layout: 0 = b3, 1 = b2, 2 = b1, 3 = b0 (descending weight).
-__device__ __forceinline__ void digits(int xi, uint32_t& d3, uint32_t& d2, uint32_t& d1, uint32_t& d0) {
-  const int b0 = (int)(int8_t)(xi & 255);
-  xi = (xi - b0) >> 8;
-  const int b1 = (int)(int8_t)(xi & 255);
-  xi = (xi - b1) >> 8;
-  const int b2 = (int)(int8_t)(xi & 255);
-  const int b3 = (xi - b2) >> 8;
-  d0 = (uint32_t)b0 & 255u;
-  d1 = (uint32_t)b1 & 255u;
-  d2 = (uint32_t)b2 & 255u;
-  d3 = (uint32_t)b3 & 255u;
+// Balanced signed byte digits: xi = b5 2^40 + b4 2^32 + .. + b1 2^8 + b0
+// with b0..b4 in [-128, 127] and |b5| <= 65 (|xi| <= 2^46), so every plane
+// is s8 and ONE MMA can take all six planes as its B operand.  Plane order
+// in the layout: 0 = b5, .., 5 = b0 (descending weight).
+__device__ __forceinline__ void digits(long long xi, uint32_t (&d)[gl::kXDig]) {
+#pragma unroll
+  for (int q = gl::kXDig - 1; q > 0; --q) {
+    const long long b = (long long)(int8_t)(xi & 255);
+    d[q] = (uint32_t)b & 255u;
+    xi = (xi - b) >> 8;
+  }
+  d[0] = (uint32_t)xi & 255u;
 }
 
 template <int L, typename T>
-__device__ __forceinline__ void split_column(const T (&v)[L], T s, uint32_t (&w)[L / 16][4][4]) {
+__device__ __forceinline__ void split_column(const T (&v)[L], double s, uint32_t (&w)[L / 16][gl::kXDig][4]) {
   // w[seg][plane][word]
 #pragma unroll
   for (int seg = 0; seg < L / 16; ++seg)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      uint32_t p0 = 0, p1 = 0, p2 = 0, p3 = 0;
+      uint32_t pw[gl::kXDig];
+#pragma unroll
+      for (int pl = 0; pl < gl::kXDig; ++pl) pw[pl] = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        uint32_t d3, d2, d1, d0;
-        digits((int)fixed_of(v[16 * seg + 4 * q + e], s), d3, d2, d1, d0);
-        p0 |= d3 << (8 * e);
-        p1 |= d2 << (8 * e);
-        p2 |= d1 << (8 * e);
-        p3 |= d0 << (8 * e);
+        uint32_t d[gl::kXDig];
+        digits(fixed_of(v[16 * seg + 4 * q + e], s), d);
+#pragma unroll
+        for (int pl = 0; pl < gl::kXDig; ++pl) pw[pl] |= d[pl] << (8 * e);
       }
-      w[seg][0][q] = p0;
-      w[seg][1][q] = p1;
-      w[seg][2][q] = p2;
-      w[seg][3][q] = p3;
+#pragma unroll
+      for (int pl = 0; pl < gl::kXDig; ++pl) w[seg][pl][q] = pw[pl];
     }
 }
 
@@ -215,7 +217,7 @@ split_planes(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, 
     red[1][threadIdx.x >> 5] = mx[1];
   }
   __syncthreads();
-  TV sc[2];
+  double sc[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     float m = 0.f;
@@ -224,7 +226,7 @@ split_planes(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, 
     int E = 0;
     if (m > 0.f) frexpf(m, &E);  // m < 2^E; float rounding is monotone, so every |x| < 2^E
     if (threadIdx.x == 0) exps[(int64_t)c * NP + j0 + h] = E;
-    sc[h] = (TV)ldexp(1.0, 30 - E);
+    sc[h] = ldexp(1.0, 46 - E);
   }
 #pragma unroll 1
   for (int sg = 0; sg < kSplitSeg; ++sg) {
@@ -232,11 +234,11 @@ split_planes(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, 
     TV v[2][16];
     load(0, base, v[0], last{});
     load(1, base, v[1], last{});
-    uint32_t w[2][1][4][4];  // [column][seg][plane][word]
+    uint32_t w[2][1][gl::kXDig][4];  // [column][seg][plane][word]
     split_column(v[0], sc[0], w[0]);
     split_column(v[1], sc[1], w[1]);
 #pragma unroll
-    for (int pl = 0; pl < 4; ++pl) {
+    for (int pl = 0; pl < gl::kXDig; ++pl) {
       uint4* dst = reinterpret_cast<uint4*>(planes + gl::x_offset(pl, j0, base, NP));
       __stcs(dst, make_uint4(w[0][0][pl][0], w[0][0][pl][1], w[0][0][pl][2], w[0][0][pl][3]));
       __stcs(dst + 1, make_uint4(w[1][0][pl][0], w[1][0][pl][1], w[1][0][pl][2], w[1][0][pl][3]));
@@ -248,7 +250,7 @@ template <int NP, int ST>
 struct Smem {
   static constexpr int S = ST;
   uint8_t a[S][2][kBK / 16][kTM][16];  // one q tile
-  uint8_t b[S][kBK / 16][4 * NP][16];  // one X-plane tile: [kc][group, plane, col][16]
+  uint8_t b[S][kBK / 16][gl::kXDig * NP][16];  // one X-plane tile: [kc][group, plane, col][16]
   uint64_t full[S], empty[S];
   uint64_t tfull[2], tempty[2];
   uint32_t tbase;
@@ -261,7 +263,7 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
                  double* __restrict__ ws1, int dbg, int pairs, int ncols2, const uint8_t* __restrict__ planes2,
                  const int* __restrict__ exps2, double* __restrict__ ws2) {
   // pairs == 2: CTAs 2 mt and 2 mt + 1 own the same 128 sketch rows and K
-  // range for two inputs (two column halves of > 96 columns that do not fit
+  // range for two inputs (two column halves of > 64 columns that do not fit
   // one CTA's TMEM); launched side by side they read each q tile once from
   // HBM and once from L2.
   const int half = pairs == 2 ? (int)(blockIdx.x & 1) : 0;
@@ -272,12 +274,13 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   Smem<NP, ST>& S = *reinterpret_cast<Smem<NP, ST>*>(smem_raw);
   constexpr int kStages = ST;
-  constexpr int kGroupCols = 5 * NP;
+  constexpr int kDig = gl::kXDig, kBlk = kDig + 1;  // digit planes, TMEM weight blocks
+  constexpr int kGroupCols = kBlk * NP;
   constexpr int kBufs = (2 * kGroupCols <= 512) ? 2 : 1;
   constexpr uint32_t kAlloc = kBufs * kGroupCols <= 64 ? 64 : kBufs * kGroupCols <= 128 ? 128
                               : kBufs * kGroupCols <= 256 ? 256 : 512;
-  static_assert(kGroupCols <= 512, "TMEM: 5 groups x NP columns must fit 512");
-  constexpr uint32_t kABytes = 2 * kTM * kBK, kBBytes = 4 * kBK * NP;
+  static_assert(kGroupCols <= 512, "TMEM: 7 weight blocks x NP columns must fit 512");
+  constexpr uint32_t kABytes = 2 * kTM * kBK, kBBytes = kDig * kBK * NP;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int mt = blockIdx.x / pairs;
   const int64_t KT = ldt / kBK;
@@ -321,14 +324,15 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       // Per K step and column group g: two MMAs share the B operand
-      // [b3 | b2 | b1 | b0] (N = 4 NG, all s8).  qh x B lands on TMEM blocks
-      // 0..3 of the group, ql x B on blocks 1..4 (D shifted by NG columns), so
-      // block w accumulates exactly the products of weight 2^(32 - 8w).  The
-      // accumulators are zeroed by the epilogue, every MMA accumulates.
-      constexpr int NG = (NP <= 64) ? NP : NP / 2;
+      // [b5 | .. | b0] (N = 6 NG, all s8).  qh x B lands on TMEM blocks
+      // 0..5 of the group, ql x B on blocks 1..6 (D shifted by NG columns),
+      // so block w accumulates exactly the products of weight 2^(48 - 8w).  The accumulators are zeroed by the epilogue, every MMA
+      // accumulates.
+      constexpr int NG = gl::np_group(NP);
       constexpr int NGRP = NP / NG;
-      constexpr uint32_t ID_HI = tc::idesc_i8(kTM, 4 * NG, true, true);
-      constexpr uint32_t ID_LO = tc::idesc_i8(kTM, 4 * NG, false, true);
+      static_assert((kDig * NG) % 16 == 0 && kDig * NG <= 256 && NP % NG == 0, "UMMA N (M = 128)");
+      constexpr uint32_t ID_HI = tc::idesc_i8(kTM, kDig * NG, true, true);
+      constexpr uint32_t ID_LO = tc::idesc_i8(kTM, kDig * NG, false, true);
       int seg_i = 0;
       for (int t = 0; t < T; ++t) {
         const int s = t % kStages;
@@ -347,10 +351,10 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
             const uint64_t al = tc::sdesc_kmajor(tc::smem_u32(&S.a[s][1][2 * ks][0][0]), kTM * 16, 128);
 #pragma unroll
             for (int g = 0; g < NGRP; ++g) {
-              const uint64_t b = tc::sdesc_kmajor(tc::smem_u32(&S.b[s][2 * ks][0][0]) + g * (4 * NG * 16),
-                                                  4 * NP * 16, 128);
-              tc::mma_i8(d + g * 5 * NG, ah, b, ID_HI, 1u);
-              tc::mma_i8(d + g * 5 * NG + NG, al, b, ID_LO, 1u);
+              const uint64_t b = tc::sdesc_kmajor(tc::smem_u32(&S.b[s][2 * ks][0][0]) + g * (kDig * NG * 16),
+                                                  kDig * NP * 16, 128);
+              tc::mma_i8(d + g * kBlk * NG, ah, b, ID_HI, 1u);
+              tc::mma_i8(d + g * kBlk * NG + NG, al, b, ID_LO, 1u);
             }
           }
         }
@@ -363,7 +367,8 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
     }
   } else if (warp >= 4) {
     // ---------------- epilogue ----------------
-    constexpr int NG = (NP <= 64) ? NP : NP / 2;
+    constexpr int NG = gl::np_group(NP);
+    static_assert(NG % 8 == 0, "epilogue drains 8 columns at a time");
     const int q = warp - 4;  // TMEM lane quadrant
     const int r = mt * kTM + q * 32 + lane;
     const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
@@ -388,20 +393,24 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
       const int* ex = exps + chunk * NP;
 #pragma unroll
       for (int c0 = 0; c0 < NP; c0 += 8) {
-        const uint32_t gbase = la + (c0 / NG) * 5 * NG + (c0 % NG);
-        uint32_t g[5][8];
+        const uint32_t gbase = la + (c0 / NG) * kBlk * NG + (c0 % NG);
+        uint32_t g[kBlk][8];
 #pragma unroll
-        for (int w = 0; w < 5; ++w) tc::tmem_ld8(gbase + w * NG, g[w]);
+        for (int w = 0; w < kBlk; ++w) tc::tmem_ld8(gbase + w * NG, g[w]);
         tc::tmem_ld_wait();
 #pragma unroll
-        for (int w = 0; w < 5; ++w) tc::tmem_st8_zero(gbase + w * NG);
+        for (int w = 0; w < kBlk; ++w) tc::tmem_st8_zero(gbase + w * NG);
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
-          // exact integer recombination of the weights 2^32, 2^24, .., 2^0
-          const long long v = ((long long)(int)g[0][jj] << 32) + ((long long)(int)g[1][jj] << 24) +
-                              ((long long)(int)g[2][jj] << 16) + ((long long)(int)g[3][jj] << 8) +
-                              (long long)(int)g[4][jj];
-          acc[c0 + jj] += ldexp((double)v, ex[c0 + jj] - 30);
+          // integer recombination of the weights 2^48, .., 2^0 in two exact
+          // int64 halves (hi: 2^48 .. 2^32 -> < 2^47; lo: 2^24 .. 2^0 ->
+          // < 2^55), then two binary64 roundings
+          const long long hi = ((long long)(int)g[0][jj] << 16) + ((long long)(int)g[1][jj] << 8) +
+                               (long long)(int)g[2][jj];
+          const long long lo = ((long long)(int)g[3][jj] << 24) + ((long long)(int)g[4][jj] << 16) +
+                               ((long long)(int)g[5][jj] << 8) + (long long)(int)g[6][jj];
+          const int e = ex[c0 + jj] - 46;
+          acc[c0 + jj] += ldexp((double)hi, e + 32) + ldexp((double)lo, e);
         }
       }
       tc::tmem_st_wait();
@@ -433,7 +442,7 @@ __global__ void reduce_splits_tc(const double* __restrict__ ws, int splits, int 
   *o = accumulate ? *o + scale * s : scale * s;
 }
 
-int np_for(int ncols) { return ncols <= 16 ? 16 : ncols <= 32 ? 32 : ncols <= 48 ? 48 : ncols <= 64 ? 64 : ncols <= 80 ? 80 : 96; }
+int np_for(int ncols) { return ncols <= 16 ? 16 : ncols <= 32 ? 32 : ncols <= 40 ? 40 : ncols <= 48 ? 48 : 64; }
 
 int dbg_flag() {
   static int v = -1;
@@ -516,7 +525,7 @@ int launch_pair(int64_t n, int c1, int c2, const uint8_t* qt, int64_t ldt, int k
   return launch_np<NP>(n, c1, qt, ldt, k, pl1, ex1, part, part_b, splits, st, h2);
 }
 
-// [out1 | out2] for c1 + c2 > 96 (each <= 64): the two inputs are split into
+// [out1 | out2] for c1 + c2 > 64 (each <= 64): the two inputs are split into
 // their own plane sets and sketched by CTA pairs of one launch that share
 // every q tile (one HBM read of the table per pair instead of per input).
 int sketch_gaussian_tc_pair(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2,
@@ -529,7 +538,7 @@ int sketch_gaussian_tc_pair(int xd1, const void* X1, int64_t ld1, int c1, int xd
   const int NP = std::max(np_for(c1), np_for(c2));
   const int nchunks = (int)((n + kChunk - 1) / kChunk);
   const int64_t ktiles = (int64_t)nchunks * kTPC;
-  const size_t planes_b = (size_t)ktiles * 4 * kBK * NP;
+  const size_t planes_b = (size_t)ktiles * gl::kXDig * kBK * NP;
   const size_t exps_b = ((size_t)NP * nchunks * sizeof(int) + 255) / 256 * 256;
   RB_REQUIRE(ws && wsb > 2 * (planes_b + exps_b) + 2048, "rb_sketch_gaussian (tensor pair): workspace too small");
   uint8_t* pl1 = (uint8_t*)ws;
@@ -549,6 +558,7 @@ int sketch_gaussian_tc_pair(int xd1, const void* X1, int64_t ld1, int c1, int xd
     switch (NP) {
       case 16: rc = launch_pair<16>(n, c1, c2, qt, ldt, k, pl1, ex1, pl2, ex2, part, part_b, &splits, st); break;
       case 32: rc = launch_pair<32>(n, c1, c2, qt, ldt, k, pl1, ex1, pl2, ex2, part, part_b, &splits, st); break;
+      case 40: rc = launch_pair<40>(n, c1, c2, qt, ldt, k, pl1, ex1, pl2, ex2, part, part_b, &splits, st); break;
       case 48: rc = launch_pair<48>(n, c1, c2, qt, ldt, k, pl1, ex1, pl2, ex2, part, part_b, &splits, st); break;
       default: rc = launch_pair<64>(n, c1, c2, qt, ldt, k, pl1, ex1, pl2, ex2, part, part_b, &splits, st); break;
     }
@@ -567,10 +577,10 @@ int sketch_gaussian_tc_pair(int xd1, const void* X1, int64_t ld1, int c1, int xd
 
 size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k) {
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
-  // room for a fused two-input call: <= 96 columns in one CTA, else two
+  // room for a fused two-input call: <= 64 columns in one CTA, else two
   // paired halves of <= 64 columns each
-  const int cols = ncols <= 96 ? 96 : 128;
-  const size_t planes = (size_t)4 * cols * nchunks * kChunk;
+  const int cols = ncols <= 64 ? 64 : 128;
+  const size_t planes = (size_t)gl::kXDig * cols * nchunks * kChunk;
   const size_t exps = ((size_t)cols * nchunks * sizeof(int) + 255) / 256 * 256;
   const size_t part = (size_t)(sm_count() + 1) * std::max(k, 64) * cols * sizeof(double);
   return planes + exps + part + 1024;
@@ -582,17 +592,17 @@ int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, co
                        int64_t n, const uint8_t* qt, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
                        double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st) {
   const int ncols = c1 + c2;
-  if (ncols > 96)
+  if (ncols > 64)
     return sketch_gaussian_tc_pair(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, qt, ldt, k, scale, out1, ldo1, out2, ldo2,
                                    acc, ws, wsb, st);
-  RB_REQUIRE(c1 >= 1 && c2 >= 0 && ncols <= 96 && k >= 1 && ldo1 >= k && out1 && (c2 == 0 || (out2 && ldo2 >= k)),
+  RB_REQUIRE(c1 >= 1 && c2 >= 0 && ncols <= 64 && k >= 1 && ldo1 >= k && out1 && (c2 == 0 || (out2 && ldo2 >= k)),
              "rb_sketch_gaussian (tensor): bad args (c1 %d, c2 %d)", c1, c2);
   RB_REQUIRE(n == 0 || (X1 && ld1 >= n && (c2 == 0 || (X2 && ld2 >= n)) && qt && ldt >= n && ldt % kBK == 0),
              "rb_sketch_gaussian (tensor): bad X/theta (ldt %% 128 required)");
   const int NP = np_for(ncols);
   const int nchunks = (int)((n + kChunk - 1) / kChunk);
   const int64_t ktiles = (int64_t)nchunks * kTPC;
-  const size_t planes_b = (size_t)ktiles * 4 * kBK * NP;
+  const size_t planes_b = (size_t)ktiles * gl::kXDig * kBK * NP;
   const size_t exps_b = ((size_t)NP * nchunks * sizeof(int) + 255) / 256 * 256;
   RB_REQUIRE(ws && wsb > planes_b + exps_b + 1024, "rb_sketch_gaussian (tensor): workspace too small");
   uint8_t* planes = (uint8_t*)ws;
@@ -608,10 +618,10 @@ int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, co
     switch (NP) {
       case 16: rc = launch_np<16>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st); break;
       case 32: rc = launch_np<32>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st); break;
+      case 40: rc = launch_np<40>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st); break;
       case 48: rc = launch_np<48>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st); break;
       case 64: rc = launch_np<64>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st); break;
-      case 80: rc = launch_np<80>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st); break;
-      default: rc = launch_np<96>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st); break;
+      default: rc = launch_np<64>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st); break;
     }
     if (rc != RB_OK) return rc;
   }

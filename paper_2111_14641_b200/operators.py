@@ -176,6 +176,10 @@ class Poisson3D(LinearOperator):
         first = Xd[:plane].contiguous()
         last = Xd[-plane:].contiguous()
         g = comm.group
+        # gloo has no device-memory point-to-point: stage the planes on the host
+        staged = Xd.is_cuda and dist.get_backend(g) != "nccl"
+        if staged:
+            first, last = first.cpu(), last.cpu()
         if rank > 0:
             lo = torch.empty_like(first)
             ops += [dist.P2POp(dist.isend, first, dist.get_global_rank(g, rank - 1) if g else rank - 1, g),
@@ -186,6 +190,9 @@ class Poisson3D(LinearOperator):
                     dist.P2POp(dist.irecv, hi, dist.get_global_rank(g, rank + 1) if g else rank + 1, g)]
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+        if staged:
+            lo = lo.to(Xd.device) if lo is not None else None
+            hi = hi.to(Xd.device) if hi is not None else None
         # contiguous (plane, cols) row-major -> column-major views
         to = lambda t: D.to_cm(t) if t is not None else None
         return to(lo), to(hi)

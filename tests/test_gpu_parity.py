@@ -144,7 +144,7 @@ def test_sketch_vs_oracle(pkg, kind, dtype):
     want = osk.apply(oop, X)
     # binary32 gaussian sketches run on the tensor pipe (exact byte-split
     # products, inputs fixed-point at 2^-30 of each 8192-row chunk max)
-    tol = 1e-9 if (kind == "gaussian" and dtype == torch.float32) else 1e-13
+    tol = 1e-11 if (kind == "gaussian" and dtype == torch.float32) else 1e-13
     assert np.linalg.norm(got - want) <= tol * np.linalg.norm(want), kind
 
 
@@ -170,7 +170,7 @@ def test_gaussian_tensor_pipe_vs_fp64(pkg, n, k, cols):
     for j in range(cols):
         wn = np.linalg.norm(want[:, j])
         assert np.linalg.norm(res["fp64"][:, j] - want[:, j]) <= 1e-13 * wn
-        assert np.linalg.norm(res["tensor"][:, j] - want[:, j]) <= 1e-8 * wn, (j, np.linalg.norm(
+        assert np.linalg.norm(res["tensor"][:, j] - want[:, j]) <= 1e-11 * wn, (j, np.linalg.norm(
             res["tensor"][:, j] - want[:, j]) / wn)
     # accumulate flag adds
     out = D.empty_cm(k, cols, torch.float64, "cuda")
@@ -202,7 +202,7 @@ def test_gaussian_tensor_pair_matches_separate_calls(pkg, c1, c2):
     got = np.concatenate([oa.cpu().numpy(), ob.cpu().numpy()], axis=1)
     for j in range(c1 + c2):
         wn = np.linalg.norm(want[:, j])
-        assert np.linalg.norm(got[:, j] - want[:, j]) <= 1e-8 * wn, j
+        assert np.linalg.norm(got[:, j] - want[:, j]) <= 1e-11 * wn, j
 
 
 def test_fused_lookahead_pair_sketch_is_bitwise_neutral(pkg):
@@ -597,3 +597,19 @@ def test_fused_scaling_is_bitwise_neutral(pkg):
         assert np.array_equal(a.Q.data, b.Q.data)
         assert np.array_equal(a.R.data, b.R.data)
         assert np.array_equal(a.S.data, b.S.data)
+
+
+@pytest.mark.parametrize("config", ["c2", "c1"])
+def test_bench_workload_sample_vs_oracle(pkg, config):
+    """The bench workload's own shape (same m, p, k, sketch kind and input
+    family) on an 8192-row sample: R against the CPU oracle within the
+    north-star tolerance, certificates of the same order (bench.py reports
+    the same numbers in cpu_baseline.parity)."""
+    import bench
+
+    cfgd = bench.CONFIGS[config]
+    _, par = bench._oracle_sample(cfgd, 8192, parity=True)
+    tol = 1e-5 if cfgd["coarse"] == "coarse" else 1e-10
+    assert par["rel_R_diff"] <= tol, par
+    d, do = par["delta"]
+    assert abs(d - do) <= 0.05 * do + 1e-12, par
