@@ -83,6 +83,24 @@ def _dist_setup():
     return world, rank, local, dev, group
 
 
+def _h2d_link(Wh, dev):
+    """Raw pinned host -> device copy bandwidth of this box (GB/s, best of
+    3, CUDA events): the floor under `e2e`, which moves all of W every step."""
+    import torch
+    src = Wh.t()[: max(1, (1 << 29) // (Wh.shape[0] * Wh.element_size()))]  # ~512 MB of contiguous rows
+    dst = torch.empty(src.shape, dtype=src.dtype, device=dev)
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dst.copy_(src, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = max(best, src.numel() * src.element_size() / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    del dst
+    return best
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -361,9 +379,12 @@ def gpu_arm(args, cfgd):
             rbgs(Wh, theta, cfg, dc).R.data
         barrier()
         t0 = time.perf_counter()
+        each = []
         for _ in range(e2e_steps):
+            ts = time.perf_counter()
             fe = rbgs(Wh, theta, cfg, dc)
             Rh = fe.R.data  # device -> host read of the result
+            each.append((time.perf_counter() - ts) * 1e3)
         barrier()
         sec = (time.perf_counter() - t0) / e2e_steps
         if group is not None:
@@ -371,7 +392,8 @@ def gpu_arm(args, cfgd):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             sec = float(t.item())
         e2e = {"value": wbytes / sec / 1e9, "unit": "GB/s", "h2d_bytes_per_step": esz * n_per * m,
-               "d2h_bytes_per_step": int(Rh.nbytes), "ms_per_step": sec * 1e3}
+               "d2h_bytes_per_step": int(Rh.nbytes), "ms_per_step": sec * 1e3,
+               "ms_each": [round(x, 2) for x in each], "h2d_link_GBps": _h2d_link(Wh, dev)}
 
     # --- roofline of the dominant kernel ---
     hbm, bf16, src = _peaks()
@@ -402,6 +424,20 @@ def gpu_arm(args, cfgd):
             roof["compute_bound"] = {"pipe": "fp32 (FMUL+FADD, reference order)", "achieved": fach,
                                      "peak": fpeak, "unit": "TFLOP/s", "frac": fach / fpeak,
                                      "flops_per_launch": d["flops"] / d["calls"]}
+        if name == "sketch_gaussian" and esz == 4:
+            # The exact six-digit split runs 12 int8 byte
+            # products per (Theta entry, X entry) on the tensor pipe, with M
+            # padded to 128 sketch rows: the binding roofline is the int8
+            # tensor pipe, 148 SMs x 16384 int8 ops per SM clock (dense).
+            mhz = (clk_summary or {}).get("sm_mhz") or 1965.0
+            ipeak = 148 * 16384 * mhz * 1e6 / 1e12
+            kpad = -(-k // 128) * 128
+            iops = d["flops"] * 12 * kpad / k
+            roof["compute_bound"] = {"pipe": "int8 tensor (tcgen05 kind::i8, 12 byte products per entry)",
+                                     "achieved": iops / (d["ms"] * 1e-3) / 1e12, "peak": ipeak,
+                                     "unit": "TOP/s", "frac": iops / (d["ms"] * 1e-3) / 1e12 / ipeak,
+                                     "ops_per_launch": iops / d["calls"],
+                                     "note": "timed per call incl. the split_planes pre-pass and the split-K reduce"}
     kernels = {kname: {"ms_per_step": d["ms"] / kscale, "calls_per_step": d["calls"] / kscale,
                        "GBps": d["bytes"] / (d["ms"] * 1e-3) / 1e9,
                        "TFLOPs": d["flops"] / (d["ms"] * 1e-3) / 1e12}

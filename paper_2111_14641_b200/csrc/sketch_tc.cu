@@ -122,43 +122,60 @@ __device__ __forceinline__ void loadL(const T* __restrict__ x, int64_t base, int
 }
 
 // x 2^(46 - E) rounded to an integer (|xi| <= 2^46): the scaling is exact in
-// binary64 (binary32 embeds exactly), so this is the one rounding.
-template <typename T>
-__device__ __forceinline__ long long fixed_of(T v, double s) {
-  return __double2ll_rn((double)v * s);
+// binary64 (binary32 embeds exactly), so this is the one rounding.  For a
+// binary32 x and 2^(46 - E) a normal binary32 (fast), the binary32 product is
+// exact too (|x 2^(46-E)| < 2^46; a product below 2^-126 rounds to integer 0
+// either way), so the binary32 path gives the same integer with no FP64 op.
+struct Scale {
+  double s;
+  float sf;
+  bool fast;
+};
+__device__ __forceinline__ long long fixed_of(float v, const Scale& s) {
+  return s.fast ? __float2ll_rn(__fmul_rn(v, s.sf)) : __double2ll_rn((double)v * s.s);
 }
+__device__ __forceinline__ long long fixed_of(double v, const Scale& s) { return __double2ll_rn(v * s.s); }
 
 // Balanced signed byte digits: xi = b5 2^40 + b4 2^32 + .. + b1 2^8 + b0
 // with b0..b4 in [-128, 127] and |b5| <= 65 (|xi| <= 2^46), so every plane
 // is s8 and ONE MMA can take all six planes as its B operand.  Plane order
 // in the layout: 0 = b5, .., 5 = b0 (descending weight).
-__device__ __forceinline__ void digits(long long xi, uint32_t (&d)[gl::kXDig]) {
+// Computed without a digit loop: y = xi + 0x80_8080_8080 has the unsigned
+// bytes b_q + 128 (q < 5) and y >> 40 = b5 (the balanced representation is
+// unique, so these are the digits), i.e. byte q of y XOR 0x80 is b_q and
+// byte 5 of y is b5.  Four entries' words are byte-transposed into one word
+// per plane (entry e in byte e).
+__device__ __forceinline__ void planes4(const long long (&xi)[4], uint32_t (&pw)[gl::kXDig]) {
+  uint32_t lo[4], hi[4];
 #pragma unroll
-  for (int q = gl::kXDig - 1; q > 0; --q) {
-    const long long b = (long long)(int8_t)(xi & 255);
-    d[q] = (uint32_t)b & 255u;
-    xi = (xi - b) >> 8;
+  for (int e = 0; e < 4; ++e) {
+    const unsigned long long y = (unsigned long long)xi[e] + 0x8080808080ull;
+    lo[e] = (uint32_t)y;
+    hi[e] = (uint32_t)(y >> 32);
   }
-  d[0] = (uint32_t)xi & 255u;
+  const uint32_t t01l = __byte_perm(lo[0], lo[1], 0x5140), t01h = __byte_perm(lo[0], lo[1], 0x7362);
+  const uint32_t t23l = __byte_perm(lo[2], lo[3], 0x5140), t23h = __byte_perm(lo[2], lo[3], 0x7362);
+  const uint32_t u01 = __byte_perm(hi[0], hi[1], 0x5140), u23 = __byte_perm(hi[2], hi[3], 0x5140);
+  pw[5] = __byte_perm(t01l, t23l, 0x5410) ^ 0x80808080u;  // b0
+  pw[4] = __byte_perm(t01l, t23l, 0x7632) ^ 0x80808080u;  // b1
+  pw[3] = __byte_perm(t01h, t23h, 0x5410) ^ 0x80808080u;  // b2
+  pw[2] = __byte_perm(t01h, t23h, 0x7632) ^ 0x80808080u;  // b3
+  pw[1] = __byte_perm(u01, u23, 0x5410) ^ 0x80808080u;    // b4
+  pw[0] = __byte_perm(u01, u23, 0x7632);                  // b5
 }
 
 template <int L, typename T>
-__device__ __forceinline__ void split_column(const T (&v)[L], double s, uint32_t (&w)[L / 16][gl::kXDig][4]) {
+__device__ __forceinline__ void split_column(const T (&v)[L], const Scale& s, uint32_t (&w)[L / 16][gl::kXDig][4]) {
   // w[seg][plane][word]
 #pragma unroll
   for (int seg = 0; seg < L / 16; ++seg)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
+      long long xi[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) xi[e] = fixed_of(v[16 * seg + 4 * q + e], s);
       uint32_t pw[gl::kXDig];
-#pragma unroll
-      for (int pl = 0; pl < gl::kXDig; ++pl) pw[pl] = 0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        uint32_t d[gl::kXDig];
-        digits(fixed_of(v[16 * seg + 4 * q + e], s), d);
-#pragma unroll
-        for (int pl = 0; pl < gl::kXDig; ++pl) pw[pl] |= d[pl] << (8 * e);
-      }
+      planes4(xi, pw);
 #pragma unroll
       for (int pl = 0; pl < gl::kXDig; ++pl) w[seg][pl][q] = pw[pl];
     }
@@ -172,10 +189,11 @@ __device__ __forceinline__ float column_max(const T (&v)[L]) {
   return m;
 }
 
-template <typename T1, typename T2>
-__global__ void __launch_bounds__(kSplitThreads)
+template <typename T1, typename T2, int MINB>
+__global__ void __launch_bounds__(kSplitThreads, MINB)
 split_planes(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, const T2* __restrict__ X2,
-             int64_t ld2, int NP, bool vec1, bool vec2, uint8_t* __restrict__ planes, int* __restrict__ exps) {
+             int64_t ld2, int NP, bool vec1, bool vec2, uint8_t* __restrict__ planes, int* __restrict__ exps,
+             bool slow) {
   // Two passes over the CTA's chunk x column pair, kSplitSeg segments of 16
   // rows per thread: the max pass reads with normal caching so that the
   // encode pass re-reads from L2; the encode pass converts both columns of
@@ -217,7 +235,7 @@ split_planes(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, 
     red[1][threadIdx.x >> 5] = mx[1];
   }
   __syncthreads();
-  double sc[2];
+  Scale sc[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     float m = 0.f;
@@ -226,14 +244,26 @@ split_planes(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, 
     int E = 0;
     if (m > 0.f) frexpf(m, &E);  // m < 2^E; float rounding is monotone, so every |x| < 2^E
     if (threadIdx.x == 0) exps[(int64_t)c * NP + j0 + h] = E;
-    sc[h] = ldexp(1.0, 46 - E);
+    sc[h].s = ldexp(1.0, 46 - E);
+    sc[h].fast = 46 - E >= -126 && 46 - E <= 127 && !slow;
+    sc[h].sf = sc[h].fast ? (float)sc[h].s : 1.f;
   }
+  // encode pass, software-pipelined: segment sg + 1 is in flight while sg
+  // is converted and stored
+  TV v[2][16], vn[2][16];
+  load(0, row0(0), vn[0], last{});
+  load(1, row0(0), vn[1], last{});
 #pragma unroll 1
   for (int sg = 0; sg < kSplitSeg; ++sg) {
     const int64_t base = row0(sg);
-    TV v[2][16];
-    load(0, base, v[0], last{});
-    load(1, base, v[1], last{});
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[h][e] = vn[h][e];
+    if (sg + 1 < kSplitSeg) {
+      load(0, row0(sg + 1), vn[0], last{});
+      load(1, row0(sg + 1), vn[1], last{});
+    }
     uint32_t w[2][1][gl::kXDig][4];  // [column][seg][plane][word]
     split_column(v[0], sc[0], w[0]);
     split_column(v[1], sc[1], w[1]);
@@ -243,6 +273,109 @@ split_planes(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, 
       __stcs(dst, make_uint4(w[0][0][pl][0], w[0][0][pl][1], w[0][0][pl][2], w[0][0][pl][3]));
       __stcs(dst + 1, make_uint4(w[1][0][pl][0], w[1][0][pl][1], w[1][0][pl][2], w[1][0][pl][3]));
     }
+  }
+}
+
+// ---- pre-pass as two streaming kernels (default) ---------------------------------
+// chunk_max: grid (nchunks, NP), one CTA per (chunk, column): every thread
+// keeps 16 vector loads in flight, then a CTA max -> the chunk exponent E.
+// encode: one thread per (16-row segment, column pair), no barrier and few
+// registers, so many segments are in flight per SM; it converts exactly as
+// split_planes does (same exponents, same integers, same plane bytes).
+template <typename T1, typename T2>
+__device__ __forceinline__ const void* col_ptr(int j, int c1, const T1* X1, int64_t ld1, int c2, const T2* X2,
+                                               int64_t ld2) {
+  if (j < c1) return X1 + (int64_t)j * ld1;
+  if (j < c1 + c2) return X2 + (int64_t)(j - c1) * ld2;
+  return nullptr;
+}
+
+template <typename T1, typename T2>
+__global__ void __launch_bounds__(256)
+chunk_max(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, const T2* __restrict__ X2, int64_t ld2,
+          int NP, bool vec1, bool vec2, int* __restrict__ exps) {
+  __shared__ float red[8];
+  const int c = blockIdx.x, j = blockIdx.y;
+  const int64_t r0 = (int64_t)c * kChunk;
+  float m = 0.f;
+  if (j < c1 + c2) {
+    const bool one = j < c1;
+    const bool vec = one ? vec1 : vec2;
+    if (one && sizeof(T1) == 4 && vec && r0 + kChunk <= n) {
+      const float4* p = reinterpret_cast<const float4*>(X1 + (int64_t)j * ld1 + r0);
+      float4 f[kChunk / 4 / 256];
+#pragma unroll
+      for (int i = 0; i < kChunk / 4 / 256; ++i) f[i] = __ldg(p + threadIdx.x + 256 * i);
+#pragma unroll
+      for (int i = 0; i < kChunk / 4 / 256; ++i)
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(f[i].x), fabsf(f[i].y)), fmaxf(fabsf(f[i].z), fabsf(f[i].w))));
+    } else if (!one && sizeof(T2) == 4 && vec && r0 + kChunk <= n) {
+      const float4* p = reinterpret_cast<const float4*>(X2 + (int64_t)(j - c1) * ld2 + r0);
+      float4 f[kChunk / 4 / 256];
+#pragma unroll
+      for (int i = 0; i < kChunk / 4 / 256; ++i) f[i] = __ldg(p + threadIdx.x + 256 * i);
+#pragma unroll
+      for (int i = 0; i < kChunk / 4 / 256; ++i)
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(f[i].x), fabsf(f[i].y)), fmaxf(fabsf(f[i].z), fabsf(f[i].w))));
+    } else {
+      const int64_t r1 = min(n, r0 + kChunk);
+      for (int64_t r = r0 + threadIdx.x; r < r1; r += 256) {
+        const double v = one ? (double)X1[(int64_t)j * ld1 + r] : (double)X2[(int64_t)(j - c1) * ld2 + r];
+        m = fmaxf(m, (float)fabs(v));
+      }
+    }
+  }
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float mm = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) mm = fmaxf(mm, red[q]);
+    int E = 0;
+    if (mm > 0.f) frexpf(mm, &E);  // mm < 2^E; float rounding is monotone, so every |x| < 2^E
+    exps[(int64_t)c * NP + j] = E;
+  }
+}
+
+template <typename T1, typename T2>
+__global__ void __launch_bounds__(256, 4)
+encode_planes(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, const T2* __restrict__ X2,
+              int64_t ld2, int NP, bool vec1, bool vec2, int64_t nseg, const int* __restrict__ exps,
+              uint8_t* __restrict__ planes) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= nseg * (NP / 2)) return;
+  // column pairs fastest: the pairs of one segment write each plane's
+  // NG x 16-byte run of the tile contiguously (whole lines per warp)
+  const int64_t seg = idx / (NP / 2);
+  const int j0 = 2 * (int)(idx % (NP / 2));
+  const int64_t base = seg * 16;
+  const int64_t chunk = base / kChunk;
+  using TV = typename std::conditional<sizeof(T1) == 4 && sizeof(T2) == 4, float, double>::type;
+  TV v[2][16];
+  Scale sc[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int j = j0 + h;
+    if (j < c1) loadL<16, T1, TV>(X1 + (int64_t)j * ld1, base, n, vec1, v[h]);
+    else if (j < c1 + c2) loadL<16, T2, TV>(X2 + (int64_t)(j - c1) * ld2, base, n, vec2, v[h]);
+    else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[h][e] = TV(0);  // UMMA N padding
+    }
+    const int E = __ldg(exps + chunk * NP + j);
+    sc[h].s = ldexp(1.0, 46 - E);
+    sc[h].fast = 46 - E >= -126 && 46 - E <= 127;
+    sc[h].sf = sc[h].fast ? (float)sc[h].s : 1.f;
+  }
+  uint32_t w[2][1][gl::kXDig][4];  // [column][seg][plane][word]
+  split_column(v[0], sc[0], w[0]);
+  split_column(v[1], sc[1], w[1]);
+#pragma unroll
+  for (int pl = 0; pl < gl::kXDig; ++pl) {
+    uint4* dst = reinterpret_cast<uint4*>(planes + gl::x_offset(pl, j0, base, NP));
+    __stcs(dst, make_uint4(w[0][0][pl][0], w[0][0][pl][1], w[0][0][pl][2], w[0][0][pl][3]));
+    __stcs(dst + 1, make_uint4(w[1][0][pl][0], w[1][0][pl][1], w[1][0][pl][2], w[1][0][pl][3]));
   }
 }
 
@@ -505,13 +638,36 @@ bool aligned16(const void* p, int64_t ld, int esz) {
 template <typename T1>
 void launch_split(int xd2, dim3 g, int64_t n, int c1, const void* X1, int64_t ld1, int c2, const void* X2, int64_t ld2,
                   int NP, uint8_t* planes, int* exps, cudaStream_t st) {
+  // RB_SPLIT_MODE=1: the single-kernel two-pass split_planes (kept for
+  // measurement); default: chunk_max + encode_planes (same bytes).
+  // RB_SPLIT_SLOW=1: binary64 conversion for binary32 inputs too (the
+  // cross-check of the binary32 fast path -- same integers by construction)
+  static int mode = -1, slow = 0;
+  if (mode < 0) {
+    const char* e = getenv("RB_SPLIT_MODE");
+    mode = e ? atoi(e) : 2;
+    const char* s = getenv("RB_SPLIT_SLOW");
+    slow = s ? atoi(s) : 0;
+  }
   const bool v1 = aligned16(X1, ld1, sizeof(T1));
-  if (xd2 == RB_F32)
-    RB_KLAUNCH split_planes<T1, float><<<g, kSplitThreads, 0, st>>>(n, c1, (const T1*)X1, ld1, c2, (const float*)X2, ld2, NP, v1,
-                                                         aligned16(X2, ld2, 4), planes, exps);
-  else
-    RB_KLAUNCH split_planes<T1, double><<<g, kSplitThreads, 0, st>>>(n, c1, (const T1*)X1, ld1, c2, (const double*)X2, ld2, NP,
-                                                          v1, aligned16(X2, ld2, 8), planes, exps);
+  const int64_t nseg = (int64_t)g.x * (kChunk / 16);
+#define RB_SPL(T2)                                                                                               \
+  do {                                                                                                           \
+    const bool v2 = aligned16(X2, ld2, sizeof(T2));                                                              \
+    if (mode == 1 || slow) {                                                                                     \
+      RB_KLAUNCH split_planes<T1, T2, 3><<<g, kSplitThreads, 0, st>>>(n, c1, (const T1*)X1, ld1, c2,             \
+                                                                      (const T2*)X2, ld2, NP, v1, v2, planes,    \
+                                                                      exps, slow != 0);                          \
+    } else {                                                                                                     \
+      RB_KLAUNCH chunk_max<T1, T2><<<dim3(g.x, NP), 256, 0, st>>>(n, c1, (const T1*)X1, ld1, c2, (const T2*)X2,   \
+                                                                  ld2, NP, v1, v2, exps);                        \
+      RB_KLAUNCH encode_planes<T1, T2><<<(unsigned)ceil_div(nseg * (NP / 2), 256), 256, 0, st>>>(                \
+          n, c1, (const T1*)X1, ld1, c2, (const T2*)X2, ld2, NP, v1, v2, nseg, exps, planes);                    \
+    }                                                                                                            \
+  } while (0)
+  if (xd2 == RB_F32) RB_SPL(float);
+  else RB_SPL(double);
+#undef RB_SPL
 }
 
 template <int NP>
