@@ -486,7 +486,9 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
             for (int g = 0; g < NGRP; ++g) {
               const uint64_t b = tc::sdesc_kmajor(tc::smem_u32(&S.b[s][2 * ks][0][0]) + g * (kDig * NG * 16),
                                                   kDig * NP * 16, 128);
-              tc::mma_i8(d + g * kBlk * NG, ah, b, ID_HI, 1u);
+              // the first qh MMA of a segment overwrites blocks 0..5 (no
+              // zeroing needed); block 6 (ql x b0 only) is zeroed by the epilogue
+              tc::mma_i8(d + g * kBlk * NG, ah, b, ID_HI, (seg_first && ks == 0) ? 0u : 1u);
               tc::mma_i8(d + g * kBlk * NG + NG, al, b, ID_LO, 1u);
             }
           }
@@ -524,6 +526,10 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
       tc::tc_fence_after();
       const uint32_t la = lane_base + buf * kGroupCols;
       const int* ex = exps + chunk * NP;
+      // With room for a second register copy (NP <= 40), the chunk's terms
+      // are staged in t[] and TMEM is handed back before the fp64 adds.
+      constexpr bool kStage = NP <= 40;
+      double t[kStage ? NP : 1];
 #pragma unroll
       for (int c0 = 0; c0 < NP; c0 += 8) {
         const uint32_t gbase = la + (c0 / NG) * kBlk * NG + (c0 % NG);
@@ -531,24 +537,40 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
 #pragma unroll
         for (int w = 0; w < kBlk; ++w) tc::tmem_ld8(gbase + w * NG, g[w]);
         tc::tmem_ld_wait();
+        if constexpr (kStage) {
+          tc::tmem_st8_zero(gbase + (kBlk - 1) * NG);
+        } else {  // (the stores also keep ptxas from overlapping groups: registers)
 #pragma unroll
-        for (int w = 0; w < kBlk; ++w) tc::tmem_st8_zero(gbase + w * NG);
+          for (int w = 0; w < kBlk; ++w) tc::tmem_st8_zero(gbase + w * NG);
+        }
 #pragma unroll
         for (int jj = 0; jj < 8; ++jj) {
           // integer recombination of the weights 2^48, .., 2^0 in two exact
           // int64 halves (hi: 2^48 .. 2^32 -> < 2^47; lo: 2^24 .. 2^0 ->
-          // < 2^55), then two binary64 roundings
+          // < 2^55), then two binary64 roundings; the scalings by 2^(e+32)
+          // and 2^e are exact (normal binary64 powers of two for every
+          // binary32 / binary64 chunk exponent), i.e. equal to ldexp
           const long long hi = ((long long)(int)g[0][jj] << 16) + ((long long)(int)g[1][jj] << 8) +
                                (long long)(int)g[2][jj];
           const long long lo = ((long long)(int)g[3][jj] << 24) + ((long long)(int)g[4][jj] << 16) +
                                ((long long)(int)g[5][jj] << 8) + (long long)(int)g[6][jj];
           const int e = ex[c0 + jj] - 46;
-          acc[c0 + jj] += ldexp((double)hi, e + 32) + ldexp((double)lo, e);
+          if constexpr (kStage) {
+            const double shi = __longlong_as_double((long long)(e + 32 + 1023) << 52);
+            const double slo = __longlong_as_double((long long)(e + 1023) << 52);
+            t[c0 + jj] = __dadd_rn(__dmul_rn((double)hi, shi), __dmul_rn((double)lo, slo));
+          } else {  // (ldexp: fewer live registers at NP = 48 / 64)
+            acc[c0 + jj] += ldexp((double)hi, e + 32) + ldexp((double)lo, e);
+          }
         }
       }
       tc::tmem_st_wait();
       tc::tc_fence_before();
       tc::mbar_arrive(&S.tempty[buf]);
+      if constexpr (kStage) {
+#pragma unroll
+        for (int j = 0; j < NP; ++j) acc[j] += t[j];
+      }
     }
     if (r < k) {
       double* dst = ws + (int64_t)blockIdx.y * k * ncols + r;
