@@ -555,16 +555,28 @@ struct Mat3 {
   int n[3];
 };
 
-__global__ void __launch_bounds__(512) sumsq3_kernel(Mat3 M, double* __restrict__ out) {
-  __shared__ double red[16];
+__global__ void __launch_bounds__(1024) sumsq3_kernel(Mat3 M, double* __restrict__ out) {
+  // one CTA per matrix; the element loop runs over the flattened m x n
+  // index with 8 independent loads in flight per thread (the matrices are
+  // k x p: a column-by-column loop was a chain of dependent L2 round trips)
+  __shared__ double red[32];
   const int b = blockIdx.x;
-  const double* A = M.a[b];
+  const double* __restrict__ A = M.a[b];
+  const int m = (int)M.m[b];
+  const int64_t lda = M.lda[b];
+  const int tot = m * M.n[b];
   double s = 0.0;
-  for (int j = 0; j < M.n[b]; ++j)
-    for (int64_t i = threadIdx.x; i < M.m[b]; i += blockDim.x) {
-      const double v = A[i + (int64_t)j * M.lda[b]];
-      s += v * v;
+  constexpr int U = 8;
+  for (int e0 = threadIdx.x; e0 < tot; e0 += U * blockDim.x) {
+    double v[U];
+#pragma unroll
+    for (int q = 0; q < U; ++q) {
+      const int e = e0 + q * blockDim.x;
+      v[q] = e < tot ? A[(int64_t)(e % m) + (int64_t)(e / m) * lda] : 0.0;
     }
+#pragma unroll
+    for (int q = 0; q < U; ++q) s += v[q] * v[q];
+  }
   s = block_sum(s, red);
   if (threadIdx.x == 0) out[b] = s;
 }
@@ -580,7 +592,8 @@ int sumsq3(int64_t m1, int n1, const double* A1, int64_t lda1, int64_t m2, int n
   M.lda[0] = lda1; M.lda[1] = lda2; M.lda[2] = lda3;
   M.m[0] = m1; M.m[1] = m2; M.m[2] = m3;
   M.n[0] = n1; M.n[1] = n2; M.n[2] = n3;
-  RB_KLAUNCH sumsq3_kernel<<<3, 512, 0, st>>>(M, out);
+  RB_REQUIRE(m1 * n1 < (1ll << 31) && m2 * n2 < (1ll << 31) && m3 * n3 < (1ll << 31), "rb_sumsq3: too large");
+  RB_KLAUNCH sumsq3_kernel<<<3, 1024, 0, st>>>(M, out);
   return check_launch("rb_sumsq3");
 }
 
