@@ -374,8 +374,8 @@ def gpu_arm(args, cfgd):
         Wh.copy_(W)
         del W
         torch.cuda.empty_cache()
-        e2e_steps = max(1, min(args.steps, 3))
-        for _ in range(min(args.warmup, 2)):  # untimed: allocator / copy-stream first use
+        e2e_steps = max(1, min(args.steps, 5))
+        for _ in range(min(args.warmup, 3)):  # untimed: allocator / copy-stream first use
             rbgs(Wh, theta, cfg, dc).R.data
         barrier()
         t0 = time.perf_counter()

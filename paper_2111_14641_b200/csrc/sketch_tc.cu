@@ -35,9 +35,11 @@
 //   warp 1 lane 0  MMA issuer: 16 tcgen05.mma (M=128, N=NP, K=32) per tile;
 //                  tcgen05.commit frees the stage; at chunk ends hands the
 //                  TMEM buffer to the epilogue (double-buffered if it fits).
-//   warps 4..7     epilogue: tcgen05.ld of the 5 int32 groups of their 32
-//                  lanes, exact recombination, fp64 scale-and-add into the
+//   warps 4..7     epilogue: tcgen05.ld of the 7 int32 weight blocks of their
+//                  32 lanes, exact recombination, fp64 scale-and-add into the
 //                  CTA's own slice of the split-K partial buffer (L2-resident).
+// Pre-pass (chunk_max + encode_planes): chunk exponents, then the six byte
+// planes in the tiled B-operand layout (gauss_layout.cuh).
 #include <stdlib.h>
 
 #include <type_traits>

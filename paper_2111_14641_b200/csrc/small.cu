@@ -555,30 +555,52 @@ struct Mat3 {
   int n[3];
 };
 
-__global__ void __launch_bounds__(1024) sumsq3_kernel(Mat3 M, double* __restrict__ out) {
-  // one CTA per matrix; the element loop runs over the flattened m x n
-  // index with 8 independent loads in flight per thread (the matrices are
-  // k x p: a column-by-column loop was a chain of dependent L2 round trips)
-  __shared__ double red[32];
+// per-matrix partial sums of the CTAs of one sumsq3 launch and arrival
+// counters (the last CTA of a matrix adds the partials in CTA order, then
+// re-arms its counter): launches on one stream are serialised
+constexpr int kSq3Ctas = 8;
+__device__ double g_sq3_part[3][kSq3Ctas];
+__device__ unsigned int g_sq3_count[3];
+
+__global__ void __launch_bounds__(512) sumsq3_kernel(Mat3 M, double* __restrict__ out) {
+  // grid (3 matrices, kSq3Ctas): each CTA loops over its share of the
+  // flattened m x n index with 8 independent loads in flight per thread
+  // (the matrices are k x p: a column-by-column loop in one CTA was a chain
+  // of dependent L2 round trips)
+  __shared__ double red[16];
+  __shared__ bool last;
   const int b = blockIdx.x;
   const double* __restrict__ A = M.a[b];
   const int m = (int)M.m[b];
   const int64_t lda = M.lda[b];
   const int tot = m * M.n[b];
+  const int stride = gridDim.y * blockDim.x;
   double s = 0.0;
   constexpr int U = 8;
-  for (int e0 = threadIdx.x; e0 < tot; e0 += U * blockDim.x) {
+  for (int e0 = blockIdx.y * blockDim.x + threadIdx.x; e0 < tot; e0 += U * stride) {
     double v[U];
 #pragma unroll
     for (int q = 0; q < U; ++q) {
-      const int e = e0 + q * blockDim.x;
+      const int e = e0 + q * stride;
       v[q] = e < tot ? A[(int64_t)(e % m) + (int64_t)(e / m) * lda] : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < U; ++q) s += v[q] * v[q];
   }
   s = block_sum(s, red);
-  if (threadIdx.x == 0) out[b] = s;
+  if (threadIdx.x == 0) {
+    g_sq3_part[b][blockIdx.y] = s;
+    __threadfence();
+    last = atomicAdd(&g_sq3_count[b], 1u) == gridDim.y - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double t = 0.0;
+    for (int q = 0; q < (int)gridDim.y; ++q) t += *(volatile double*)&g_sq3_part[b][q];
+    out[b] = t;
+    g_sq3_count[b] = 0;
+  }
 }
 
 int sumsq3(int64_t m1, int n1, const double* A1, int64_t lda1, int64_t m2, int n2, const double* A2, int64_t lda2,
@@ -593,7 +615,7 @@ int sumsq3(int64_t m1, int n1, const double* A1, int64_t lda1, int64_t m2, int n
   M.m[0] = m1; M.m[1] = m2; M.m[2] = m3;
   M.n[0] = n1; M.n[1] = n2; M.n[2] = n3;
   RB_REQUIRE(m1 * n1 < (1ll << 31) && m2 * n2 < (1ll << 31) && m3 * n3 < (1ll << 31), "rb_sumsq3: too large");
-  RB_KLAUNCH sumsq3_kernel<<<3, 1024, 0, st>>>(M, out);
+  RB_KLAUNCH sumsq3_kernel<<<dim3(3, kSq3Ctas), 512, 0, st>>>(M, out);
   return check_launch("rb_sumsq3");
 }
 

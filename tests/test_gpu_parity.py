@@ -205,6 +205,71 @@ def test_gaussian_tensor_pair_matches_separate_calls(pkg, c1, c2):
         assert np.linalg.norm(got[:, j] - want[:, j]) <= 1e-11 * wn, j
 
 
+@pytest.mark.parametrize("scale", [1e-30, 1e-40, 1e30, 1.0])
+def test_gaussian_tensor_extreme_magnitudes(pkg, scale):
+    """Chunk exponents at both ends of binary32: 2^(46-E) leaves the normal
+    binary32 range below ~1e-25 (the pre-pass then scales in binary64),
+    subnormal entries, exact zeros and an all-zero column."""
+    rbgs, sketching, D = pkg
+    n, k, cols = 40_000, 200, 6
+    g = np.random.Generator(np.random.Philox(int(-math.log10(scale)) + 50))
+    X = g.standard_normal((n, cols)) * scale
+    X[::5, 1] *= 1e-6
+    X[::3, 2] = 0.0
+    X[:, 3] = 0.0
+    X[:100, 4] = 1e-45  # binary32 subnormals (2^-149)
+    X = X.astype(np.float32).astype(np.float64)
+    op = sketching.gaussian_operator(k, n, 17)
+    tab = op.device_tables("cuda", 0, n)
+    Xd = _dev(X, torch.float32)
+    sc = 1.0 / (2048 * math.sqrt(k))
+    res = {}
+    for mode in ("tensor", "fp64"):
+        out = D.empty_cm(k, cols, torch.float64, "cuda")
+        D.sketch_gaussian(Xd, tab["theta"], tab["ldt"], k, sc, out, False, mode)
+        res[mode] = out.cpu().numpy()
+    assert np.all(np.isfinite(res["tensor"]))
+    assert np.all(res["tensor"][:, 3] == 0.0)
+    for j in range(cols):
+        wn = np.linalg.norm(res["fp64"][:, j])
+        assert np.linalg.norm(res["tensor"][:, j] - res["fp64"][:, j]) <= 1e-11 * wn, j
+
+
+def test_gaussian_prepass_variants_same_bits(pkg):
+    """The streaming pre-pass (chunk_max + encode_planes), the single-kernel
+    split_planes (RB_SPLIT_MODE=1) and its binary64 conversion path
+    (RB_SPLIT_SLOW=1) write the same planes: the sketch bits agree."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import hashlib, math, sys, torch
+sys.path.insert(0, %r)
+from paper_2111_14641_b200 import _device as D, sketching
+g = torch.Generator().manual_seed(4)
+n, k = 50_001, 300
+X = (torch.randn(n, 70, generator=g, dtype=torch.float64) * torch.logspace(0, -9, 70, dtype=torch.float64))
+X[::4] *= 1e-20
+Xd = X.to(torch.float32).cuda().t().contiguous().t()
+tab = sketching.gaussian_operator(k, n, 3).device_tables("cuda", 0, n)
+o1 = D.empty_cm(k, 30, torch.float64, "cuda"); o2 = D.empty_cm(k, 40, torch.float64, "cuda")
+D.sketch_gaussian2(Xd[:, :30], Xd[:, 30:], tab["theta"], tab["ldt"], k, 1.0, o1, o2, False, "tensor")
+o3 = D.empty_cm(k, 60, torch.float64, "cuda")
+D.sketch_gaussian(Xd[:, 10:], tab["theta"], tab["ldt"], k, 1.0, o3, False, "tensor")
+print(hashlib.sha256(o1.cpu().numpy().tobytes() + o2.cpu().numpy().tobytes() + o3.cpu().numpy().tobytes()).hexdigest())
+""" % (os.path.dirname(os.path.dirname(os.path.abspath(__file__))),)
+    shas = set()
+    for env in ({}, {"RB_SPLIT_MODE": "1"}, {"RB_SPLIT_SLOW": "1"}):
+        e = dict(os.environ)
+        e.pop("RB_SPLIT_MODE", None)
+        e.pop("RB_SPLIT_SLOW", None)
+        e.update(env)
+        out = subprocess.run([sys.executable, "-c", code], env=e, capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        shas.add(out.stdout.strip().splitlines()[-1])
+    assert len(shas) == 1, shas
+
+
 def test_fused_lookahead_pair_sketch_is_bitwise_neutral(pkg):
     """p = 64: [Q'_i | W_(i+1)] (128 columns) runs as one paired launch."""
     rbgs, sketching, D = pkg
