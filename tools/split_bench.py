@@ -23,7 +23,9 @@ from paper_2111_14641_b200 import sketching, workloads  # noqa: E402
 
 
 def main():
-    n, p, k = 1_000_000, 40, 1600
+    n = int(os.environ.get("SB_N", 1_000_000))
+    p = int(os.environ.get("SB_P", 40))
+    k = int(os.environ.get("SB_K", 1600))
     dev = torch.device("cuda", 0)
     W = workloads.trig_device(n, 2 * p, 7, 0, n, torch.float32, dev)
     g = torch.Generator(device=dev).manual_seed(3)
