@@ -375,8 +375,13 @@ def gpu_arm(args, cfgd):
         del W
         torch.cuda.empty_cache()
         e2e_steps = max(1, min(args.steps, 5))
-        for _ in range(min(args.warmup, 3)):  # untimed: allocator / copy-stream first use
-            rbgs(Wh, theta, cfg, dc).R.data
+        # untimed: allocator / copy-stream first use.  Same assignment pattern as
+        # the timed loop (the previous result stays alive while the next call
+        # allocates its Q), so the caching allocator holds both Q buffers before
+        # timing starts instead of cudaMalloc'ing the second in timed step 1.
+        for _ in range(max(2, min(args.warmup, 3))):
+            fe = rbgs(Wh, theta, cfg, dc)
+            Rh = fe.R.data
         barrier()
         t0 = time.perf_counter()
         each = []
