@@ -53,18 +53,30 @@ inline int load_tri_const(int p, const double* R, int64_t ldr, cudaStream_t st) 
 }
 
 // One row: x (registers, PB >= p columns) <- x R^{-1}, dot form, l ascending
-// with the (even, odd) pairing of trsm_right_kernel -- the same roundings.
+// (shared by trsm_right_kernel and the fused projection prologue).
 template <int PB>
 __device__ __forceinline__ void tri_solve_row(double (&x)[PB], int p) {
+  // Columns j, j+1 as two independent FMA chains (the runtime `j < p` guard
+  // otherwise keeps ptxas from interleaving across columns, leaving one
+  // dependent DFMA chain per thread).  Each chain keeps its own order:
+  // l = 0..j-1 ascending, then column j+1 takes its l = j term once x[j] is
+  // final -- the same roundings as the one-column loop.
 #pragma unroll
-  for (int j = 0; j < PB; ++j) {
-    if (j < p) {
+  for (int j = 0; j < PB; j += 2) {
+    if (j + 1 < PB && j + 1 < p) {
+      double s0 = x[j], s1 = x[j + 1];
+#pragma unroll
+      for (int l = 0; l < j; ++l) {
+        s0 = fma(-x[l], c_tri_R[l + j * kTriLd], s0);
+        s1 = fma(-x[l], c_tri_R[l + (j + 1) * kTriLd], s1);
+      }
+      x[j] = s0 * c_tri_inv[j];
+      s1 = fma(-x[j], c_tri_R[j + (j + 1) * kTriLd], s1);
+      x[j + 1] = s1 * c_tri_inv[j + 1];
+    } else if (j < p) {
       double s = x[j];
 #pragma unroll
-      for (int l2 = 0; l2 < (j + 1) / 2; ++l2) {
-        s = fma(-x[2 * l2], c_tri_R[2 * l2 + j * kTriLd], s);
-        if (2 * l2 + 1 < j) s = fma(-x[2 * l2 + 1], c_tri_R[2 * l2 + 1 + j * kTriLd], s);
-      }
+      for (int l = 0; l < j; ++l) s = fma(-x[l], c_tri_R[l + j * kTriLd], s);
       x[j] = s * c_tri_inv[j];
     }
   }
