@@ -262,7 +262,7 @@ project_staged(int64_t n, int c, int p, const float* __restrict__ Q, int64_t ldq
       double x[PB];
 #pragma unroll
       for (int j = 0; j < PB; ++j) x[j] = j < pf ? (double)Qf[row + (int64_t)j * ldqf] : 0.0;
-      tri_solve_row<PB>(x, pf);
+      tri_solve_row<PB, 1>(x, pf);  // one chain: the projection kernel is register-tight
 #pragma unroll
       for (int j = 0; j < PB; ++j)
         if (j < pf) Qf[row + (int64_t)j * ldqf] = (float)x[j];

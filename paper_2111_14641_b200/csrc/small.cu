@@ -168,7 +168,7 @@ trsm_right_kernel(int64_t n, int p, const TI* B, int64_t ldb, TO* Xo, int64_t ld
   double x[PB];
 #pragma unroll
   for (int j = 0; j < PB; ++j) x[j] = j < p ? (double)B[r + (int64_t)j * ldb] : 0.0;
-  tri_solve_row<PB>(x, p);
+  tri_solve_row<PB, (PB <= 40 ? 4 : 2)>(x, p);
 #pragma unroll
   for (int j = 0; j < PB; ++j)
     if (j < p) Xo[r + (int64_t)j * ldx] = (TO)x[j];

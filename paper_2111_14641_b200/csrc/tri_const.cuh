@@ -54,30 +54,41 @@ inline int load_tri_const(int p, const double* R, int64_t ldr, cudaStream_t st) 
 
 // One row: x (registers, PB >= p columns) <- x R^{-1}, dot form, l ascending
 // (shared by trsm_right_kernel and the fused projection prologue).
-template <int PB>
+template <int PB, int CH = 2>
 __device__ __forceinline__ void tri_solve_row(double (&x)[PB], int p) {
-  // Columns j, j+1 as two independent FMA chains (the runtime `j < p` guard
-  // otherwise keeps ptxas from interleaving across columns, leaving one
-  // dependent DFMA chain per thread).  Each chain keeps its own order:
-  // l = 0..j-1 ascending, then column j+1 takes its l = j term once x[j] is
-  // final -- the same roundings as the one-column loop.
+  // CH columns at a time as independent FMA chains (the runtime `j < p`
+  // guard otherwise keeps ptxas from interleaving across columns, leaving
+  // one dependent DFMA chain per thread; the standalone TRSM uses CH = 4 up
+  // to 40 columns, the register-tight fused projection prologue CH = 1).  Each chain keeps its own order: l
+  // ascending over the finished columns, then the group's earlier columns
+  // in ascending order once they are final -- the one-column roundings.
 #pragma unroll
-  for (int j = 0; j < PB; j += 2) {
-    if (j + 1 < PB && j + 1 < p) {
-      double s0 = x[j], s1 = x[j + 1];
+  for (int j = 0; j < PB; j += CH) {
+    if (j + CH <= PB && j + CH <= p) {
+      double s[CH];
 #pragma unroll
-      for (int l = 0; l < j; ++l) {
-        s0 = fma(-x[l], c_tri_R[l + j * kTriLd], s0);
-        s1 = fma(-x[l], c_tri_R[l + (j + 1) * kTriLd], s1);
+      for (int c = 0; c < CH; ++c) s[c] = x[j + c];
+#pragma unroll
+      for (int l = 0; l < j; ++l)
+#pragma unroll
+        for (int c = 0; c < CH; ++c) s[c] = fma(-x[l], c_tri_R[l + (j + c) * kTriLd], s[c]);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        x[j + c] = s[c] * c_tri_inv[j + c];
+#pragma unroll
+        for (int c2 = c + 1; c2 < CH; ++c2) s[c2] = fma(-x[j + c], c_tri_R[j + c + (j + c2) * kTriLd], s[c2]);
       }
-      x[j] = s0 * c_tri_inv[j];
-      s1 = fma(-x[j], c_tri_R[j + (j + 1) * kTriLd], s1);
-      x[j + 1] = s1 * c_tri_inv[j + 1];
-    } else if (j < p) {
-      double s = x[j];
+    } else {
 #pragma unroll
-      for (int l = 0; l < j; ++l) s = fma(-x[l], c_tri_R[l + j * kTriLd], s);
-      x[j] = s * c_tri_inv[j];
+      for (int c = 0; c < CH; ++c) {
+        const int jj = j + c;
+        if (jj < PB && jj < p) {
+          double t = x[jj];
+#pragma unroll
+          for (int l = 0; l < jj; ++l) t = fma(-x[l], c_tri_R[l + jj * kTriLd], t);
+          x[jj] = t * c_tri_inv[jj];
+        }
+      }
     }
   }
 }
