@@ -172,9 +172,10 @@ def _oracle_sample(cfgd, n_s, parity=False, order="reference"):
     m, p, k = cfgd["m"], cfgd["p"], min(cfgd["k"], n_s)
     if cfgd["gen"] == "trig":
         W = WL.trig_host(n_s, m, SEED_W)
+    elif cfgd["gen"] == "lowrank":
+        W = WL.lowrank_host(n_s, m, SEED_W)
     else:
-        g = np.random.Generator(np.random.Philox(SEED_W))
-        W = g.standard_normal((n_s, m)) * np.logspace(0, -6, m)
+        W = WL.colscaled_host(n_s, m, SEED_W)
     if cfgd["dtype"] == "f32":
         W = W.astype(np.float32).astype(np.float64)
     op = osk.materialize(osk.OracleSketch(cfgd["kind"], k, n_s, SEED_THETA))

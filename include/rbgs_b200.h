@@ -17,6 +17,13 @@
  *     operators are keyed by global row, so shards compose by summation);
  *   - every call is asynchronous on `stream` (a cudaStream_t, NULL = legacy
  *     default stream) and never synchronises the host;
+ *   - concurrency: the library keeps no per-call device state of its own
+ *     except the constant-bank copy of R used by the tall right solves
+ *     (rb_trsm_right, rb_project_trsm); calls of those two on different
+ *     streams of one device are serialised with an event (not inside a
+ *     stream capture: a captured graph must not replay concurrently with
+ *     other streams' solves on its device).  `ws` scratch belongs to the
+ *     call's stream: two streams must pass different workspaces;
  *   - return value: RB_OK, or a negative RB_E* code with a message in
  *     rb_last_error();  numerical failures (non-PD pivot) are reported
  *     through device-side `info` words, as LAPACK does;
@@ -44,6 +51,10 @@ extern "C" {
 /* Step-3 arithmetic order in coarse mode */
 #define RB_ORDER_REFERENCE 0  /* separately rounded multiply and subtract  */
 #define RB_ORDER_FMA 1        /* fused multiply-subtract (not bit-exact)    */
+#define RB_ORDER_REFERENCE_SCALAR 2  /* RB_ORDER_REFERENCE issued as scalar
+                                        FMUL + FADD instead of the packed
+                                        FFMA2(-0) + FADD2 pair: same bits,
+                                        the cross-check of the packed form */
 
 const char* rb_version(void);
 const char* rb_last_error(void);
@@ -160,10 +171,12 @@ int rb_gemm_f32(int transA, int transB, int m, int n, int k, float alpha,
                 float* C, int64_t ldc, void* stream);
 /* out[0..2] = sums of squares of three binary64 matrices (one launch; the
  * per-block finiteness words of P_i, S_i, R_ii -- rbgs.py:380-388 through
- * the reference's Matrix() checks). */
+ * the reference's Matrix() checks).  ws: >= 256 bytes of the caller's
+ * scratch (CTA partials and arrival counters; no device globals). */
 int rb_sumsq3(int64_t m1, int n1, const double* A1, int64_t lda1,
               int64_t m2, int n2, const double* A2, int64_t lda2,
-              int64_t m3, int n3, const double* A3, int64_t lda3, double* out, void* stream);
+              int64_t m3, int n3, const double* A3, int64_t lda3, double* out,
+              void* ws, size_t ws_bytes, void* stream);
 /* Symmetric rank-k update, upper triangle: C = alpha A^T A + beta C for a
  * tall binary64 A (k x n, C n x n; cuBLAS DSYRK) -- the basis Gram of the
  * GMRES conditioning history (krylov.py:98-103, 247-257). */

@@ -103,8 +103,21 @@ def gemm_ordered(alpha, A, B, beta=0.0, C=None, fmt="fine"):
     return _finite(acc.astype(np.float64))
 
 
+# tests may route the binary32 Step 3 through the plain-C restatement of the
+# same order (oracle/cproj, pinned bit-identical to gemm_ordered by
+# tests/test_oracle_golden.py); the bench's CPU arms keep the numpy loop,
+# which has the reference's own cost profile (a Python loop over l).
+FAST_PROJECT = False
+
+
 def project(Q, X, W, fmt="coarse"):
     """Step 3: Q' = W - Q X in reference order (rbgs.py:369-370)."""
+    if FAST_PROJECT and fmt == "coarse" and np.asarray(W).shape[1] <= 64 and np.asarray(Q).shape[1] > 0:
+        from . import cproj
+        Q32 = np.asarray(Q, dtype=np.float64).astype(np.float32)
+        W32 = np.asarray(W, dtype=np.float64).astype(np.float32)
+        X32 = np.asarray(X, dtype=np.float64).astype(np.float32).astype(np.float64)
+        return _finite(cproj.project_f32(Q32, X32, W32).astype(np.float64))
     return gemm_ordered(-1.0, Q, X, 1.0, W, fmt)
 
 

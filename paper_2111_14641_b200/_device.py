@@ -292,7 +292,8 @@ def sumsq3(A1, A2, A3, out):
     args = []
     for A in (A1, A2, A3):
         args += [A.shape[0], A.shape[1], ptr(A), ld(A)]
-    call("rb_sumsq3", *args, ptr(out), st(out.device))
+    ws, wsb = _ws(1, 1, 1, out.device)
+    call("rb_sumsq3", *args, ptr(out), ws, wsb, st(out.device))
 
 
 def richardson(S, P, l, X, T):

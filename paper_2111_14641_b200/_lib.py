@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(HERE, "librbgs_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "rbgs_b200.h")
 
 F32, F64 = 0, 1
-ORDER_REFERENCE, ORDER_FMA = 0, 1
+ORDER_REFERENCE, ORDER_FMA, ORDER_REFERENCE_SCALAR = 0, 1, 2
 
 _i, _i64, _u64, _sz, _d = ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_double
 _f = ctypes.c_float
@@ -46,7 +46,7 @@ SIGNATURES = {
     "rb_trsm_right": [_i, _i, _i64, _i, _p, _i64, _p, _i64, _p, _i64, _p],
     "rb_gemm_f64": [_i, _i, _i, _i, _i, _d, _p, _i64, _p, _i64, _d, _p, _i64, _p, _sz, _p],
     "rb_gemm_f32": [_i, _i, _i, _i, _i, _f, _p, _i64, _p, _i64, _f, _p, _i64, _p],
-    "rb_sumsq3": [_i64, _i, _p, _i64, _i64, _i, _p, _i64, _i64, _i, _p, _i64, _p, _p],
+    "rb_sumsq3": [_i64, _i, _p, _i64, _i64, _i, _p, _i64, _i64, _i, _p, _i64, _p, _p, _sz, _p],
     "rb_syrk_f64": [_i, _i64, _d, _p, _i64, _d, _p, _i64, _p],
     "rb_cross": [_i, _i, _i64, _i, _i, _p, _i64, _p, _i64, _p, _i64, _i, _p, _sz, _p],
     "rb_potrf_upper": [_i, _p, _i64, _p, _i64, _p, _p],
@@ -142,18 +142,24 @@ def call(name, *args):
 # workspace
 
 class Workspace:
-    """One growable device scratch buffer per device (sketch split partials,
-    reduction partials, QR reflectors)."""
+    """One growable device scratch buffer per (device, stream) (sketch split
+    partials, reduction partials, QR reflectors): calls are asynchronous on
+    the caller's stream, so two streams of one device must never share
+    scratch (include/rbgs_b200.h, conventions)."""
 
     _pool = {}
 
     @classmethod
     def get(cls, nbytes, device):
-        key = torch.device(device).index if torch.device(device).index is not None else torch.cuda.current_device()
+        idx = torch.device(device).index if torch.device(device).index is not None else torch.cuda.current_device()
+        key = (idx, torch.cuda.current_stream(idx).cuda_stream)
         buf = cls._pool.get(key)
         if buf is None or buf.numel() < nbytes:
             nb = max(int(nbytes), 64 << 20)
-            buf = torch.empty(nb, dtype=torch.uint8, device=f"cuda:{key}")
+            if buf is not None:
+                # the old buffer may still be read by queued work of its stream
+                del cls._pool[key]
+            buf = torch.empty(nb, dtype=torch.uint8, device=f"cuda:{idx}")
             cls._pool[key] = buf
         return buf
 

@@ -66,7 +66,7 @@ int cross(int, int, int64_t, int, int, const void*, int64_t, const void*, int64_
           size_t, cudaStream_t);
 int syrk_f64(int, int64_t, double, const double*, int64_t, double, double*, int64_t, cudaStream_t);
 int sumsq3(int64_t, int, const double*, int64_t, int64_t, int, const double*, int64_t, int64_t, int, const double*,
-           int64_t, double*, cudaStream_t);
+           int64_t, double*, void*, size_t, cudaStream_t);
 int gemm_f32(int, int, int, int, int, float, const float*, int64_t, const float*, int64_t, float, float*, int64_t,
              cudaStream_t);
 int potrf_upper(int, const double*, int64_t, double*, int64_t, int*, cudaStream_t);
@@ -180,8 +180,8 @@ int rb_gemm_f64(int tA, int tB, int m, int n, int k, double alpha, const double*
 }
 
 int rb_sumsq3(int64_t m1, int n1, const double* A1, int64_t lda1, int64_t m2, int n2, const double* A2, int64_t lda2,
-              int64_t m3, int n3, const double* A3, int64_t lda3, double* out, void* s) {
-  return rb::sumsq3(m1, n1, A1, lda1, m2, n2, A2, lda2, m3, n3, A3, lda3, out, as_stream(s));
+              int64_t m3, int n3, const double* A3, int64_t lda3, double* out, void* ws, size_t wsb, void* s) {
+  return rb::sumsq3(m1, n1, A1, lda1, m2, n2, A2, lda2, m3, n3, A3, lda3, out, ws, wsb, as_stream(s));
 }
 
 int rb_syrk_f64(int n, int64_t k, double alpha, const double* A, int64_t lda, double beta, double* C, int64_t ldc,

@@ -6,11 +6,14 @@
 // p column accumulators of each.  Per entry and per l the arithmetic is
 //     acc = fl32(acc + fl32(q * (-x)))  ==  fl32(acc - fl32(q * x)),
 // i.e. the reference's separately rounded multiply and subtract, l
-// ascending, as scalar FMUL + FADD (__fmul_rn / __fadd_rn are never
-// contracted).  NOTE: packed mul.rn.f32x2 + add.rn.f32x2 cannot be used for
-// this -- ptxas 12.9 fuses the pair into FFMA2 even with -fmad=false (checked
-// in SASS), which would break bit-identity.  The packed FFMA2 form is what
-// the opt-in RB_ORDER_FMA mode uses.
+// ascending: scalar FMUL + FADD (__fmul_rn / __fadd_rn are never contracted)
+// or, in the staged kernel (default), the same two roundings as packed
+// FFMA2(q, -x, nz) + FADD2 with nz = -0.0f passed at run time -- ptxas
+// cannot see the addend is -0 and so cannot contract the pair (it does fuse
+// a literal mul.rn.f32x2 + add.rn.f32x2 into one FFMA2 even with
+// -fmad=false, checked in SASS).  RB_ORDER_REFERENCE_SCALAR forces the
+// scalar form (same bits; the cross-check of the packed one).  One packed
+// FFMA2 per two columns (one rounding) is the opt-in RB_ORDER_FMA mode.
 // Fine (binary64) path: one row per thread, __dmul_rn / __dsub_rn.
 //
 // W and Qp may alias (Q' written over W_i: DeviceConfig.overwrite_w): every
@@ -546,7 +549,7 @@ struct FusedTrsm {
 template <typename TQ, typename TW, int PB>
 void launch_pb(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, const double* X, int64_t ldx,
                const void* W, int64_t ldw, void* Qp, int64_t ldqp, double* partial, float* xs,
-               bool staged, cudaStream_t st, const FusedTrsm& fz) {
+               bool staged, bool scalar, cudaStream_t st, const FusedTrsm& fz) {
   if (mode == 2) {
     const int grid = ceil_div(n, kThreads);
     RB_KLAUNCH project_fine<TQ, TW, PB><<<grid, kThreads, 0, st>>>(n, c, p, (const TQ*)Q, ldq, X, ldx, (const TW*)W,
@@ -579,7 +582,7 @@ void launch_pb(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, co
       n, c, p, (const float*)Q, ldq, xs, (const TW*)W, ldw, (float*)Qp, ldqp, partial, -0.0f,     \
       (float*)fz.Qf, fz.ldqf, fz.Rf, fz.ldrf, fz.pf, rows)
       if (mode == 1) RB_ST(1);
-      else if (packed_enabled()) RB_ST(2);
+      else if (packed_enabled() && !scalar) RB_ST(2);
       else RB_ST(0);
 #undef RB_ST
       return;
@@ -607,10 +610,10 @@ void launch_pb(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, co
 template <typename TQ, typename TW>
 int launch_tw(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, const double* X, int64_t ldx,
               const void* W, int64_t ldw, void* Qp, int64_t ldqp, double* partial, float* xs, bool staged,
-              cudaStream_t st, const FusedTrsm& fz = FusedTrsm()) {
+              bool scalar, cudaStream_t st, const FusedTrsm& fz = FusedTrsm()) {
 #define RB_PB(V)                                                                                    \
   if (p <= V) {                                                                                     \
-    launch_pb<TQ, TW, V>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st, fz); \
+    launch_pb<TQ, TW, V>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, scalar, st, fz); \
     return V;                                                                                       \
   }
   RB_PB(4) RB_PB(8) RB_PB(12) RB_PB(16) RB_PB(20) RB_PB(24) RB_PB(32) RB_PB(40) RB_PB(48) RB_PB(64)
@@ -675,7 +678,8 @@ int project_trsm(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t
     return project(q_dtype, w_dtype, compute_dtype, order, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, norms2, ws,
                    ws_bytes, st);
   }
-  const int lrc = load_tri_const(pf, Rf, ldrf, st);
+  std::lock_guard<std::mutex> lock(tri_mutex());
+  const int lrc = load_tri_const_locked(pf, Rf, ldrf, st);
   if (lrc != RB_OK) return lrc;
   FusedTrsm fz;
   fz.Qf = Qf;
@@ -683,8 +687,10 @@ int project_trsm(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t
   fz.Rf = Rf;
   fz.ldrf = ldrf;
   fz.pf = pf;
-  return project_impl(q_dtype, w_dtype, compute_dtype, order, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, norms2,
-                      ws, ws_bytes, st, fz);
+  const int rc = project_impl(q_dtype, w_dtype, compute_dtype, order, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp,
+                              norms2, ws, ws_bytes, st, fz);
+  tri_const_done_locked(st);
+  return rc;
 }
 
 namespace {
@@ -695,8 +701,10 @@ int project_impl(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t
              (long long)n, c, p);
   RB_REQUIRE(c == 0 || (Q && ldq >= n && X && ldx >= c), "rb_project: bad Q/X");
   RB_REQUIRE(W && ldw >= n && Qp && ldqp >= n, "rb_project: bad W/Qp");
-  RB_REQUIRE(order == RB_ORDER_REFERENCE || order == RB_ORDER_FMA, "rb_project: bad order %d", order);
+  RB_REQUIRE(order == RB_ORDER_REFERENCE || order == RB_ORDER_FMA || order == RB_ORDER_REFERENCE_SCALAR,
+             "rb_project: bad order %d", order);
   const int mode = compute_dtype == RB_F64 ? 2 : (order == RB_ORDER_FMA ? 1 : 0);
+  const bool scalar = order == RB_ORDER_REFERENCE_SCALAR;
   const bool q32 = q_dtype == RB_F32, w32 = w_dtype == RB_F32;
   // binary32 Q with 16-B aligned columns streams through the staged kernel
   const bool staged = mode != 2 && q32 && c > 0 && rpt_override() == 0 && (uintptr_t)Q % 16 == 0 &&
@@ -715,10 +723,10 @@ int project_impl(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t
     return check_launch("rb_project");
   }
   RB_REQUIRE(fz.pf == 0 || staged, "rb_project: fused scaling needs the staged kernel");
-  if (q32 && w32) launch_tw<float, float>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st, fz);
-  else if (q32) launch_tw<float, double>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st, fz);
-  else if (w32) launch_tw<double, float>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st);
-  else launch_tw<double, double>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, st);
+  if (q32 && w32) launch_tw<float, float>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, scalar, st, fz);
+  else if (q32) launch_tw<float, double>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, scalar, st, fz);
+  else if (w32) launch_tw<double, float>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, scalar, st);
+  else launch_tw<double, double>(mode, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp, partial, xs, staged, scalar, st);
   if (norms2) RB_KLAUNCH sum_pairs<<<1, kThreads, 0, st>>>(partial, grid, norms2);
   return check_launch("rb_project");
 }

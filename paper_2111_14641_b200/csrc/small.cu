@@ -330,12 +330,14 @@ __global__ void copy_f64(int m, int n, const double* __restrict__ A, int64_t lda
 template <typename TI, typename TO>
 void trsm_right_launch(int64_t n, int p, const void* B, int64_t ldb, const double* R, int64_t ldr, void* X,
                        int64_t ldx, cudaStream_t st) {
-  if (load_tri_const(p, R, ldr, st) != RB_OK) return;
+  std::lock_guard<std::mutex> lock(tri_mutex());
+  if (load_tri_const_locked(p, R, ldr, st) != RB_OK) return;
 #define RB_TR(V)                                                                                          \
   if (p <= V) {                                                                                           \
     constexpr int RPT = 1;                                                                                \
     RB_KLAUNCH trsm_right_kernel<TI, TO, V, RPT><<<ceil_div(n, (int64_t)RPT * kThreads), kThreads, 0, st>>>( \
         n, p, (const TI*)B, ldb, (TO*)X, ldx);                                                            \
+    tri_const_done_locked(st);                                                                            \
     return;                                                                                               \
   }
   RB_TR(4) RB_TR(8) RB_TR(12) RB_TR(16) RB_TR(24) RB_TR(32) RB_TR(40) RB_TR(48) RB_TR(64)
@@ -555,14 +557,14 @@ struct Mat3 {
   int n[3];
 };
 
-// per-matrix partial sums of the CTAs of one sumsq3 launch and arrival
-// counters (the last CTA of a matrix adds the partials in CTA order, then
-// re-arms its counter): launches on one stream are serialised
+// Each CTA writes its partial into the caller's workspace; the last CTA of a
+// matrix (arrival counter, also in the workspace, zeroed by the host wrapper
+// in stream order) adds the partials in CTA order.  No device globals: two
+// streams with their own workspaces never share state.
 constexpr int kSq3Ctas = 8;
-__device__ double g_sq3_part[3][kSq3Ctas];
-__device__ unsigned int g_sq3_count[3];
 
-__global__ void __launch_bounds__(512) sumsq3_kernel(Mat3 M, double* __restrict__ out) {
+__global__ void __launch_bounds__(512) sumsq3_kernel(Mat3 M, double* __restrict__ out,
+                                                     double* __restrict__ part, unsigned int* __restrict__ count) {
   // grid (3 matrices, kSq3Ctas): each CTA loops over its share of the
   // flattened m x n index with 8 independent loads in flight per thread
   // (the matrices are k x p: a column-by-column loop in one CTA was a chain
@@ -589,33 +591,37 @@ __global__ void __launch_bounds__(512) sumsq3_kernel(Mat3 M, double* __restrict_
   }
   s = block_sum(s, red);
   if (threadIdx.x == 0) {
-    g_sq3_part[b][blockIdx.y] = s;
+    part[b * kSq3Ctas + blockIdx.y] = s;
     __threadfence();
-    last = atomicAdd(&g_sq3_count[b], 1u) == gridDim.y - 1;
+    last = atomicAdd(&count[b], 1u) == gridDim.y - 1;
   }
   __syncthreads();
   if (last && threadIdx.x == 0) {
     __threadfence();
     double t = 0.0;
-    for (int q = 0; q < (int)gridDim.y; ++q) t += *(volatile double*)&g_sq3_part[b][q];
+    for (int q = 0; q < (int)gridDim.y; ++q) t += *(volatile double*)&part[b * kSq3Ctas + q];
     out[b] = t;
-    g_sq3_count[b] = 0;
   }
 }
 
 int sumsq3(int64_t m1, int n1, const double* A1, int64_t lda1, int64_t m2, int n2, const double* A2, int64_t lda2,
-           int64_t m3, int n3, const double* A3, int64_t lda3, double* out, cudaStream_t st) {
+           int64_t m3, int n3, const double* A3, int64_t lda3, double* out, void* ws, size_t wsb, cudaStream_t st) {
   RB_REQUIRE(out && m1 >= 0 && m2 >= 0 && m3 >= 0 && n1 >= 0 && n2 >= 0 && n3 >= 0 &&
                  (m1 * n1 == 0 || (A1 && lda1 >= m1)) && (m2 * n2 == 0 || (A2 && lda2 >= m2)) &&
                  (m3 * n3 == 0 || (A3 && lda3 >= m3)),
              "rb_sumsq3: bad args");
+  constexpr size_t kPart = 3 * kSq3Ctas * sizeof(double);
+  RB_REQUIRE(ws && wsb >= kPart + 4 * sizeof(unsigned int) && (uintptr_t)ws % 8 == 0, "rb_sumsq3: workspace");
   Mat3 M;
   M.a[0] = A1; M.a[1] = A2; M.a[2] = A3;
   M.lda[0] = lda1; M.lda[1] = lda2; M.lda[2] = lda3;
   M.m[0] = m1; M.m[1] = m2; M.m[2] = m3;
   M.n[0] = n1; M.n[1] = n2; M.n[2] = n3;
   RB_REQUIRE(m1 * n1 < (1ll << 31) && m2 * n2 < (1ll << 31) && m3 * n3 < (1ll << 31), "rb_sumsq3: too large");
-  RB_KLAUNCH sumsq3_kernel<<<dim3(3, kSq3Ctas), 512, 0, st>>>(M, out);
+  double* part = (double*)ws;
+  unsigned int* count = (unsigned int*)((char*)ws + kPart);
+  cudaMemsetAsync(count, 0, 3 * sizeof(unsigned int), st);
+  RB_KLAUNCH sumsq3_kernel<<<dim3(3, kSq3Ctas), 512, 0, st>>>(M, out, part, count);
   return check_launch("rb_sumsq3");
 }
 

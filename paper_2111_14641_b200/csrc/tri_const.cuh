@@ -11,10 +11,18 @@
 //
 // Each translation unit that includes this header gets its own copy (the
 // anonymous namespace); load_tri_const() refreshes THIS unit's copy,
-// stream-ordered (a pack kernel into a per-device staging buffer, then one
-// device-to-symbol copy -- both graph-capturable).  One solve per stream at
-// a time, which is how the sweep issues them.
+// stream-ordered: a pack kernel into a per-device staging array (a device
+// global, so no allocation -- legal inside graph capture), then one
+// device-to-symbol copy.  The bank is per device, not per stream, so a solve
+// issued on another stream than the previous one first waits (event) for
+// the previous stream's consumer kernel: two streams' solves on one device
+// are serialised, never interleaved (tri_const_done() records that event).
+// Inside a stream capture the cross-stream wait is not recorded; a captured
+// graph must not replay concurrently with other streams' solves on its
+// device (include/rbgs_b200.h, conventions).
 #pragma once
+
+#include <mutex>
 
 #include "common.cuh"
 
@@ -24,10 +32,12 @@ namespace {
 constexpr int kTriLd = 64;
 // [0, 64 * 64): R column-major, ld 64, zero padded; then 1 / R_jj (0 for j >= p)
 __constant__ double c_tri[kTriLd * kTriLd + kTriLd];
+__device__ double g_tri_stage[kTriLd * kTriLd + kTriLd];
 #define c_tri_R c_tri
 #define c_tri_inv (c_tri + kTriLd * kTriLd)
 
-__global__ void tri_pack_kernel(int p, const double* __restrict__ R, int64_t ldr, double* __restrict__ dst) {
+__global__ void tri_pack_kernel(int p, const double* __restrict__ R, int64_t ldr) {
+  double* dst = g_tri_stage;
   for (int e = threadIdx.x; e < kTriLd * kTriLd; e += blockDim.x) {
     const int i = e % kTriLd, j = e / kTriLd;
     dst[e] = (i < p && j < p) ? R[i + (int64_t)j * ldr] : 0.0;
@@ -36,20 +46,57 @@ __global__ void tri_pack_kernel(int p, const double* __restrict__ R, int64_t ldr
     dst[kTriLd * kTriLd + j] = j < p ? 1.0 / R[j + (int64_t)j * ldr] : 0.0;
 }
 
-inline int load_tri_const(int p, const double* R, int64_t ldr, cudaStream_t st) {
-  static double* staging[64] = {nullptr};
+struct TriOwner {
+  cudaStream_t last = nullptr;
+  bool used = false;
+  cudaEvent_t done = nullptr;  // recorded after the last consumer on `last`
+  bool done_valid = false;
+};
+
+inline std::mutex& tri_mutex() {
+  static std::mutex mu;
+  return mu;
+}
+
+inline TriOwner& tri_owner(int dev) {
+  static TriOwner owners[64];
+  return owners[dev & 63];
+}
+
+inline bool stream_capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  return cs != cudaStreamCaptureStatusNone;
+}
+
+// Call with the tri mutex held (load_tri_const .. tri_const_done bracket one
+// consumer launch).
+inline int load_tri_const_locked(int p, const double* R, int64_t ldr, cudaStream_t st) {
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!staging[dev]) {
-    if (cudaMalloc(&staging[dev], (kTriLd * kTriLd + kTriLd) * sizeof(double)) != cudaSuccess) {
-      set_error("tri_const: staging allocation failed");
-      return RB_ECUDA;
-    }
-  }
-  RB_KLAUNCH tri_pack_kernel<<<1, 256, 0, st>>>(p, R, ldr, staging[dev]);
-  cudaMemcpyToSymbolAsync(c_tri, staging[dev], (kTriLd * kTriLd + kTriLd) * sizeof(double), 0,
+  TriOwner& o = tri_owner(dev);
+  if (o.used && o.last != st && o.done_valid && !stream_capturing(st))
+    cudaStreamWaitEvent(st, o.done, 0);  // the previous stream's solve has read the bank
+  RB_KLAUNCH tri_pack_kernel<<<1, 256, 0, st>>>(p, R, ldr);
+  void* stage = nullptr;
+  cudaGetSymbolAddress(&stage, g_tri_stage);
+  cudaMemcpyToSymbolAsync(c_tri, stage, (kTriLd * kTriLd + kTriLd) * sizeof(double), 0,
                           cudaMemcpyDeviceToDevice, st);
   return check_launch("tri_const load");
+}
+
+inline void tri_const_done_locked(cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  TriOwner& o = tri_owner(dev);
+  o.last = st;
+  o.used = true;
+  if (stream_capturing(st)) {
+    o.done_valid = false;
+    return;
+  }
+  if (!o.done) cudaEventCreateWithFlags(&o.done, cudaEventDisableTiming);
+  o.done_valid = o.done && cudaEventRecord(o.done, st) == cudaSuccess;
 }
 
 // One row: x (registers, PB >= p columns) <- x R^{-1}, dot form, l ascending

@@ -942,6 +942,10 @@ def rbgs(W, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None, *, _eager: 
         off = cfg.partition.offsets()
         copy_stream = torch.cuda.Stream(dev)
         copy_stream.wait_stream(torch.cuda.current_stream(dev))
+        # the uploads write Wd on copy_stream: the caching allocator must not
+        # hand its memory to the current stream while they may be in flight
+        # (e.g. after a block raises before the later uploads completed)
+        Wd.record_stream(copy_stream)
         events = []
         with torch.cuda.stream(copy_stream):
             for b in range(cfg.partition.num_blocks):
@@ -980,7 +984,16 @@ def rbgs(W, theta, cfg: RbgsConfig, device_cfg: DeviceConfig = None, *, _eager: 
     # (type, message, block index) is exactly the reference's.
     deferred = (not _eager and not destroys_input and _deferrable(cfg)
                 and os.environ.get("RB_EAGER_STATUS", "0") != "1")
-    sweep = _sweep_blocks(Wd, n, theta, cfg, dc, q_storage, deferred, events)
+    try:
+        sweep = _sweep_blocks(Wd, n, theta, cfg, dc, q_storage, deferred, events)
+    except BaseException:
+        if events is not None:
+            # a block raised: no stream reads the remaining uploads, so
+            # order them before anything that may reuse Wd's memory
+            cur = torch.cuda.current_stream(dev)
+            for ev in events:
+                cur.wait_event(ev)
+        raise
     if deferred and not sweep._deferred_ok():
         global REPLAYS
         REPLAYS += 1

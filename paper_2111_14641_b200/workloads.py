@@ -34,6 +34,29 @@ def trig_host(n: int, m: int, seed: int, rows=None) -> np.ndarray:
     return np.asfortranarray(np.sin(10.0 * a) / (np.cos(100.0 * a) + 1.1))
 
 
+def lowrank_host(n: int, m: int, seed: int, smin: float = 1e-7, orthonormal: bool = False) -> np.ndarray:
+    """C3 on the host (parity samples): U diag(sigma) V^T, U n x m and V m x m
+    N(0,1) from numpy Generator(Philox(seed)) (as BASELINE.json writes it:
+    not orthonormalised), sigma logspaced 1 .. smin.  orthonormal=True gives
+    the certified companion of SURVEY.md 8(d) (U, V with orthonormal
+    columns, so cond(W) = 1 / smin exactly)."""
+    g = np.random.Generator(np.random.Philox(seed))
+    U = g.standard_normal((n, m))
+    V = g.standard_normal((m, m))
+    if orthonormal:
+        U = np.linalg.qr(U)[0]
+        V = np.linalg.qr(V)[0]
+    sig = np.logspace(0.0, math.log10(smin), m)
+    return np.asfortranarray((U * sig[None, :]) @ V.T)
+
+
+def colscaled_host(n: int, m: int, seed: int, lo: float = 1e-6) -> np.ndarray:
+    """C5 on the host (parity samples): G diag(logspace(0, log10(lo), m)),
+    G N(0,1) from numpy Generator(Philox(seed))."""
+    g = np.random.Generator(np.random.Philox(seed))
+    return np.asfortranarray(g.standard_normal((n, m)) * np.logspace(0.0, math.log10(lo), m)[None, :])
+
+
 def trig_device(n: int, m: int, seed: int, row0: int = 0, n_local: int = None, dtype=torch.float32,
                 device=None, chunk_cols: int = 64) -> torch.Tensor:
     """Rows row0 .. row0+n_local-1 of the trig family, column-major on device."""

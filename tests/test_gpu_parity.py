@@ -143,7 +143,7 @@ def test_sketch_vs_oracle(pkg, kind, dtype):
     got = out.cpu().numpy()
     want = osk.apply(oop, X)
     # binary32 gaussian sketches run on the tensor pipe (exact byte-split
-    # products, inputs fixed-point at 2^-30 of each 8192-row chunk max)
+    # products, inputs fixed-point at 2^-46 of each 16384-row chunk max)
     tol = 1e-11 if (kind == "gaussian" and dtype == torch.float32) else 1e-13
     assert np.linalg.norm(got - want) <= tol * np.linalg.norm(want), kind
 

@@ -218,46 +218,73 @@ def test_sharded_srht_kronecker_split_matches_fwht():
     assert np.linalg.norm(out - want) <= 1e-13 * np.linalg.norm(want)
 
 
-def _digits(xi):
-    """Balanced signed byte digits of sketch_tc.cu::digits."""
-    b0 = ((xi & 255) ^ 128) - 128
-    xi = (xi - b0) >> 8
-    b1 = ((xi & 255) ^ 128) - 128
-    xi = (xi - b1) >> 8
-    b2 = ((xi & 255) ^ 128) - 128
-    b3 = (xi - b2) >> 8
-    return b3, b2, b1, b0
+def _digits6(xi):
+    """The six balanced signed byte digits of sketch_tc.cu::planes4:
+    y = xi + 0x80_8080_8080 has the unsigned bytes b_q + 128 (q < 5) and
+    y >> 40 = b5; returns (b5, b4, b3, b2, b1, b0)."""
+    y = xi + 0x8080808080
+    b = [((y >> (8 * q)) & 255) - 128 for q in range(5)]
+    b5 = y >> 40
+    return (b5, b[4], b[3], b[2], b[1], b[0])
 
 
 def test_int8_ozaki_split_is_exact():
-    """The tensor-core gaussian sketch: q = 256 qh + ql, xi = sum b_w 2^(8w)
-    with balanced digits; the five shifted int32 blocks recombine to the
-    exact integer q . xi, and no block can overflow int32 over a chunk."""
+    """The tensor-core gaussian sketch as shipped (csrc/sketch_tc.cu): per
+    (column, 16384-row chunk) x = xi 2^(E-46), |xi| <= 2^46, six balanced
+    signed byte digits; q = 256 qh + ql.  One MMA multiplies qh by the six
+    digit planes, a second ql shifted by one block, so the seven int32 TMEM
+    blocks hold the weights 2^48 .. 2^0.  Checks: digits in s8 range, exact
+    recombination of q . xi over the chunk, every block and every prefix
+    sum < 2^31 (no int32 overflow; < 2^16 per row, < 2^30 per chunk), and
+    the two-half int64 recombination of the epilogue."""
     g = np.random.Generator(np.random.Philox(2))
     rows = 16384
     q = osk.gaussian_int16(3, 1, np.arange(rows))[0].astype(np.int64)
-    q[:4] = [32767, -32767, 32639, -32640]
-    x = g.standard_normal(rows).astype(np.float32)
-    E = math.frexp(float(np.max(np.abs(x))))[1]
-    xi = np.rint(x.astype(np.float64) * 2.0 ** (30 - E)).astype(np.int64)
-    assert np.max(np.abs(xi)) <= 2 ** 30
-    b3, b2, b1, b0 = _digits(xi)
-    for b in (b2, b1, b0):
-        assert b.min() >= -128 and b.max() <= 127
-    assert np.abs(b3).max() <= 65
-    assert np.array_equal(b3 * 2 ** 24 + b2 * 2 ** 16 + b1 * 2 ** 8 + b0, xi)
-    qh, ql = q >> 8, q & 255
-    assert qh.min() >= -128 and qh.max() <= 127 and ql.min() >= 0 and ql.max() <= 255
-    blocks = [qh * b3, qh * b2 + ql * b3, qh * b1 + ql * b2, qh * b0 + ql * b1, ql * b0]
-    for blk in blocks:
-        assert np.abs(blk).max() < 2 ** 16
-        assert abs(int(blk.sum())) < 2 ** 31 and np.abs(np.cumsum(blk)).max() < 2 ** 31
-    total = sum(int(blk.sum()) << (8 * (4 - w)) for w, blk in enumerate(blocks))
-    assert total == int(np.dot(q, xi))
-    # and the fixed-point representation is exact for binary32 entries near
-    # the chunk max, rounded at 2^(E-31) absolute below it
-    err = np.abs(xi * 2.0 ** (E - 30) - x.astype(np.float64))
-    assert err.max() <= 2.0 ** (E - 31)
+    q[:4] = [32767, -32767, 32639, -32768]  # extreme int16 table values
+    for case in range(3):
+        x = g.standard_normal(rows).astype(np.float32)
+        if case == 1:
+            x[:8] = [np.float32(3.4e38), np.float32(-3.4e38), 1e-30, -1e-30, 0.0, -0.0, 1e-45, 2.0 ** -126]
+        if case == 2:  # columns spanning many binades (the chunk max rules the scale)
+            x *= np.float32(2.0) ** g.integers(-40, 1, rows).astype(np.float32)
+        m = float(np.max(np.abs(x.astype(np.float64))))
+        E = math.frexp(m)[1]
+        xi = np.rint(x.astype(np.float64) * 2.0 ** (46 - E)).astype(np.int64)
+        assert np.max(np.abs(xi)) <= 2 ** 46
+        b5, b4, b3, b2, b1, b0 = _digits6(xi)
+        for b in (b4, b3, b2, b1, b0):
+            assert b.min() >= -128 and b.max() <= 127
+        assert np.abs(b5).max() <= 65
+        digits = (b5, b4, b3, b2, b1, b0)  # weights 2^40 .. 2^0
+        assert np.array_equal(sum(d << (8 * (5 - i)) for i, d in enumerate(digits)), xi)
+        qh, ql = q >> 8, q & 255
+        assert qh.min() >= -128 and qh.max() <= 127 and ql.min() >= 0 and ql.max() <= 255
+        # block w (w = 0..6) carries weight 2^(48 - 8w): qh x digit w, ql x digit w - 1
+        blocks = []
+        for w in range(7):
+            blk = np.zeros(rows, dtype=np.int64)
+            if w < 6:
+                blk += qh * digits[w]
+            if w >= 1:
+                blk += ql * digits[w - 1]
+            blocks.append(blk)
+        for blk in blocks:
+            assert np.abs(blk).max() < 2 ** 16
+            assert np.abs(np.cumsum(blk)).max() < 2 ** 30
+        sums = [int(blk.sum()) for blk in blocks]
+        total = sum(s_ << (48 - 8 * w) for w, s_ in enumerate(sums))
+        assert total == int(np.dot(q, xi))
+        # the epilogue's two exact int64 halves: hi = weights 2^48..2^32 (/2^32), lo = 2^24..2^0
+        hi = (sums[0] << 16) + (sums[1] << 8) + sums[2]
+        lo = (sums[3] << 24) + (sums[4] << 16) + (sums[5] << 8) + sums[6]
+        assert abs(hi) < 2 ** 47 and abs(lo) < 2 ** 55
+        assert (hi << 32) + lo == total
+        # fixed point: binary32 entries within 22 binades of the chunk max are
+        # exact; the rest round at 2^(E-47) absolute
+        err = np.abs(xi * 2.0 ** (E - 46) - x.astype(np.float64))
+        assert err.max() <= 2.0 ** (E - 47)
+        near = np.abs(x.astype(np.float64)) >= 2.0 ** (E - 23)
+        assert np.all(err[near] == 0.0)
 
 
 def test_reference_order_projection_is_sequential_fp32():

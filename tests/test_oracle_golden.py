@@ -138,3 +138,31 @@ def test_oracle_krylov_matches_reference():
                     cfg_kw=dict(interblock="sketched_cholqr(1)"))
     assert goldens.rel(rep["solution"], z["p3/x"]) <= 1e-6
     assert np.allclose(np.array(rep["residual_history"])[:, 1], z["p3/hist"][:, 1], rtol=1e-4)
+
+
+def test_cproj_restatement_matches_numpy_oracle_and_golden():
+    """oracle/cproj (plain C, -ffp-contract=off) is bit-identical to the numpy
+    restatement of kernels.gemm coarse and to the reference's own outputs."""
+    from oracle import cproj, sweep as osw
+    z = goldens.load("gemm")
+    t = 0
+    while f"Q{t}" in z.files:
+        Q, X, W = z[f"Q{t}"], z[f"X{t}"], z[f"W{t}"]
+        if W.shape[1] <= 64 and Q.shape[1] > 0:
+            got = cproj.project_f32(Q.astype(np.float32), X.astype(np.float32).astype(np.float64),
+                                    W.astype(np.float32)).astype(np.float64)
+            assert np.array_equal(got, z[f"coarse{t}"]), t
+        t += 1
+    g = np.random.Generator(np.random.Philox(12))
+    for n, c, p in [(3001, 77, 64), (129, 5, 1), (4096, 200, 40)]:
+        Q = g.standard_normal((n, c)).astype(np.float32)
+        X = g.standard_normal((c, p))
+        W = g.standard_normal((n, p)).astype(np.float32)
+        want = osw.gemm_ordered(-1.0, Q, X, 1.0, W, "coarse")
+        assert np.array_equal(cproj.project_f32(Q, X, W).astype(np.float64), want), (n, c, p)
+    # the tall-TRSM order restatement solves the system (reference: dtrsm)
+    import scipy.linalg
+    R = np.triu(g.standard_normal((41, 41))) + 8 * np.eye(41)
+    B = g.standard_normal((5000, 41))
+    want = scipy.linalg.solve_triangular(R, B.T, trans="T").T
+    assert np.abs(cproj.trsm_right_fma(B, R) - want).max() <= 1e-13 * np.abs(want).max()
