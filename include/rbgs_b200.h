@@ -159,16 +159,25 @@ int rb_trsm_right(int in_dtype, int out_dtype, int64_t n, int p, const void* B, 
                   const double* R, int64_t ldr, void* Xout, int64_t ldx, void* stream);
 
 /* ---- small fp64 kernels (Steps 2, 4-5, 7; rbgs.py:144-225, 267-290, 428-443)
- * C = alpha op(A) op(B) + beta C, fp64, op = transpose when trans != 0.    */
+ * All hand-written (csrc/kdim.cu, small.cu): no library GEMMs.
+ * C = alpha op(A) B + beta C, fp64 (numpy's `@` in the reference's LS
+ * solvers, kernels.py / rbgs.py:144-212), op = transpose when transA != 0;
+ * transB must be 0.  Split over K into ws (summed in split order:
+ * deterministic) when the tile grid alone cannot fill the GPU.            */
 int rb_gemm_f64(int transA, int transB, int m, int n, int k, double alpha,
                 const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
                 double* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
-/* binary32 C = alpha op(A) op(B) + beta C (cuBLAS SGEMM, default math mode:
- * no TF32) -- the Step-2 solvers in unique-coarse mode (fine = COARSE),
- * where the reference runs them in float32 (rbgs.py:144-212, prec.dtype). */
+/* binary32 C = alpha op(A) B + beta C with binary32 accumulation -- the
+ * Step-2 solvers in unique-coarse mode (fine = COARSE), where the reference
+ * runs them in float32 (rbgs.py:144-212, prec.dtype).                     */
 int rb_gemm_f32(int transA, int transB, int m, int n, int k, float alpha,
                 const float* A, int64_t lda, const float* B, int64_t ldb, float beta,
-                float* C, int64_t ldc, void* stream);
+                float* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
+/* Certification sums (rbgs.py:428-443) in ONE cooperative launch:
+ * out[0] = ||I - S^T S||_F^2, out[1] = ||P - S R||_F^2, out[2] = ||P||_F^2
+ * for S, P (k x m) and R (m x m), fixed summation order.                 */
+int rb_certify(int k, int m, const double* S, int64_t lds, const double* P, int64_t ldp,
+               const double* R, int64_t ldr, double* out, void* ws, size_t ws_bytes, void* stream);
 /* out[0..2] = sums of squares of three binary64 matrices (one launch; the
  * per-block finiteness words of P_i, S_i, R_ii -- rbgs.py:380-388 through
  * the reference's Matrix() checks).  ws: >= 256 bytes of the caller's
@@ -177,11 +186,11 @@ int rb_sumsq3(int64_t m1, int n1, const double* A1, int64_t lda1,
               int64_t m2, int n2, const double* A2, int64_t lda2,
               int64_t m3, int n3, const double* A3, int64_t lda3, double* out,
               void* ws, size_t ws_bytes, void* stream);
-/* Symmetric rank-k update, upper triangle: C = alpha A^T A + beta C for a
- * tall binary64 A (k x n, C n x n; cuBLAS DSYRK) -- the basis Gram of the
+/* Symmetric rank-k update: C = alpha A^T A + beta C for a tall binary64 A
+ * (k x n, C n x n; the full product is formed) -- the basis Gram of the
  * GMRES conditioning history (krylov.py:98-103, 247-257). */
 int rb_syrk_f64(int n, int64_t k, double alpha, const double* A, int64_t lda, double beta,
-                double* C, int64_t ldc, void* stream);
+                double* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
 /* Tall Gram / cross product: out (p x q fp64) = A^T B for n-row A (n x p)
  * and B (n x q), inputs f32 or f64, fp64 accumulation (fused l2 stage).  */
 int rb_cross(int a_dtype, int b_dtype, int64_t n, int p, int q, const void* A, int64_t lda,
@@ -209,12 +218,15 @@ int rb_sumsq(int dtype, int64_t m, int n, const void* A, int64_t lda, int minus_
 
 /* ---- composite Step-2 / Step-4-5 solvers ---------------------------------
  * Richardson (rbgs.py:144-156): X (c x p) after l sweeps of
- * X <- X + S^T (P - S X) from X = 0.  T is a k x p fp64 scratch.         */
+ * X <- X + S^T (P - S X) from X = 0.  T is a k x p fp64 scratch.  ONE
+ * cooperative launch (grid barriers between the split-K GEMM phases).
+ * p <= 64.                                                               */
 int rb_ls_richardson(int k, int c, int p, const double* S, int64_t lds, const double* P,
                      int64_t ldp, int l, double* X, int64_t ldx, double* T, int64_t ldt,
                      void* ws, size_t ws_bytes, void* stream);
 /* One sketched-CholQR pass on the k x p sketch Sp (rbgs.py:282-289):
- * G = Sp^T Sp, R = chol(G) (info as rb_potrf_upper), Sout = Sp R^{-1}.   */
+ * G = Sp^T Sp, R = chol(G) (info as rb_potrf_upper), Sout = Sp R^{-1}
+ * (rows solved in rb_trsm_right's order).  ONE cooperative launch.       */
 int rb_sketched_cholqr_small(int k, int p, const double* Sp, int64_t lds, double* R,
                              int64_t ldr, double* Sout, int64_t ldso, int* info,
                              void* ws, size_t ws_bytes, void* stream);

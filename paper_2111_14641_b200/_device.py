@@ -237,23 +237,25 @@ def trsm_right(B, R, out):
 def gemm(tA, tB, alpha, A, B, beta, C):
     m, n = C.shape
     k = A.shape[0] if tA else A.shape[1]
-    # cuBLAS DGEMM: no workspace of ours
+    ws, wsb = _ws(max(m, k), n, max(m, 64), C.device)
     call("rb_gemm_f64", int(tA), int(tB), m, n, k, alpha, ptr(A), ld(A), ptr(B), ld(B), beta, ptr(C), ld(C),
-         None, 0, st(C.device))
+         ws, wsb, st(C.device))
 
 
 def gemm32(tA, tB, alpha, A, B, beta, C):
-    """binary32 C = alpha op(A) op(B) + beta C (cuBLAS SGEMM, no TF32)."""
+    """binary32 C = alpha op(A) B + beta C (own kernel, binary32 accumulation)."""
     m, n = C.shape
     k = A.shape[0] if tA else A.shape[1]
+    ws, wsb = _ws(max(m, k), n, max(m, 64), C.device)
     call("rb_gemm_f32", int(tA), int(tB), m, n, k, alpha, ptr(A), ld(A), ptr(B), ld(B), beta, ptr(C), ld(C),
-         st(C.device))
+         ws, wsb, st(C.device))
 
 
 def syrk(A, C):
-    """Upper triangle of C = A^T A (binary64, cuBLAS DSYRK)."""
+    """Upper triangle of C = A^T A (binary64; the full product is formed)."""
     k, n = A.shape
-    call("rb_syrk_f64", n, k, 1.0, ptr(A), ld(A), 0.0, ptr(C), ld(C), st(C.device))
+    ws, wsb = _ws(max(n, 64), n, n, C.device)
+    call("rb_syrk_f64", n, k, 1.0, ptr(A), ld(A), 0.0, ptr(C), ld(C), ws, wsb, st(C.device))
 
 
 def cross(A, B, out, accumulate=False):
@@ -302,6 +304,13 @@ def richardson(S, P, l, X, T):
     ws, wsb = _ws(max(k, c), max(p, 64), max(k, c, 64), S.device)
     call("rb_ls_richardson", k, c, p, ptr(S), ld(S), ptr(P), ld(P), l, ptr(X), ld(X), ptr(T), ld(T), ws, wsb,
          st(S.device))
+
+
+def certify_sums(S, P, R, out):
+    """out[0:3] = ||I - S^T S||^2, ||P - S R||^2, ||P||^2 (one launch)."""
+    k, m = S.shape
+    ws, wsb = _ws(max(k, 64), m, k, S.device)
+    call("rb_certify", k, m, ptr(S), ld(S), ptr(P), ld(P), ptr(R), ld(R), ptr(out), ws, wsb, st(S.device))
 
 
 def sketched_cholqr_small(Sp, R, Sout, info):

@@ -64,11 +64,14 @@ int gemm_f64(int, int, int, int, int, double, const double*, int64_t, const doub
              int64_t, void*, size_t, cudaStream_t);
 int cross(int, int, int64_t, int, int, const void*, int64_t, const void*, int64_t, double*, int64_t, int, void*,
           size_t, cudaStream_t);
-int syrk_f64(int, int64_t, double, const double*, int64_t, double, double*, int64_t, cudaStream_t);
+int syrk_f64(int, int64_t, double, const double*, int64_t, double, double*, int64_t, void*, size_t, cudaStream_t);
 int sumsq3(int64_t, int, const double*, int64_t, int64_t, int, const double*, int64_t, int64_t, int, const double*,
            int64_t, double*, void*, size_t, cudaStream_t);
 int gemm_f32(int, int, int, int, int, float, const float*, int64_t, const float*, int64_t, float, float*, int64_t,
-             cudaStream_t);
+             void*, size_t, cudaStream_t);
+int certify(int, int, const double*, int64_t, const double*, int64_t, const double*, int64_t, double*, void*, size_t,
+            cudaStream_t);
+size_t kdim_ws_bytes(int k, int m);
 int potrf_upper(int, const double*, int64_t, double*, int64_t, int*, cudaStream_t);
 int trsm_left_upper(int, int, const double*, int64_t, double*, int64_t, int*, cudaStream_t);
 int geqrf_small(int, int, double*, int64_t, double*, int64_t, void*, size_t, cudaStream_t);
@@ -103,7 +106,9 @@ size_t rb_workspace_bytes(int64_t n, int ncols, int k) {
   size_t b = tiles > norms ? tiles : norms;
   b = b > single ? b : single;
   const size_t g = rb::gauss_tc_ws_bytes(n, ncols, k);
-  return (b > g ? b : g) + (1u << 20);
+  b = b > g ? b : g;
+  const size_t kd = rb::kdim_ws_bytes(k, ncols > k ? ncols : k);
+  return (b > kd ? b : kd) + (1u << 20);
 }
 
 int rb_project(int qd, int wd, int cd, int order, int64_t n, int c, int p, const void* Q, int64_t ldq,
@@ -170,8 +175,13 @@ int rb_trsm_right(int ind, int outd, int64_t n, int p, const void* B, int64_t ld
 }
 
 int rb_gemm_f32(int tA, int tB, int m, int n, int k, float alpha, const float* A, int64_t lda, const float* B,
-                int64_t ldb, float beta, float* C, int64_t ldc, void* s) {
-  return rb::gemm_f32(tA, tB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, as_stream(s));
+                int64_t ldb, float beta, float* C, int64_t ldc, void* ws, size_t wsb, void* s) {
+  return rb::gemm_f32(tA, tB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, ws, wsb, as_stream(s));
+}
+
+int rb_certify(int k, int m, const double* S, int64_t lds, const double* P, int64_t ldp, const double* R,
+               int64_t ldr, double* out, void* ws, size_t wsb, void* s) {
+  return rb::certify(k, m, S, lds, P, ldp, R, ldr, out, ws, wsb, as_stream(s));
 }
 
 int rb_gemm_f64(int tA, int tB, int m, int n, int k, double alpha, const double* A, int64_t lda, const double* B,
@@ -185,8 +195,8 @@ int rb_sumsq3(int64_t m1, int n1, const double* A1, int64_t lda1, int64_t m2, in
 }
 
 int rb_syrk_f64(int n, int64_t k, double alpha, const double* A, int64_t lda, double beta, double* C, int64_t ldc,
-                void* s) {
-  return rb::syrk_f64(n, k, alpha, A, lda, beta, C, ldc, as_stream(s));
+                void* ws, size_t wsb, void* s) {
+  return rb::syrk_f64(n, k, alpha, A, lda, beta, C, ldc, ws, wsb, as_stream(s));
 }
 
 int rb_cross(int ad, int bd, int64_t n, int p, int q, const void* A, int64_t lda, const void* B, int64_t ldb,

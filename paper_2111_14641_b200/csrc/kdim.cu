@@ -1,0 +1,566 @@
+// The k-dimensional steps of a block, hand-written for sm_100a (no library
+// GEMMs on the per-block path):
+//
+//   rb_ls_richardson        Step 2, l sweeps X <- X + S^T (P - S X) from
+//                           X = 0 (rbgs.py:144-156) as ONE cooperative
+//                           launch: every GEMM is split over the K
+//                           dimension across the whole grid, partial tiles
+//                           go to the caller's workspace and are summed in
+//                           split order (deterministic), grid barriers
+//                           separate the phases.
+//   rb_sketched_cholqr_small  one sketched-CholQR pass on the k x p sketch
+//                           (rbgs.py:282-289): G = S'^T S' (split-K over the
+//                           grid), R = chol(G) with dpotrf semantics
+//                           (kernels.py:234-247; info = first bad column),
+//                           Sout = S' R^{-1} -- ONE cooperative launch.
+//   rb_certify              Step 7 (rbgs.py:428-443): ||I - S^T S||_F^2,
+//                           ||P - S R||_F^2, ||P||_F^2 -- ONE cooperative
+//                           launch.
+//
+// Arithmetic: binary64 DFMA on the CUDA cores (B200's FP64 tensor rate is
+// the same as its DFMA rate, and these shapes -- p <= 64 columns, K <= a
+// few thousand -- are latency-, not throughput-bound).  Every reduction has
+// a fixed order, so results are bit-reproducible run to run.  The numpy
+// expression order is kept where it rounds: T = P - (S X) (the product is
+// formed, then subtracted), X = X + (S^T T).
+#include <cooperative_groups.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace rb {
+
+int sm_count();
+
+namespace {
+
+constexpr int kKT = 256;  // threads per CTA
+constexpr int kKC = 32;   // K rows staged per chunk
+constexpr int kTM = 64;   // output rows per tile
+
+// One TM x PB output tile of op(A) B over the K range [kb, ke):
+//   TRANS_A = false: op(A)[i, kk] = A[i + kk * lda]   (A is M x K)
+//   TRANS_A = true : op(A)[i, kk] = A[kk + i * lda]   (A is K x M, op = ^T)
+//   B[kk, j] = B[kk + j * ldb]                        (K x N)
+// Thread t owns rows 2 (t / 8) + {0, 1} and columns t % 8 + 8 ci, ci < PB / 8,
+// accumulated in ascending kk within the range.  Rows >= mrows / columns
+// >= ncols are computed on zeros.
+template <int PB, bool TRANS_A>
+__device__ __forceinline__ void tile_gemm(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
+                                          int64_t ldb, int m0, int mrows, int ncols, int64_t kb, int64_t ke,
+                                          double (&acc)[2][PB / 8], double* smem) {
+  double* sA = smem;             // [kKC][kTM]
+  double* sB = smem + kKC * kTM; // [kKC][PB]
+  const int tid = threadIdx.x;
+  const int ty = tid >> 3, tx = tid & 7;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < PB / 8; ++b) acc[a][b] = 0.0;
+  for (int64_t k0 = kb; k0 < ke; k0 += kKC) {
+    const int kc = (int)min((int64_t)kKC, ke - k0);
+    __syncthreads();
+    for (int e = tid; e < kKC * kTM; e += kKT) {
+      int i, kk;
+      if (TRANS_A) { kk = e % kKC; i = e / kKC; } else { i = e % kTM; kk = e / kTM; }
+      double v = 0.0;
+      if (i < mrows && kk < kc) v = TRANS_A ? A[(k0 + kk) + (int64_t)(m0 + i) * lda] : A[(m0 + i) + (k0 + kk) * lda];
+      sA[kk * kTM + i] = v;
+    }
+    for (int e = tid; e < kKC * PB; e += kKT) {
+      const int kk = e % kKC, j = e / kKC;
+      sB[kk * PB + j] = (j < ncols && kk < kc) ? B[(k0 + kk) + (int64_t)j * ldb] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < kKC; ++kk) {
+      const double a0 = sA[kk * kTM + 2 * ty], a1 = sA[kk * kTM + 2 * ty + 1];
+#pragma unroll
+      for (int ci = 0; ci < PB / 8; ++ci) {
+        const double b = sB[kk * PB + tx + 8 * ci];
+        acc[0][ci] = fma(a0, b, acc[0][ci]);
+        acc[1][ci] = fma(a1, b, acc[1][ci]);
+      }
+    }
+  }
+}
+
+template <int PB>
+constexpr size_t tile_smem() { return (size_t)kKC * (kTM + PB) * sizeof(double); }
+
+// K ranges: `splits` contiguous ranges of a multiple of kKC rows each.
+__device__ __forceinline__ void split_range(int64_t K, int splits, int s, int64_t& kb, int64_t& ke) {
+  const int64_t chunks = (K + kKC - 1) / kKC;
+  const int64_t per = (chunks + splits - 1) / splits;
+  kb = min(K, (int64_t)s * per * kKC);
+  ke = min(K, (int64_t)(s + 1) * per * kKC);
+}
+
+// Store a tile's partial: ws_tile[j * kTM + i] (column-major kTM x PB).
+template <int PB>
+__device__ __forceinline__ void store_partial(double* __restrict__ dst, const double (&acc)[2][PB / 8]) {
+  const int ty = threadIdx.x >> 3, tx = threadIdx.x & 7;
+#pragma unroll
+  for (int ci = 0; ci < PB / 8; ++ci) {
+    dst[(tx + 8 * ci) * kTM + 2 * ty] = acc[0][ci];
+    dst[(tx + 8 * ci) * kTM + 2 * ty + 1] = acc[1][ci];
+  }
+}
+
+// Sum of the splits of element (i, j) of tile `t` in split order.
+template <int PB>
+__device__ __forceinline__ double sum_splits(const double* __restrict__ ws, int tiles, int splits, int t, int i,
+                                             int j) {
+  double s = 0.0;
+  for (int q = 0; q < splits; ++q) s += ws[((int64_t)q * tiles + t) * (kTM * PB) + j * kTM + i];
+  return s;
+}
+
+// Split counts: enough (tile, split) items to cover the grid, each split at
+// least kKC rows.
+__device__ __forceinline__ int splits_for(int tiles, int64_t K, int grid) {
+  const int64_t chunks = max((int64_t)1, (K + kKC - 1) / kKC);
+  return (int)max((int64_t)1, min(chunks, (int64_t)((grid + tiles - 1) / tiles)));
+}
+
+// ============================ Richardson ====================================
+template <int PB>
+__global__ void __launch_bounds__(kKT)
+richardson_coop(int k, int c, int p, const double* __restrict__ S, int64_t lds, const double* __restrict__ P,
+                int64_t ldp, int l, double* __restrict__ X, int64_t ldx, double* __restrict__ T, int64_t ldt,
+                double* __restrict__ ws) {
+  extern __shared__ __align__(16) double smem[];
+  cg::grid_group grid = cg::this_grid();
+  const int G = gridDim.x;
+  const int tilesX = (c + kTM - 1) / kTM, tilesT = (k + kTM - 1) / kTM;
+  const int splitsX = splits_for(tilesX, k, G), splitsT = splits_for(tilesT, c, G);
+  const int64_t nthreads = (int64_t)G * kKT;
+  const int64_t gtid = (int64_t)blockIdx.x * kKT + threadIdx.x;
+  for (int sweep = 0; sweep < l; ++sweep) {
+    if (sweep > 0) {
+      // T = P - (S X): partials of S X over splits of c
+      for (int it = blockIdx.x; it < tilesT * splitsT; it += G) {
+        const int t = it % tilesT, s = it / tilesT;
+        int64_t kb, ke;
+        split_range(c, splitsT, s, kb, ke);
+        double acc[2][PB / 8];
+        tile_gemm<PB, false>(S, lds, X, ldx, t * kTM, min(kTM, k - t * kTM), p, kb, ke, acc, smem);
+        store_partial<PB>(ws + (int64_t)it * (kTM * PB), acc);
+      }
+      grid.sync();
+      for (int64_t e = gtid; e < (int64_t)k * p; e += nthreads) {
+        const int r = (int)(e % k), j = (int)(e / k);
+        const double sx = sum_splits<PB>(ws, tilesT, splitsT, r / kTM, r % kTM, j);
+        T[r + (int64_t)j * ldt] = P[r + (int64_t)j * ldp] - sx;
+      }
+      grid.sync();
+    }
+    // X = X + S^T T (first sweep: X = S^T P, since X = 0 and P - S 0 = P)
+    const double* Tin = sweep == 0 ? P : T;
+    const int64_t ldtin = sweep == 0 ? ldp : ldt;
+    for (int it = blockIdx.x; it < tilesX * splitsX; it += G) {
+      const int t = it % tilesX, s = it / tilesX;
+      int64_t kb, ke;
+      split_range(k, splitsX, s, kb, ke);
+      double acc[2][PB / 8];
+      tile_gemm<PB, true>(S, lds, Tin, ldtin, t * kTM, min(kTM, c - t * kTM), p, kb, ke, acc, smem);
+      store_partial<PB>(ws + (int64_t)it * (kTM * PB), acc);
+    }
+    grid.sync();
+    for (int64_t e = gtid; e < (int64_t)c * p; e += nthreads) {
+      const int a = (int)(e % c), j = (int)(e / c);
+      const double st = sum_splits<PB>(ws, tilesX, splitsX, a / kTM, a % kTM, j);
+      double* xp = X + a + (int64_t)j * ldx;
+      *xp = sweep == 0 ? st : *xp + st;
+    }
+    grid.sync();
+  }
+}
+
+// ============================ sketched CholQR ===============================
+// Cholesky of the p x p matrix in shared memory (upper, right-looking, dpotrf
+// semantics): returns 0 or the 1-based column of the first pivot <= 0 / NaN.
+__device__ int chol_smem(double* Sm, int p, int* bad_sh) {
+  if (threadIdx.x == 0) *bad_sh = 0;
+  __syncthreads();
+  for (int j = 0; j < p; ++j) {
+    const double d = Sm[j + j * p];
+    if (!(d > 0.0)) {
+      if (threadIdx.x == 0) *bad_sh = j + 1;
+      break;
+    }
+    const double r = sqrt(d);
+    for (int cc = j + 1 + threadIdx.x; cc < p; cc += blockDim.x) Sm[j + cc * p] /= r;
+    __syncthreads();
+    if (threadIdx.x == 0) Sm[j + j * p] = r;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5, ny = blockDim.x >> 5;
+    for (int b = j + 1 + ty; b < p; b += ny) {
+      const double sjb = Sm[j + b * p];
+      for (int a = j + 1 + tx; a <= b; a += 32) Sm[a + b * p] -= Sm[j + a * p] * sjb;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  return *bad_sh;
+}
+
+template <int PB>
+__global__ void __launch_bounds__(kKT)
+cholqr_coop(int k, int p, const double* __restrict__ Sp, int64_t lds, double* __restrict__ R, int64_t ldr,
+            double* __restrict__ Sout, int64_t ldso, int* __restrict__ info, double* __restrict__ ws) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int bad;
+  cg::grid_group grid = cg::this_grid();
+  const int G = gridDim.x;
+  const int splits = splits_for(1, k, G);
+  // G = S'^T S' (p x p, one tile), split over the k rows
+  for (int s = blockIdx.x; s < splits; s += G) {
+    int64_t kb, ke;
+    split_range(k, splits, s, kb, ke);
+    double acc[2][PB / 8];
+    tile_gemm<PB, true>(Sp, lds, Sp, lds, 0, p, p, kb, ke, acc, smem);
+    store_partial<PB>(ws + (int64_t)s * (kTM * PB), acc);
+  }
+  grid.sync();
+  double* Rg = ws + (int64_t)splits * (kTM * PB);  // R (p x p) + 1 / diag, for all CTAs
+  if (blockIdx.x == 0) {
+    double* Gm = smem;  // p x p, column-major
+    for (int e = threadIdx.x; e < p * p; e += kKT) {
+      const int i = e % p, j = e / p;
+      Gm[e] = i <= j ? sum_splits<PB>(ws, 1, splits, 0, i, j) : 0.0;
+    }
+    __syncthreads();
+    const int b = chol_smem(Gm, p, &bad);
+    for (int e = threadIdx.x; e < p * p; e += kKT) {
+      const int i = e % p, j = e / p;
+      const double v = i <= j ? Gm[e] : 0.0;
+      R[i + (int64_t)j * ldr] = v;
+      Rg[e] = v;
+    }
+    for (int j = threadIdx.x; j < p; j += kKT) Rg[p * p + j] = 1.0 / Gm[j + j * p];
+    if (threadIdx.x == 0) *info = b;
+  }
+  grid.sync();
+  // Sout = S' R^{-1}: one row per thread, fp64, l ascending (rb_trsm_right's
+  // order: t = fma(-x_l, R_lj, t), x_j = t * (1 / R_jj))
+  double* Rs = smem;
+  for (int e = threadIdx.x; e < p * p + p; e += kKT) Rs[e] = Rg[e];
+  __syncthreads();
+  for (int64_t r = (int64_t)blockIdx.x * kKT + threadIdx.x; r < k; r += (int64_t)G * kKT) {
+    double x[PB];
+#pragma unroll
+    for (int j = 0; j < PB; ++j) x[j] = j < p ? Sp[r + (int64_t)j * lds] : 0.0;
+#pragma unroll
+    for (int j = 0; j < PB; ++j) {
+      if (j < p) {
+        double t = x[j];
+#pragma unroll
+        for (int l2 = 0; l2 < j; ++l2) t = fma(-x[l2], Rs[l2 + j * p], t);
+        x[j] = t * Rs[p * p + j];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < PB; ++j)
+      if (j < p) Sout[r + (int64_t)j * ldso] = x[j];
+  }
+}
+
+// ============================ certification =================================
+// out[0] = ||I - S^T S||_F^2, out[1] = ||P - S R||_F^2, out[2] = ||P||_F^2
+// (rbgs.py:428-443); S, P k x m, R m x m.  Tiles of 64 x 64; the split-K
+// partials are summed in split order, then the squares in a fixed
+// two-stage order.
+__global__ void __launch_bounds__(kKT)
+certify_coop(int k, int m, const double* __restrict__ S, int64_t lds, const double* __restrict__ P, int64_t ldp,
+             const double* __restrict__ R, int64_t ldr, double* __restrict__ out, double* __restrict__ ws) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double red[kKT / 32];
+  cg::grid_group grid = cg::this_grid();
+  const int G = gridDim.x;
+  constexpr int PB = 64;
+  const int mt = (m + kTM - 1) / kTM, kt = (k + kTM - 1) / kTM;
+  const int tilesG = mt * mt, tilesE = kt * mt;
+  const int splitsG = splits_for(tilesG, k, G), splitsE = splits_for(tilesE, m, G);
+  double* wsG = ws;
+  double* wsE = ws + (int64_t)tilesG * splitsG * (kTM * PB);
+  double* part = wsE + (int64_t)tilesE * splitsE * (kTM * PB);  // [3][G]
+  for (int it = blockIdx.x; it < tilesG * splitsG + tilesE * splitsE; it += G) {
+    double acc[2][PB / 8];
+    if (it < tilesG * splitsG) {  // (S^T S) tile (ti, tj), split s over k
+      const int t = it % tilesG, s = it / tilesG;
+      const int ti = t % mt, tj = t / mt;
+      int64_t kb, ke;
+      split_range(k, splitsG, s, kb, ke);
+      tile_gemm<PB, true>(S, lds, S + (int64_t)tj * kTM * lds, lds, ti * kTM, min(kTM, m - ti * kTM),
+                          min(kTM, m - tj * kTM), kb, ke, acc, smem);
+      store_partial<PB>(wsG + (int64_t)it * (kTM * PB), acc);
+    } else {  // (S R) tile (ti over k, tj over m), split s over m
+      const int i2 = it - tilesG * splitsG;
+      const int t = i2 % tilesE, s = i2 / tilesE;
+      const int ti = t % kt, tj = t / kt;
+      int64_t kb, ke;
+      split_range(m, splitsE, s, kb, ke);
+      tile_gemm<PB, false>(S, lds, R + (int64_t)tj * kTM * ldr, ldr, ti * kTM, min(kTM, k - ti * kTM),
+                           min(kTM, m - tj * kTM), kb, ke, acc, smem);
+      store_partial<PB>(wsE + (int64_t)i2 * (kTM * PB), acc);
+    }
+  }
+  grid.sync();
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+  const int64_t nthreads = (int64_t)G * kKT, gtid = (int64_t)blockIdx.x * kKT + threadIdx.x;
+  for (int64_t e = gtid; e < (int64_t)m * m; e += nthreads) {
+    const int i = (int)(e % m), j = (int)(e / m);
+    const int t = (i / kTM) + (j / kTM) * mt;
+    const double g = sum_splits<PB>(wsG, tilesG, splitsG, t, i % kTM, j % kTM);
+    const double d = (i == j ? 1.0 : 0.0) - g;
+    a0 += d * d;
+  }
+  for (int64_t e = gtid; e < (int64_t)k * m; e += nthreads) {
+    const int r = (int)(e % k), j = (int)(e / k);
+    const int t = (r / kTM) + (j / kTM) * kt;
+    const double sr = sum_splits<PB>(wsE, tilesE, splitsE, t, r % kTM, j % kTM);
+    const double pv = P[r + (int64_t)j * ldp];
+    const double d = pv - sr;
+    a1 += d * d;
+    a2 += pv * pv;
+  }
+  a0 = block_sum(a0, red);
+  a1 = block_sum(a1, red);
+  a2 = block_sum(a2, red);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = a0;
+    part[G + blockIdx.x] = a1;
+    part[2 * G + blockIdx.x] = a2;
+  }
+  grid.sync();
+  if (blockIdx.x == 0 && threadIdx.x < 3) {
+    double s = 0.0;
+    for (int q = 0; q < G; ++q) s += part[threadIdx.x * G + q];
+    out[threadIdx.x] = s;
+  }
+}
+
+// ============================ generic GEMM ==================================
+// C = alpha op(A) B + beta C (op = transpose when tA), type T in and out
+// (double: binary64; float: the binary32 Step-2 solvers of unique-coarse
+// mode, rbgs.py:144-212 with prec.dtype = float32).  128 x 64 tiles, 256
+// threads, 8 x 4 accumulators per thread fed by LDS.128; split over K into
+// the workspace (summed in split order by gemm_reduce) when the tile grid is
+// too small to fill the GPU, else the epilogue is applied in place.
+constexpr int kGM = 128, kGN = 64, kGK = 16;
+
+template <typename T, bool TRANS_A>
+__global__ void __launch_bounds__(256)
+gemm_tiles(int m, int n, int64_t K, const T* __restrict__ A, int64_t lda, const T* __restrict__ B, int64_t ldb,
+           int64_t chunk, T alpha, T beta, T* __restrict__ C, int64_t ldc, T* __restrict__ ws) {
+  using V4 = typename std::conditional<sizeof(T) == 8, double4, float4>::type;
+  __shared__ __align__(32) T sA[kGK][kGM];
+  __shared__ __align__(32) T sB[kGK][kGN];
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;  // rows 8 ty.., cols 4 tx..
+  const int m0 = blockIdx.x * kGM, n0 = blockIdx.y * kGN;
+  const int64_t kb = (int64_t)blockIdx.z * chunk, ke = min(K, kb + chunk);
+  T acc[8][4];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = T(0);
+  for (int64_t k0 = kb; k0 < ke; k0 += kGK) {
+    __syncthreads();
+    for (int e = tid; e < kGK * kGM; e += 256) {
+      int i, kk;
+      if (TRANS_A) { kk = e % kGK; i = e / kGK; } else { i = e % kGM; kk = e / kGM; }
+      const int64_t kg = k0 + kk;
+      T v = T(0);
+      if (m0 + i < m && kg < ke) v = TRANS_A ? A[kg + (int64_t)(m0 + i) * lda] : A[(m0 + i) + kg * lda];
+      sA[kk][i] = v;
+    }
+    for (int e = tid; e < kGK * kGN; e += 256) {
+      const int kk = e % kGK, j = e / kGK;
+      const int64_t kg = k0 + kk;
+      sB[kk][j] = (n0 + j < n && kg < ke) ? B[kg + (int64_t)(n0 + j) * ldb] : T(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kGK; ++kk) {
+      T a[8], b[4];
+      const V4 a0 = *reinterpret_cast<const V4*>(&sA[kk][8 * ty]);
+      const V4 a1 = *reinterpret_cast<const V4*>(&sA[kk][8 * ty + 4]);
+      const V4 b0 = *reinterpret_cast<const V4*>(&sB[kk][4 * tx]);
+      a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
+      a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
+      b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc[q][t] = fma(a[q], b[t], acc[q][t]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int i = m0 + 8 * ty + q, j = n0 + 4 * tx + t;
+      if (i < m && j < n) {
+        if (ws) {
+          ws[(int64_t)blockIdx.z * m * n + i + (int64_t)j * m] = acc[q][t];
+        } else {
+          T* c = C + i + (int64_t)j * ldc;
+          *c = beta == T(0) ? alpha * acc[q][t] : alpha * acc[q][t] + beta * *c;
+        }
+      }
+    }
+}
+
+template <typename T>
+__global__ void gemm_reduce(const T* __restrict__ ws, int splits, int m, int n, T alpha, T beta, T* __restrict__ C,
+                            int64_t ldc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tot = (int64_t)m * n;
+  if (e >= tot) return;
+  T s = T(0);
+  for (int q = 0; q < splits; ++q) s += ws[(int64_t)q * tot + e];
+  const int i = (int)(e % m), j = (int)(e / m);
+  T* c = C + i + (int64_t)j * ldc;
+  *c = beta == T(0) ? alpha * s : alpha * s + beta * *c;
+}
+
+template <typename T>
+int gemm_generic(int tA, int m, int n, int64_t K, T alpha, const T* A, int64_t lda, const T* B, int64_t ldb, T beta,
+                 T* C, int64_t ldc, void* ws, size_t wsb, cudaStream_t st, const char* what) {
+  if (m == 0 || n == 0) return RB_OK;
+  const int mt = (m + kGM - 1) / kGM, nt = (n + kGN - 1) / kGN;
+  const int64_t tiles = (int64_t)mt * nt;
+  const int64_t want = 2 * (int64_t)sm_count();
+  int64_t splits = 1;
+  if (tiles < want && K > 4 * kGK) splits = std::min<int64_t>((want + tiles - 1) / tiles, (K + 4 * kGK - 1) / (4 * kGK));
+  const size_t per = (size_t)m * n * sizeof(T);
+  if (splits > 1 && (!ws || splits * per > wsb)) splits = ws ? std::max<int64_t>(1, (int64_t)(wsb / per)) : 1;
+  splits = std::min<int64_t>(splits, 65535);
+  int64_t chunk = K > 0 ? (K + splits - 1) / splits : 0;
+  chunk = (chunk + kGK - 1) / kGK * kGK;
+  if (chunk == 0) chunk = kGK;
+  splits = std::max<int64_t>(1, (K + chunk - 1) / chunk);
+  T* part = splits > 1 ? (T*)ws : nullptr;
+  RB_REQUIRE(mt <= INT32_MAX && nt <= 65535, "%s: too large", what);
+  const dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)splits);
+  if (tA) RB_KLAUNCH gemm_tiles<T, true><<<grid, 256, 0, st>>>(m, n, K, A, lda, B, ldb, chunk, alpha, beta, C, ldc, part);
+  else RB_KLAUNCH gemm_tiles<T, false><<<grid, 256, 0, st>>>(m, n, K, A, lda, B, ldb, chunk, alpha, beta, C, ldc, part);
+  if (part) RB_KLAUNCH gemm_reduce<T><<<ceil_div((int64_t)m * n, 256), 256, 0, st>>>(part, (int)splits, m, n, alpha,
+                                                                                     beta, C, ldc);
+  return check_launch(what);
+}
+
+// ---- launch helpers -----------------------------------------------------------
+template <typename K>
+int coop_launch(K kern, size_t smem, void** args, cudaStream_t st, int max_grid, int* grid_out, const char* what) {
+  static int dev_cached = -1;
+  (void)dev_cached;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kKT, smem);
+  RB_REQUIRE(per_sm >= 1, "%s: kernel does not fit an SM", what);
+  int grid = std::min(max_grid, sm_count() * std::min(per_sm, 2));
+  grid = std::max(grid, 1);
+  *grid_out = grid;
+  ++g_launches;
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kKT), args, smem, st);
+  if (e != cudaSuccess) {
+    set_error("%s: cooperative launch failed: %s", what, cudaGetErrorString(e));
+    return RB_ECUDA;
+  }
+  return check_launch(what);
+}
+
+}  // namespace
+
+// Workspace of the cooperative k-dimensional kernels (upper bound): split-K
+// partial tiles for a grid of 2 CTAs per SM plus the output tiles.
+size_t kdim_ws_bytes(int k, int m) {
+  const size_t grid = 2 * (size_t)sm_count();
+  const size_t tiles = (size_t)((k + kTM - 1) / kTM + 1) * ((m + kTM - 1) / kTM + 1);
+  return (grid + tiles + 4) * (size_t)kTM * 64 * sizeof(double) + 3 * grid * sizeof(double) + 4096;
+}
+
+int ls_richardson(int k, int c, int p, const double* S, int64_t lds, const double* P, int64_t ldp, int l, double* X,
+                  int64_t ldx, double* T, int64_t ldt, void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(k >= 1 && c >= 1 && p >= 1 && p <= 64 && l >= 1 && S && P && X && T && lds >= k && ldp >= k &&
+                 ldx >= c && ldt >= k,
+             "rb_ls_richardson: bad args (k=%d c=%d p=%d l=%d)", k, c, p, l);
+  const int tilesX = (c + kTM - 1) / kTM, tilesT = (k + kTM - 1) / kTM;
+  // every phase's items use at most max(grid, tiles) tiles of kTM x 64 doubles
+  const int max_grid = sm_count();  // one CTA per SM: fewer CTAs per grid barrier
+  const size_t need = (size_t)(2 * sm_count() + std::max(tilesX, tilesT)) * kTM * 64 * sizeof(double);
+  RB_REQUIRE(ws && wsb >= need, "rb_ls_richardson: workspace too small (%zu < %zu)", wsb, need);
+  int grid = 0;
+  void* args[] = {&k, &c, &p, (void*)&S, &lds, (void*)&P, &ldp, &l, &X, &ldx, &T, &ldt, &ws};
+#define RB_RI(V)                                                                                         \
+  if (p <= V) return coop_launch(richardson_coop<V>, tile_smem<V>(), args, st, max_grid, &grid, "rb_ls_richardson");
+  RB_RI(8) RB_RI(16) RB_RI(24) RB_RI(32) RB_RI(40) RB_RI(48) RB_RI(64)
+#undef RB_RI
+  return RB_EINVAL;
+}
+
+int sketched_cholqr_small(int k, int p, const double* Sp, int64_t lds, double* R, int64_t ldr, double* Sout,
+                          int64_t ldso, int* info, void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(k >= 1 && p >= 1 && p <= 64 && Sp && R && Sout && info && lds >= k && ldr >= p && ldso >= k,
+             "rb_sketched_cholqr_small: bad args (k=%d p=%d)", k, p);
+  const int max_grid = sm_count();
+  const size_t need = (size_t)(max_grid + 1) * kTM * 64 * sizeof(double) + (size_t)(p * p + p) * sizeof(double);
+  RB_REQUIRE(ws && wsb >= need, "rb_sketched_cholqr_small: workspace too small");
+  // enough CTAs for the k-row split of the Gram and one row per thread in
+  // the solve, no more (grid barriers cost per CTA)
+  const int want = std::max(1, std::min(max_grid, std::max((k + kKT - 1) / kKT, (k + 4 * kKC - 1) / (4 * kKC))));
+  int grid = 0;
+  void* args[] = {&k, &p, (void*)&Sp, &lds, &R, &ldr, &Sout, &ldso, &info, &ws};
+#define RB_CQ(V)                                                                                            \
+  if (p <= V) {                                                                                             \
+    const size_t sm = std::max(tile_smem<V>(), (size_t)(V * V + V) * sizeof(double));                      \
+    return coop_launch(cholqr_coop<V>, sm, args, st, want, &grid, "rb_sketched_cholqr_small");             \
+  }
+  RB_CQ(8) RB_CQ(16) RB_CQ(24) RB_CQ(32) RB_CQ(40) RB_CQ(48) RB_CQ(64)
+#undef RB_CQ
+  return RB_EINVAL;
+}
+
+int certify(int k, int m, const double* S, int64_t lds, const double* P, int64_t ldp, const double* R, int64_t ldr,
+            double* out, void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(k >= 1 && m >= 1 && S && P && R && out && lds >= k && ldp >= k && ldr >= m,
+             "rb_certify: bad args (k=%d m=%d)", k, m);
+  const int max_grid = sm_count();
+  const int mt = (m + kTM - 1) / kTM, kt = (k + kTM - 1) / kTM;
+  const size_t need = ((size_t)(mt * mt + kt * mt) + 2 * (size_t)max_grid) * kTM * 64 * sizeof(double) +
+                      3 * (size_t)max_grid * sizeof(double);
+  RB_REQUIRE(ws && wsb >= need, "rb_certify: workspace too small (%zu < %zu)", wsb, need);
+  int grid = 0;
+  void* args[] = {&k, &m, (void*)&S, &lds, (void*)&P, &ldp, (void*)&R, &ldr, &out, &ws};
+  return coop_launch(certify_coop, tile_smem<64>(), args, st, max_grid, &grid, "rb_certify");
+}
+
+int gemm_f64(int tA, int tB, int m, int n, int k, double alpha, const double* A, int64_t lda, const double* B,
+             int64_t ldb, double beta, double* C, int64_t ldc, void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(m >= 0 && n >= 0 && k >= 0 && C && ldc >= std::max(m, 1) && tB == 0 &&
+                 (k == 0 || (A && B && lda >= (tA ? k : m) && ldb >= k)),
+             "rb_gemm_f64: bad args (op(B) must be B)");
+  return gemm_generic<double>(tA, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, ws, wsb, st, "rb_gemm_f64");
+}
+
+int gemm_f32(int tA, int tB, int m, int n, int k, float alpha, const float* A, int64_t lda, const float* B,
+             int64_t ldb, float beta, float* C, int64_t ldc, void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(m >= 0 && n >= 0 && k >= 0 && C && ldc >= std::max(m, 1) && tB == 0 &&
+                 (k == 0 || (A && B && lda >= (tA ? k : m) && ldb >= k)),
+             "rb_gemm_f32: bad args (op(B) must be B)");
+  return gemm_generic<float>(tA, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, ws, wsb, st, "rb_gemm_f32");
+}
+
+// Upper triangle of C = alpha A^T A + beta C (the full product is formed;
+// the strictly lower part of C is written too)
+int syrk_f64(int n, int64_t k, double alpha, const double* A, int64_t lda, double beta, double* C, int64_t ldc,
+             void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(n >= 0 && k >= 0 && C && ldc >= std::max(n, 1) && (k == 0 || (A && lda >= k)), "rb_syrk_f64: bad args");
+  return gemm_generic<double>(1, n, n, k, alpha, A, lda, A, lda, beta, C, ldc, ws, wsb, st, "rb_syrk_f64");
+}
+
+}  // namespace rb

@@ -3,8 +3,6 @@
 // certification (rbgs.py:428-443), the tall triangular scaling of Steps 4-5
 // (rbgs.py:284, kernels.py:250-270) and the Householder QR used by the
 // direct LS solver and the GMRES least-squares problem (kernels.py:216-231).
-#include <cublas_v2.h>
-
 #include <mutex>
 
 #include "common.cuh"
@@ -346,72 +344,6 @@ void trsm_right_launch(int64_t n, int p, const void* B, int64_t ldb, const doubl
 
 }  // namespace
 
-// Plain fp64 GEMMs (Richardson sweeps, Gram matrices, certification) go to
-// cuBLAS DGEMM: they are library GEMMs in the sense of the build rules, and
-// cuBLAS' DMMA kernels beat a hand-rolled split-K fp64 kernel at these
-// small, latency-bound shapes.  One handle per device, stream set per call.
-static cublasHandle_t cublas_handle() {
-  static cublasHandle_t h[64] = {nullptr};
-  static std::mutex mu;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> g(mu);
-  if (!h[dev]) cublasCreate(&h[dev]);
-  return h[dev];
-}
-
-int dgemm(int tA, int tB, int m, int n, int k, double alpha, const double* A, int64_t lda, const double* B,
-          int64_t ldb, double beta, double* C, int64_t ldc, cudaStream_t st) {
-  if (m == 0 || n == 0) return RB_OK;
-  cublasHandle_t h = cublas_handle();
-  RB_REQUIRE(h, "cuBLAS handle creation failed");
-  cublasSetStream(h, st);
-  const cublasStatus_t s = cublasDgemm(h, tA ? CUBLAS_OP_T : CUBLAS_OP_N, tB ? CUBLAS_OP_T : CUBLAS_OP_N, m, n, k,
-                                       &alpha, A, (int)std::max<int64_t>(lda, 1), B, (int)std::max<int64_t>(ldb, 1),
-                                       &beta, C, (int)ldc);
-  ++g_launches;
-  RB_REQUIRE(s == CUBLAS_STATUS_SUCCESS, "cublasDgemm failed (%d)", (int)s);
-  return check_launch("dgemm");
-}
-
-int syrk_f64(int n, int64_t k, double alpha, const double* A, int64_t lda, double beta, double* C, int64_t ldc,
-             cudaStream_t st) {
-  RB_REQUIRE(n >= 0 && k >= 0 && k <= INT32_MAX && C && ldc >= std::max(n, 1) && (k == 0 || (A && lda >= k)),
-             "rb_syrk_f64: bad args");
-  if (n == 0) return RB_OK;
-  cublasHandle_t h = cublas_handle();
-  RB_REQUIRE(h, "cuBLAS handle creation failed");
-  cublasSetStream(h, st);
-  const cublasStatus_t s = cublasDsyrk(h, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, n, (int)k, &alpha, A,
-                                       (int)std::max<int64_t>(lda, 1), &beta, C, (int)ldc);
-  ++g_launches;
-  RB_REQUIRE(s == CUBLAS_STATUS_SUCCESS, "cublasDsyrk failed (%d)", (int)s);
-  return check_launch("syrk");
-}
-
-int gemm_f32(int tA, int tB, int m, int n, int k, float alpha, const float* A, int64_t lda, const float* B,
-             int64_t ldb, float beta, float* C, int64_t ldc, cudaStream_t st) {
-  RB_REQUIRE(m >= 0 && n >= 0 && k >= 0 && C && ldc >= std::max(m, 1), "rb_gemm_f32: bad args");
-  if (m == 0 || n == 0) return RB_OK;
-  cublasHandle_t h = cublas_handle();
-  RB_REQUIRE(h, "cuBLAS handle creation failed");
-  cublasSetStream(h, st);
-  cublasSetMathMode(h, CUBLAS_DEFAULT_MATH);
-  const cublasStatus_t s = cublasSgemm(h, tA ? CUBLAS_OP_T : CUBLAS_OP_N, tB ? CUBLAS_OP_T : CUBLAS_OP_N, m, n, k,
-                                       &alpha, A, (int)std::max<int64_t>(lda, 1), B, (int)std::max<int64_t>(ldb, 1),
-                                       &beta, C, (int)ldc);
-  ++g_launches;
-  RB_REQUIRE(s == CUBLAS_STATUS_SUCCESS, "cublasSgemm failed (%d)", (int)s);
-  return check_launch("sgemm");
-}
-
-// ============================== entry points ================================
-int gemm_f64(int tA, int tB, int m, int n, int k, double alpha, const double* A, int64_t lda, const double* B,
-             int64_t ldb, double beta, double* C, int64_t ldc, void* ws, size_t wsb, cudaStream_t st) {
-  RB_REQUIRE(m >= 0 && n >= 0 && k >= 0 && C && ldc >= std::max(m, 1), "rb_gemm_f64: bad args");
-  return dgemm(tA, tB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, st);
-}
-
 // Tall-skinny cross product out = A^T B for p, q <= 8 (the l2 stage's
 // Q'^T Q' at block width 4 / 8): the split-K tile kernel
 // would multiply a 128 x 16 register tile of mostly padding per row.  Here
@@ -635,28 +567,6 @@ int convert(int ind, int outd, int64_t m, int n, const void* X, int64_t ldx, voi
   else if (outd == RB_F32) RB_KLAUNCH convert_kernel<double, float><<<grid, 256, 0, st>>>(m, n, (const double*)X, ldx, (float*)Y, ldy);
   else RB_KLAUNCH convert_kernel<double, double><<<grid, 256, 0, st>>>(m, n, (const double*)X, ldx, (double*)Y, ldy);
   return check_launch("rb_convert");
-}
-
-int ls_richardson(int k, int c, int p, const double* S, int64_t lds, const double* P, int64_t ldp, int l, double* X,
-                  int64_t ldx, double* T, int64_t ldt, void* ws, size_t wsb, cudaStream_t st) {
-  RB_REQUIRE(k >= 1 && c >= 1 && p >= 1 && l >= 1 && S && P && X && T, "rb_ls_richardson: bad args");
-  // sweep 1 from X = 0 is exactly S^T P (rbgs.py:153-155)
-  int rc = dgemm(1, 0, c, p, k, 1.0, S, lds, P, ldp, 0.0, X, ldx, st);
-  for (int it = 1; it < l && rc == RB_OK; ++it) {
-    RB_KLAUNCH copy_f64<<<ceil_div((int64_t)k * p, 256), 256, 0, st>>>(k, p, P, ldp, T, ldt);
-    rc = dgemm(0, 0, k, p, c, -1.0, S, lds, X, ldx, 1.0, T, ldt, st);  // T = P - S X
-    if (rc == RB_OK) rc = dgemm(1, 0, c, p, k, 1.0, S, lds, T, ldt, 1.0, X, ldx, st);
-  }
-  return rc;
-}
-
-int sketched_cholqr_small(int k, int p, const double* Sp, int64_t lds, double* R, int64_t ldr, double* Sout,
-                          int64_t ldso, int* info, void* ws, size_t wsb, cudaStream_t st) {
-  RB_REQUIRE(k >= 1 && p >= 1 && p <= 64 && Sp && R && Sout && info, "rb_sketched_cholqr_small: bad args");
-  int rc = dgemm(1, 0, p, p, k, 1.0, Sp, lds, Sp, lds, 0.0, R, ldr, st);  // G in R
-  if (rc == RB_OK) rc = potrf_upper(p, R, ldr, R, ldr, info, st);
-  if (rc == RB_OK) rc = trsm_right(RB_F64, RB_F64, k, p, Sp, lds, R, ldr, Sout, ldso, st);
-  return rc;
 }
 
 }  // namespace rb

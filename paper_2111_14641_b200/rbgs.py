@@ -262,7 +262,7 @@ def _householder_direct_dev(S, P, X, scr, sync=True, u=None):
 def _solve_ls_f32(name, param, S, offsets, P, X, scr):
     """Step 2 in binary32 (fine = COARSE): the reference casts S and P_i to
     float32 and runs the solver in float32 BLAS (rbgs.py:144-212); here
-    cuBLAS SGEMM (no TF32) on the device.  X comes back as binary64 values
+    the library's own binary32 GEMM (binary32 accumulation, no TF32).  X comes back as binary64 values
     of the binary32 solution (`X.astype(np.float64)`)."""
     k, c = S.shape
     p = P.shape[1]
@@ -476,9 +476,8 @@ class RbgsSweep:
                     self._sketch_reduce(Qcur, Sp)
                 if it == 0:
                     sp_qp = Sp.clone() if self.cfg.certify_blocks else None
-                G = scr.G[:w, :w]
-                D.gemm(1, 0, 1.0, Sp, Sp, 0.0, G)
-                D.potrf(G, RS, scr.info[it % 4:it % 4 + 1])
+                # G = Sp^T Sp, R_S = chol(G), Ss = Sp R_S^{-1}: one launch
+                D.sketched_cholqr_small(Sp, RS, scr.Ss[:, :w], scr.info[it % 4:it % 4 + 1])
                 last = it == l - 1
                 # resketch sketches the binary64 Q_i before it is rounded to
                 # the slot's format (rbgs.py:286-287 sketches fp64 Q)
@@ -499,12 +498,12 @@ class RbgsSweep:
                     D.gemm(0, 0, 1.0, RS, Rt, 0.0, Rn)
                     Rt.copy_(Rn)
                 Qcur = out
-            Si = scr.Si[:, :w]
             if self.cfg.resketch:
+                Si = scr.Si[:, :w]
                 self._sketch_reduce(Qcur, Si)
                 D.convert(Qcur, slot)
             else:
-                D.trsm_right(Sp, RS, Si)
+                Si = scr.Ss[:, :w]  # the last pass's Sp R_S^{-1}
             return Rt, Si, sp_qp
         # l2_plus_cholqr -- Gram realisation of the l2 stage:
         # R' = chol(Q'^T Q'), S* = (Theta Q') R'^{-1} = Theta Q*, then the
@@ -1012,15 +1011,10 @@ def certify(S, P, R, device=None) -> CertReport:
         Sd, Pd, Rd = _dev_f64(S, dev), _dev_f64(P, dev), _dev_f64(R, dev)
         k, m = Sd.shape
         out = torch.zeros(3, dtype=torch.float64, device=dev)
-        D.sumsq(Pd, out[2:3])
         if m:
-            G = D.empty_cm(m, m, torch.float64, dev)
-            D.gemm(1, 0, 1.0, Sd, Sd, 0.0, G)
-            D.sumsq(G, out[0:1], minus_identity=True)
-            T = D.empty_cm(k, m, torch.float64, dev)
-            T.copy_(Pd)
-            D.gemm(0, 0, -1.0, Sd, Rd, 1.0, T)
-            D.sumsq(T, out[1:2])
+            D.certify_sums(Sd, Pd, Rd, out)
+        else:
+            D.sumsq(Pd, out[2:3])
         o = out.cpu().numpy()
     if not np.all(np.isfinite(o)):
         raise ValueError("Matrix entries must be finite")

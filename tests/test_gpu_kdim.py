@@ -1,0 +1,108 @@
+"""The hand-written k-dimensional kernels (csrc/kdim.cu) against numpy /
+the oracle: Richardson (rbgs.py:144-156), one sketched-CholQR pass
+(rbgs.py:282-289), certification (rbgs.py:428-443) and the generic
+binary64 / binary32 GEMMs.  Tolerances: binary64 reassociation level
+(the kernels and OpenBLAS sum in different fixed orders); the results are
+also checked to be bit-reproducible run to run."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import sweep as osw
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def D():
+    from paper_2111_14641_b200 import _device
+
+    return _device
+
+
+def _dev(A, dtype=torch.float64):
+    from paper_2111_14641_b200 import _device as Dm
+
+    return Dm.to_cm(torch.from_numpy(np.asfortranarray(A)), dtype, "cuda")
+
+
+def _orth(g, k, c):
+    return np.linalg.qr(g.standard_normal((k, c)))[0] + 1e-3 * g.standard_normal((k, c))
+
+
+@pytest.mark.parametrize("k,c,p,l", [(1600, 760, 40, 5), (2048, 960, 64, 5), (400, 190, 10, 5), (100, 7, 3, 1),
+                                     (488, 240, 4, 2), (1024, 480, 32, 3)])
+def test_richardson_vs_oracle(D, k, c, p, l):
+    g = np.random.Generator(np.random.Philox(k + c))
+    S = _orth(g, k, c)
+    P = g.standard_normal((k, p))
+    X = D.empty_cm(c, p, torch.float64, "cuda")
+    T = D.empty_cm(k, p, torch.float64, "cuda")
+    Sd, Pd = _dev(S), _dev(P)
+    D.richardson(Sd, Pd, l, X, T)
+    got = X.cpu().numpy()
+    want = osw.ls_richardson(S, P, l)
+    assert np.linalg.norm(got - want) <= 1e-13 * np.linalg.norm(want)
+    X2 = torch.zeros_like(X)
+    D.richardson(Sd, Pd, l, X2, T)
+    assert torch.equal(X, X2)
+
+
+@pytest.mark.parametrize("k,p", [(1600, 40), (2048, 64), (400, 10), (1024, 32), (488, 4), (70, 37)])
+def test_sketched_cholqr_small_vs_numpy(D, k, p):
+    import scipy.linalg
+
+    g = np.random.Generator(np.random.Philox(p))
+    Sp = g.standard_normal((k, p)) @ np.diag(np.logspace(0, -4, p))
+    R = D.empty_cm(p, p, torch.float64, "cuda")
+    So = D.empty_cm(k, p, torch.float64, "cuda")
+    info = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    D.sketched_cholqr_small(_dev(Sp), R, So, info)
+    assert int(info.item()) == 0
+    Rw = osw.cholesky_upper(Sp.T @ Sp)
+    assert np.linalg.norm(R.cpu().numpy() - Rw) <= 1e-12 * np.linalg.norm(Rw)
+    Sw = scipy.linalg.solve_triangular(Rw, Sp.T, trans="T").T
+    assert np.linalg.norm(So.cpu().numpy() - Sw) <= 1e-10 * np.linalg.norm(Sw)
+    # not positive definite: dpotrf's 1-based column
+    Sb = Sp.copy()
+    Sb[:, 5 % p] = 0.0  # an exactly zero pivot
+    D.sketched_cholqr_small(_dev(Sb), R, So, info)
+    want = 1 + (5 % p)
+    assert int(info.item()) == want
+
+
+@pytest.mark.parametrize("k,m", [(1600, 800), (400, 200), (2048, 1024), (96, 5)])
+def test_certify_sums_vs_numpy(D, k, m):
+    g = np.random.Generator(np.random.Philox(m))
+    S = _orth(g, k, m)
+    R = np.triu(g.standard_normal((m, m)))
+    P = S @ R + 1e-6 * g.standard_normal((k, m))
+    out = torch.zeros(3, dtype=torch.float64, device="cuda")
+    D.certify_sums(_dev(S), _dev(P), _dev(R), out)
+    o = out.cpu().numpy()
+    want = [np.linalg.norm(np.eye(m) - S.T @ S) ** 2, np.linalg.norm(P - S @ R) ** 2, np.linalg.norm(P) ** 2]
+    assert np.allclose(o[[0, 2]], np.array(want)[[0, 2]], rtol=1e-11)
+    # ||P - S R|| is a cancellation (~1e-6 of ||P||): absolute binary64 level
+    assert abs(o[1] - want[1]) <= 1e-12 * want[2] + 1e-9 * want[1]
+
+
+@pytest.mark.parametrize("tA,m,n,k", [(1, 760, 40, 1600), (0, 1600, 40, 760), (1, 240, 240, 300_000),
+                                      (0, 300_000, 60, 240), (1, 3, 2, 5), (0, 1, 1, 1)])
+@pytest.mark.parametrize("dt", [torch.float64, torch.float32])
+def test_gemm_vs_numpy(D, tA, m, n, k, dt):
+    g = np.random.Generator(np.random.Philox(m + n))
+    A = g.standard_normal((k, m) if tA else (m, k))
+    B = g.standard_normal((k, n))
+    C0 = g.standard_normal((m, n))
+    Ad, Bd = _dev(A, dt), _dev(B, dt)
+    for alpha, beta in ((1.0, 0.0), (-1.0, 1.0), (0.5, 2.0)):
+        C = _dev(C0, dt)
+        (D.gemm if dt == torch.float64 else D.gemm32)(tA, 0, alpha, Ad, Bd, beta, C)
+        Aw = A.astype(np.float32).astype(np.float64) if dt == torch.float32 else A
+        Bw = B.astype(np.float32).astype(np.float64) if dt == torch.float32 else B
+        Cw = C0.astype(np.float32).astype(np.float64) if dt == torch.float32 else C0
+        want = alpha * ((Aw.T if tA else Aw) @ Bw) + beta * Cw
+        scale = np.abs(Aw.T if tA else Aw) @ np.abs(Bw) + np.abs(Cw)
+        u = 2.0 ** -24 if dt == torch.float32 else 2.0 ** -53
+        assert np.all(np.abs(C.double().cpu().numpy() - want) <= 4 * k * u * scale + 1e-300)
