@@ -237,7 +237,7 @@ def trsm_right(B, R, out):
 def gemm(tA, tB, alpha, A, B, beta, C):
     m, n = C.shape
     k = A.shape[0] if tA else A.shape[1]
-    ws, wsb = _ws(max(m, k), n, max(m, 64), C.device)
+    ws, wsb = _ws(1, 1, 1, C.device)  # split-K partials: <= 2 x SMs x 128 x 64 doubles
     call("rb_gemm_f64", int(tA), int(tB), m, n, k, alpha, ptr(A), ld(A), ptr(B), ld(B), beta, ptr(C), ld(C),
          ws, wsb, st(C.device))
 
@@ -246,7 +246,7 @@ def gemm32(tA, tB, alpha, A, B, beta, C):
     """binary32 C = alpha op(A) B + beta C (own kernel, binary32 accumulation)."""
     m, n = C.shape
     k = A.shape[0] if tA else A.shape[1]
-    ws, wsb = _ws(max(m, k), n, max(m, 64), C.device)
+    ws, wsb = _ws(1, 1, 1, C.device)
     call("rb_gemm_f32", int(tA), int(tB), m, n, k, alpha, ptr(A), ld(A), ptr(B), ld(B), beta, ptr(C), ld(C),
          ws, wsb, st(C.device))
 
@@ -254,7 +254,7 @@ def gemm32(tA, tB, alpha, A, B, beta, C):
 def syrk(A, C):
     """Upper triangle of C = A^T A (binary64; the full product is formed)."""
     k, n = A.shape
-    ws, wsb = _ws(max(n, 64), n, n, C.device)
+    ws, wsb = _ws(1, 1, 1, C.device)
     call("rb_syrk_f64", n, k, 1.0, ptr(A), ld(A), 0.0, ptr(C), ld(C), ws, wsb, st(C.device))
 
 

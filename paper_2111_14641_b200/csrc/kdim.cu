@@ -127,56 +127,172 @@ __device__ __forceinline__ int splits_for(int tiles, int64_t K, int grid) {
 }
 
 // ============================ Richardson ====================================
+// ---- Richardson, v2 ----------------------------------------------------------
+// Each GEMM phase is cut into at most gridDim.x items (128-row output tile x
+// K split, tiles x splits <= grid: one item per CTA, no tail round).  An
+// item streams its K range in chunks of kR2K rows, the next chunk's global
+// loads in flight (registers) while the current one is multiplied from
+// shared memory; it writes its partial tile, and the LAST item of a tile to
+// arrive (arrival counter) sums the tile's partials in split order and
+// applies the epilogue -- deterministic, and no separate reduction phase.
+// Two grid barriers per sweep (after T, after X).
+constexpr int kR2M = 128;  // output rows per tile
+constexpr int kR2K = 32;   // K rows per chunk
+
 template <int PB>
-__global__ void __launch_bounds__(kKT)
-richardson_coop(int k, int c, int p, const double* __restrict__ S, int64_t lds, const double* __restrict__ P,
-                int64_t ldp, int l, double* __restrict__ X, int64_t ldx, double* __restrict__ T, int64_t ldt,
-                double* __restrict__ ws) {
-  extern __shared__ __align__(16) double smem[];
+struct R2Smem {
+  double a[kR2K][kR2M + 4];  // +4: the transposed (Sᵀ) stores hit 4-way, not 32-way, bank conflicts
+  double b[kR2K][PB];
+  int last;
+};
+
+template <int PB, bool TRANS_A>
+__device__ __forceinline__ void r2_item(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
+                                        int64_t ldb, int m0, int mrows, int ncols, int64_t kb, int64_t ke,
+                                        double (&acc)[4][PB / 8], R2Smem<PB>& sm) {
+  constexpr int LA = kR2K * kR2M / kKT, LB = (kR2K * PB + kKT - 1) / kKT;
+  const int tid = threadIdx.x, ty = tid >> 3, tx = tid & 7;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < PB / 8; ++b) acc[a][b] = 0.0;
+  double ra[LA], rb[LB];
+  auto load = [&](int64_t k0) {
+    const int kc = (int)min((int64_t)kR2K, ke - k0);
+#pragma unroll
+    for (int q = 0; q < LA; ++q) {
+      const int e = tid + q * kKT;
+      int i, kk;
+      if (TRANS_A) { kk = e % kR2K; i = e / kR2K; } else { i = e % kR2M; kk = e / kR2M; }
+      ra[q] = (i < mrows && kk < kc) ? (TRANS_A ? A[(k0 + kk) + (int64_t)(m0 + i) * lda]
+                                                : A[(m0 + i) + (k0 + kk) * lda]) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < LB; ++q) {
+      const int e = tid + q * kKT;
+      const int kk = e % kR2K, j = e / kR2K;
+      rb[q] = (e < kR2K * PB && j < ncols && kk < kc) ? B[(k0 + kk) + (int64_t)j * ldb] : 0.0;
+    }
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int q = 0; q < LA; ++q) {
+      const int e = tid + q * kKT;
+      int i, kk;
+      if (TRANS_A) { kk = e % kR2K; i = e / kR2K; } else { i = e % kR2M; kk = e / kR2M; }
+      sm.a[kk][i] = ra[q];
+    }
+#pragma unroll
+    for (int q = 0; q < LB; ++q) {
+      const int e = tid + q * kKT;
+      if (e < kR2K * PB) sm.b[e % kR2K][e / kR2K] = rb[q];
+    }
+  };
+  if (kb < ke) load(kb);
+  for (int64_t k0 = kb; k0 < ke; k0 += kR2K) {
+    __syncthreads();  // previous chunk consumed
+    stash();
+    __syncthreads();
+    if (k0 + kR2K < ke) load(k0 + kR2K);  // in flight during the multiply
+#pragma unroll 4
+    for (int kk = 0; kk < kR2K; ++kk) {
+      const double2 a01 = *reinterpret_cast<const double2*>(&sm.a[kk][4 * ty]);
+      const double2 a23 = *reinterpret_cast<const double2*>(&sm.a[kk][4 * ty + 2]);
+#pragma unroll
+      for (int ci = 0; ci < PB / 8; ++ci) {
+        const double b = sm.b[kk][tx + 8 * ci];
+        acc[0][ci] = fma(a01.x, b, acc[0][ci]);
+        acc[1][ci] = fma(a01.y, b, acc[1][ci]);
+        acc[2][ci] = fma(a23.x, b, acc[2][ci]);
+        acc[3][ci] = fma(a23.y, b, acc[3][ci]);
+      }
+    }
+  }
+}
+
+// Item partial -> ws (column-major kR2M x PB per item); returns true in
+// every thread of the CTA that arrived last for its tile.
+template <int PB>
+__device__ __forceinline__ bool r2_publish(double* __restrict__ part, const double (&acc)[4][PB / 8],
+                                           unsigned int* __restrict__ cnt, int splits, R2Smem<PB>& sm) {
+  const int ty = threadIdx.x >> 3, tx = threadIdx.x & 7;
+#pragma unroll
+  for (int ci = 0; ci < PB / 8; ++ci)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) __stcg(&part[(tx + 8 * ci) * kR2M + 4 * ty + q], acc[q][ci]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int prev = atomicAdd(cnt, 1u);
+    sm.last = prev == (unsigned int)(splits - 1);
+    if (sm.last) *cnt = 0u;  // re-armed for the next phase (after the grid barrier)
+  }
+  __syncthreads();
+  if (sm.last) __threadfence();
+  return sm.last;
+}
+
+template <int PB>
+__global__ void __launch_bounds__(kKT, 1)
+richardson_v2(int k, int c, int p, const double* __restrict__ S, int64_t lds, const double* __restrict__ P,
+              int64_t ldp, int l, double* __restrict__ X, int64_t ldx, double* __restrict__ T, int64_t ldt,
+              double* __restrict__ ws, unsigned int* __restrict__ cnt, int splitsT, int splitsX) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  R2Smem<PB>& sm = *reinterpret_cast<R2Smem<PB>*>(smraw);
   cg::grid_group grid = cg::this_grid();
   const int G = gridDim.x;
-  const int tilesX = (c + kTM - 1) / kTM, tilesT = (k + kTM - 1) / kTM;
-  const int splitsX = splits_for(tilesX, k, G), splitsT = splits_for(tilesT, c, G);
-  const int64_t nthreads = (int64_t)G * kKT;
-  const int64_t gtid = (int64_t)blockIdx.x * kKT + threadIdx.x;
+  const int tilesT = (k + kR2M - 1) / kR2M, tilesX = (c + kR2M - 1) / kR2M;
+  auto krange = [](int64_t K, int splits, int s, int64_t& kb, int64_t& ke) {
+    const int64_t chunks = (K + kR2K - 1) / kR2K;
+    kb = (chunks * s / splits) * kR2K;
+    ke = min(K, (chunks * (s + 1) / splits) * kR2K);
+  };
+  const int tid = threadIdx.x;
   for (int sweep = 0; sweep < l; ++sweep) {
     if (sweep > 0) {
-      // T = P - (S X): partials of S X over splits of c
+      // T = P - (S X): tile t of T's rows, split s over c
       for (int it = blockIdx.x; it < tilesT * splitsT; it += G) {
-        const int t = it % tilesT, s = it / tilesT;
+        const int t = it % tilesT, sp = it / tilesT;
         int64_t kb, ke;
-        split_range(c, splitsT, s, kb, ke);
-        double acc[2][PB / 8];
-        tile_gemm<PB, false>(S, lds, X, ldx, t * kTM, min(kTM, k - t * kTM), p, kb, ke, acc, smem);
-        store_partial<PB>(ws + (int64_t)it * (kTM * PB), acc);
-      }
-      grid.sync();
-      for (int64_t e = gtid; e < (int64_t)k * p; e += nthreads) {
-        const int r = (int)(e % k), j = (int)(e / k);
-        const double sx = sum_splits<PB>(ws, tilesT, splitsT, r / kTM, r % kTM, j);
-        T[r + (int64_t)j * ldt] = P[r + (int64_t)j * ldp] - sx;
+        krange(c, splitsT, sp, kb, ke);
+        const int mrows = min(kR2M, k - t * kR2M);
+        double acc[4][PB / 8];
+        r2_item<PB, false>(S, lds, X, ldx, t * kR2M, mrows, p, kb, ke, acc, sm);
+        double* base = ws + (int64_t)t * splitsT * (kR2M * PB);
+        if (r2_publish<PB>(base + (int64_t)sp * (kR2M * PB), acc, cnt + t, splitsT, sm)) {
+          for (int e = tid; e < mrows * p; e += kKT) {
+            const int i = e % mrows, j = e / mrows;
+            double sx = 0.0;
+            for (int q = 0; q < splitsT; ++q) sx += __ldcg(&base[(int64_t)q * (kR2M * PB) + j * kR2M + i]);
+            const int r = t * kR2M + i;
+            T[r + (int64_t)j * ldt] = P[r + (int64_t)j * ldp] - sx;
+          }
+        }
       }
       grid.sync();
     }
-    // X = X + S^T T (first sweep: X = S^T P, since X = 0 and P - S 0 = P)
+    // X = X + S^T T (sweep 0: X = S^T P, since X = 0 and P - S 0 = P)
     const double* Tin = sweep == 0 ? P : T;
     const int64_t ldtin = sweep == 0 ? ldp : ldt;
     for (int it = blockIdx.x; it < tilesX * splitsX; it += G) {
-      const int t = it % tilesX, s = it / tilesX;
+      const int t = it % tilesX, sp = it / tilesX;
       int64_t kb, ke;
-      split_range(k, splitsX, s, kb, ke);
-      double acc[2][PB / 8];
-      tile_gemm<PB, true>(S, lds, Tin, ldtin, t * kTM, min(kTM, c - t * kTM), p, kb, ke, acc, smem);
-      store_partial<PB>(ws + (int64_t)it * (kTM * PB), acc);
+      krange(k, splitsX, sp, kb, ke);
+      const int mrows = min(kR2M, c - t * kR2M);
+      double acc[4][PB / 8];
+      r2_item<PB, true>(S, lds, Tin, ldtin, t * kR2M, mrows, p, kb, ke, acc, sm);
+      double* base = ws + (int64_t)(tilesT * splitsT + t * splitsX) * (kR2M * PB);
+      if (r2_publish<PB>(base + (int64_t)sp * (kR2M * PB), acc, cnt + tilesT + t, splitsX, sm)) {
+        for (int e = tid; e < mrows * p; e += kKT) {
+          const int i = e % mrows, j = e / mrows;
+          double st = 0.0;
+          for (int q = 0; q < splitsX; ++q) st += __ldcg(&base[(int64_t)q * (kR2M * PB) + j * kR2M + i]);
+          double* xp = X + (t * kR2M + i) + (int64_t)j * ldx;
+          *xp = sweep == 0 ? st : *xp + st;
+        }
+      }
     }
-    grid.sync();
-    for (int64_t e = gtid; e < (int64_t)c * p; e += nthreads) {
-      const int a = (int)(e % c), j = (int)(e / c);
-      const double st = sum_splits<PB>(ws, tilesX, splitsX, a / kTM, a % kTM, j);
-      double* xp = X + a + (int64_t)j * ldx;
-      *xp = sweep == 0 ? st : *xp + st;
-    }
-    grid.sync();
+    if (sweep + 1 < l) grid.sync();
   }
 }
 
@@ -207,47 +323,54 @@ __device__ int chol_smem(double* Sm, int p, int* bad_sh) {
   return *bad_sh;
 }
 
+// One launch, one grid barrier: Gram items (k split) -> the last to arrive
+// sums them in split order and factors G in shared memory; then every CTA
+// solves its rows of Sout = S' R^{-1}.
 template <int PB>
-__global__ void __launch_bounds__(kKT)
-cholqr_coop(int k, int p, const double* __restrict__ Sp, int64_t lds, double* __restrict__ R, int64_t ldr,
-            double* __restrict__ Sout, int64_t ldso, int* __restrict__ info, double* __restrict__ ws) {
-  extern __shared__ __align__(16) double smem[];
+__global__ void __launch_bounds__(kKT, 1)
+cholqr_v2(int k, int p, const double* __restrict__ Sp, int64_t lds, double* __restrict__ R, int64_t ldr,
+          double* __restrict__ Sout, int64_t ldso, int* __restrict__ info, double* __restrict__ ws,
+          unsigned int* __restrict__ cnt, int splits) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  R2Smem<PB>& sm = *reinterpret_cast<R2Smem<PB>*>(smraw);
+  double* smd = reinterpret_cast<double*>(smraw);
   __shared__ int bad;
   cg::grid_group grid = cg::this_grid();
   const int G = gridDim.x;
-  const int splits = splits_for(1, k, G);
-  // G = S'^T S' (p x p, one tile), split over the k rows
-  for (int s = blockIdx.x; s < splits; s += G) {
-    int64_t kb, ke;
-    split_range(k, splits, s, kb, ke);
-    double acc[2][PB / 8];
-    tile_gemm<PB, true>(Sp, lds, Sp, lds, 0, p, p, kb, ke, acc, smem);
-    store_partial<PB>(ws + (int64_t)s * (kTM * PB), acc);
-  }
-  grid.sync();
-  double* Rg = ws + (int64_t)splits * (kTM * PB);  // R (p x p) + 1 / diag, for all CTAs
-  if (blockIdx.x == 0) {
-    double* Gm = smem;  // p x p, column-major
-    for (int e = threadIdx.x; e < p * p; e += kKT) {
-      const int i = e % p, j = e / p;
-      Gm[e] = i <= j ? sum_splits<PB>(ws, 1, splits, 0, i, j) : 0.0;
+  double* Rg = ws + (int64_t)splits * (kR2M * PB);  // R (p x p) + 1 / diag for every CTA
+  for (int it = blockIdx.x; it < splits; it += G) {
+    const int64_t chunks = (k + kR2K - 1) / kR2K;
+    const int64_t kb = (chunks * it / splits) * kR2K, ke = min((int64_t)k, (chunks * (it + 1) / splits) * kR2K);
+    double acc[4][PB / 8];
+    r2_item<PB, true>(Sp, lds, Sp, lds, 0, p, p, kb, ke, acc, sm);
+    if (r2_publish<PB>(ws + (int64_t)it * (kR2M * PB), acc, cnt, splits, sm)) {
+      __syncthreads();
+      double* Gm = smd;  // p x p, column-major (the item's smem is free now)
+      for (int e = threadIdx.x; e < p * p; e += kKT) {
+        const int i = e % p, j = e / p;
+        double g = 0.0;
+        if (i <= j)
+          for (int q = 0; q < splits; ++q) g += __ldcg(&ws[(int64_t)q * (kR2M * PB) + j * kR2M + i]);
+        Gm[e] = g;
+      }
+      __syncthreads();
+      const int b = chol_smem(Gm, p, &bad);
+      for (int e = threadIdx.x; e < p * p; e += kKT) {
+        const int i = e % p, j = e / p;
+        const double v = i <= j ? Gm[e] : 0.0;
+        R[i + (int64_t)j * ldr] = v;
+        Rg[e] = v;
+      }
+      for (int j = threadIdx.x; j < p; j += kKT) Rg[p * p + j] = 1.0 / Gm[j + j * p];
+      if (threadIdx.x == 0) *info = b;
+      __threadfence();
     }
-    __syncthreads();
-    const int b = chol_smem(Gm, p, &bad);
-    for (int e = threadIdx.x; e < p * p; e += kKT) {
-      const int i = e % p, j = e / p;
-      const double v = i <= j ? Gm[e] : 0.0;
-      R[i + (int64_t)j * ldr] = v;
-      Rg[e] = v;
-    }
-    for (int j = threadIdx.x; j < p; j += kKT) Rg[p * p + j] = 1.0 / Gm[j + j * p];
-    if (threadIdx.x == 0) *info = b;
   }
   grid.sync();
   // Sout = S' R^{-1}: one row per thread, fp64, l ascending (rb_trsm_right's
   // order: t = fma(-x_l, R_lj, t), x_j = t * (1 / R_jj))
-  double* Rs = smem;
-  for (int e = threadIdx.x; e < p * p + p; e += kKT) Rs[e] = Rg[e];
+  double* Rs = smd;
+  for (int e = threadIdx.x; e < p * p + p; e += kKT) Rs[e] = __ldcg(&Rg[e]);
   __syncthreads();
   for (int64_t r = (int64_t)blockIdx.x * kKT + threadIdx.x; r < k; r += (int64_t)G * kKT) {
     double x[PB];
@@ -479,7 +602,7 @@ int coop_launch(K kern, size_t smem, void** args, cudaStream_t st, int max_grid,
 // Workspace of the cooperative k-dimensional kernels (upper bound): split-K
 // partial tiles for a grid of 2 CTAs per SM plus the output tiles.
 size_t kdim_ws_bytes(int k, int m) {
-  const size_t grid = 2 * (size_t)sm_count();
+  const size_t grid = 4 * (size_t)sm_count();
   const size_t tiles = (size_t)((k + kTM - 1) / kTM + 1) * ((m + kTM - 1) / kTM + 1);
   return (grid + tiles + 4) * (size_t)kTM * 64 * sizeof(double) + 3 * grid * sizeof(double) + 4096;
 }
@@ -489,15 +612,20 @@ int ls_richardson(int k, int c, int p, const double* S, int64_t lds, const doubl
   RB_REQUIRE(k >= 1 && c >= 1 && p >= 1 && p <= 64 && l >= 1 && S && P && X && T && lds >= k && ldp >= k &&
                  ldx >= c && ldt >= k,
              "rb_ls_richardson: bad args (k=%d c=%d p=%d l=%d)", k, c, p, l);
-  const int tilesX = (c + kTM - 1) / kTM, tilesT = (k + kTM - 1) / kTM;
-  // every phase's items use at most max(grid, tiles) tiles of kTM x 64 doubles
-  const int max_grid = sm_count();  // one CTA per SM: fewer CTAs per grid barrier
-  const size_t need = (size_t)(2 * sm_count() + std::max(tilesX, tilesT)) * kTM * 64 * sizeof(double);
-  RB_REQUIRE(ws && wsb >= need, "rb_ls_richardson: workspace too small (%zu < %zu)", wsb, need);
+  const int G = sm_count();  // one CTA per SM: items <= G, fewer CTAs per grid barrier
+  const int tilesT = (k + kR2M - 1) / kR2M, tilesX = (c + kR2M - 1) / kR2M;
+  int splitsT = std::max(1, std::min(G / tilesT, (c + kR2K - 1) / kR2K));
+  int splitsX = std::max(1, std::min(G / tilesX, (k + kR2K - 1) / kR2K));
+  // partial tiles of both phases (live at once), then the arrival counters
+  const size_t part = (size_t)(tilesT * splitsT + tilesX * splitsX) * kR2M * 64 * sizeof(double);
+  const size_t ncnt = (size_t)(tilesT + tilesX);
+  RB_REQUIRE(ws && wsb >= part + ncnt * sizeof(unsigned int), "rb_ls_richardson: workspace too small");
+  unsigned int* cnt = (unsigned int*)((char*)ws + part);
+  cudaMemsetAsync(cnt, 0, ncnt * sizeof(unsigned int), st);
   int grid = 0;
-  void* args[] = {&k, &c, &p, (void*)&S, &lds, (void*)&P, &ldp, &l, &X, &ldx, &T, &ldt, &ws};
-#define RB_RI(V)                                                                                         \
-  if (p <= V) return coop_launch(richardson_coop<V>, tile_smem<V>(), args, st, max_grid, &grid, "rb_ls_richardson");
+  void* args[] = {&k, &c, &p, (void*)&S, &lds, (void*)&P, &ldp, &l, &X, &ldx, &T, &ldt, &ws, &cnt, &splitsT, &splitsX};
+#define RB_RI(V)                                                                                          \
+  if (p <= V) return coop_launch(richardson_v2<V>, sizeof(R2Smem<V>), args, st, G, &grid, "rb_ls_richardson");
   RB_RI(8) RB_RI(16) RB_RI(24) RB_RI(32) RB_RI(40) RB_RI(48) RB_RI(64)
 #undef RB_RI
   return RB_EINVAL;
@@ -507,18 +635,21 @@ int sketched_cholqr_small(int k, int p, const double* Sp, int64_t lds, double* R
                           int64_t ldso, int* info, void* ws, size_t wsb, cudaStream_t st) {
   RB_REQUIRE(k >= 1 && p >= 1 && p <= 64 && Sp && R && Sout && info && lds >= k && ldr >= p && ldso >= k,
              "rb_sketched_cholqr_small: bad args (k=%d p=%d)", k, p);
-  const int max_grid = sm_count();
-  const size_t need = (size_t)(max_grid + 1) * kTM * 64 * sizeof(double) + (size_t)(p * p + p) * sizeof(double);
-  RB_REQUIRE(ws && wsb >= need, "rb_sketched_cholqr_small: workspace too small");
-  // enough CTAs for the k-row split of the Gram and one row per thread in
-  // the solve, no more (grid barriers cost per CTA)
-  const int want = std::max(1, std::min(max_grid, std::max((k + kKT - 1) / kKT, (k + 4 * kKC - 1) / (4 * kKC))));
+  // CTAs: enough for one row per thread in the solve and >= 4 chunks of
+  // rows per Gram item, no more (grid barrier cost grows with the grid)
+  const int G = std::max(1, std::min(sm_count(), std::max((k + kKT - 1) / kKT, (k + 4 * kR2K - 1) / (4 * kR2K))));
+  int splits = std::max(1, std::min(G, (k + kR2K - 1) / kR2K));
+  const size_t part = (size_t)splits * kR2M * 64 * sizeof(double) + (size_t)(p * p + p) * sizeof(double);
+  const size_t cnt_off = (part + 255) / 256 * 256;
+  RB_REQUIRE(ws && wsb >= cnt_off + 256, "rb_sketched_cholqr_small: workspace too small");
+  unsigned int* cnt = (unsigned int*)((char*)ws + cnt_off);
+  cudaMemsetAsync(cnt, 0, sizeof(unsigned int), st);
   int grid = 0;
-  void* args[] = {&k, &p, (void*)&Sp, &lds, &R, &ldr, &Sout, &ldso, &info, &ws};
-#define RB_CQ(V)                                                                                            \
-  if (p <= V) {                                                                                             \
-    const size_t sm = std::max(tile_smem<V>(), (size_t)(V * V + V) * sizeof(double));                      \
-    return coop_launch(cholqr_coop<V>, sm, args, st, want, &grid, "rb_sketched_cholqr_small");             \
+  void* args[] = {&k, &p, (void*)&Sp, &lds, &R, &ldr, &Sout, &ldso, &info, &ws, &cnt, &splits};
+#define RB_CQ(V)                                                                                             \
+  if (p <= V) {                                                                                              \
+    const size_t sm = std::max(sizeof(R2Smem<V>), (size_t)(V * V + V) * sizeof(double));                     \
+    return coop_launch(cholqr_v2<V>, sm, args, st, G, &grid, "rb_sketched_cholqr_small");                   \
   }
   RB_CQ(8) RB_CQ(16) RB_CQ(24) RB_CQ(32) RB_CQ(40) RB_CQ(48) RB_CQ(64)
 #undef RB_CQ
