@@ -126,171 +126,167 @@ __device__ __forceinline__ int splits_for(int tiles, int64_t K, int grid) {
   return (int)max((int64_t)1, min(chunks, (int64_t)((grid + tiles - 1) / tiles)));
 }
 
-// ============================ Richardson ====================================
-// ---- Richardson, v2 ----------------------------------------------------------
-// Each GEMM phase is cut into at most gridDim.x items (128-row output tile x
-// K split, tiles x splits <= grid: one item per CTA, no tail round).  An
-// item streams its K range in chunks of kR2K rows, the next chunk's global
-// loads in flight (registers) while the current one is multiplied from
-// shared memory; it writes its partial tile, and the LAST item of a tile to
-// arrive (arrival counter) sums the tile's partials in split order and
-// applies the epilogue -- deterministic, and no separate reduction phase.
-// Two grid barriers per sweep (after T, after X).
-constexpr int kR2M = 128;  // output rows per tile
-constexpr int kR2K = 32;   // K rows per chunk
+// ============================ full-K tile items ==============================
+// An item computes one MR x PB output tile of op(A) B over the WHOLE K range
+// inside one CTA -- no split over CTAs, hence no cross-CTA partial
+// reductions (their chains of dependent L2 round trips dominated the split-K
+// versions of these small GEMMs).  The CTA's 256 threads form KG K-groups of
+// TG = 256 / KG threads; a K-group thread owns 2 rows x PB / 8 columns and
+// the chunk's kk in its slice; chunks of kIC rows stream through two
+// shared-memory stages by 8-byte cp.async (the next chunk in flight while
+// the current one is multiplied).  The K-groups' tiles are added in group
+// order through shared memory: every output is a fixed-order sum.
+//   TN = false: op(A)[i, kk] = A[i + kk * lda]  (rows of S: T = P - S X)
+//   TN = true : op(A)[i, kk] = A[kk + i * lda]  (columns of S: S^T T, S^T S)
+constexpr int kIC = 128;  // K rows per chunk
+constexpr int kIP = kIC + 2;  // padded K stride (16-B aligned rows, conflict-free column reads)
 
-template <int PB>
-struct R2Smem {
-  double a[kR2K][kR2M + 4];  // +4: the transposed (Sᵀ) stores hit 4-way, not 32-way, bank conflicts
-  double b[kR2K][PB];
-  int last;
+template <int PB, int MR>
+struct ItemSmem {
+  static constexpr int KG = 256 / (MR / 2 * 8);
+  double a[2][MR * kIP];      // NN: [kk][i] (stride MR), TN: [i][kk] (stride kIP)
+  double b[2][PB * kIP];      // [j][kk]
+  double red[KG][MR * PB];
 };
 
-template <int PB, bool TRANS_A>
-__device__ __forceinline__ void r2_item(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
-                                        int64_t ldb, int m0, int mrows, int ncols, int64_t kb, int64_t ke,
-                                        double (&acc)[4][PB / 8], R2Smem<PB>& sm) {
-  constexpr int LA = kR2K * kR2M / kKT, LB = (kR2K * PB + kKT - 1) / kKT;
-  const int tid = threadIdx.x, ty = tid >> 3, tx = tid & 7;
+__device__ __forceinline__ void cpa8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(s)), "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Result: sm.red[0][j * MR + i] (valid rows / columns only), ready after the
+// function returns (ends with a barrier).
+template <int PB, int MR, bool TN>
+__device__ void tile_item(const double* __restrict__ A, int64_t lda, const double* __restrict__ B, int64_t ldb,
+                          int m0, int mrows, int ncols, int64_t K, ItemSmem<PB, MR>& sm) {
+  constexpr int KG = ItemSmem<PB, MR>::KG, TG = 256 / KG, SL = kIC / KG;
+  const int tid = threadIdx.x, g = tid / TG, u = tid % TG;
+  const int rg = u % (MR / 2), cg = u / (MR / 2);  // rows 2 rg, 2 rg + 1; columns cg + 8 ci
+  double acc[2][PB / 8];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < PB / 8; ++b) acc[a][b] = 0.0;
-  double ra[LA], rb[LB];
-  auto load = [&](int64_t k0) {
-    const int kc = (int)min((int64_t)kR2K, ke - k0);
-#pragma unroll
-    for (int q = 0; q < LA; ++q) {
-      const int e = tid + q * kKT;
+  const int nch = (int)((K + kIC - 1) / kIC);
+  auto issue = [&](int ch) {
+    const int st = ch & 1;
+    const int64_t k0 = (int64_t)ch * kIC;
+    const int kc = (int)min((int64_t)kIC, K - k0);
+    double* sa = sm.a[st];
+    double* sb = sm.b[st];
+    for (int e = tid; e < MR * kIC; e += 256) {
       int i, kk;
-      if (TRANS_A) { kk = e % kR2K; i = e / kR2K; } else { i = e % kR2M; kk = e / kR2M; }
-      ra[q] = (i < mrows && kk < kc) ? (TRANS_A ? A[(k0 + kk) + (int64_t)(m0 + i) * lda]
-                                                : A[(m0 + i) + (k0 + kk) * lda]) : 0.0;
+      if (TN) { kk = e % kIC; i = e / kIC; } else { i = e % MR; kk = e / MR; }
+      double* dst = TN ? &sa[i * kIP + kk] : &sa[kk * MR + i];
+      if (i < mrows && kk < kc) cpa8(dst, TN ? &A[(k0 + kk) + (int64_t)(m0 + i) * lda] : &A[(m0 + i) + (k0 + kk) * lda]);
+      else *dst = 0.0;
     }
-#pragma unroll
-    for (int q = 0; q < LB; ++q) {
-      const int e = tid + q * kKT;
-      const int kk = e % kR2K, j = e / kR2K;
-      rb[q] = (e < kR2K * PB && j < ncols && kk < kc) ? B[(k0 + kk) + (int64_t)j * ldb] : 0.0;
+    for (int e = tid; e < PB * kIC; e += 256) {
+      const int kk = e % kIC, j = e / kIC;
+      if (j < ncols && kk < kc) cpa8(&sb[j * kIP + kk], &B[(k0 + kk) + (int64_t)j * ldb]);
+      else sb[j * kIP + kk] = 0.0;
     }
+    cpa_commit();
   };
-  auto stash = [&]() {
-#pragma unroll
-    for (int q = 0; q < LA; ++q) {
-      const int e = tid + q * kKT;
-      int i, kk;
-      if (TRANS_A) { kk = e % kR2K; i = e / kR2K; } else { i = e % kR2M; kk = e / kR2M; }
-      sm.a[kk][i] = ra[q];
+  if (nch > 0) issue(0);
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) {
+      issue(ch + 1);
+      cpa_wait<1>();
+    } else {
+      cpa_wait<0>();
     }
-#pragma unroll
-    for (int q = 0; q < LB; ++q) {
-      const int e = tid + q * kKT;
-      if (e < kR2K * PB) sm.b[e % kR2K][e / kR2K] = rb[q];
-    }
-  };
-  if (kb < ke) load(kb);
-  for (int64_t k0 = kb; k0 < ke; k0 += kR2K) {
-    __syncthreads();  // previous chunk consumed
-    stash();
     __syncthreads();
-    if (k0 + kR2K < ke) load(k0 + kR2K);  // in flight during the multiply
+    const double* sa = sm.a[ch & 1];
+    const double* sb = sm.b[ch & 1];
 #pragma unroll 4
-    for (int kk = 0; kk < kR2K; ++kk) {
-      const double2 a01 = *reinterpret_cast<const double2*>(&sm.a[kk][4 * ty]);
-      const double2 a23 = *reinterpret_cast<const double2*>(&sm.a[kk][4 * ty + 2]);
+    for (int q = 0; q < SL; ++q) {
+      const int kk = g * SL + q;
+      double a0, a1;
+      if (TN) {
+        a0 = sa[(2 * rg) * kIP + kk];
+        a1 = sa[(2 * rg + 1) * kIP + kk];
+      } else {
+        const double2 aa = *reinterpret_cast<const double2*>(&sa[kk * MR + 2 * rg]);
+        a0 = aa.x;
+        a1 = aa.y;
+      }
 #pragma unroll
       for (int ci = 0; ci < PB / 8; ++ci) {
-        const double b = sm.b[kk][tx + 8 * ci];
-        acc[0][ci] = fma(a01.x, b, acc[0][ci]);
-        acc[1][ci] = fma(a01.y, b, acc[1][ci]);
-        acc[2][ci] = fma(a23.x, b, acc[2][ci]);
-        acc[3][ci] = fma(a23.y, b, acc[3][ci]);
+        const double b = sb[(cg + 8 * ci) * kIP + kk];
+        acc[0][ci] = fma(a0, b, acc[0][ci]);
+        acc[1][ci] = fma(a1, b, acc[1][ci]);
       }
     }
+    __syncthreads();  // stage (ch & 1) is reissued two chunks later
   }
-}
-
-// Item partial -> ws (column-major kR2M x PB per item); returns true in
-// every thread of the CTA that arrived last for its tile.
-template <int PB>
-__device__ __forceinline__ bool r2_publish(double* __restrict__ part, const double (&acc)[4][PB / 8],
-                                           unsigned int* __restrict__ cnt, int splits, R2Smem<PB>& sm) {
-  const int ty = threadIdx.x >> 3, tx = threadIdx.x & 7;
 #pragma unroll
-  for (int ci = 0; ci < PB / 8; ++ci)
-#pragma unroll
-    for (int q = 0; q < 4; ++q) __stcg(&part[(tx + 8 * ci) * kR2M + 4 * ty + q], acc[q][ci]);
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int prev = atomicAdd(cnt, 1u);
-    sm.last = prev == (unsigned int)(splits - 1);
-    if (sm.last) *cnt = 0u;  // re-armed for the next phase (after the grid barrier)
+  for (int ci = 0; ci < PB / 8; ++ci) {
+    sm.red[g][(cg + 8 * ci) * MR + 2 * rg] = acc[0][ci];
+    sm.red[g][(cg + 8 * ci) * MR + 2 * rg + 1] = acc[1][ci];
   }
   __syncthreads();
-  if (sm.last) __threadfence();
-  return sm.last;
+  for (int e = tid; e < MR * PB; e += 256) {
+    double s = sm.red[0][e];
+#pragma unroll
+    for (int q = 1; q < KG; ++q) s += sm.red[q][e];
+    sm.red[0][e] = s;
+  }
+  __syncthreads();
 }
 
+// ============================ Richardson ====================================
+// Per sweep two phases, each one item per CTA (grid-stride if there are
+// more), separated by grid barriers:
+//   T = P - (S X)      items: 16-row tiles of T, K = c
+//   X = X + (S^T T)    items:  8-row tiles of X, K = k
 template <int PB>
-__global__ void __launch_bounds__(kKT, 1)
-richardson_v2(int k, int c, int p, const double* __restrict__ S, int64_t lds, const double* __restrict__ P,
-              int64_t ldp, int l, double* __restrict__ X, int64_t ldx, double* __restrict__ T, int64_t ldt,
-              double* __restrict__ ws, unsigned int* __restrict__ cnt, int splitsT, int splitsX) {
+struct RichSmem {
+  union {
+    ItemSmem<PB, 16> nn;
+    ItemSmem<PB, 8> tn;
+  };
+};
+
+template <int PB>
+__global__ void __launch_bounds__(256, 1)
+richardson_v3(int k, int c, int p, const double* __restrict__ S, int64_t lds, const double* __restrict__ P,
+              int64_t ldp, int l, double* __restrict__ X, int64_t ldx, double* __restrict__ T, int64_t ldt) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  R2Smem<PB>& sm = *reinterpret_cast<R2Smem<PB>*>(smraw);
+  RichSmem<PB>& sm = *reinterpret_cast<RichSmem<PB>*>(smraw);
   cg::grid_group grid = cg::this_grid();
   const int G = gridDim.x;
-  const int tilesT = (k + kR2M - 1) / kR2M, tilesX = (c + kR2M - 1) / kR2M;
-  auto krange = [](int64_t K, int splits, int s, int64_t& kb, int64_t& ke) {
-    const int64_t chunks = (K + kR2K - 1) / kR2K;
-    kb = (chunks * s / splits) * kR2K;
-    ke = min(K, (chunks * (s + 1) / splits) * kR2K);
-  };
-  const int tid = threadIdx.x;
+  const int tilesT = (k + 15) / 16, tilesX = (c + 7) / 8;
   for (int sweep = 0; sweep < l; ++sweep) {
     if (sweep > 0) {
-      // T = P - (S X): tile t of T's rows, split s over c
-      for (int it = blockIdx.x; it < tilesT * splitsT; it += G) {
-        const int t = it % tilesT, sp = it / tilesT;
-        int64_t kb, ke;
-        krange(c, splitsT, sp, kb, ke);
-        const int mrows = min(kR2M, k - t * kR2M);
-        double acc[4][PB / 8];
-        r2_item<PB, false>(S, lds, X, ldx, t * kR2M, mrows, p, kb, ke, acc, sm);
-        double* base = ws + (int64_t)t * splitsT * (kR2M * PB);
-        if (r2_publish<PB>(base + (int64_t)sp * (kR2M * PB), acc, cnt + t, splitsT, sm)) {
-          for (int e = tid; e < mrows * p; e += kKT) {
-            const int i = e % mrows, j = e / mrows;
-            double sx = 0.0;
-            for (int q = 0; q < splitsT; ++q) sx += __ldcg(&base[(int64_t)q * (kR2M * PB) + j * kR2M + i]);
-            const int r = t * kR2M + i;
-            T[r + (int64_t)j * ldt] = P[r + (int64_t)j * ldp] - sx;
-          }
+      for (int t = blockIdx.x; t < tilesT; t += G) {
+        const int mrows = min(16, k - 16 * t);
+        tile_item<PB, 16, false>(S + 16 * t, lds, X, ldx, 0, mrows, p, c, sm.nn);
+        for (int e = threadIdx.x; e < mrows * p; e += 256) {
+          const int i = e % mrows, j = e / mrows;
+          const int64_t r = 16 * t + i;
+          T[r + (int64_t)j * ldt] = P[r + (int64_t)j * ldp] - sm.nn.red[0][j * 16 + i];
         }
+        __syncthreads();
       }
       grid.sync();
     }
-    // X = X + S^T T (sweep 0: X = S^T P, since X = 0 and P - S 0 = P)
+    // sweep 0: X = S^T P (X = 0 and P - S 0 = P exactly)
     const double* Tin = sweep == 0 ? P : T;
     const int64_t ldtin = sweep == 0 ? ldp : ldt;
-    for (int it = blockIdx.x; it < tilesX * splitsX; it += G) {
-      const int t = it % tilesX, sp = it / tilesX;
-      int64_t kb, ke;
-      krange(k, splitsX, sp, kb, ke);
-      const int mrows = min(kR2M, c - t * kR2M);
-      double acc[4][PB / 8];
-      r2_item<PB, true>(S, lds, Tin, ldtin, t * kR2M, mrows, p, kb, ke, acc, sm);
-      double* base = ws + (int64_t)(tilesT * splitsT + t * splitsX) * (kR2M * PB);
-      if (r2_publish<PB>(base + (int64_t)sp * (kR2M * PB), acc, cnt + tilesT + t, splitsX, sm)) {
-        for (int e = tid; e < mrows * p; e += kKT) {
-          const int i = e % mrows, j = e / mrows;
-          double st = 0.0;
-          for (int q = 0; q < splitsX; ++q) st += __ldcg(&base[(int64_t)q * (kR2M * PB) + j * kR2M + i]);
-          double* xp = X + (t * kR2M + i) + (int64_t)j * ldx;
-          *xp = sweep == 0 ? st : *xp + st;
-        }
+    for (int t = blockIdx.x; t < tilesX; t += G) {
+      const int mrows = min(8, c - 8 * t);
+      tile_item<PB, 8, true>(S + (int64_t)8 * t * lds, lds, Tin, ldtin, 0, mrows, p, k, sm.tn);
+      for (int e = threadIdx.x; e < mrows * p; e += 256) {
+        const int i = e % mrows, j = e / mrows;
+        double* xp = X + (8 * t + i) + (int64_t)j * ldx;
+        const double v = sm.tn.red[0][j * 8 + i];
+        *xp = sweep == 0 ? v : *xp + v;
       }
+      __syncthreads();
     }
     if (sweep + 1 < l) grid.sync();
   }
@@ -323,56 +319,54 @@ __device__ int chol_smem(double* Sm, int p, int* bad_sh) {
   return *bad_sh;
 }
 
-// One launch, one grid barrier: Gram items (k split) -> the last to arrive
-// sums them in split order and factors G in shared memory; then every CTA
-// solves its rows of Sout = S' R^{-1}.
+// G = S'^T S' (8-row items over the p columns, K = k), grid barrier; CTA 0
+// factors G; grid barrier; every CTA solves its rows of Sout = S' R^{-1}.
 template <int PB>
-__global__ void __launch_bounds__(kKT, 1)
-cholqr_v2(int k, int p, const double* __restrict__ Sp, int64_t lds, double* __restrict__ R, int64_t ldr,
-          double* __restrict__ Sout, int64_t ldso, int* __restrict__ info, double* __restrict__ ws,
-          unsigned int* __restrict__ cnt, int splits) {
+__global__ void __launch_bounds__(256, 1)
+cholqr_v3(int k, int p, const double* __restrict__ Sp, int64_t lds, double* __restrict__ R, int64_t ldr,
+          double* __restrict__ Sout, int64_t ldso, int* __restrict__ info, double* __restrict__ ws) {
   extern __shared__ __align__(16) unsigned char smraw[];
-  R2Smem<PB>& sm = *reinterpret_cast<R2Smem<PB>*>(smraw);
+  ItemSmem<PB, 8>& sm = *reinterpret_cast<ItemSmem<PB, 8>*>(smraw);
   double* smd = reinterpret_cast<double*>(smraw);
   __shared__ int bad;
   cg::grid_group grid = cg::this_grid();
   const int G = gridDim.x;
-  double* Rg = ws + (int64_t)splits * (kR2M * PB);  // R (p x p) + 1 / diag for every CTA
-  for (int it = blockIdx.x; it < splits; it += G) {
-    const int64_t chunks = (k + kR2K - 1) / kR2K;
-    const int64_t kb = (chunks * it / splits) * kR2K, ke = min((int64_t)k, (chunks * (it + 1) / splits) * kR2K);
-    double acc[4][PB / 8];
-    r2_item<PB, true>(Sp, lds, Sp, lds, 0, p, p, kb, ke, acc, sm);
-    if (r2_publish<PB>(ws + (int64_t)it * (kR2M * PB), acc, cnt, splits, sm)) {
-      __syncthreads();
-      double* Gm = smd;  // p x p, column-major (the item's smem is free now)
-      for (int e = threadIdx.x; e < p * p; e += kKT) {
-        const int i = e % p, j = e / p;
-        double g = 0.0;
-        if (i <= j)
-          for (int q = 0; q < splits; ++q) g += __ldcg(&ws[(int64_t)q * (kR2M * PB) + j * kR2M + i]);
-        Gm[e] = g;
-      }
-      __syncthreads();
-      const int b = chol_smem(Gm, p, &bad);
-      for (int e = threadIdx.x; e < p * p; e += kKT) {
-        const int i = e % p, j = e / p;
-        const double v = i <= j ? Gm[e] : 0.0;
-        R[i + (int64_t)j * ldr] = v;
-        Rg[e] = v;
-      }
-      for (int j = threadIdx.x; j < p; j += kKT) Rg[p * p + j] = 1.0 / Gm[j + j * p];
-      if (threadIdx.x == 0) *info = b;
-      __threadfence();
+  double* Gg = ws;              // p x p (ld p)
+  double* Rg = ws + p * p;      // R (p x p) + 1 / diag
+  for (int t = blockIdx.x; t < (p + 7) / 8; t += G) {
+    const int mrows = min(8, p - 8 * t);
+    tile_item<PB, 8, true>(Sp + (int64_t)8 * t * lds, lds, Sp, lds, 0, mrows, p, k, sm);
+    for (int e = threadIdx.x; e < mrows * p; e += 256) {
+      const int i = e % mrows, j = e / mrows;
+      Gg[(8 * t + i) + j * p] = sm.red[0][j * 8 + i];
     }
+    __syncthreads();
+  }
+  grid.sync();
+  if (blockIdx.x == 0) {
+    double* Gm = smd;
+    for (int e = threadIdx.x; e < p * p; e += 256) {
+      const int i = e % p, j = e / p;
+      Gm[e] = i <= j ? __ldcg(&Gg[e]) : 0.0;
+    }
+    __syncthreads();
+    const int b = chol_smem(Gm, p, &bad);
+    for (int e = threadIdx.x; e < p * p; e += 256) {
+      const int i = e % p, j = e / p;
+      const double v = i <= j ? Gm[e] : 0.0;
+      R[i + (int64_t)j * ldr] = v;
+      Rg[e] = v;
+    }
+    for (int j = threadIdx.x; j < p; j += 256) Rg[p * p + j] = 1.0 / Gm[j + j * p];
+    if (threadIdx.x == 0) *info = b;
   }
   grid.sync();
   // Sout = S' R^{-1}: one row per thread, fp64, l ascending (rb_trsm_right's
   // order: t = fma(-x_l, R_lj, t), x_j = t * (1 / R_jj))
   double* Rs = smd;
-  for (int e = threadIdx.x; e < p * p + p; e += kKT) Rs[e] = __ldcg(&Rg[e]);
+  for (int e = threadIdx.x; e < p * p + p; e += 256) Rs[e] = __ldcg(&Rg[e]);
   __syncthreads();
-  for (int64_t r = (int64_t)blockIdx.x * kKT + threadIdx.x; r < k; r += (int64_t)G * kKT) {
+  for (int64_t r = (int64_t)blockIdx.x * 256 + threadIdx.x; r < k; r += (int64_t)G * 256) {
     double x[PB];
 #pragma unroll
     for (int j = 0; j < PB; ++j) x[j] = j < p ? Sp[r + (int64_t)j * lds] : 0.0;
@@ -612,20 +606,15 @@ int ls_richardson(int k, int c, int p, const double* S, int64_t lds, const doubl
   RB_REQUIRE(k >= 1 && c >= 1 && p >= 1 && p <= 64 && l >= 1 && S && P && X && T && lds >= k && ldp >= k &&
                  ldx >= c && ldt >= k,
              "rb_ls_richardson: bad args (k=%d c=%d p=%d l=%d)", k, c, p, l);
-  const int G = sm_count();  // one CTA per SM: items <= G, fewer CTAs per grid barrier
-  const int tilesT = (k + kR2M - 1) / kR2M, tilesX = (c + kR2M - 1) / kR2M;
-  int splitsT = std::max(1, std::min(G / tilesT, (c + kR2K - 1) / kR2K));
-  int splitsX = std::max(1, std::min(G / tilesX, (k + kR2K - 1) / kR2K));
-  // partial tiles of both phases (live at once), then the arrival counters
-  const size_t part = (size_t)(tilesT * splitsT + tilesX * splitsX) * kR2M * 64 * sizeof(double);
-  const size_t ncnt = (size_t)(tilesT + tilesX);
-  RB_REQUIRE(ws && wsb >= part + ncnt * sizeof(unsigned int), "rb_ls_richardson: workspace too small");
-  unsigned int* cnt = (unsigned int*)((char*)ws + part);
-  cudaMemsetAsync(cnt, 0, ncnt * sizeof(unsigned int), st);
+  (void)ws;
+  (void)wsb;
+  // one item per CTA where possible (every phase's tile count), at most one CTA per SM
+  const int items = std::max(l > 1 ? (k + 15) / 16 : 1, (c + 7) / 8);
+  const int G = std::max(1, std::min(sm_count(), items));
   int grid = 0;
-  void* args[] = {&k, &c, &p, (void*)&S, &lds, (void*)&P, &ldp, &l, &X, &ldx, &T, &ldt, &ws, &cnt, &splitsT, &splitsX};
-#define RB_RI(V)                                                                                          \
-  if (p <= V) return coop_launch(richardson_v2<V>, sizeof(R2Smem<V>), args, st, G, &grid, "rb_ls_richardson");
+  void* args[] = {&k, &c, &p, (void*)&S, &lds, (void*)&P, &ldp, &l, &X, &ldx, &T, &ldt};
+#define RB_RI(V)                                                                                           \
+  if (p <= V) return coop_launch(richardson_v3<V>, sizeof(RichSmem<V>), args, st, G, &grid, "rb_ls_richardson");
   RB_RI(8) RB_RI(16) RB_RI(24) RB_RI(32) RB_RI(40) RB_RI(48) RB_RI(64)
 #undef RB_RI
   return RB_EINVAL;
@@ -635,21 +624,15 @@ int sketched_cholqr_small(int k, int p, const double* Sp, int64_t lds, double* R
                           int64_t ldso, int* info, void* ws, size_t wsb, cudaStream_t st) {
   RB_REQUIRE(k >= 1 && p >= 1 && p <= 64 && Sp && R && Sout && info && lds >= k && ldr >= p && ldso >= k,
              "rb_sketched_cholqr_small: bad args (k=%d p=%d)", k, p);
-  // CTAs: enough for one row per thread in the solve and >= 4 chunks of
-  // rows per Gram item, no more (grid barrier cost grows with the grid)
-  const int G = std::max(1, std::min(sm_count(), std::max((k + kKT - 1) / kKT, (k + 4 * kR2K - 1) / (4 * kR2K))));
-  int splits = std::max(1, std::min(G, (k + kR2K - 1) / kR2K));
-  const size_t part = (size_t)splits * kR2M * 64 * sizeof(double) + (size_t)(p * p + p) * sizeof(double);
-  const size_t cnt_off = (part + 255) / 256 * 256;
-  RB_REQUIRE(ws && wsb >= cnt_off + 256, "rb_sketched_cholqr_small: workspace too small");
-  unsigned int* cnt = (unsigned int*)((char*)ws + cnt_off);
-  cudaMemsetAsync(cnt, 0, sizeof(unsigned int), st);
+  RB_REQUIRE(ws && wsb >= (size_t)(2 * p * p + p) * sizeof(double), "rb_sketched_cholqr_small: workspace");
+  // CTAs: the Gram's 8-row items and one row per thread in the solve
+  const int G = std::max(1, std::min(sm_count(), std::max((p + 7) / 8, (k + 255) / 256)));
   int grid = 0;
-  void* args[] = {&k, &p, (void*)&Sp, &lds, &R, &ldr, &Sout, &ldso, &info, &ws, &cnt, &splits};
-#define RB_CQ(V)                                                                                             \
-  if (p <= V) {                                                                                              \
-    const size_t sm = std::max(sizeof(R2Smem<V>), (size_t)(V * V + V) * sizeof(double));                     \
-    return coop_launch(cholqr_v2<V>, sm, args, st, G, &grid, "rb_sketched_cholqr_small");                   \
+  void* args[] = {&k, &p, (void*)&Sp, &lds, &R, &ldr, &Sout, &ldso, &info, &ws};
+#define RB_CQ(V)                                                                                            \
+  if (p <= V) {                                                                                             \
+    const size_t sm = std::max(sizeof(ItemSmem<V, 8>), (size_t)(V * V + V) * sizeof(double));               \
+    return coop_launch(cholqr_v3<V>, sm, args, st, G, &grid, "rb_sketched_cholqr_small");                  \
   }
   RB_CQ(8) RB_CQ(16) RB_CQ(24) RB_CQ(32) RB_CQ(40) RB_CQ(48) RB_CQ(64)
 #undef RB_CQ
