@@ -292,6 +292,144 @@ richardson_v3(int k, int c, int p, const double* __restrict__ S, int64_t lds, co
   }
 }
 
+// ---- Richardson, v4: S resident in shared memory ------------------------------
+// S (k x c) is cut into an R x C grid of blocks, one per CTA (R C <= grid),
+// loaded ONCE into that CTA's shared memory and kept there for all l
+// sweeps; per sweep only the small operands move (X c x p, T k x p, both
+// L2-resident):
+//   A  CTA (r, cb): partial T_r^(cb) = S_(r,cb) X_cb   -> ws   | barrier
+//      every CTA: T = P - sum_cb (cb ascending), grid-stride  | barrier
+//   B  CTA (r, cb): partial X_cb^(r) = S_(r,cb)^T T_r  -> ws   | barrier
+//      every CTA: X = X + sum_r (r ascending), grid-stride    | barrier
+// Fixed summation orders throughout (deterministic).  In-block products:
+// a thread owns up to 8 rows x 4 consecutive columns of the block's output.
+constexpr int kV4Smem = 200 * 1024;
+
+struct V4Part {
+  int R, C, br, bc;
+};
+
+// out (nrows x p, ld ldo, row-major in smem or strided) = Aop (nrows x K) B (K x p),
+// A element (i, kk) at a[i * ai + kk * ak], B element (kk, j) at b[kk * bk + j].
+__device__ __forceinline__ void v4_block_gemm(const double* __restrict__ a, int ai, int ak, const double* __restrict__ b,
+                                              int bk, int nrows, int K, int p, double* __restrict__ dst,
+                                              int64_t ld_j, int64_t ld_i) {
+  const int TC = (p + 3) / 4, TR = 256 / TC;
+  const int tid = threadIdx.x;
+  const int tc = tid % TC, tr = tid / TC;
+  if (tr >= TR) return;
+  const int j0 = 4 * tc;
+  for (int i0 = tr; i0 < nrows; i0 += 8 * TR) {
+    double acc[8][4];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc[q][t] = 0.0;
+    for (int kk = 0; kk < K; ++kk) {
+      double bv[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) bv[t] = (j0 + t < p) ? b[kk * bk + j0 + t] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int i = i0 + q * TR;
+        const double av = i < nrows ? a[i * ai + kk * ak] : 0.0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc[q][t] = fma(av, bv[t], acc[q][t]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int i = i0 + q * TR;
+      if (i < nrows)
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (j0 + t < p) dst[(j0 + t) * ld_j + i * ld_i] = acc[q][t];
+    }
+  }
+}
+
+// sum_{q < n} x[q * stride] in q order; loads issued 8 at a time (L2,
+// bypassing L1: the partials were written by other CTAs since the last
+// barrier), so a long sum costs n / 8 round trips, not n
+__device__ __forceinline__ double sum_strided(const double* __restrict__ x, int64_t stride, int n) {
+  double s = 0.0;
+  int q = 0;
+  for (; q + 8 <= n; q += 8) {
+    double v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) v[t] = __ldcg(x + (int64_t)(q + t) * stride);
+#pragma unroll
+    for (int t = 0; t < 8; ++t) s += v[t];
+  }
+  for (; q < n; ++q) s += __ldcg(x + (int64_t)q * stride);
+  return s;
+}
+
+__global__ void __launch_bounds__(256, 1)
+richardson_v4(int k, int c, int p, const double* __restrict__ S, int64_t lds, const double* __restrict__ P,
+              int64_t ldp, int l, double* __restrict__ X, int64_t ldx, double* __restrict__ T, int64_t ldt,
+              double* __restrict__ ws, V4Part pt) {
+  extern __shared__ __align__(16) double v4s[];
+  cg::grid_group grid = cg::this_grid();
+  const int nblk = pt.R * pt.C;
+  const int b = blockIdx.x;
+  const bool own = b < nblk;
+  const int rb = own ? b / pt.C : 0, cb = own ? b % pt.C : 0;
+  const int r0 = rb * pt.br, a0 = cb * pt.bc;
+  const int nr = own ? max(0, min(pt.br, k - r0)) : 0, na = own ? max(0, min(pt.bc, c - a0)) : 0;
+  double* Sb = v4s;                       // [a][r], stride br (column-major block)
+  double* Op = v4s + pt.br * pt.bc;       // X_cb as [a][j] (stride p) or T_r as [r][j] (stride p)
+  double* wsA = ws;                                   // [cb][j][r]: C * p * k
+  double* wsB = ws + (int64_t)pt.C * p * k;           // [rb][j][a]: R * p * c
+  // the block of S, once
+  for (int e = threadIdx.x; e < nr * na; e += 256) {
+    const int r = e % nr, a = e / nr;
+    cpa8(&Sb[a * pt.br + r], &S[(r0 + r) + (int64_t)(a0 + a) * lds]);
+  }
+  cpa_commit();
+  const int64_t nthreads = (int64_t)gridDim.x * 256, gtid = (int64_t)b * 256 + threadIdx.x;
+  for (int sweep = 0; sweep < l; ++sweep) {
+    if (sweep > 0) {
+      // A: partial T = S_(r,cb) X_cb
+      for (int e = threadIdx.x; e < na * p; e += 256) {
+        const int a = e % na, j = e / na;
+        Op[a * p + j] = X[(a0 + a) + (int64_t)j * ldx];
+      }
+      cpa_wait<0>();
+      __syncthreads();
+      if (nr > 0)
+        v4_block_gemm(Sb, 1, pt.br, Op, p, nr, na, p, wsA + (int64_t)cb * p * k + r0, k, 1);
+      grid.sync();
+      for (int64_t e = gtid; e < (int64_t)k * p; e += nthreads) {
+        const int r = (int)(e % k), j = (int)(e / k);
+        const double sx = sum_strided(wsA + (int64_t)j * k + r, (int64_t)p * k, pt.C);
+        T[r + (int64_t)j * ldt] = P[r + (int64_t)j * ldp] - sx;
+      }
+      grid.sync();
+    }
+    // B: partial X = S_(r,cb)^T T_r (sweep 0: T = P)
+    const double* Tin = sweep == 0 ? P : T;
+    const int64_t ldtin = sweep == 0 ? ldp : ldt;
+    for (int e = threadIdx.x; e < nr * p; e += 256) {
+      const int r = e % nr, j = e / nr;
+      Op[r * p + j] = __ldcg(&Tin[(r0 + r) + (int64_t)j * ldtin]);
+    }
+    cpa_wait<0>();
+    __syncthreads();
+    if (na > 0)
+      v4_block_gemm(Sb, pt.br, 1, Op, p, na, nr, p, wsB + (int64_t)rb * p * c + a0, c, 1);
+    grid.sync();
+    for (int64_t e = gtid; e < (int64_t)c * p; e += nthreads) {
+      const int a = (int)(e % c), j = (int)(e / c);
+      const double st = sum_strided(wsB + (int64_t)j * c + a, (int64_t)p * c, pt.R);
+      double* xp = X + a + (int64_t)j * ldx;
+      *xp = sweep == 0 ? st : *xp + st;
+    }
+    if (sweep + 1 < l) grid.sync();
+    __syncthreads();
+  }
+}
+
 // ============================ sketched CholQR ===============================
 // Cholesky of the p x p matrix in shared memory (upper, right-looking, dpotrf
 // semantics): returns 0 or the 1-based column of the first pivot <= 0 / NaN.
@@ -601,20 +739,50 @@ size_t kdim_ws_bytes(int k, int m) {
   return (grid + tiles + 4) * (size_t)kTM * 64 * sizeof(double) + 3 * grid * sizeof(double) + 4096;
 }
 
+// Block grid of S for richardson_v4: C column blocks, R = G / C row blocks,
+// C chosen so the blocks are about square (balanced partial reductions);
+// nullopt-like (R = 0) when a block does not fit the shared-memory budget.
+static V4Part v4_partition(int k, int c, int p, int G) {
+  V4Part best{0, 0, 0, 0};
+  size_t best_cost = (size_t)-1;
+  for (int C = 1; C <= std::min(c, G); ++C) {
+    const int R = std::min(k, G / C);
+    if (R < 1) break;
+    const int br = (k + R - 1) / R, bc = (c + C - 1) / C;
+    const size_t smem = ((size_t)br * bc + (size_t)std::max(br, bc) * p) * sizeof(double);
+    if (smem > (size_t)kV4Smem) continue;
+    // per-sweep cost model: block FMAs (both phases) + reduction loads per thread
+    const size_t cost = 2 * (size_t)br * bc * p / 64 + ((size_t)k * C + (size_t)c * R) * p / ((size_t)G * 256) * 400;
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = V4Part{(k + br - 1) / br, (c + bc - 1) / bc, br, bc};
+    }
+  }
+  return best;
+}
+
 int ls_richardson(int k, int c, int p, const double* S, int64_t lds, const double* P, int64_t ldp, int l, double* X,
                   int64_t ldx, double* T, int64_t ldt, void* ws, size_t wsb, cudaStream_t st) {
   RB_REQUIRE(k >= 1 && c >= 1 && p >= 1 && p <= 64 && l >= 1 && S && P && X && T && lds >= k && ldp >= k &&
                  ldx >= c && ldt >= k,
              "rb_ls_richardson: bad args (k=%d c=%d p=%d l=%d)", k, c, p, l);
-  (void)ws;
-  (void)wsb;
-  // one item per CTA where possible (every phase's tile count), at most one CTA per SM
+  const int G = sm_count();
+  V4Part pt = v4_partition(k, c, p, G);
+  if (pt.R > 0) {
+    const size_t need = ((size_t)pt.C * p * k + (size_t)pt.R * p * c) * sizeof(double);
+    RB_REQUIRE(ws && wsb >= need, "rb_ls_richardson: workspace too small (%zu < %zu)", wsb, need);
+    int grid = 0;
+    void* args[] = {&k, &c, &p, (void*)&S, &lds, (void*)&P, &ldp, &l, &X, &ldx, &T, &ldt, &ws, &pt};
+    const size_t smem = ((size_t)pt.br * pt.bc + (size_t)std::max(pt.br, pt.bc) * p) * sizeof(double);
+    return coop_launch(richardson_v4, smem, args, st, pt.R * pt.C, &grid, "rb_ls_richardson");
+  }
+  // S too large for the grid's shared memory: full-K tile items
   const int items = std::max(l > 1 ? (k + 15) / 16 : 1, (c + 7) / 8);
-  const int G = std::max(1, std::min(sm_count(), items));
+  const int G3 = std::max(1, std::min(G, items));
   int grid = 0;
   void* args[] = {&k, &c, &p, (void*)&S, &lds, (void*)&P, &ldp, &l, &X, &ldx, &T, &ldt};
 #define RB_RI(V)                                                                                           \
-  if (p <= V) return coop_launch(richardson_v3<V>, sizeof(RichSmem<V>), args, st, G, &grid, "rb_ls_richardson");
+  if (p <= V) return coop_launch(richardson_v3<V>, sizeof(RichSmem<V>), args, st, G3, &grid, "rb_ls_richardson");
   RB_RI(8) RB_RI(16) RB_RI(24) RB_RI(32) RB_RI(40) RB_RI(48) RB_RI(64)
 #undef RB_RI
   return RB_EINVAL;
