@@ -31,6 +31,22 @@
 
 namespace cg = cooperative_groups;
 
+// RB_KDIM_TRACE (tools/kdim_trace.cu only): CTA 0 records %globaltimer at
+// phase boundaries into g_kdim_trace.
+#ifdef RB_KDIM_TRACE
+__device__ unsigned long long g_kdim_trace[256];
+__device__ __forceinline__ void kdim_mark(int slot) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_kdim_trace[slot & 255] = t;
+  }
+}
+#define KDIM_MARK(s) kdim_mark(s)
+#else
+#define KDIM_MARK(s) ((void)0)
+#endif
+
 namespace rb {
 
 int sm_count();
@@ -304,6 +320,7 @@ richardson_v3(int k, int c, int p, const double* __restrict__ S, int64_t lds, co
 // Fixed summation orders throughout (deterministic).  In-block products:
 // a thread owns up to 8 rows x 4 consecutive columns of the block's output.
 constexpr int kV4Smem = 200 * 1024;
+constexpr int kV4T = 256;  // threads per CTA of richardson_v4 (DMMA saturates with few warps)
 
 struct V4Part {
   int R, C, br, bc;
@@ -311,39 +328,74 @@ struct V4Part {
 
 // out (nrows x p, ld ldo, row-major in smem or strided) = Aop (nrows x K) B (K x p),
 // A element (i, kk) at a[i * ai + kk * ak], B element (kk, j) at b[kk * bk + j].
+// C (nrows x p) = A (nrows x K) B (K x p) from shared memory on the FP64
+// tensor pipe: mma.sync m16n8k4 f64 (DMMA).  A element (i, kk) at
+// a[i * ai + kk * ak], B element (kk, j) at b[kk * bk + j]; C element (i, j)
+// stored to dst[j * ld_j + i * ld_i].  A warp owns one 16-row tile and all
+// p / 8 column tiles of it (the A fragment is loaded once per k-step for
+// all of them): 2 + p / 8 shared loads per p / 8 MMAs of 512 FMAs each --
+// the FMA-per-load ratio the CUDA-core version lacked.  Out-of-range rows /
+// columns / k are read as zero.
+template <int NTMAX>
 __device__ __forceinline__ void v4_block_gemm(const double* __restrict__ a, int ai, int ak, const double* __restrict__ b,
                                               int bk, int nrows, int K, int p, double* __restrict__ dst,
                                               int64_t ld_j, int64_t ld_i) {
-  const int TC = (p + 3) / 4, TR = 256 / TC;
-  const int tid = threadIdx.x;
-  const int tc = tid % TC, tr = tid / TC;
-  if (tr >= TR) return;
-  const int j0 = 4 * tc;
-  for (int i0 = tr; i0 < nrows; i0 += 8 * TR) {
-    double acc[8][4];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int ntiles = (p + 7) / 8;
+  for (int mt = warp; mt * 16 < nrows; mt += nwarps) {
+    const int m0 = mt * 16;
+    double acc[NTMAX][4];
 #pragma unroll
-    for (int q = 0; q < 8; ++q)
+    for (int n = 0; n < NTMAX; ++n)
 #pragma unroll
-      for (int t = 0; t < 4; ++t) acc[q][t] = 0.0;
-    for (int kk = 0; kk < K; ++kk) {
-      double bv[4];
+      for (int q = 0; q < 4; ++q) acc[n][q] = 0.0;
+    const int r0 = m0 + g, r1 = m0 + g + 8;
+    const bool v0 = r0 < nrows, v1 = r1 < nrows;
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const int kk = k0 + t;
+      const bool kv = kk < K;
+      const double a0 = (v0 && kv) ? a[r0 * ai + kk * ak] : 0.0;
+      const double a1 = (v1 && kv) ? a[r1 * ai + kk * ak] : 0.0;
 #pragma unroll
-      for (int t = 0; t < 4; ++t) bv[t] = (j0 + t < p) ? b[kk * bk + j0 + t] : 0.0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int i = i0 + q * TR;
-        const double av = i < nrows ? a[i * ai + kk * ak] : 0.0;
-#pragma unroll
-        for (int t = 0; t < 4; ++t) acc[q][t] = fma(av, bv[t], acc[q][t]);
+      for (int n = 0; n < NTMAX; ++n) {
+        if (n < ntiles) {
+          const int col = n * 8 + g;
+          const double b0 = (kv && col < p) ? b[kk * bk + col] : 0.0;
+          asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                       : "+d"(acc[n][0]), "+d"(acc[n][1]), "+d"(acc[n][2]), "+d"(acc[n][3])
+                       : "d"(a0), "d"(a1), "d"(b0));
+        }
       }
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int i = i0 + q * TR;
-      if (i < nrows)
+    for (int n = 0; n < NTMAX; ++n) {
+      if (n < ntiles) {
+        const int c0 = n * 8 + 2 * t, c1 = c0 + 1;
+        if (v0 && c0 < p) dst[c0 * ld_j + r0 * ld_i] = acc[n][0];
+        if (v0 && c1 < p) dst[c1 * ld_j + r0 * ld_i] = acc[n][1];
+        if (v1 && c0 < p) dst[c0 * ld_j + r1 * ld_i] = acc[n][2];
+        if (v1 && c1 < p) dst[c1 * ld_j + r1 * ld_i] = acc[n][3];
+      }
+    }
+  }
+}
+
+// Op[i * p + j] = M[i + j * ldm] for i < rows, j < p (L2 loads, 8 in flight)
+__device__ __forceinline__ void stage_op(const double* __restrict__ M, int64_t ldm, int rows, int p,
+                                         double* __restrict__ Op, int pst) {
+  const int tot = rows * p, nt = blockDim.x;
+  for (int e0 = threadIdx.x; e0 < tot; e0 += 8 * nt) {
+    double v[8];
 #pragma unroll
-        for (int t = 0; t < 4; ++t)
-          if (j0 + t < p) dst[(j0 + t) * ld_j + i * ld_i] = acc[q][t];
+    for (int t = 0; t < 8; ++t) {
+      const int e = e0 + t * nt;
+      v[t] = e < tot ? __ldcg(&M[(e % rows) + (int64_t)(e / rows) * ldm]) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const int e = e0 + t * nt;
+      if (e < tot) Op[(e % rows) * pst + e / rows] = v[t];
     }
   }
 }
@@ -365,7 +417,7 @@ __device__ __forceinline__ double sum_strided(const double* __restrict__ x, int6
   return s;
 }
 
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(kV4T, 1)
 richardson_v4(int k, int c, int p, const double* __restrict__ S, int64_t lds, const double* __restrict__ P,
               int64_t ldp, int l, double* __restrict__ X, int64_t ldx, double* __restrict__ T, int64_t ldt,
               double* __restrict__ ws, V4Part pt) {
@@ -377,48 +429,54 @@ richardson_v4(int k, int c, int p, const double* __restrict__ S, int64_t lds, co
   const int rb = own ? b / pt.C : 0, cb = own ? b % pt.C : 0;
   const int r0 = rb * pt.br, a0 = cb * pt.bc;
   const int nr = own ? max(0, min(pt.br, k - r0)) : 0, na = own ? max(0, min(pt.bc, c - a0)) : 0;
-  double* Sb = v4s;                       // [a][r], stride br (column-major block)
-  double* Op = v4s + pt.br * pt.bc;       // X_cb as [a][j] (stride p) or T_r as [r][j] (stride p)
+  // strides padded for 16-byte vector loads: even block column stride, row
+  // stride of the staged operand a multiple of 4 doubles
+  const int bst = (pt.br + 1) & ~1, pst = (p + 3) & ~3;
+  double* Sb = v4s;                                  // [a][r], stride bst (column-major block)
+  double* Op = v4s + (((int64_t)bst * pt.bc + 3) & ~3);  // X_cb as [a][j] or T_r as [r][j], stride pst
   double* wsA = ws;                                   // [cb][j][r]: C * p * k
   double* wsB = ws + (int64_t)pt.C * p * k;           // [rb][j][a]: R * p * c
   // the block of S, once
-  for (int e = threadIdx.x; e < nr * na; e += 256) {
+  for (int e = threadIdx.x; e < nr * na; e += kV4T) {
     const int r = e % nr, a = e / nr;
-    cpa8(&Sb[a * pt.br + r], &S[(r0 + r) + (int64_t)(a0 + a) * lds]);
+    cpa8(&Sb[a * bst + r], &S[(r0 + r) + (int64_t)(a0 + a) * lds]);
   }
   cpa_commit();
-  const int64_t nthreads = (int64_t)gridDim.x * 256, gtid = (int64_t)b * 256 + threadIdx.x;
+  KDIM_MARK(0);
+  const int64_t nthreads = (int64_t)gridDim.x * kV4T, gtid = (int64_t)b * kV4T + threadIdx.x;
   for (int sweep = 0; sweep < l; ++sweep) {
     if (sweep > 0) {
       // A: partial T = S_(r,cb) X_cb
-      for (int e = threadIdx.x; e < na * p; e += 256) {
-        const int a = e % na, j = e / na;
-        Op[a * p + j] = X[(a0 + a) + (int64_t)j * ldx];
-      }
+      // X_cb (written by other CTAs: L2 loads), 8 loads in flight per thread
+      stage_op(X + a0, ldx, na, p, Op, pst);
       cpa_wait<0>();
       __syncthreads();
+      KDIM_MARK(8 * sweep + 1);
       if (nr > 0)
-        v4_block_gemm(Sb, 1, pt.br, Op, p, nr, na, p, wsA + (int64_t)cb * p * k + r0, k, 1);
+        v4_block_gemm<8>(Sb, 1, bst, Op, pst, nr, na, p, wsA + (int64_t)cb * p * k + r0, k, 1);
+      KDIM_MARK(8 * sweep + 2);
       grid.sync();
+      KDIM_MARK(8 * sweep + 3);
       for (int64_t e = gtid; e < (int64_t)k * p; e += nthreads) {
         const int r = (int)(e % k), j = (int)(e / k);
         const double sx = sum_strided(wsA + (int64_t)j * k + r, (int64_t)p * k, pt.C);
         T[r + (int64_t)j * ldt] = P[r + (int64_t)j * ldp] - sx;
       }
       grid.sync();
+      KDIM_MARK(8 * sweep + 4);
     }
     // B: partial X = S_(r,cb)^T T_r (sweep 0: T = P)
     const double* Tin = sweep == 0 ? P : T;
     const int64_t ldtin = sweep == 0 ? ldp : ldt;
-    for (int e = threadIdx.x; e < nr * p; e += 256) {
-      const int r = e % nr, j = e / nr;
-      Op[r * p + j] = __ldcg(&Tin[(r0 + r) + (int64_t)j * ldtin]);
-    }
+    stage_op(Tin + r0, ldtin, nr, p, Op, pst);
     cpa_wait<0>();
     __syncthreads();
+    KDIM_MARK(8 * sweep + 5);
     if (na > 0)
-      v4_block_gemm(Sb, pt.br, 1, Op, p, na, nr, p, wsB + (int64_t)rb * p * c + a0, c, 1);
+      v4_block_gemm<8>(Sb, bst, 1, Op, pst, na, nr, p, wsB + (int64_t)rb * p * c + a0, c, 1);
+    KDIM_MARK(8 * sweep + 6);
     grid.sync();
+    KDIM_MARK(8 * sweep + 7);
     for (int64_t e = gtid; e < (int64_t)c * p; e += nthreads) {
       const int a = (int)(e % c), j = (int)(e / c);
       const double st = sum_strided(wsB + (int64_t)j * c + a, (int64_t)p * c, pt.R);
@@ -426,6 +484,7 @@ richardson_v4(int k, int c, int p, const double* __restrict__ S, int64_t lds, co
       *xp = sweep == 0 ? st : *xp + st;
     }
     if (sweep + 1 < l) grid.sync();
+    KDIM_MARK(8 * sweep + 8);
     __syncthreads();
   }
 }
@@ -521,6 +580,152 @@ cholqr_v3(int k, int p, const double* __restrict__ Sp, int64_t lds, double* __re
     for (int j = 0; j < PB; ++j)
       if (j < p) Sout[r + (int64_t)j * ldso] = x[j];
   }
+}
+
+// Upper Cholesky of the p x p matrix Gm (column-major, smem) with ONE
+// block barrier per column: at step j every thread reads the (final) row j,
+// forms the scaled entries R_ja = G_ja / R_jj on the fly and updates its
+// trailing entries G_ab -= R_ja R_jb (j < a <= b) -- the operations and
+// per-element order of chol_smem, so the same bits -- while the owners of
+// row j write R_jc into Rm (a separate array, no read/write overlap).
+// Returns 0 or the 1-based column of the first pivot <= 0 / NaN (dpotrf).
+__device__ int chol_onebar(double* Gm, double* Rm, int p, int* bad_sh) {
+  if (threadIdx.x == 0) *bad_sh = 0;
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) Rm[e] = 0.0;
+  __syncthreads();
+  for (int j = 0; j < p; ++j) {
+    const double d = Gm[j + j * p];
+    if (!(d > 0.0)) {
+      if (threadIdx.x == 0) *bad_sh = j + 1;
+      break;
+    }
+    const double r = sqrt(d);
+    const int m = p - j - 1;  // trailing order
+    for (int c = j + threadIdx.x; c < p; c += blockDim.x) Rm[j + c * p] = c == j ? r : Gm[j + c * p] / r;
+    // trailing upper entries (a, b), j < a <= b < p, enumerated column by column
+    for (int e = threadIdx.x; e < m * (m + 1) / 2; e += blockDim.x) {
+      int bb = (int)((sqrtf(8.f * e + 1.f) - 1.f) * 0.5f);  // column index within the trailing block
+      while ((bb + 1) * (bb + 2) / 2 <= e) ++bb;
+      while (bb * (bb + 1) / 2 > e) --bb;
+      const int aa = e - bb * (bb + 1) / 2;
+      const int A = j + 1 + aa, B = j + 1 + bb;
+      Gm[A + B * p] -= (Gm[j + A * p] / r) * (Gm[j + B * p] / r);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  return *bad_sh;
+}
+
+// x <- x R^{-1} for one row (R in smem, ld ldr; inv[j] = 1 / R_jj), the
+// order of rb_trsm_right's tri_solve_row: per column, t = x_j, then
+// t = fma(-x_l, R_lj, t) for l ascending, x_j = t * inv_j; CH columns at a
+// time as independent chains (each keeps its own l-ascending order).
+template <int PB, int CH>
+__device__ __forceinline__ void tri_solve_smem(double (&x)[PB], int p, const double* Rm, int ldr, const double* inv) {
+#pragma unroll
+  for (int j = 0; j < PB; j += CH) {
+    if (j + CH <= PB && j + CH <= p) {
+      double s[CH];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) s[c] = x[j + c];
+#pragma unroll
+      for (int l = 0; l < j; ++l)
+#pragma unroll
+        for (int c = 0; c < CH; ++c) s[c] = fma(-x[l], Rm[l + (j + c) * ldr], s[c]);
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        x[j + c] = s[c] * inv[j + c];
+#pragma unroll
+        for (int c2 = c + 1; c2 < CH; ++c2) s[c2] = fma(-x[j + c], Rm[j + c + (j + c2) * ldr], s[c2]);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int jj = j + c;
+        if (jj < PB && jj < p) {
+          double t = x[jj];
+#pragma unroll
+          for (int l = 0; l < jj; ++l) t = fma(-x[l], Rm[l + jj * ldr], t);
+          x[jj] = t * inv[jj];
+        }
+      }
+    }
+  }
+}
+
+// v4: the Gram split over K across CTAs (each loads its row slice of S' once,
+// 8 loads in flight per thread), a distributed fixed-order reduction of the
+// partials, the factorization on CTA 0, then the row solves.
+template <int PB>
+__global__ void __launch_bounds__(256, 1)
+cholqr_v4(int k, int p, const double* __restrict__ Sp, int64_t lds, double* __restrict__ R, int64_t ldr,
+          double* __restrict__ Sout, int64_t ldso, int* __restrict__ info, double* __restrict__ ws, int ks) {
+  extern __shared__ __align__(16) double c4s[];
+  __shared__ int bad;
+  cg::grid_group grid = cg::this_grid();
+  const int G = gridDim.x;
+  const int pp = p * p;
+  double* part = ws;                       // [G][p * p] (upper triangle used)
+  double* Gg = ws + (int64_t)G * pp;       // reduced G
+  double* Rg = Gg + pp;                    // R + 1 / diag
+  KDIM_MARK(100);
+  // phase 1: this CTA's rows [q ks, (q + 1) ks) of S' -> smem [r][j], then the upper triangle
+  {
+    const int r0 = blockIdx.x * ks, nr = max(0, min(ks, k - r0));
+    double* sl = c4s;  // nr x p, row-major
+    stage_op(Sp + r0, lds, nr, p, sl, p);
+    __syncthreads();
+    KDIM_MARK(110);
+    // the slice's Gram on the FP64 tensor pipe (full p x p; the upper triangle is used)
+    v4_block_gemm<8>(sl, 1, p, sl, p, p, nr, p, part + (int64_t)blockIdx.x * pp, p, 1);
+  }
+  KDIM_MARK(101);
+  grid.sync();
+  KDIM_MARK(102);
+  // phase 2: G = sum over CTAs (CTA order), upper triangle
+  for (int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x; e < pp; e += (int64_t)G * 256) {
+    const int i = (int)(e % p), j = (int)(e / p);
+    if (i <= j) Gg[e] = sum_strided(part + e, pp, G);
+  }
+  grid.sync();
+  KDIM_MARK(103);
+  if (blockIdx.x == 0) {
+    double* Gm = c4s;
+    for (int e = threadIdx.x; e < pp; e += 256) {
+      const int i = e % p, j = e / p;
+      Gm[e] = i <= j ? __ldcg(&Gg[e]) : 0.0;
+    }
+    __syncthreads();
+    double* Rm = c4s + pp;
+    const int b = chol_onebar(Gm, Rm, p, &bad);
+    for (int e = threadIdx.x; e < pp; e += 256) {
+      const int i = e % p, j = e / p;
+      const double v = i <= j ? Rm[e] : 0.0;
+      R[i + (int64_t)j * ldr] = v;
+      Rg[e] = v;
+    }
+    for (int j = threadIdx.x; j < p; j += 256) Rg[pp + j] = 1.0 / Rm[j + j * p];
+    if (threadIdx.x == 0) *info = b;
+  }
+  KDIM_MARK(104);
+  grid.sync();
+  KDIM_MARK(105);
+  // Sout = S' R^{-1}: one row per thread, fp64, l ascending (rb_trsm_right's
+  // order: t = fma(-x_l, R_lj, t), x_j = t * (1 / R_jj))
+  double* Rs = c4s;
+  for (int e = threadIdx.x; e < pp + p; e += 256) Rs[e] = __ldcg(&Rg[e]);
+  __syncthreads();
+  for (int64_t r = (int64_t)blockIdx.x * 256 + threadIdx.x; r < k; r += (int64_t)G * 256) {
+    double x[PB];
+#pragma unroll
+    for (int j = 0; j < PB; ++j) x[j] = j < p ? Sp[r + (int64_t)j * lds] : 0.0;
+    tri_solve_smem<PB, (PB < 32 ? 4 : 2)>(x, p, Rs, p, Rs + pp);
+#pragma unroll
+    for (int j = 0; j < PB; ++j)
+      if (j < p) Sout[r + (int64_t)j * ldso] = x[j];
+  }
+  KDIM_MARK(106);
 }
 
 // ============================ certification =================================
@@ -710,18 +915,19 @@ int gemm_generic(int tA, int m, int n, int64_t K, T alpha, const T* A, int64_t l
 
 // ---- launch helpers -----------------------------------------------------------
 template <typename K>
-int coop_launch(K kern, size_t smem, void** args, cudaStream_t st, int max_grid, int* grid_out, const char* what) {
+int coop_launch(K kern, size_t smem, void** args, cudaStream_t st, int max_grid, int* grid_out, const char* what,
+                int nthreads = kKT) {
   static int dev_cached = -1;
   (void)dev_cached;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kKT, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthreads, smem);
   RB_REQUIRE(per_sm >= 1, "%s: kernel does not fit an SM", what);
   int grid = std::min(max_grid, sm_count() * std::min(per_sm, 2));
   grid = std::max(grid, 1);
   *grid_out = grid;
   ++g_launches;
-  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kKT), args, smem, st);
+  const cudaError_t e = cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(nthreads), args, smem, st);
   if (e != cudaSuccess) {
     set_error("%s: cooperative launch failed: %s", what, cudaGetErrorString(e));
     return RB_ECUDA;
@@ -742,6 +948,11 @@ size_t kdim_ws_bytes(int k, int m) {
 // Block grid of S for richardson_v4: C column blocks, R = G / C row blocks,
 // C chosen so the blocks are about square (balanced partial reductions);
 // nullopt-like (R = 0) when a block does not fit the shared-memory budget.
+static size_t v4_smem(int br, int bc, int p) {
+  const size_t bst = (size_t)((br + 1) & ~1), pst = (size_t)((p + 3) & ~3);
+  return (((bst * bc + 3) & ~(size_t)3) + (size_t)std::max(br, bc) * pst) * sizeof(double);
+}
+
 static V4Part v4_partition(int k, int c, int p, int G) {
   V4Part best{0, 0, 0, 0};
   size_t best_cost = (size_t)-1;
@@ -749,10 +960,10 @@ static V4Part v4_partition(int k, int c, int p, int G) {
     const int R = std::min(k, G / C);
     if (R < 1) break;
     const int br = (k + R - 1) / R, bc = (c + C - 1) / C;
-    const size_t smem = ((size_t)br * bc + (size_t)std::max(br, bc) * p) * sizeof(double);
+    const size_t smem = v4_smem(br, bc, p);
     if (smem > (size_t)kV4Smem) continue;
     // per-sweep cost model: block FMAs (both phases) + reduction loads per thread
-    const size_t cost = 2 * (size_t)br * bc * p / 64 + ((size_t)k * C + (size_t)c * R) * p / ((size_t)G * 256) * 400;
+    const size_t cost = 2 * (size_t)br * bc * p / 64 + ((size_t)k * C + (size_t)c * R) * p / ((size_t)G * kV4T) * 400;
     if (cost < best_cost) {
       best_cost = cost;
       best = V4Part{(k + br - 1) / br, (c + bc - 1) / bc, br, bc};
@@ -773,8 +984,8 @@ int ls_richardson(int k, int c, int p, const double* S, int64_t lds, const doubl
     RB_REQUIRE(ws && wsb >= need, "rb_ls_richardson: workspace too small (%zu < %zu)", wsb, need);
     int grid = 0;
     void* args[] = {&k, &c, &p, (void*)&S, &lds, (void*)&P, &ldp, &l, &X, &ldx, &T, &ldt, &ws, &pt};
-    const size_t smem = ((size_t)pt.br * pt.bc + (size_t)std::max(pt.br, pt.bc) * p) * sizeof(double);
-    return coop_launch(richardson_v4, smem, args, st, pt.R * pt.C, &grid, "rb_ls_richardson");
+    const size_t smem = v4_smem(pt.br, pt.bc, p);
+    return coop_launch(richardson_v4, smem, args, st, pt.R * pt.C, &grid, "rb_ls_richardson", kV4T);
   }
   // S too large for the grid's shared memory: full-K tile items
   const int items = std::max(l > 1 ? (k + 15) / 16 : 1, (c + 7) / 8);
@@ -792,16 +1003,17 @@ int sketched_cholqr_small(int k, int p, const double* Sp, int64_t lds, double* R
                           int64_t ldso, int* info, void* ws, size_t wsb, cudaStream_t st) {
   RB_REQUIRE(k >= 1 && p >= 1 && p <= 64 && Sp && R && Sout && info && lds >= k && ldr >= p && ldso >= k,
              "rb_sketched_cholqr_small: bad args (k=%d p=%d)", k, p);
-  RB_REQUIRE(ws && wsb >= (size_t)(2 * p * p + p) * sizeof(double), "rb_sketched_cholqr_small: workspace");
-  // CTAs: the Gram's 8-row items and one row per thread in the solve
-  const int G = std::max(1, std::min(sm_count(), std::max((p + 7) / 8, (k + 255) / 256)));
+  // CTAs: row slices of <= 64 rows for the Gram (one load round each), at
+  // least one row per thread for the solve
+  const int G = std::max(1, std::min(sm_count(), std::max((k + 63) / 64, (k + 255) / 256)));
+  int ks = (k + G - 1) / G;
+  const size_t need = ((size_t)G * p * p + 2 * (size_t)p * p + p) * sizeof(double);
+  RB_REQUIRE(ws && wsb >= need, "rb_sketched_cholqr_small: workspace too small");
   int grid = 0;
-  void* args[] = {&k, &p, (void*)&Sp, &lds, &R, &ldr, &Sout, &ldso, &info, &ws};
+  void* args[] = {&k, &p, (void*)&Sp, &lds, &R, &ldr, &Sout, &ldso, &info, &ws, &ks};
+  const size_t sm = std::max((size_t)ks * p, (size_t)(2 * p * p + p)) * sizeof(double);
 #define RB_CQ(V)                                                                                            \
-  if (p <= V) {                                                                                             \
-    const size_t sm = std::max(sizeof(ItemSmem<V, 8>), (size_t)(V * V + V) * sizeof(double));               \
-    return coop_launch(cholqr_v3<V>, sm, args, st, G, &grid, "rb_sketched_cholqr_small");                  \
-  }
+  if (p <= V) return coop_launch(cholqr_v4<V>, sm, args, st, G, &grid, "rb_sketched_cholqr_small");
   RB_CQ(8) RB_CQ(16) RB_CQ(24) RB_CQ(32) RB_CQ(40) RB_CQ(48) RB_CQ(64)
 #undef RB_CQ
   return RB_EINVAL;

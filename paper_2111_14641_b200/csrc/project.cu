@@ -199,7 +199,7 @@ project_coarse(int64_t n, int c, int p, const TQ* __restrict__ Q, int64_t ldq,
 // q values and PB / CS / 4 LDS.128 for 2 * RPT * PB / CS FP instructions
 // (RPT = 4, CS = 2 at p = 40: 6 loads per 160 FP).  The CTA covering the
 // ragged end of the rows fills its stages with ordinary loads instead.
-constexpr int kKQ = 16;          // l rows per stage
+constexpr int kKQ = 12;          // l rows per stage (79 KB of stages: leaves room for a lean sketch CTA)
 constexpr int kStagedRows = 512;  // rows per CTA
 constexpr int kQS = 3;   // stage buffers
 

@@ -985,10 +985,11 @@ int sketch_sparse_sign_tab(int xd, int64_t n, int ncols, const void* X, int64_t 
 size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k);
 int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2, int c2,
                        int64_t n, const uint8_t* qt, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
-                       double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st);
+                       double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st, bool lean = false);
 
 // [out1 | out2] = scale * (q @ [X1 | X2]).  mode 0 = auto (tensor pipe when
-// every input is binary32), 1 = fp64 CUDA cores, 2 = tensor pipe.
+// every input is binary32), 1 = fp64 CUDA cores, 2 = tensor pipe, 3 = tensor
+// pipe with the lean CTA (<= 64 columns; made to run beside the projection).
 int sketch_gaussian2(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2, int c2,
                      int64_t n, const uint8_t* theta, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
                      double* out2, int64_t ldo2, int acc, int mode, void* ws, size_t wsb, cudaStream_t st) {
@@ -997,8 +998,11 @@ int sketch_gaussian2(int xd1, const void* X1, int64_t ld1, int c1, int xd2, cons
              "rb_sketch_gaussian: bad args");
   RB_REQUIRE(n == 0 || (X1 && ld1 >= n && (c2 == 0 || (X2 && ld2 >= n)) && theta && ldt >= n),
              "rb_sketch_gaussian: bad X/theta");
-  RB_REQUIRE(mode >= 0 && mode <= 2, "rb_sketch_gaussian: bad mode %d", mode);
-  const bool tc = mode == 2 || (mode == 0 && xd1 == RB_F32 && (c2 == 0 || xd2 == RB_F32));
+  RB_REQUIRE(mode >= 0 && mode <= 3, "rb_sketch_gaussian: bad mode %d", mode);
+  if (mode == 3 && c1 + c2 <= 64)
+    return sketch_gaussian_tc(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, theta, ldt, k, scale, out1, ldo1, out2, ldo2,
+                              acc, ws, wsb, st, true);
+  const bool tc = mode >= 2 || (mode == 0 && xd1 == RB_F32 && (c2 == 0 || xd2 == RB_F32));
   // > 64 columns: CTA pairs sharing the table stream (RB_TC_PAIR=0: two passes)
   static const int pair = getenv("RB_TC_PAIR") ? atoi(getenv("RB_TC_PAIR")) : 1;
   if (tc && (c1 + c2 <= 64 || (pair && c2 > 0)))

@@ -391,12 +391,17 @@ struct Smem {
   uint32_t tbase;
 };
 
-template <int NP, int ST>
-__global__ void __launch_bounds__(kThreads, 1)
-gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt, int k,
-                 const uint8_t* __restrict__ planes1, const int* __restrict__ exps1, int tiles_per_cta,
-                 double* __restrict__ ws1, int dbg, int pairs, int ncols2, const uint8_t* __restrict__ planes2,
-                 const int* __restrict__ exps2, double* __restrict__ ws2) {
+// LEAN: 192 threads (producer warp 0, MMA warp 1, epilogue warps 2..5 on TMEM
+// lane quadrants warp & 3), <= 168 registers, two stages -- sized to share
+// an SM with one CTA of the staged projection, so the sketch of the NEXT
+// block's W runs on the tensor pipe while the projection keeps the FP32
+// pipe busy (the sweep issues them on two streams).
+template <int NP, int ST, bool LEAN>
+__device__ __forceinline__ void
+gauss_tc_body(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt, int k,
+              const uint8_t* __restrict__ planes1, const int* __restrict__ exps1, int tiles_per_cta,
+              double* __restrict__ ws1, int dbg, int pairs, int ncols2, const uint8_t* __restrict__ planes2,
+              const int* __restrict__ exps2, double* __restrict__ ws2) {
   // pairs == 2: CTAs 2 mt and 2 mt + 1 own the same 128 sketch rows and K
   // range for two inputs (two column halves of > 64 columns that do not fit
   // one CTA's TMEM); launched side by side they read each q tile once from
@@ -502,11 +507,11 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
         }
       }
     }
-  } else if (warp >= 4) {
+  } else if (LEAN ? (warp >= 2 && warp < 6) : warp >= 4) {
     // ---------------- epilogue ----------------
     constexpr int NG = gl::np_group(NP);
     static_assert(NG % 8 == 0, "epilogue drains 8 columns at a time");
-    const int q = warp - 4;  // TMEM lane quadrant
+    const int q = warp & 3;  // TMEM lane quadrant (warps may only touch lanes 32 (warp % 4) ..)
     const int r = mt * kTM + q * 32 + lane;
     const uint32_t lane_base = tbase + ((uint32_t)(q * 32) << 16);
     double acc[NP];  // this row's fp64 partial sketch, all columns
@@ -530,7 +535,7 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
       const int* ex = exps + chunk * NP;
       // With room for a second register copy (NP <= 40), the chunk's terms
       // are staged in t[] and TMEM is handed back before the fp64 adds.
-      constexpr bool kStage = NP <= 40;
+      constexpr bool kStage = NP <= 40 && !LEAN;
       double t[kStage ? NP : 1];
 #pragma unroll
       for (int c0 = 0; c0 < NP; c0 += 8) {
@@ -586,6 +591,27 @@ gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t l
   if (warp == 2) tc::tmem_dealloc(tbase, kAlloc);
 }
 
+template <int NP, int ST>
+__global__ void __launch_bounds__(kThreads, 1)
+gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt, int k,
+                 const uint8_t* __restrict__ planes1, const int* __restrict__ exps1, int tiles_per_cta,
+                 double* __restrict__ ws1, int dbg, int pairs, int ncols2, const uint8_t* __restrict__ planes2,
+                 const int* __restrict__ exps2, double* __restrict__ ws2) {
+  gauss_tc_body<NP, ST, false>(n, ncols, qt, ldt, k, planes1, exps1, tiles_per_cta, ws1, dbg, pairs, ncols2, planes2,
+                               exps2, ws2);
+}
+
+constexpr int kLeanThreads = 192;
+template <int NP, int ST>
+__global__ void __launch_bounds__(kLeanThreads, 2)  // (2 x 192 threads: <= 168 registers)
+gauss_tc_lean(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt, int k,
+              const uint8_t* __restrict__ planes1, const int* __restrict__ exps1, int tiles_per_cta,
+              double* __restrict__ ws1, int dbg, int pairs, int ncols2, const uint8_t* __restrict__ planes2,
+              const int* __restrict__ exps2, double* __restrict__ ws2) {
+  gauss_tc_body<NP, ST, true>(n, ncols, qt, ldt, k, planes1, exps1, tiles_per_cta, ws1, dbg, pairs, ncols2, planes2,
+                              exps2, ws2);
+}
+
 __global__ void reduce_splits_tc(const double* __restrict__ ws, int splits, int k, int c1, int ncols, double scale,
                                  double* __restrict__ out1, int64_t ldo1, double* __restrict__ out2, int64_t ldo2,
                                  int accumulate) {
@@ -618,7 +644,8 @@ struct Half2 {  // the second input of a paired launch (pairs == 2)
 
 template <int NP>
 int launch_np(int64_t n, int ncols, const uint8_t* qt, int64_t ldt, int k, const uint8_t* planes, const int* exps,
-              double* part, size_t part_bytes, int* splits_out, cudaStream_t st, const Half2& h2 = Half2()) {
+              double* part, size_t part_bytes, int* splits_out, cudaStream_t st, const Half2& h2 = Half2(),
+              bool lean = false) {
   const int mt = ceil_div(k, kTM);
   // one wave: floor(SMs / m-tiles) K ranges of equal tile counts.  A paired
   // launch keeps the same K ranges (two waves of CTA pairs), so each input's
@@ -647,7 +674,13 @@ int launch_np(int64_t n, int ncols, const uint8_t* qt, int64_t ldt, int k, const
         n, ncols, qt, ldt, k, planes, exps, tpc, part, dbg_flag(), h2.pairs, h2.ncols, h2.planes, h2.exps,       \
         part + part_bytes / sizeof(double));                                                                     \
   }
-  if (st_req >= 4 && kMax >= 4) RB_GL((kMax >= 4 ? 4 : 1))
+  if (lean && h2.pairs == 1) {
+    // two stages: shares the SM with one projection CTA
+    const size_t smem = sizeof(Smem<NP, 2>) + 1024;
+    cudaFuncSetAttribute(gauss_tc_lean<NP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    RB_KLAUNCH gauss_tc_lean<NP, 2><<<dim3(mt, splits), kLeanThreads, smem, st>>>(
+        n, ncols, qt, ldt, k, planes, exps, tpc, part, dbg_flag(), 1, 0, nullptr, nullptr, nullptr);
+  } else if (st_req >= 4 && kMax >= 4) RB_GL((kMax >= 4 ? 4 : 1))
   else if (st_req >= 3 && kMax >= 3) RB_GL((kMax >= 3 ? 3 : 1))
   else RB_GL(2)
 #undef RB_GL
@@ -770,7 +803,7 @@ size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k) {
 // binary32 or binary64 (n rows); c2 may be 0.
 int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2, int c2,
                        int64_t n, const uint8_t* qt, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
-                       double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st) {
+                       double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st, bool lean) {
   const int ncols = c1 + c2;
   if (ncols > 64)
     return sketch_gaussian_tc_pair(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, qt, ldt, k, scale, out1, ldo1, out2, ldo2,
@@ -796,12 +829,12 @@ int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, co
     else launch_split<double>(xd2, g, n, c1, X1, ld1, c2, X2, ld2, NP, planes, exps, st);
     int rc;
     switch (NP) {
-      case 16: rc = launch_np<16>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st); break;
-      case 32: rc = launch_np<32>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st); break;
-      case 40: rc = launch_np<40>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st); break;
-      case 48: rc = launch_np<48>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st); break;
-      case 64: rc = launch_np<64>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st); break;
-      default: rc = launch_np<64>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st); break;
+      case 16: rc = launch_np<16>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st, Half2(), lean); break;
+      case 32: rc = launch_np<32>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st, Half2(), lean); break;
+      case 40: rc = launch_np<40>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st, Half2(), lean); break;
+      case 48: rc = launch_np<48>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st, Half2(), lean); break;
+      case 64: rc = launch_np<64>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st, Half2(), lean); break;
+      default: rc = launch_np<64>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st, Half2(), lean); break;
     }
     if (rc != RB_OK) return rc;
   }

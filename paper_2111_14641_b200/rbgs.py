@@ -648,6 +648,36 @@ class RbgsSweep:
                            False, sketching.GAUSS_MODE)
         self.comm.allreduce_(outA, outB)
 
+    # -- sketch / projection overlap -------------------------------------------
+    def _overlap_ok(self, Wn):
+        """The next block's W sketch can run beside this block's projection:
+        gaussian kind on the tensor pipe, <= 40 columns (the lean sketch CTA
+        and one staged-projection CTA share an SM), binary32 Q."""
+        return (OVERLAP and self._fusable(Wn, Wn) and Wn.shape[1] <= 40 and self.q_dtype == torch.float32
+                and self.compute == F32 and self.order == ORDER_REFERENCE)
+
+    def _fork_next_sketch(self, Wn, Pn):
+        """Sketch W_(i+1) into Pn on a high-priority side stream (lean CTAs,
+        tensor pipe) while the current stream runs this block's projection
+        (FP32 pipe); returns the event the consumer waits for."""
+        dev = self.device
+        cur = torch.cuda.current_stream(dev)
+        side = _SIDE_STREAMS.get(dev.index)
+        if side is None:  # one per device, shared by every sweep (and its workspace)
+            side = _SIDE_STREAMS[dev.index] = torch.cuda.Stream(dev, priority=-1)
+        side.wait_stream(cur)
+        ev = self._lookahead_event
+        self._lookahead_event = None
+        tab = self.theta.device_tables(dev, self.row0, Wn.shape[0])
+        with torch.cuda.stream(side):
+            if ev is not None:
+                side.wait_event(ev)
+            D.sketch_gaussian(Wn, tab["theta"], tab["ldt"], self.theta.k,
+                              1.0 / (sketching.GAUSS_GRID * math.sqrt(self.theta.k)), Pn, False, "lean")
+            done = torch.cuda.Event()
+            done.record(side)
+        return done
+
     def _push(self, i, j0, j1, w, W, Wn=None):
         scr = self._scr
         cfg = self.cfg
@@ -678,6 +708,13 @@ class RbgsSweep:
         norms.zero_()
         scr.info.zero_()
         sp_given = None
+        fork = None
+        if c and Wn is not None and self._next_P is None and self._overlap_ok(Wn):
+            # the next block's Step 1 does not depend on this block: issue it
+            # first, on the side stream, so it overlaps the projection
+            Pn = scr.Pn[scr.pn_flip][:, :Wn.shape[1]]
+            scr.pn_flip ^= 1
+            fork = (self._fork_next_sketch(Wn, Pn), Pn)
         if c:
             X = scr.X[:c, :w]
             self._solve_ls(self.S[:, :c], Pi, X)
@@ -694,7 +731,15 @@ class RbgsSweep:
             else:
                 D.project(self.Q[:, :c], X, W, slot, self.compute, self.order, norms[0:2])
             Qp = slot
-            if Wn is not None and self._next_P is None and self._fusable(slot, Wn):
+            if fork is not None:
+                # Step 4's sketch of Q' on this stream, then join the side
+                # stream's Step 1 of the next block; one allreduce for both
+                sp_given = scr.Sp[:, :w]
+                self._sketch(slot, sp_given)
+                torch.cuda.current_stream(self.device).wait_event(fork[0])
+                self.comm.allreduce_(sp_given, fork[1])
+                self._next_P = (self._key(Wn), fork[1])
+            elif Wn is not None and self._next_P is None and self._fusable(slot, Wn):
                 sp_given = scr.Sp[:, :w]
                 Pn = scr.Pn[scr.pn_flip][:, :Wn.shape[1]]
                 scr.pn_flip ^= 1
@@ -838,6 +883,10 @@ class RbgsSweep:
 
 
 REPLAYS = 0  # one-shot factorizations replayed eagerly after a deferred-status failure
+# next-block sketch overlapped with the projection (RB_OVERLAP=0: one fused
+# two-input sketch after the projection instead)
+OVERLAP = os.environ.get("RB_OVERLAP", "1") != "0"
+_SIDE_STREAMS = {}
 
 
 def _deferrable(cfg) -> bool:
