@@ -564,17 +564,23 @@ void launch_pb(int mode, int64_t n, int c, int p, const void* Q, int64_t ldq, co
       constexpr int RPT = PB <= 20 ? 2 : 4;
       constexpr int CS = PB <= 20 ? 1 : PB <= 40 ? 2 : 4;
       constexpr int NT = kStagedRows / RPT * CS;
-      constexpr size_t smem = staged_smem<PB, RPT, CS, NT>();
+      // RB_PROJECT_SMEM_PAD (measurement knob): extra dynamic shared memory,
+      // e.g. 120000 to force one CTA per SM
+      static const size_t pad = getenv("RB_PROJECT_SMEM_PAD") ? (size_t)atol(getenv("RB_PROJECT_SMEM_PAD")) : 0;
+      const size_t smem = staged_smem<PB, RPT, CS, NT>() + pad;
       const int rows = staged_rows_per_cta(n, NT);
       const int grid = ceil_div(n, (int64_t)rows);
       static bool attr = false;
       if (!attr) {
-        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
+        const int mx = 227 * 1024 - 1024;  // room for the static shared arrays
+        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+        // maximum shared-memory carveout, like the lean sketch kernel: CTAs of
+        // two kernels share an SM only under one L1 / shared split
+        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        cudaFuncSetAttribute(project_staged<TW, PB, RPT, CS, NT, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
         attr = true;
       }
 #define RB_ST(M)                                                                                  \

@@ -678,6 +678,7 @@ int launch_np(int64_t n, int ncols, const uint8_t* qt, int64_t ldt, int k, const
     // two stages: shares the SM with one projection CTA
     const size_t smem = sizeof(Smem<NP, 2>) + 1024;
     cudaFuncSetAttribute(gauss_tc_lean<NP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(gauss_tc_lean<NP, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     RB_KLAUNCH gauss_tc_lean<NP, 2><<<dim3(mt, splits), kLeanThreads, smem, st>>>(
         n, ncols, qt, ldt, k, planes, exps, tpc, part, dbg_flag(), 1, 0, nullptr, nullptr, nullptr);
   } else if (st_req >= 4 && kMax >= 4) RB_GL((kMax >= 4 ? 4 : 1))

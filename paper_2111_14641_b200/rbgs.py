@@ -883,9 +883,14 @@ class RbgsSweep:
 
 
 REPLAYS = 0  # one-shot factorizations replayed eagerly after a deferred-status failure
-# next-block sketch overlapped with the projection (RB_OVERLAP=0: one fused
-# two-input sketch after the projection instead)
-OVERLAP = os.environ.get("RB_OVERLAP", "1") != "0"
+# next-block sketch overlapped with the projection on a side stream
+# (RB_OVERLAP=1).  Off by default: measured on B200 (tools/overlap_probe.py,
+# profiles/r02_overlap_probe.json) the two kernels do co-reside, but the
+# projection's LDS traffic and the sketch's UMMA operand reads share each
+# SM's shared-memory bandwidth, and the pair takes as long as the two in
+# series (2.89 vs 2.77 ms at C2's last block); the default is the fused
+# two-input sketch after the projection (one table pass).
+OVERLAP = os.environ.get("RB_OVERLAP", "0") == "1"
 _SIDE_STREAMS = {}
 
 
