@@ -52,6 +52,8 @@ class Comm:
 
     def __init__(self, group=None):
         self.group = group
+        self.collectives = 0  # collectives issued (one per block in the sweep)
+        self._bufs = {}
         if group is None or not torch.distributed.is_available() or not torch.distributed.is_initialized():
             self.world, self.rank = 1, 0
             self.group = None
@@ -65,13 +67,31 @@ class Comm:
 
     def allreduce_(self, *tensors):
         """In-place sum of every tensor across ranks, as ONE collective: the
-        tensors are packed into a single fp64 buffer, reduced, unpacked."""
+        tensors are packed into a persistent fp64 buffer (grown on demand,
+        no per-call allocation), reduced, unpacked."""
+        tensors = tuple(t for t in tensors if t is not None and t.numel() > 0)
         if not self.active or not tensors:
             return tensors
+        self.collectives += 1
         if len(tensors) == 1 and tensors[0].is_contiguous():
             torch.distributed.all_reduce(tensors[0], group=self.group)
             return tensors
-        flat = torch.cat([t.reshape(-1) if t.is_contiguous() else t.t().reshape(-1) for t in tensors])
+        total = sum(t.numel() for t in tensors)
+        dev = tensors[0].device
+        buf = self._bufs.get(dev)
+        if buf is None or buf.numel() < total:
+            buf = torch.empty(max(total, 1 << 16), dtype=torch.float64, device=dev)
+            self._bufs[dev] = buf
+        flat = buf[:total]
+        off = 0
+        for t in tensors:
+            n = t.numel()
+            dst = flat[off:off + n]
+            if t.is_contiguous():
+                dst.view_as(t).copy_(t)
+            else:  # column-major 2-D view: its transpose is contiguous
+                dst.view(t.shape[1], t.shape[0]).copy_(t.t())
+            off += n
         torch.distributed.all_reduce(flat, group=self.group)
         off = 0
         for t in tensors:
@@ -79,7 +99,7 @@ class Comm:
             src = flat[off:off + n]
             if t.is_contiguous():
                 t.copy_(src.view_as(t))
-            else:  # column-major 2-D view: its transpose is contiguous
+            else:
                 t.t().copy_(src.view(t.shape[1], t.shape[0]))
             off += n
         return tensors

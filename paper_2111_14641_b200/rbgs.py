@@ -397,6 +397,8 @@ class RbgsSweep:
         self._fuse_scaling = False
         self._pending_scale = None
         self._lookahead_event = None  # upload event of the lookahead block (pinned host W)
+        self._pending = []  # this block's partials (norms, l2 Gram) not yet allreduced
+        self._g_given = None  # l2 stage: Q'^T Q' reduced with the block's sketches
 
     # -- small utilities ---------------------------------------------------
     def _sketch(self, X, out):
@@ -404,7 +406,20 @@ class RbgsSweep:
 
     def _sketch_reduce(self, X, out):
         self._sketch(X, out)
-        self.comm.allreduce_(out)
+        self._reduce(out)
+
+    def _reduce(self, *tensors):
+        """Allreduce of this block's sketch partials, with the block's other
+        pending partials -- the norms (rbgs.py:373-374, projection epilogue),
+        the l2 stage's tall Gram -- riding along: one collective per block
+        (PAPER.md:200)."""
+        pend = self._pending
+        self._pending = []
+        self.comm.allreduce_(*tensors, *pend)
+
+    def _flush_norms(self):
+        if self._pending:
+            self._reduce()
 
     def _as_block(self, W_i, w):
         """Device view of this rank's rows of block W_i (dtype kept: binary32
@@ -510,13 +525,16 @@ class RbgsSweep:
         # sketched CholQR of Q*: R'' = chol(S*^T S*), R_ii = R'' R',
         # Q_i = Q' R_ii^{-1}, S_i = S* R''^{-1}.
         G = scr.G[:w, :w]
-        D.cross(Qp, Qp, G)
-        if reuse or sp_given is not None:
+        if self._g_given is not None:  # reduced with the block's sketches
             Sp.copy_(Pi if reuse else sp_given)
-            self.comm.allreduce_(G)
         else:
-            self._sketch(Qp, Sp)
-            self.comm.allreduce_(G, Sp)
+            D.cross(Qp, Qp, G)
+            if reuse or sp_given is not None:
+                Sp.copy_(Pi if reuse else sp_given)
+                self._reduce(G)
+            else:
+                self._sketch(Qp, Sp)
+                self._reduce(G, Sp)
         sp_qp = Sp.clone() if self.cfg.certify_blocks else None
         R1 = scr.R1[:w, :w]
         D.potrf(G, R1, scr.info[0:1])
@@ -578,7 +596,7 @@ class RbgsSweep:
         s2 = D.empty_cm(k, 1, torch.float64, dev)
         nrm = torch.zeros(w + 1, dtype=torch.float64, device=dev)
         D.sumsq(Qp, nrm[w:w + 1])
-        self.comm.allreduce_(nrm[w:w + 1])
+        self._reduce(nrm[w:w + 1])
         sp_qp = None
         if self.cfg.certify_blocks:
             sp_qp = D.empty_cm(k, w, torch.float64, dev)
@@ -646,7 +664,7 @@ class RbgsSweep:
         D.sketch_gaussian2(A, B, tab["theta"], tab["ldt"], self.theta.k,
                            1.0 / (sketching.GAUSS_GRID * math.sqrt(self.theta.k)), outA, outB,
                            False, sketching.GAUSS_MODE)
-        self.comm.allreduce_(outA, outB)
+        self._reduce(outA, outB)
 
     # -- sketch / projection overlap -------------------------------------------
     def _overlap_ok(self, Wn):
@@ -682,6 +700,22 @@ class RbgsSweep:
         scr = self._scr
         cfg = self.cfg
         c = self.cols_done
+        norms = scr.norms
+        norms.zero_()
+        scr.info.zero_()
+        sharded = self.comm.active
+        if not c:
+            # Q' = W_1 itself (rbgs.py:371-372): ||W_1|| = ||Q'_1||, read in its
+            # own format; sharded, the partial rides Step 1's allreduce
+            D.sumsq(W, norms[0:1])
+            norms[1:2].copy_(norms[0:1])
+            if sharded:
+                self._pending.append(norms[0:2])
+                if self.inter[0] == "l2_plus_cholqr" and not cfg.certify_blocks:
+                    # the l2 stage's W_1^T W_1 rides Step 1's allreduce too
+                    self._g_given = scr.G[:w, :w]
+                    D.cross(W, W, self._g_given)
+                    self._pending.append(self._g_given)
         # Step 1 (possibly already done by the previous block's fused pass)
         nxt = self._next_P
         self._next_P = None
@@ -696,6 +730,17 @@ class RbgsSweep:
                 self._sketch_pair(W, Wn, Pi, Pn)
                 self._next_P = (self._key(Wn), Pn)
                 Wn = None
+            elif Wn is not None and c == 0 and sharded and not cfg.certify_blocks:
+                # row-sharded, any kind: Step 1 of blocks 1 and 2 (and the
+                # norms of W_1) in one allreduce
+                Pn = scr.Pn[scr.pn_flip][:, :Wn.shape[1]]
+                scr.pn_flip ^= 1
+                self._wait_lookahead()
+                self._sketch(W, Pi)
+                self._sketch(Wn, Pn)
+                self._reduce(Pi, Pn)
+                self._next_P = (self._key(Wn), Pn)
+                Wn = None
             else:
                 self._sketch_reduce(W, Pi)
         Pu = Pi  # as sketched (the inter-block step re-sketches Q' unrounded)
@@ -704,10 +749,9 @@ class RbgsSweep:
             Pi = scr.Pr[:, :w]
             D.convert(scr.P32[:, :w], Pi)
         slot = self.Q[:, j0:j1]
-        norms = scr.norms
-        norms.zero_()
-        scr.info.zero_()
         sp_given = None
+        if c:
+            self._g_given = None
         fork = None
         if c and Wn is not None and self._next_P is None and self._overlap_ok(Wn):
             # the next block's Step 1 does not depend on this block: issue it
@@ -730,14 +774,16 @@ class RbgsSweep:
                 D.project_trsm(self.Q[:, :c], X, W, slot, self.compute, self.order, norms[0:2], Qf, RSf)
             else:
                 D.project(self.Q[:, :c], X, W, slot, self.compute, self.order, norms[0:2])
-            Qp = slot
+            if sharded:
+                # the norm partials join the block's next allreduce
+                self._pending.append(norms[0:2])
             if fork is not None:
                 # Step 4's sketch of Q' on this stream, then join the side
                 # stream's Step 1 of the next block; one allreduce for both
                 sp_given = scr.Sp[:, :w]
                 self._sketch(slot, sp_given)
                 torch.cuda.current_stream(self.device).wait_event(fork[0])
-                self.comm.allreduce_(sp_given, fork[1])
+                self._reduce(sp_given, fork[1])
                 self._next_P = (self._key(Wn), fork[1])
             elif Wn is not None and self._next_P is None and self._fusable(slot, Wn):
                 sp_given = scr.Sp[:, :w]
@@ -746,14 +792,27 @@ class RbgsSweep:
                 self._wait_lookahead()
                 self._sketch_pair(slot, Wn, sp_given, Pn)
                 self._next_P = (self._key(Wn), Pn)
+            elif (Wn is not None and self._next_P is None and sharded and not cfg.certify_blocks
+                  and self.inter[0] in ("sketched_cholqr", "l2_plus_cholqr")):
+                # row-sharded, any sketch kind: Step 4's sketch of Q'_i, Step 1
+                # of block i+1, the norms (and the l2 stage's tall Gram) in
+                # ONE allreduce (one synchronization per block)
+                sp_given = scr.Sp[:, :w]
+                Pn = scr.Pn[scr.pn_flip][:, :Wn.shape[1]]
+                scr.pn_flip ^= 1
+                self._wait_lookahead()
+                self._sketch(slot, sp_given)
+                self._sketch(Wn, Pn)
+                if self.inter[0] == "l2_plus_cholqr":
+                    self._g_given = scr.G[:w, :w]
+                    D.cross(slot, slot, self._g_given)
+                self._reduce(sp_given, Pn, self._g_given)
+                self._next_P = (self._key(Wn), Pn)
+            Qp = slot
         else:
-            # Q' = W_1 itself (rbgs.py:371-372): read it in its own format
-            D.sumsq(W, norms[0:1])
             Qp = W
-        self.comm.allreduce_(norms[0:2])
-        if not c:
-            norms[1:2].copy_(norms[0:1])
         Rii, Si, sp_qp = self._interblock(Qp, Pu, slot, block1=(c == 0), sp_given=sp_given)
+        self._flush_norms()
         # finiteness of everything the block produced (Matrix() checks)
         if Pi.dtype == torch.float64 and Si.dtype == torch.float64 and Rii.dtype == torch.float64:
             D.sumsq3(Pi, Si, Rii, norms[2:5])
