@@ -293,13 +293,20 @@ def gpu_arm(args, cfgd):
     torch.cuda.synchronize()
 
     # Default: the factorization captured once as a CUDA graph (RbgsPlan)
-    # and replayed -- every kernel of every block per step, plus the host
-    # read of the block statuses and the certification.  In-place runs
-    # (C5 shard) and --no-graph use the eager one-shot rbgs().
-    # (single rank only: NCCL collectives inside a captured graph are not
-    # exercised on this one-GPU pod, so sharded runs stay eager)
-    use_graph = not inplace and not args.no_graph and world == 1
-    plan = RbgsPlan(W, theta, cfg, dc) if use_graph else None
+    # and replayed -- every kernel of every block per step (with NCCL, the
+    # one allreduce per block is captured too), plus the host read of the
+    # block statuses and the certification.  In-place runs (C5 shard),
+    # gloo-backed runs (host collectives cannot be captured) and --no-graph
+    # use the eager one-shot rbgs().
+    backend = dist.get_backend(group) if group is not None else "none"
+    use_graph = not inplace and not args.no_graph and backend in ("none", "nccl")
+    plan, graph_note = None, None
+    if use_graph:
+        try:
+            plan = RbgsPlan(W, theta, cfg, dc)
+        except Exception as exc:  # capture unsupported here: eager, and say so
+            graph_note = f"graph capture failed ({type(exc).__name__}: {exc}); eager"
+            plan = None
 
     def step():
         return plan.replay() if plan is not None else rbgs(W, theta, cfg, dc)
@@ -317,6 +324,8 @@ def gpu_arm(args, cfgd):
         torch.cuda.synchronize()
 
     # --- timed region: K factorizations, W resident in HBM ---
+    comm_obj = dc.comm
+    coll0 = comm_obj.collectives if comm_obj is not None else 0
     n0 = _lib.launch_count()
     timer = None
     with Clocks(local) as clk, (D.timed_kernels() if plan is None else _nullctx()) as timer:
@@ -351,6 +360,7 @@ def gpu_arm(args, cfgd):
         # instrumented step outside the timed region
         barrier()
         n1 = _lib.launch_count()
+        coll0 = comm_obj.collectives if comm_obj is not None else 0
         with D.timed_kernels() as timer:
             rbgs(W, theta, cfg, dc)
             torch.cuda.synchronize()
@@ -362,6 +372,9 @@ def gpu_arm(args, cfgd):
         ms = float(t.item())
     ksum = timer.summary()
     kscale = ksteps  # kernel records cover this many steps
+    coll_per_block = None
+    if comm_obj is not None and comm_obj.active:
+        coll_per_block = (comm_obj.collectives - coll0) / (ksteps * cfg.partition.num_blocks)
     cert = f.cert
     wbytes = esz * n * m
     value = wbytes / (ms * 1e-3) / 1e9
@@ -467,7 +480,9 @@ def gpu_arm(args, cfgd):
             "config": {"workload": cfgd["desc"], "n": n, "m": m, "p": p, "k": k, "sketch": cfgd["kind"],
                        "interblock": "sketched_cholqr(1)", "ls_solver": "richardson(5)",
                        "projection_order": args.order, "parallelism": f"rows{world}",
-                       "execution": "cuda-graph replay (RbgsPlan)" if plan is not None else "eager rbgs()",
+                       "execution": ("cuda-graph replay (RbgsPlan)" if plan is not None
+                                     else (graph_note or "eager rbgs()")),
+                       "collectives_per_block": coll_per_block,
                        "kernel_timing": ("one instrumented eager step after the timed region"
                                          if plan is not None else "CUDA events inside the timed region"),
                        "l2": "inputs larger than L2 (W = %.1f GB)" % (wbytes / 1e9)},

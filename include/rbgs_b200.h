@@ -231,6 +231,16 @@ int rb_sketched_cholqr_small(int k, int p, const double* Sp, int64_t lds, double
                              int64_t ldr, double* Sout, int64_t ldso, int* info,
                              void* ws, size_t ws_bytes, void* stream);
 
+/* l2_plus_cholqr without a host branch (rbgs.py:293-302): given both
+ * outcomes of the Gram stage -- (A) R_a, S_a from R' = chol(Q'^T Q') and the
+ * sketched CholQR of Q' R'^{-1}, (B) R_b, S_b from the one-pass sketched
+ * CholQR of Q' -- keep A when *info_sel == 0 (R' existed), else B: R (p x p),
+ * S (k x p) and *info_out = the kept path's Cholesky info.              */
+int rb_l2_select(int k, int p, const int* info_sel, const int* info_a, const int* info_b,
+                 const double* Ra, int64_t ldra, const double* Sa, int64_t ldsa,
+                 const double* Rb, int64_t ldrb, const double* Sb, int64_t ldsb,
+                 double* R, int64_t ldr, double* S, int64_t lds, int* info_out, void* stream);
+
 /* ---- K10  operator: 7-point Dirichlet Laplacian (C4, krylov.py:129-130) --
  * Y = A X on an nx*ny*nz_local slab (x fastest) of the global grid; halo
  * planes (nx*ny rows each, NULL = Dirichlet boundary) supply the z

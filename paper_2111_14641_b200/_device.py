@@ -313,6 +313,12 @@ def certify_sums(S, P, R, out):
     call("rb_certify", k, m, ptr(S), ld(S), ptr(P), ld(P), ptr(R), ld(R), ptr(out), ws, wsb, st(S.device))
 
 
+def l2_select(info_sel, info_a, info_b, Ra, Sa, Rb, Sb, R, S, info_out):
+    k, p = S.shape
+    call("rb_l2_select", k, p, ptr(info_sel), ptr(info_a), ptr(info_b), ptr(Ra), ld(Ra), ptr(Sa), ld(Sa), ptr(Rb),
+         ld(Rb), ptr(Sb), ld(Sb), ptr(R), ld(R), ptr(S), ld(S), ptr(info_out), st(S.device))
+
+
 def sketched_cholqr_small(Sp, R, Sout, info):
     k, p = Sp.shape
     ws, wsb = _ws(k, p, k, Sp.device)

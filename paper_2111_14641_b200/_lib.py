@@ -47,6 +47,7 @@ SIGNATURES = {
     "rb_gemm_f64": [_i, _i, _i, _i, _i, _d, _p, _i64, _p, _i64, _d, _p, _i64, _p, _sz, _p],
     "rb_gemm_f32": [_i, _i, _i, _i, _i, _f, _p, _i64, _p, _i64, _f, _p, _i64, _p, _sz, _p],
     "rb_certify": [_i, _i, _p, _i64, _p, _i64, _p, _i64, _p, _p, _sz, _p],
+    "rb_l2_select": [_i, _i, _p, _p, _p, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, _p],
     "rb_sumsq3": [_i64, _i, _p, _i64, _i64, _i, _p, _i64, _i64, _i, _p, _i64, _p, _p, _sz, _p],
     "rb_syrk_f64": [_i, _i64, _d, _p, _i64, _d, _p, _i64, _p, _sz, _p],
     "rb_cross": [_i, _i, _i64, _i, _i, _p, _i64, _p, _i64, _p, _i64, _i, _p, _sz, _p],

@@ -72,6 +72,8 @@ int gemm_f32(int, int, int, int, int, float, const float*, int64_t, const float*
 int certify(int, int, const double*, int64_t, const double*, int64_t, const double*, int64_t, double*, void*, size_t,
             cudaStream_t);
 size_t kdim_ws_bytes(int k, int m);
+int l2_select(int, int, const int*, const int*, const int*, const double*, int64_t, const double*, int64_t,
+              const double*, int64_t, const double*, int64_t, double*, int64_t, double*, int64_t, int*, cudaStream_t);
 int potrf_upper(int, const double*, int64_t, double*, int64_t, int*, cudaStream_t);
 int trsm_left_upper(int, int, const double*, int64_t, double*, int64_t, int*, cudaStream_t);
 int geqrf_small(int, int, double*, int64_t, double*, int64_t, void*, size_t, cudaStream_t);
@@ -177,6 +179,13 @@ int rb_trsm_right(int ind, int outd, int64_t n, int p, const void* B, int64_t ld
 int rb_gemm_f32(int tA, int tB, int m, int n, int k, float alpha, const float* A, int64_t lda, const float* B,
                 int64_t ldb, float beta, float* C, int64_t ldc, void* ws, size_t wsb, void* s) {
   return rb::gemm_f32(tA, tB, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc, ws, wsb, as_stream(s));
+}
+
+int rb_l2_select(int k, int p, const int* info_sel, const int* info_a, const int* info_b, const double* Ra,
+                 int64_t ldra, const double* Sa, int64_t ldsa, const double* Rb, int64_t ldrb, const double* Sb,
+                 int64_t ldsb, double* R, int64_t ldr, double* S, int64_t lds, int* info_out, void* s) {
+  return rb::l2_select(k, p, info_sel, info_a, info_b, Ra, ldra, Sa, ldsa, Rb, ldrb, Sb, ldsb, R, ldr, S, lds,
+                       info_out, as_stream(s));
 }
 
 int rb_certify(int k, int m, const double* S, int64_t lds, const double* P, int64_t ldp, const double* R,

@@ -1033,6 +1033,44 @@ int certify(int k, int m, const double* S, int64_t lds, const double* P, int64_t
   return coop_launch(certify_coop, tile_smem<64>(), args, st, max_grid, &grid, "rb_certify");
 }
 
+// l2_plus_cholqr without a host branch (rbgs.py:293-302): both outcomes of
+// the Gram stage are computed on the device -- (A) R' = chol(Q'^T Q') then
+// the sketched CholQR of Q' R'^{-1}, (B) the one-pass sketched CholQR of Q'
+// (the same R_ii in exact arithmetic, used when Q'^T Q' is numerically
+// indefinite) -- and this kernel keeps A when info[0] == 0, else B, writing
+// the chosen R_ii, S_i and status word (info[1] = the chosen path's
+// Cholesky info; info[0] is only the selector).
+__global__ void l2_select_kernel(int k, int p, const int* __restrict__ info_sel, const int* __restrict__ info_a,
+                                 const int* __restrict__ info_b, const double* __restrict__ Ra, int64_t ldra,
+                                 const double* __restrict__ Sa, int64_t ldsa, const double* __restrict__ Rb,
+                                 int64_t ldrb, const double* __restrict__ Sb, int64_t ldsb, double* __restrict__ R,
+                                 int64_t ldr, double* __restrict__ S, int64_t lds, int* __restrict__ info_out) {
+  const bool a = *info_sel == 0;
+  const int64_t tot = (int64_t)k * p + (int64_t)p * p;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+    if (e < (int64_t)k * p) {
+      const int r = (int)(e % k), j = (int)(e / k);
+      S[r + j * lds] = a ? Sa[r + j * ldsa] : Sb[r + j * ldsb];
+    } else {
+      const int64_t f = e - (int64_t)k * p;
+      const int i = (int)(f % p), j = (int)(f / p);
+      R[i + j * ldr] = a ? Ra[i + j * ldra] : Rb[i + j * ldrb];
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *info_out = a ? *info_a : *info_b;
+}
+
+int l2_select(int k, int p, const int* info_sel, const int* info_a, const int* info_b, const double* Ra, int64_t ldra,
+              const double* Sa, int64_t ldsa, const double* Rb, int64_t ldrb, const double* Sb, int64_t ldsb, double* R,
+              int64_t ldr, double* S, int64_t lds, int* info_out, cudaStream_t st) {
+  RB_REQUIRE(k >= 1 && p >= 1 && info_sel && info_a && info_b && Ra && Sa && Rb && Sb && R && S && info_out,
+             "rb_l2_select: bad args");
+  const int64_t tot = (int64_t)k * p + (int64_t)p * p;
+  RB_KLAUNCH l2_select_kernel<<<(int)std::min<int64_t>(ceil_div(tot, 256), 2 * sm_count()), 256, 0, st>>>(
+      k, p, info_sel, info_a, info_b, Ra, ldra, Sa, ldsa, Rb, ldrb, Sb, ldsb, R, ldr, S, lds, info_out);
+  return check_launch("rb_l2_select");
+}
+
 int gemm_f64(int tA, int tB, int m, int n, int k, double alpha, const double* A, int64_t lda, const double* B,
              int64_t ldb, double beta, double* C, int64_t ldc, void* ws, size_t wsb, cudaStream_t st) {
   RB_REQUIRE(m >= 0 && n >= 0 && k >= 0 && C && ldc >= std::max(m, 1) && tB == 0 &&

@@ -190,10 +190,14 @@ class _Scratch:
         self.Rt = D.empty_cm(w, w, f64, device)
         self.Pr = D.empty_cm(k, w, f64, device)  # binary32-rounded P_i (fine = COARSE)
         self.P32 = D.empty_cm(k, w, torch.float32, device)
+        self.Rb = D.empty_cm(w, w, f64, device)  # l2 stage, fallback path
+        self.Sb = D.empty_cm(k, w, f64, device)
         self.norms = torch.zeros(8, dtype=f64, device=device)  # [w2, q2, fin, ...]
-        self.info = torch.zeros(8, dtype=torch.int32, device=device)
+        # status words: [0..3] checked per block (Cholesky infos), [6..7]
+        # solver / RGS, [8..10] the l2 stage's two paths (selector, A, B)
+        self.info = torch.zeros(16, dtype=torch.int32, device=device)
         self.status_host = torch.zeros(8, dtype=f64).pin_memory()
-        self.info_host = torch.zeros(8, dtype=torch.int32).pin_memory()
+        self.info_host = torch.zeros(16, dtype=torch.int32).pin_memory()
 
 
 # ---------------------------------------------------------------------------
@@ -536,22 +540,28 @@ class RbgsSweep:
                 self._sketch(Qp, Sp)
                 self._reduce(G, Sp)
         sp_qp = Sp.clone() if self.cfg.certify_blocks else None
+        # No host branch (deferrable, graph-capturable): both outcomes of the
+        # Gram stage run on the device and rb_l2_select keeps one.
+        #  (A) R' = chol(Q'^T Q'), S* = Sp R'^{-1}, R'' = chol(S*^T S*),
+        #      R_ii = R'' R', S_i = S* R''^{-1}
+        #  (B) Q' too ill-conditioned for the Gram (info != 0): the one-pass
+        #      sketched CholQR of Q' -- the same R_ii in exact arithmetic.
+        info = scr.info
         R1 = scr.R1[:w, :w]
-        D.potrf(G, R1, scr.info[0:1])
-        torch.cuda.current_stream(self.device).synchronize()
-        if int(scr.info[0]) != 0:
-            # Q' too ill-conditioned for the Gram stage: the sketched CholQR
-            # of Q' computes the same R_ii in exact arithmetic.
-            return self._one_pass_from_sketch(Qp, Sp, slot, sp_qp)
+        D.potrf(G, R1, info[8:9])
         Ss = scr.Ss[:, :w]
         D.trsm_right(Sp, R1, Ss)
-        G2 = scr.G[:w, :w]
-        D.gemm(1, 0, 1.0, Ss, Ss, 0.0, G2)
         R2 = scr.R2[:w, :w]
-        D.potrf(G2, R2, scr.info[1:2])
+        Sa = scr.T[:, :w]
+        D.sketched_cholqr_small(Ss, R2, Sa, info[9:10])
+        Ra = scr.G[:w, :w]  # (G is consumed)
+        D.gemm(0, 0, 1.0, R2, R1, 0.0, Ra)
+        Rb = scr.Rb[:w, :w]
+        Sb = scr.Sb[:, :w]
+        D.sketched_cholqr_small(Sp, Rb, Sb, info[10:11])
         Rt = scr.Rt[:w, :w]
-        D.gemm(0, 0, 1.0, R2, R1, 0.0, Rt)
         Si = scr.Si[:, :w]
+        D.l2_select(info[8:9], info[9:10], info[10:11], Ra, Sa, Rb, Sb, Rt, Si, info[1:2])
         if self.cfg.resketch:
             q64 = self._tmp(w)
             D.trsm_right(Qp, Rt, q64)
@@ -559,26 +569,6 @@ class RbgsSweep:
             D.convert(q64, slot)
         else:
             D.trsm_right(Qp, Rt, slot)
-            D.trsm_right(Ss, R2, Si)
-        return Rt, Si, sp_qp
-
-    def _one_pass_from_sketch(self, Qp, Sp, slot, sp_qp):
-        scr = self._scr
-        w = Qp.shape[1]
-        G = scr.G[:w, :w]
-        D.gemm(1, 0, 1.0, Sp, Sp, 0.0, G)
-        Rt = scr.Rt[:w, :w]
-        scr.info[0:2].zero_()
-        D.potrf(G, Rt, scr.info[1:2])
-        Si = scr.Si[:, :w]
-        if self.cfg.resketch:
-            q64 = self._tmp(w)
-            D.trsm_right(Qp, Rt, q64)
-            self._sketch_reduce(q64, Si)
-            D.convert(q64, slot)
-        else:
-            D.trsm_right(Qp, Rt, slot)
-            D.trsm_right(Sp, Rt, Si)
         return Rt, Si, sp_qp
 
     def _interblock_rgs(self, Qp, slot):
@@ -892,7 +882,7 @@ class RbgsSweep:
         without data-dependent host branches)."""
         B = len(self.offsets) - 1
         self._deferred = (torch.zeros(B, 8, dtype=torch.float64, device=self.device),
-                          torch.zeros(B, 8, dtype=torch.int32, device=self.device))
+                          torch.zeros(B, 16, dtype=torch.int32, device=self.device))
 
     def _deferred_ok(self) -> bool:
         """One host read of every block's status words; True when no block
@@ -955,9 +945,9 @@ _SIDE_STREAMS = {}
 
 def _deferrable(cfg) -> bool:
     """Inter-block variants whose block step has no data-dependent host
-    branch (the l2 stage falls back on a Cholesky failure; RGS reads its
-    column norms), and no per-block certificate read."""
-    return parse_method(cfg.interblock)[0] == "sketched_cholqr" and not cfg.certify_blocks
+    branch (RGS reads its column norms; the l2 stage selects its fallback on
+    the device), and no per-block certificate read."""
+    return parse_method(cfg.interblock)[0] in ("sketched_cholqr", "l2_plus_cholqr") and not cfg.certify_blocks
 
 
 def _sweep_blocks(Wd, n, theta, cfg, dc, q_storage, deferred, events=None):
@@ -1008,7 +998,8 @@ class RbgsPlan:
                 and W.dtype in (torch.float32, torch.float64)):
             raise ShapeError("RbgsPlan needs W as a column-major binary32/binary64 CUDA tensor")
         if not _deferrable(cfg):
-            raise ValueError("RbgsPlan needs a sketched_cholqr inter-block variant without certify_blocks")
+            raise ValueError("RbgsPlan needs a sketched_cholqr / l2_plus_cholqr inter-block variant without "
+                             "certify_blocks")
         if dc.overwrite_w:
             raise ValueError("RbgsPlan cannot overwrite its own input")
         if cfg.partition.total_cols != W.shape[1]:
