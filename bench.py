@@ -286,7 +286,7 @@ def gpu_arm(args, cfgd):
     else:
         theta = sketching.SketchOperator(cfgd["kind"], k, n, SEED_THETA)
         theta.device_tables(dev)
-    cfg = RbgsConfig(partition=BlockPartition.uniform(m, p), interblock="sketched_cholqr(1)",
+    cfg = RbgsConfig(partition=BlockPartition.uniform(m, p), interblock=args.interblock,
                      coarse=COARSE if cfgd["coarse"] == "coarse" else FINE)
     dc = DeviceConfig(device=dev, projection_order=args.order, comm=Comm(group) if group else None,
                       shard=shard if world > 1 else None, overwrite_w=inplace)
@@ -478,7 +478,7 @@ def gpu_arm(args, cfgd):
             "scaling": "weak", "vs_baseline": None,
             "dtype": "f32-coarse/f64-fine" if cfgd["coarse"] == "coarse" else "f64", "data": "synthetic",
             "config": {"workload": cfgd["desc"], "n": n, "m": m, "p": p, "k": k, "sketch": cfgd["kind"],
-                       "interblock": "sketched_cholqr(1)", "ls_solver": "richardson(5)",
+                       "interblock": args.interblock, "ls_solver": "richardson(5)",
                        "projection_order": args.order, "parallelism": f"rows{world}",
                        "execution": ("cuda-graph replay (RbgsPlan)" if plan is not None
                                      else (graph_note or "eager rbgs()")),
@@ -583,7 +583,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--order", default="reference", choices=["reference", "fma"])
+    ap.add_argument("--order", default=None, choices=["reference", "fma", "tc"],
+                    help="Step-3 order (default: the config's own, see CONFIGS 'order')")
+    ap.add_argument("--interblock", default="sketched_cholqr(1)",
+                    help="inter-block QR (reference default: l2_plus_cholqr; one sketch pass: sketched_cholqr(1))")
     ap.add_argument("--sample-rows", type=int, default=None,
                     help="rows of the CPU sample (default 4096 reference arm, 8192 cpu_baseline)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -591,6 +594,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="eager rbgs() per step instead of a captured RbgsPlan")
     args = ap.parse_args()
     cfgd = CONFIGS[args.config]
+    if args.order is None:
+        args.order = cfgd.get("order", "reference")
     if args.impl == "reference":
         reference_arm(args, cfgd)
     elif cfgd.get("krylov"):

@@ -55,6 +55,10 @@ extern "C" {
                                         FMUL + FADD instead of the packed
                                         FFMA2(-0) + FADD2 pair: same bits,
                                         the cross-check of the packed form */
+#define RB_ORDER_TC 3         /* tensor pipe: Q X as three tcgen05 kind::tf32
+                                 products of the hi/lo split operands
+                                 (3xTF32, fp32 accumulation), binary32-level
+                                 accuracy, HBM-bound; not the reference order */
 
 const char* rb_version(void);
 const char* rb_last_error(void);

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(HERE, "librbgs_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "rbgs_b200.h")
 
 F32, F64 = 0, 1
-ORDER_REFERENCE, ORDER_FMA, ORDER_REFERENCE_SCALAR = 0, 1, 2
+ORDER_REFERENCE, ORDER_FMA, ORDER_REFERENCE_SCALAR, ORDER_TC = 0, 1, 2, 3
 
 _i, _i64, _u64, _sz, _d = ctypes.c_int, ctypes.c_int64, ctypes.c_uint64, ctypes.c_size_t, ctypes.c_double
 _f = ctypes.c_float

@@ -15,7 +15,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librbgs_b200.so")
-SOURCES = ["capi.cu", "project.cu", "sketch.cu", "sketch_tc.cu", "small.cu", "stencil.cu", "kdim.cu"]
+SOURCES = ["capi.cu", "project.cu", "sketch.cu", "sketch_tc.cu", "small.cu", "stencil.cu", "kdim.cu", "project_tc.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-O3", "--expt-relaxed-constexpr"]

@@ -647,8 +647,29 @@ int grid_rows(int mode, int p, bool ff) {
 }  // namespace
 
 int trsm_right(int, int, int64_t, int, const void*, int64_t, const double*, int64_t, void*, int64_t, cudaStream_t);
+int project_tc_launch(int w_dtype, int64_t n, int c, int p, const float* Q, int64_t ldq, const double* X,
+                      int64_t ldx, const void* W, int64_t ldw, float* Qp, int64_t ldqp, double* norms2, void* ws,
+                      size_t wsb, cudaStream_t st, double* partial_out, int* grid_out);
+size_t project_tc_ws_bytes(int c, int p);
 
 namespace {
+// norms2 = (sum of the tensor-core kernel's CTA pairs) + (the tail call's pair)
+__global__ void sum_pairs_plus(const double* __restrict__ partial, int count, const double* __restrict__ extra,
+                               double* __restrict__ out) {
+  __shared__ double red[kThreads / 32];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    a += partial[2 * i];
+    b += partial[2 * i + 1];
+  }
+  const double sa = block_sum(a, red);
+  const double sb = block_sum(b, red);
+  if (threadIdx.x == 0) {
+    out[0] = sa + (extra ? extra[0] : 0.0);
+    out[1] = sb + (extra ? extra[1] : 0.0);
+  }
+}
+
 int project_impl(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t n, int c, int p, const void* Q,
                  int64_t ldq, const double* X, int64_t ldx, const void* W, int64_t ldw, void* Qp, int64_t ldqp,
                  double* norms2, void* ws, size_t ws_bytes, cudaStream_t st, const FusedTrsm& fz);
@@ -707,8 +728,38 @@ int project_impl(int q_dtype, int w_dtype, int compute_dtype, int order, int64_t
              (long long)n, c, p);
   RB_REQUIRE(c == 0 || (Q && ldq >= n && X && ldx >= c), "rb_project: bad Q/X");
   RB_REQUIRE(W && ldw >= n && Qp && ldqp >= n, "rb_project: bad W/Qp");
-  RB_REQUIRE(order == RB_ORDER_REFERENCE || order == RB_ORDER_FMA || order == RB_ORDER_REFERENCE_SCALAR,
+  RB_REQUIRE(order == RB_ORDER_REFERENCE || order == RB_ORDER_FMA || order == RB_ORDER_REFERENCE_SCALAR ||
+                 order == RB_ORDER_TC,
              "rb_project: bad order %d", order);
+  if (order == RB_ORDER_TC) {
+    // tensor pipe, 3xTF32 (project_tc.cu): binary32 Q with 16-B aligned
+    // columns; rows past the last whole 128-row tile and every other
+    // layout take the FMA order on the CUDA cores
+    const bool ok = compute_dtype == RB_F32 && q_dtype == RB_F32 && c > 0 && (uintptr_t)Q % 16 == 0 &&
+                    ldq % 4 == 0 && fz.pf == 0 && n >= 128;
+    if (!ok)
+      return project_impl(q_dtype, w_dtype, compute_dtype, RB_ORDER_FMA, n, c, p, Q, ldq, X, ldx, W, ldw, Qp, ldqp,
+                          norms2, ws, ws_bytes, st, fz);
+    const int64_t nt = n / 128 * 128;
+    const size_t tcb = (project_tc_ws_bytes(c, p) + 255) / 256 * 256;
+    RB_REQUIRE(ws && ws_bytes >= tcb + 256 && (uintptr_t)ws % 256 == 0, "rb_project (tc): workspace too small");
+    int grid = 0;
+    int rc = project_tc_launch(w_dtype, nt, c, p, (const float*)Q, ldq, X, ldx, W, ldw, (float*)Qp, ldqp, norms2, ws,
+                               tcb, st, nullptr, &grid);
+    if (rc != RB_OK) return rc;
+    double* tailn = norms2 ? (double*)((char*)ws + tcb) : nullptr;  // 2 doubles
+    if (nt < n) {
+      const size_t esw = w_dtype == RB_F32 ? 4 : 8;
+      rc = project_impl(q_dtype, w_dtype, compute_dtype, RB_ORDER_FMA, n - nt, c, p, (const float*)Q + nt, ldq, X,
+                        ldx, (const char*)W + nt * esw, ldw, (float*)Qp + nt, ldqp, tailn,
+                        (char*)ws + tcb + 256, ws_bytes - tcb - 256, st, fz);
+      if (rc != RB_OK) return rc;
+    } else if (tailn) {
+      cudaMemsetAsync(tailn, 0, 2 * sizeof(double), st);
+    }
+    if (norms2) RB_KLAUNCH sum_pairs_plus<<<1, kThreads, 0, st>>>((const double*)ws, grid, tailn, norms2);
+    return check_launch("rb_project (tc)");
+  }
   const int mode = compute_dtype == RB_F64 ? 2 : (order == RB_ORDER_FMA ? 1 : 0);
   const bool scalar = order == RB_ORDER_REFERENCE_SCALAR;
   const bool q32 = q_dtype == RB_F32, w32 = w_dtype == RB_F32;

@@ -41,7 +41,7 @@ import torch
 
 from . import _device as D
 from . import sketching
-from ._lib import F32, F64, ORDER_FMA, ORDER_REFERENCE, require_cuda
+from ._lib import F32, F64, ORDER_FMA, ORDER_REFERENCE, ORDER_TC, require_cuda
 from .comm import Comm, RowShard
 from .errors import (
     CertificationError,
@@ -112,8 +112,12 @@ class DeviceConfig:
     q_dtype           storage of Q (default binary32 when cfg.coarse is
                       COARSE, else binary64); binary64 keeps the reference's
                       fp64 Q (e.g. for Arnoldi, whose operator reads fp64 Q).
-    projection_order  "reference" (bit-identical Step 3) or "fma" (fused
-                      multiply-subtract, faster, not bit-identical).
+    projection_order  "reference" (bit-identical Step 3), "fma" (fused
+                      multiply-subtract on the CUDA cores) or "tc" (tensor
+                      pipe, 3xTF32: HBM-bound); the last two are faster and
+                      not bit-identical -- for inputs whose R is insensitive
+                      to the Step-3 rounding order (bench.py gates them on
+                      the measured oracle drift).
     comm / shard      row sharding: this rank's rows and the group that owns
                       the other shards (comm.py).  Default: all rows here.
     overwrite_w       one-shot rbgs() only: Q is written over W's own device
@@ -364,9 +368,9 @@ class RbgsSweep:
         self.offsets = cfg.partition.offsets()
         self.compute = F32 if cfg.coarse.format == "coarse" else F64
         self.q_dtype = dc.q_dtype or (torch.float32 if self.compute == F32 else torch.float64)
-        if dc.projection_order not in ("reference", "fma"):
-            raise ValueError("projection_order must be 'reference' or 'fma'")
-        self.order = ORDER_FMA if dc.projection_order == "fma" else ORDER_REFERENCE
+        if dc.projection_order not in ("reference", "fma", "tc"):
+            raise ValueError("projection_order must be 'reference', 'fma' or 'tc'")
+        self.order = {"fma": ORDER_FMA, "tc": ORDER_TC}.get(dc.projection_order, ORDER_REFERENCE)
         dev = self.device
         k = theta.k
         if _q_storage is not None:  # Q over W's storage (DeviceConfig.overwrite_w)

@@ -125,11 +125,39 @@ def test_trsm_right_tail_columns_at_scale(D, p, dt):
     assert np.abs(want[:4096].astype(np.float64) - ref).max() <= 1e-6 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("n,c,p", [((1 << 18) + 77, 960, 64), (1 << 18, 64, 64), (1 << 17, 480, 32),
+                                   ((1 << 17) + 5, 200, 40), (4096, 12, 4), (100, 30, 8)])
+def test_project_tensor_pipe_3xtf32_accuracy(D, n, c, p):
+    """RB_ORDER_TC: Q X from three tcgen05 kind::tf32 products of the split
+    operands, fp32 accumulation.  Not the reference order; bound: the exact
+    W - fl32(Q) fl32(X) within (c 2^-21 + 2^-23) (|Q| |X| + |W|)."""
+    g = np.random.Generator(np.random.Philox(500 + c + p))
+    Q = g.standard_normal((n, c), dtype=np.float32)
+    X = g.standard_normal((c, p)) * 0.1
+    W = g.standard_normal((n, p), dtype=np.float32)
+    Qd = D.empty_cm(n, c, torch.float32, "cuda")
+    Qd.copy_(torch.from_numpy(Q))
+    out = D.empty_cm(n, p, torch.float32, "cuda")
+    norms = torch.zeros(2, dtype=torch.float64, device="cuda")
+    D.project(Qd, _dev(X, torch.float64), _dev(W, torch.float32), out, 0, 3, norms)
+    X32 = X.astype(np.float32).astype(np.float64)
+    Q64 = Q.astype(np.float64)
+    exact = W.astype(np.float64) - Q64 @ X32
+    bound = (c * 2.0 ** -21 + 2.0 ** -23) * (np.abs(Q64) @ np.abs(X32) + np.abs(W.astype(np.float64)))
+    got = out.cpu().numpy().astype(np.float64)
+    assert np.all(np.abs(got - exact) <= bound), float(np.max(np.abs(got - exact) / bound))
+    nw, nq = norms.cpu().numpy()
+    assert math.isclose(nw, float(np.sum(W.astype(np.float64) ** 2)), rel_tol=1e-12)
+    assert math.isclose(nq, float(np.sum(got ** 2)), rel_tol=1e-12)
+
+
 # ---------------------------------------------------------------------------
 # config families (BASELINE.json configs[0..4]) vs the CPU oracle
 
 
 def _sweep_pair(W, op_dev, op_orc, m, p, coarse, interblock="sketched_cholqr(1)", dc=None):
+    """Device sweep vs oracle sweep on the same W and operator (the device
+    Step-3 order from dc; the oracle always runs the reference order)."""
     from paper_2111_14641_b200.kernels import COARSE, FINE, BlockPartition
     from paper_2111_14641_b200.rbgs import RbgsConfig, rbgs
 
@@ -253,3 +281,19 @@ def test_c4_block_gmres_poisson_48_vs_oracle(D):
     assert np.allclose(h[:, 1], ho[:, 1], rtol=1e-3), np.max(np.abs(h[:, 1] / ho[:, 1] - 1))
     x, xo = rep.solution.data, orc["solution"]
     assert np.linalg.norm(x - xo) <= 1e-5 * np.linalg.norm(xo)
+
+
+def test_c5_family_tensor_pipe_projection_vs_oracle(D):
+    """The C5 family with Step 3 on the tensor pipe (3xTF32, RB_ORDER_TC): the
+    order differs from the reference's, so R is checked against the
+    oracle's reference-order R at the bench's gate, 1e-6 (well inside the
+    north star's 1e-5); the certificates of the same order."""
+    from paper_2111_14641_b200 import sketching, workloads
+    from paper_2111_14641_b200.rbgs import DeviceConfig
+
+    n, m, p, k = 32768, 1024, 64, 2048
+    W = workloads.colscaled_host(n, m, 7)
+    r = _sweep_pair(W, sketching.gaussian_operator(k, n, 11), osk.materialize(osk.OracleSketch("gaussian", k, n, 11)),
+                    m, p, "coarse", dc=DeviceConfig(projection_order="tc"))
+    assert r["rel_R"] <= 1e-6, r
+    assert _same_order(r["delta"][0], r["delta"][1], 1.5) and _same_order(r["condQ"][0], r["condQ"][1], 1.1)
