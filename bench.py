@@ -527,7 +527,8 @@ def gpu_arm_krylov(args, cfgd):
     cfg = RbgsConfig()
 
     def step():
-        return krylov.block_gmres(A, B, theta, p, restarts=1, cfg=cfg, device_cfg=dc)
+        return krylov.block_gmres(A, B, theta, p, restarts=1, cfg=cfg, device_cfg=dc,
+                                  diagnostics=args.diagnostics)
 
     for _ in range(args.warmup):
         rep = step()
@@ -564,7 +565,7 @@ def gpu_arm_krylov(args, cfgd):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32-coarse/f64-fine", "data": "synthetic",
             "config": {"workload": cfgd["desc"], "n": n, "m": cfgd["m"], "p_blocks": p, "block_width": mp,
-                       "k": k, "sketch": "sparse_sign(8)", "restarts": 1, "parallelism": f"zslab{world}",
+                       "k": k, "sketch": "sparse_sign(8)", "restarts": 1, "diagnostics": args.diagnostics, "parallelism": f"zslab{world}",
                        "l2": "inputs larger than L2 (basis = %.1f GB)" % (wbytes / 1e9)},
             "rel_residual": rep.residual_history[-1][1], "iterations": len(rep.residual_history),
             "basis_cond_last": rep.basis_cond_history[-1], "cert_last": list(rep.cert_history[-1]),
@@ -589,6 +590,8 @@ def main():
                     help="inter-block QR (reference default: l2_plus_cholqr; one sketch pass: sketched_cholqr(1))")
     ap.add_argument("--sample-rows", type=int, default=None,
                     help="rows of the CPU sample (default 4096 reference arm, 8192 cpu_baseline)")
+    ap.add_argument("--diagnostics", default="full", choices=["full", "sketched"],
+                    help="c4: per-iterate GMRES diagnostics (full = the reference's, krylov.py:247-257)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="eager rbgs() per step instead of a captured RbgsPlan")

@@ -174,13 +174,80 @@ def _cond2_dev(Q, comm):
     return float(math.sqrt(ev[-1] / ev[0]))
 
 
+def _sketched_history(A, X, Bd, bn, sweep, cands, Hf, Rf, mp, c, bk, comm, history, conds, certs, pair, it,
+                      colsq):
+    """diagnostics="sketched": histories from k-dimensional data; one
+    n-dimensional correction and one true residual per cycle (the last
+    candidate: the sketched residual is non-increasing in j)."""
+    dev = Bd.device
+    k = sweep.S.shape[0]
+    # sketched residuals of the nested problems: ||R_first - H Z_j|| per column
+    est = []
+    for t, (w, Z, rows) in enumerate(cands):
+        if bk and t == len(cands) - 1:
+            # breakdown candidate (krylov.py:258-268): || P_1 - [P_2.. | pending] Z ||
+            PA = D.empty_cm(k, c, torch.float64, dev)
+            PA[:, :c - mp].copy_(sweep.P[:, mp:c])
+            PA[:, c - mp:].copy_(sweep.pending_P.tensor)
+            Rk = D.empty_cm(k, mp, torch.float64, dev)
+            Rk.copy_(sweep.P[:, :mp])
+            D.gemm(0, 0, -1.0, PA, Z, 1.0, Rk)
+        else:
+            Rk = D.empty_cm(rows, mp, torch.float64, dev)
+            Rk.copy_(Rf[:rows])
+            Hj = D.empty_cm(rows, w, torch.float64, dev)
+            Hj.copy_(Hf[:rows, :w])
+            D.gemm(0, 0, -1.0, Hj, Z, 1.0, Rk)
+        est.append((Rk * Rk).sum(0).sqrt())
+    rels = (torch.stack(est) / bn).amax(1).cpu().tolist()
+    # cond(S[:, :rows]) brackets cond(Q[:, :rows]) (epsilon-embedding); one
+    # k-dimensional Gram, leading principal blocks on the host
+    rmax = max(r for _, _, r in cands)
+    G = D.empty_cm(rmax, rmax, torch.float64, dev)
+    Sc = D.empty_cm(k, rmax, torch.float64, dev)
+    Sc.copy_(sweep.S[:, :rmax])
+    D.gemm(1, 0, 1.0, Sc, Sc, 0.0, G)
+    Gh = G.cpu().numpy()
+    Gh = np.triu(Gh) + np.triu(Gh, 1).T
+    # the last candidate in n dimensions, with its true residual
+    w, Z, _ = cands[-1]
+    U = D.empty_cm(Bd.shape[0], mp, torch.float64, dev)
+    Zc = D.empty_cm(w, mp, torch.float64, dev)
+    Zc.copy_(Z)
+    D.gemm(0, 0, 1.0, sweep.Q[:, :w], Zc, 0.0, U)
+    Rr = Bd - A._apply_dev(D.to_cm(X + U), torch.float64)
+    rels[-1] = float((colsq(Rr).sqrt() / bn).max())
+    for t, (_, _, r) in enumerate(cands):
+        it += 1
+        history.append((it, rels[t]))
+        ev = np.linalg.eigvalsh(Gh[:r, :r])
+        conds.append(float("inf") if ev.size == 0 or ev[0] <= 0.0 else float(math.sqrt(ev[-1] / ev[0])))
+        certs.append(pair)
+    return U, rels[-1], it
+
+
 def block_gmres(A: LinearOperator, B, theta, p: int, restarts: int = 1, cfg=None, tol: float = 0.0,
-                matvec_precision: PrecisionSpec = FINE, device_cfg: DeviceConfig = None) -> KrylovSolveReport:
+                matvec_precision: PrecisionSpec = FINE, device_cfg: DeviceConfig = None,
+                diagnostics: str = "full") -> KrylovSolveReport:
     """Restarted block GMRES over a sketch-orthonormal basis (krylov.py:170-281).
 
     RBGS backend only (the reference's classical backend is a baseline,
     out of scope).  With a sharded DeviceConfig, B, the solution and every
-    operator block hold this rank's rows; residual norms are global."""
+    operator block hold this rank's rows; residual norms are global.
+
+    diagnostics  "full" (default, the reference's histories, krylov.py:247-257:
+                 per inner iterate one n-dimensional correction, one operator
+                 apply for the true residual and the basis condition number);
+                 "sketched": the inner-iterate histories come from k-dimensional
+                 data only -- the residual of iterate j is the sketched one,
+                 ||R_first - H Z_j|| column-wise (= ||Theta r_j|| up to the
+                 certified orthonormality of S; eq. 4.4), the basis
+                 condition that of S[:, :rows] (the epsilon-embedding bracket
+                 of cond(Q)) -- and only the LAST iterate of a cycle is formed
+                 in n dimensions, with ONE true residual; its history entry
+                 is the true value."""
+    if diagnostics not in ("full", "sketched"):
+        raise ValueError(f"unknown diagnostics mode {diagnostics!r}")
     require_cuda()
     dc = _device_cfg(device_cfg, A)
     dev = D.cuda_device(dc.device)
@@ -250,7 +317,10 @@ def block_gmres(A: LinearOperator, B, theta, p: int, restarts: int = 1, cfg=None
                 PA[:, c - mp:].copy_(sweep.pending_P.tensor)
                 cands.append((c, _ls_qr_dev(PA, sweep.P[:, :mp]), c))
             U_best, rel_best = None, None
-            if cands:
+            if cands and diagnostics == "sketched":
+                U_best, rel_best, it = _sketched_history(A, X, Bd, bn, sweep, cands, Hf, Rf, mp, c, bk, comm,
+                                                         history, conds, certs, pair, it, colsq)
+            elif cands:
                 wmax = max(w for w, _, _ in cands)
                 Zb = D.zeros_cm(wmax, mp * len(cands), torch.float64, dev)
                 for t, (w, Z, _) in enumerate(cands):

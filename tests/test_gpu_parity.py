@@ -585,6 +585,33 @@ def test_block_gmres_poisson3d_vs_reference_golden(pkg):
     assert np.allclose(np.array(rep.basis_cond_history), z["p3/conds"], rtol=1e-2)
 
 
+def test_block_gmres_sketched_diagnostics(pkg):
+    """diagnostics="sketched" (the reference's per-iterate
+    diagnostics, krylov.py:247-257, made optional): same solution and final
+    true residual as the full mode; the k-dimensional residual estimates sit
+    inside the epsilon-embedding bracket of the true ones."""
+    rbgs, sketching, D = pkg
+    from paper_2111_14641_b200 import krylov, operators
+
+    z = goldens.load("krylov")
+    nx = int(z["p3/nx"])
+    A = operators.Poisson3D(nx, nx, nx)
+    op = sketching.sparse_sign_operator(72, nx ** 3, 11)
+    cfg = rbgs.RbgsConfig(interblock="sketched_cholqr(1)")
+    full = krylov.block_gmres(A, z["p3/B"], op, 8, restarts=2, cfg=cfg)
+    sk = krylov.block_gmres(A, z["p3/B"], op, 8, restarts=2, cfg=cfg, diagnostics="sketched")
+    assert goldens.rel(sk.solution.data, full.solution.data) <= 1e-12
+    hf, hs = np.array(full.residual_history), np.array(sk.residual_history)
+    assert hf.shape == hs.shape
+    last = [7 * c - 1 for c in (1, 2)]  # the cycle's last iterate carries the true residual
+    assert np.allclose(hs[last, 1], hf[last, 1], rtol=1e-10)
+    assert np.all(hs[:, 1] <= 2.0 * hf[:, 1]) and np.all(hs[:, 1] >= 0.5 * hf[:, 1])
+    cf, cs = np.array(full.basis_cond_history), np.array(sk.basis_cond_history)
+    assert np.all(cs <= 3.0 * cf) and np.all(cs >= cf / 3.0)
+    with pytest.raises(ValueError):
+        krylov.block_gmres(A, z["p3/B"], op, 8, diagnostics="none")
+
+
 def test_sparse_sign_table_path_matches_hashed_path(pkg):
     """The pre-bucketed table (fixed summation order) and the per-row hashing
     path sketch with the same operator; ragged tiles and shards included."""

@@ -18,7 +18,19 @@ KEYS = {
     "dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct_peak",
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_pct_peak",
     "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_active_pct",
-    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active": "fma_pipe_pct",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active": "fma_pipe_inst_pct",
+    # pipe-CYCLE metrics (what "pipe busy" means; inst_executed under-reports packed FFMA2)
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active": "fma_pipe_cycles_pct",
+    "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active": "fmaheavy_pipe_cycles_pct",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_cycles_pct",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pipe_cycles_pct",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active": "alu_pipe_cycles_pct",
+    "sm__cycles_active.avg": "sm_cycles_active_avg",
+    "sm__cycles_elapsed.avg.per_second": "sm_clock_hz",
+    "gpc__cycles_elapsed.avg.per_second": "gpc_clock_hz",
+    "dram__cycles_elapsed.avg.per_second": "dram_clock_hz",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed": "smem_wavefronts_pct",
+    "lts__t_sector_hit_rate.pct": "l2_hit_pct",
     "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
     "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active": "imma_pipe_pct",
     "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
@@ -34,7 +46,9 @@ def main(path, alg=None):
     hdr, units, vals = rows[0], rows[1], rows[2]
     out = {"report": path.split("/")[-1], "kernel": vals[hdr.index("Kernel Name")][:120]}
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-             "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0}
+             "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6, "ms": 1e-3, "s": 1.0,
+             "hz": 1.0, "Khz": 1e3, "Mhz": 1e6, "Ghz": 1e9, "cycle/nsecond": 1e9, "cycle/usecond": 1e6,
+             "cycle/second": 1.0}
     for i, name in enumerate(hdr):
         if name in KEYS:
             v = vals[i].replace(",", "")
