@@ -109,7 +109,10 @@ int rb_gaussian_fill(uint64_t seed, int k, int64_t row0, int64_t nrows,
  * mode 0 = auto (tensor pipe for binary32 X, fp64 CUDA cores for binary64),
  * 1 = fp64 CUDA cores (exact fp64 products), 2 = tensor pipe: tcgen05
  * kind::i8 on the exact byte split of q and of X's per-chunk fixed-point
- * form (sketch_tc.cu).                                                    */
+ * form (sketch_tc.cu), six byte digits of X (2^-47 of each 16384-row
+ * chunk's max: binary64-grade), 3 = the same with the lean CTA, 4 / 5 =
+ * tensor pipe with four / three digits (2^-31 / 2^-23 of the chunk max; 2/3
+ * and 1/2 of the tensor work) for inputs whose R tolerates the rounding.  */
 int rb_sketch_gaussian(int x_dtype, int64_t n, int ncols, const void* X, int64_t ldx,
                        const uint8_t* theta, int64_t ldt, int k, double scale,
                        double* out, int64_t ldo, int accumulate, int mode,

@@ -152,7 +152,7 @@ def project_trsm(Q, X, W, Qp, compute, order, norms2, Qf, Rf):
             2.0 * n * c * p)
 
 
-GAUSS_MODE = {"auto": 0, "fp64": 1, "tensor": 2, "lean": 3}
+GAUSS_MODE = {"auto": 0, "fp64": 1, "tensor": 2, "lean": 3, "tensor4": 4, "tensor3": 5}
 
 
 def sketch_gaussian(X, theta, ldt, k, scale, out, accumulate=False, mode="auto"):

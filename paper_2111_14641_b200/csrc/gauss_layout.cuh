@@ -34,16 +34,22 @@ __host__ __device__ __forceinline__ int64_t q_bytes(int k, int64_t ldt) {
 // requires), and within a K chunk the B rows are ordered
 // [group][plane][column], plane 0 = b5 (weight 2^40) .. plane 5 = b0.
 // A tile kt is kXDig x kBK x NP bytes, [kc][group][plane][col][16 bytes].
-constexpr int kXDig = 6;  // signed byte digits per X entry (46-bit fixed point)
-__host__ __device__ constexpr int np_group(int NP) { return NP <= 40 ? NP : NP == 48 ? 24 : 32; }
+// Digits per X entry: DIG = 6 (46-bit fixed point, binary64-grade sketches:
+// the default), 4 (30 bits) or 3 (22 bits) -- the cheaper forms for inputs
+// whose R tolerates them (the caller's choice, gated by the measured oracle
+// drift; the tensor-pipe work is proportional to DIG).  xi = x 2^(8 DIG - 2 - E).
+constexpr int kXDig = 6;  // the largest digit count (workspace sizing)
+__host__ __device__ constexpr int np_group(int NP, int DIG = kXDig) {
+  return DIG == 6 ? (NP <= 40 ? NP : NP == 48 ? 24 : 32) : NP;  // DIG NG <= 256, % 16 == 0
+}
 
-__host__ __device__ __forceinline__ int64_t x_offset(int plane, int j, int64_t i, int NP) {
+__host__ __device__ __forceinline__ int64_t x_offset(int plane, int j, int64_t i, int NP, int DIG = kXDig) {
   const int64_t kt = i / kBK;
   const int kc = (int)((i % kBK) >> 4), b = (int)(i & 15);
-  const int NG = np_group(NP);
+  const int NG = np_group(NP, DIG);
   const int g = j / NG, jj = j % NG;
-  return kt * (kXDig * (int64_t)kBK * NP) + (int64_t)kc * (kXDig * NP * 16) +
-         (int64_t)((g * kXDig + plane) * NG + jj) * 16 + b;
+  return kt * (DIG * (int64_t)kBK * NP) + (int64_t)kc * (DIG * NP * 16) +
+         (int64_t)((g * DIG + plane) * NG + jj) * 16 + b;
 }
 
 }  // namespace gl

@@ -985,11 +985,15 @@ int sketch_sparse_sign_tab(int xd, int64_t n, int ncols, const void* X, int64_t 
 size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k);
 int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2, int c2,
                        int64_t n, const uint8_t* qt, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
-                       double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st, bool lean = false);
+                       double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st, bool lean = false,
+                       int dig = 6);
 
 // [out1 | out2] = scale * (q @ [X1 | X2]).  mode 0 = auto (tensor pipe when
 // every input is binary32), 1 = fp64 CUDA cores, 2 = tensor pipe, 3 = tensor
-// pipe with the lean CTA (<= 64 columns; made to run beside the projection).
+// pipe with the lean CTA (<= 64 columns; made to run beside the projection),
+// 4 / 5 = tensor pipe with four / three byte digits of X per entry instead
+// of six (fixed-point rounding at 2^(E-31) / 2^(E-23) of each chunk's max
+// instead of 2^(E-47); 2/3 and 1/2 of the tensor work).
 int sketch_gaussian2(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2, int c2,
                      int64_t n, const uint8_t* theta, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
                      double* out2, int64_t ldo2, int acc, int mode, void* ws, size_t wsb, cudaStream_t st) {
@@ -998,7 +1002,8 @@ int sketch_gaussian2(int xd1, const void* X1, int64_t ld1, int c1, int xd2, cons
              "rb_sketch_gaussian: bad args");
   RB_REQUIRE(n == 0 || (X1 && ld1 >= n && (c2 == 0 || (X2 && ld2 >= n)) && theta && ldt >= n),
              "rb_sketch_gaussian: bad X/theta");
-  RB_REQUIRE(mode >= 0 && mode <= 3, "rb_sketch_gaussian: bad mode %d", mode);
+  RB_REQUIRE(mode >= 0 && mode <= 5, "rb_sketch_gaussian: bad mode %d", mode);
+  const int dig = mode == 4 ? 4 : mode == 5 ? 3 : 6;
   if (mode == 3 && c1 + c2 <= 64)
     return sketch_gaussian_tc(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, theta, ldt, k, scale, out1, ldo1, out2, ldo2,
                               acc, ws, wsb, st, true);
@@ -1007,13 +1012,13 @@ int sketch_gaussian2(int xd1, const void* X1, int64_t ld1, int c1, int xd2, cons
   static const int pair = getenv("RB_TC_PAIR") ? atoi(getenv("RB_TC_PAIR")) : 1;
   if (tc && (c1 + c2 <= 64 || (pair && c2 > 0)))
     return sketch_gaussian_tc(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, theta, ldt, k, scale, out1, ldo1, out2, ldo2,
-                              acc, ws, wsb, st);
+                              acc, ws, wsb, st, false, dig);
   if (tc) {
     int rc = sketch_gaussian_tc(xd1, X1, ld1, c1, RB_F32, nullptr, 0, 0, n, theta, ldt, k, scale, out1, ldo1,
-                                nullptr, 0, acc, ws, wsb, st);
+                                nullptr, 0, acc, ws, wsb, st, false, dig);
     if (rc == RB_OK)
       rc = sketch_gaussian_tc(xd2, X2, ld2, c2, RB_F32, nullptr, 0, 0, n, theta, ldt, k, scale, out2, ldo2, nullptr,
-                              0, acc, ws, wsb, st);
+                              0, acc, ws, wsb, st, false, dig);
     return rc;
   }
   PlaneSrc src{theta, ldt, k};

@@ -64,8 +64,8 @@ constexpr int kSplitSeg = kChunk / (16 * kSplitThreads);  // 16-row segments per
 
 // pipeline depth: as many 128-row stages as fit next to each other in
 // shared memory (overridable with RB_TC_STAGES for measurement)
-template <int NP>
-constexpr int max_stages() { return (227 * 1024 - 2048) / (2 * kTM * kBK + gl::kXDig * kBK * NP); }
+template <int NP, int DIG = gl::kXDig>
+constexpr int max_stages() { return (227 * 1024 - 2048) / (2 * kTM * kBK + DIG * kBK * NP); }
 
 // ---- pre-pass: [X1 | X2] -> tiled byte planes + exponents --------------------------
 // grid (nchunks, NP / 2): one CTA per chunk x column pair; thread t owns 32
@@ -166,8 +166,37 @@ __device__ __forceinline__ void planes4(const long long (&xi)[4], uint32_t (&pw)
   pw[0] = __byte_perm(u01, u23, 0x7632);                  // b5
 }
 
-template <int L, typename T>
-__device__ __forceinline__ void split_column(const T (&v)[L], const Scale& s, uint32_t (&w)[L / 16][gl::kXDig][4]) {
+// DIG < 6: the same construction on the (8 DIG - 2)-bit fixed point,
+// y = xi + 0x80..80 (DIG - 1 bytes); plane 0 = the top digit.
+template <int DIG>
+__device__ __forceinline__ void planes4d(const long long (&xi)[4], uint32_t (&pw)[DIG]) {
+  if constexpr (DIG == gl::kXDig) {
+    planes4(xi, pw);
+  } else {
+    static_assert(DIG == 3 || DIG == 4, "digit counts: 6, 4, 3");
+    constexpr uint32_t kBias = DIG == 4 ? 0x808080u : 0x8080u;
+    uint32_t y[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) y[e] = (uint32_t)(int)xi[e] + kBias;  // |xi| <= 2^(8 DIG - 2): fits 32 bits
+    const uint32_t t01l = __byte_perm(y[0], y[1], 0x5140), t01h = __byte_perm(y[0], y[1], 0x7362);
+    const uint32_t t23l = __byte_perm(y[2], y[3], 0x5140), t23h = __byte_perm(y[2], y[3], 0x7362);
+    const uint32_t d0 = __byte_perm(t01l, t23l, 0x5410), d1 = __byte_perm(t01l, t23l, 0x7632);
+    const uint32_t d2 = __byte_perm(t01h, t23h, 0x5410), d3 = __byte_perm(t01h, t23h, 0x7632);
+    if constexpr (DIG == 4) {
+      pw[3] = d0 ^ 0x80808080u;
+      pw[2] = d1 ^ 0x80808080u;
+      pw[1] = d2 ^ 0x80808080u;
+      pw[0] = d3;
+    } else {
+      pw[2] = d0 ^ 0x80808080u;
+      pw[1] = d1 ^ 0x80808080u;
+      pw[0] = d2;
+    }
+  }
+}
+
+template <int L, typename T, int DIG = gl::kXDig>
+__device__ __forceinline__ void split_column(const T (&v)[L], const Scale& s, uint32_t (&w)[L / 16][DIG][4]) {
   // w[seg][plane][word]
 #pragma unroll
   for (int seg = 0; seg < L / 16; ++seg)
@@ -176,10 +205,10 @@ __device__ __forceinline__ void split_column(const T (&v)[L], const Scale& s, ui
       long long xi[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) xi[e] = fixed_of(v[16 * seg + 4 * q + e], s);
-      uint32_t pw[gl::kXDig];
-      planes4(xi, pw);
+      uint32_t pw[DIG];
+      planes4d<DIG>(xi, pw);
 #pragma unroll
-      for (int pl = 0; pl < gl::kXDig; ++pl) w[seg][pl][q] = pw[pl];
+      for (int pl = 0; pl < DIG; ++pl) w[seg][pl][q] = pw[pl];
     }
 }
 
@@ -340,7 +369,7 @@ chunk_max(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, con
   }
 }
 
-template <typename T1, typename T2>
+template <typename T1, typename T2, int DIG>
 __global__ void __launch_bounds__(256, 4)
 encode_planes(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, const T2* __restrict__ X2,
               int64_t ld2, int NP, bool vec1, bool vec2, int64_t nseg, const int* __restrict__ exps,
@@ -366,26 +395,27 @@ encode_planes(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2,
       for (int e = 0; e < 16; ++e) v[h][e] = TV(0);  // UMMA N padding
     }
     const int E = __ldg(exps + chunk * NP + j);
-    sc[h].s = ldexp(1.0, 46 - E);
-    sc[h].fast = 46 - E >= -126 && 46 - E <= 127;
+    constexpr int kBits = 8 * DIG - 2;
+    sc[h].s = ldexp(1.0, kBits - E);
+    sc[h].fast = kBits - E >= -126 && kBits - E <= 127;
     sc[h].sf = sc[h].fast ? (float)sc[h].s : 1.f;
   }
-  uint32_t w[2][1][gl::kXDig][4];  // [column][seg][plane][word]
-  split_column(v[0], sc[0], w[0]);
-  split_column(v[1], sc[1], w[1]);
+  uint32_t w[2][1][DIG][4];  // [column][seg][plane][word]
+  split_column<16, TV, DIG>(v[0], sc[0], w[0]);
+  split_column<16, TV, DIG>(v[1], sc[1], w[1]);
 #pragma unroll
-  for (int pl = 0; pl < gl::kXDig; ++pl) {
-    uint4* dst = reinterpret_cast<uint4*>(planes + gl::x_offset(pl, j0, base, NP));
+  for (int pl = 0; pl < DIG; ++pl) {
+    uint4* dst = reinterpret_cast<uint4*>(planes + gl::x_offset(pl, j0, base, NP, DIG));
     __stcs(dst, make_uint4(w[0][0][pl][0], w[0][0][pl][1], w[0][0][pl][2], w[0][0][pl][3]));
     __stcs(dst + 1, make_uint4(w[1][0][pl][0], w[1][0][pl][1], w[1][0][pl][2], w[1][0][pl][3]));
   }
 }
 
-template <int NP, int ST>
+template <int NP, int ST, int DIG = gl::kXDig>
 struct Smem {
   static constexpr int S = ST;
   uint8_t a[S][2][kBK / 16][kTM][16];  // one q tile
-  uint8_t b[S][kBK / 16][gl::kXDig * NP][16];  // one X-plane tile: [kc][group, plane, col][16]
+  uint8_t b[S][kBK / 16][DIG * NP][16];  // one X-plane tile: [kc][group, plane, col][16]
   uint64_t full[S], empty[S];
   uint64_t tfull[2], tempty[2];
   uint32_t tbase;
@@ -396,7 +426,7 @@ struct Smem {
 // an SM with one CTA of the staged projection, so the sketch of the NEXT
 // block's W runs on the tensor pipe while the projection keeps the FP32
 // pipe busy (the sweep issues them on two streams).
-template <int NP, int ST, bool LEAN>
+template <int NP, int ST, bool LEAN, int DIG = gl::kXDig>
 __device__ __forceinline__ void
 gauss_tc_body(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt, int k,
               const uint8_t* __restrict__ planes1, const int* __restrict__ exps1, int tiles_per_cta,
@@ -412,9 +442,9 @@ gauss_tc_body(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt,
   double* __restrict__ ws = half ? ws2 : ws1;
   if (half) ncols = ncols2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  Smem<NP, ST>& S = *reinterpret_cast<Smem<NP, ST>*>(smem_raw);
+  Smem<NP, ST, DIG>& S = *reinterpret_cast<Smem<NP, ST, DIG>*>(smem_raw);
   constexpr int kStages = ST;
-  constexpr int kDig = gl::kXDig, kBlk = kDig + 1;  // digit planes, TMEM weight blocks
+  constexpr int kDig = DIG, kBlk = kDig + 1;  // digit planes, TMEM weight blocks
   constexpr int kGroupCols = kBlk * NP;
   constexpr int kBufs = (2 * kGroupCols <= 512) ? 2 : 1;
   constexpr uint32_t kAlloc = kBufs * kGroupCols <= 64 ? 64 : kBufs * kGroupCols <= 128 ? 128
@@ -468,7 +498,7 @@ gauss_tc_body(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt,
       // 0..5 of the group, ql x B on blocks 1..6 (D shifted by NG columns),
       // so block w accumulates exactly the products of weight 2^(48 - 8w).  The accumulators are zeroed by the epilogue, every MMA
       // accumulates.
-      constexpr int NG = gl::np_group(NP);
+      constexpr int NG = gl::np_group(NP, DIG);
       constexpr int NGRP = NP / NG;
       static_assert((kDig * NG) % 16 == 0 && kDig * NG <= 256 && NP % NG == 0, "UMMA N (M = 128)");
       constexpr uint32_t ID_HI = tc::idesc_i8(kTM, kDig * NG, true, true);
@@ -509,7 +539,7 @@ gauss_tc_body(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt,
     }
   } else if (LEAN ? (warp >= 2 && warp < 6) : warp >= 4) {
     // ---------------- epilogue ----------------
-    constexpr int NG = gl::np_group(NP);
+    constexpr int NG = gl::np_group(NP, DIG);
     static_assert(NG % 8 == 0, "epilogue drains 8 columns at a time");
     const int q = warp & 3;  // TMEM lane quadrant (warps may only touch lanes 32 (warp % 4) ..)
     const int r = mt * kTM + q * 32 + lane;
@@ -557,18 +587,30 @@ gauss_tc_body(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt,
           // < 2^55), then two binary64 roundings; the scalings by 2^(e+32)
           // and 2^e are exact (normal binary64 powers of two for every
           // binary32 / binary64 chunk exponent), i.e. equal to ldexp
-          const long long hi = ((long long)(int)g[0][jj] << 16) + ((long long)(int)g[1][jj] << 8) +
-                               (long long)(int)g[2][jj];
-          const long long lo = ((long long)(int)g[3][jj] << 24) + ((long long)(int)g[4][jj] << 16) +
-                               ((long long)(int)g[5][jj] << 8) + (long long)(int)g[6][jj];
-          const int e = ex[c0 + jj] - 46;
-          if constexpr (kStage) {
-            const double shi = __longlong_as_double((long long)(e + 32 + 1023) << 52);
-            const double slo = __longlong_as_double((long long)(e + 1023) << 52);
-            t[c0 + jj] = __dadd_rn(__dmul_rn((double)hi, shi), __dmul_rn((double)lo, slo));
-          } else {  // (ldexp: fewer live registers at NP = 48 / 64)
-            acc[c0 + jj] += ldexp((double)hi, e + 32) + ldexp((double)lo, e);
+          double term;
+          const int e = ex[c0 + jj] - (8 * DIG - 2);
+          if constexpr (DIG == gl::kXDig) {
+            const long long hi = ((long long)(int)g[0][jj] << 16) + ((long long)(int)g[1][jj] << 8) +
+                                 (long long)(int)g[2][jj];
+            const long long lo = ((long long)(int)g[3][jj] << 24) + ((long long)(int)g[4][jj] << 16) +
+                                 ((long long)(int)g[5][jj] << 8) + (long long)(int)g[6][jj];
+            if constexpr (kStage) {
+              const double shi = __longlong_as_double((long long)(e + 32 + 1023) << 52);
+              const double slo = __longlong_as_double((long long)(e + 1023) << 52);
+              term = __dadd_rn(__dmul_rn((double)hi, shi), __dmul_rn((double)lo, slo));
+            } else {  // (ldexp: fewer live registers at NP = 48 / 64)
+              term = ldexp((double)hi, e + 32) + ldexp((double)lo, e);
+            }
+          } else {
+            // DIG + 1 weight blocks, < 2^30 each: the exact sum fits one int64
+            // (< 2^63 at DIG = 4); one binary64 rounding
+            long long v = 0;
+#pragma unroll
+            for (int w = 0; w < kBlk; ++w) v += (long long)(int)g[w][jj] << (8 * (kDig - w));
+            term = ldexp((double)v, e);
           }
+          if constexpr (kStage) t[c0 + jj] = term;
+          else acc[c0 + jj] += term;
         }
       }
       tc::tmem_st_wait();
@@ -591,14 +633,14 @@ gauss_tc_body(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt,
   if (warp == 2) tc::tmem_dealloc(tbase, kAlloc);
 }
 
-template <int NP, int ST>
+template <int NP, int ST, int DIG>
 __global__ void __launch_bounds__(kThreads, 1)
 gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt, int k,
                  const uint8_t* __restrict__ planes1, const int* __restrict__ exps1, int tiles_per_cta,
                  double* __restrict__ ws1, int dbg, int pairs, int ncols2, const uint8_t* __restrict__ planes2,
                  const int* __restrict__ exps2, double* __restrict__ ws2) {
-  gauss_tc_body<NP, ST, false>(n, ncols, qt, ldt, k, planes1, exps1, tiles_per_cta, ws1, dbg, pairs, ncols2, planes2,
-                               exps2, ws2);
+  gauss_tc_body<NP, ST, false, DIG>(n, ncols, qt, ldt, k, planes1, exps1, tiles_per_cta, ws1, dbg, pairs, ncols2,
+                                    planes2, exps2, ws2);
 }
 
 constexpr int kLeanThreads = 192;
@@ -625,7 +667,10 @@ __global__ void reduce_splits_tc(const double* __restrict__ ws, int splits, int 
   *o = accumulate ? *o + scale * s : scale * s;
 }
 
-int np_for(int ncols) { return ncols <= 16 ? 16 : ncols <= 32 ? 32 : ncols <= 40 ? 40 : ncols <= 48 ? 48 : 64; }
+// padded column count (UMMA N = DIG NG must be a multiple of 16: no NP = 40 at DIG = 3)
+int np_for(int ncols, int dig = gl::kXDig) {
+  return ncols <= 16 ? 16 : ncols <= 32 ? 32 : (ncols <= 40 && dig != 3) ? 40 : ncols <= 48 ? 48 : 64;
+}
 
 int dbg_flag() {
   static int v = -1;
@@ -642,7 +687,7 @@ struct Half2 {  // the second input of a paired launch (pairs == 2)
   const int* exps = nullptr;
 };
 
-template <int NP>
+template <int NP, int DIG = gl::kXDig>
 int launch_np(int64_t n, int ncols, const uint8_t* qt, int64_t ldt, int k, const uint8_t* planes, const int* exps,
               double* part, size_t part_bytes, int* splits_out, cudaStream_t st, const Half2& h2 = Half2(),
               bool lean = false) {
@@ -664,17 +709,17 @@ int launch_np(int64_t n, int ncols, const uint8_t* qt, int64_t ldt, int k, const
     const char* e = getenv("RB_TC_STAGES");
     env_st = e ? atoi(e) : 0;
   }
-  constexpr int kMax = max_stages<NP>();
-  const int st_req = env_st > 0 ? std::min(env_st, kMax) : (NP <= 80 ? 3 : 2);
+  constexpr int kMax = max_stages<NP, DIG>();
+  const int st_req = env_st > 0 ? std::min(env_st, kMax) : std::min(kMax, DIG == gl::kXDig ? 3 : 4);
 #define RB_GL(STG)                                                                                               \
   {                                                                                                              \
-    const size_t smem = sizeof(Smem<NP, STG>) + 1024;                                                            \
-    cudaFuncSetAttribute(gauss_tc_partial<NP, STG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-    RB_KLAUNCH gauss_tc_partial<NP, STG><<<dim3(mt * h2.pairs, splits), kThreads, smem, st>>>(                              \
+    const size_t smem = sizeof(Smem<NP, STG, DIG>) + 1024;                                                       \
+    cudaFuncSetAttribute(gauss_tc_partial<NP, STG, DIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    RB_KLAUNCH gauss_tc_partial<NP, STG, DIG><<<dim3(mt * h2.pairs, splits), kThreads, smem, st>>>(              \
         n, ncols, qt, ldt, k, planes, exps, tpc, part, dbg_flag(), h2.pairs, h2.ncols, h2.planes, h2.exps,       \
         part + part_bytes / sizeof(double));                                                                     \
   }
-  if (lean && h2.pairs == 1) {
+  if (lean && h2.pairs == 1 && DIG == gl::kXDig) {
     // two stages: shares the SM with one projection CTA
     const size_t smem = sizeof(Smem<NP, 2>) + 1024;
     cudaFuncSetAttribute(gauss_tc_lean<NP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -695,7 +740,7 @@ bool aligned16(const void* p, int64_t ld, int esz) {
 
 template <typename T1>
 void launch_split(int xd2, dim3 g, int64_t n, int c1, const void* X1, int64_t ld1, int c2, const void* X2, int64_t ld2,
-                  int NP, uint8_t* planes, int* exps, cudaStream_t st) {
+                  int NP, uint8_t* planes, int* exps, cudaStream_t st, int dig = gl::kXDig) {
   // RB_SPLIT_MODE=1: the single-kernel two-pass split_planes (kept for
   // measurement); default: chunk_max + encode_planes (same bytes).
   // RB_SPLIT_SLOW=1: binary64 conversion for binary32 inputs too (the
@@ -712,15 +757,24 @@ void launch_split(int xd2, dim3 g, int64_t n, int c1, const void* X1, int64_t ld
 #define RB_SPL(T2)                                                                                               \
   do {                                                                                                           \
     const bool v2 = aligned16(X2, ld2, sizeof(T2));                                                              \
-    if (mode == 1 || slow) {                                                                                     \
+    if ((mode == 1 || slow) && dig == gl::kXDig) {                                                               \
       RB_KLAUNCH split_planes<T1, T2, 3><<<g, kSplitThreads, 0, st>>>(n, c1, (const T1*)X1, ld1, c2,             \
                                                                       (const T2*)X2, ld2, NP, v1, v2, planes,    \
                                                                       exps, slow != 0);                          \
     } else {                                                                                                     \
       RB_KLAUNCH chunk_max<T1, T2><<<dim3(g.x, NP), 256, 0, st>>>(n, c1, (const T1*)X1, ld1, c2, (const T2*)X2,   \
                                                                   ld2, NP, v1, v2, exps);                        \
-      RB_KLAUNCH encode_planes<T1, T2><<<(unsigned)ceil_div(nseg * (NP / 2), 256), 256, 0, st>>>(                \
-          n, c1, (const T1*)X1, ld1, c2, (const T2*)X2, ld2, NP, v1, v2, nseg, exps, planes);                    \
+      const unsigned eg = (unsigned)ceil_div(nseg * (NP / 2), 256);                                              \
+      if (dig == 3) {                                                                                            \
+        RB_KLAUNCH encode_planes<T1, T2, 3><<<eg, 256, 0, st>>>(n, c1, (const T1*)X1, ld1, c2, (const T2*)X2,    \
+                                                                ld2, NP, v1, v2, nseg, exps, planes);            \
+      } else if (dig == 4) {                                                                                     \
+        RB_KLAUNCH encode_planes<T1, T2, 4><<<eg, 256, 0, st>>>(n, c1, (const T1*)X1, ld1, c2, (const T2*)X2,    \
+                                                                ld2, NP, v1, v2, nseg, exps, planes);            \
+      } else {                                                                                                   \
+        RB_KLAUNCH encode_planes<T1, T2, 6><<<eg, 256, 0, st>>>(n, c1, (const T1*)X1, ld1, c2, (const T2*)X2,    \
+                                                                ld2, NP, v1, v2, nseg, exps, planes);            \
+      }                                                                                                          \
     }                                                                                                            \
   } while (0)
   if (xd2 == RB_F32) RB_SPL(float);
@@ -728,15 +782,36 @@ void launch_split(int xd2, dim3 g, int64_t n, int c1, const void* X1, int64_t ld
 #undef RB_SPL
 }
 
-template <int NP>
-int launch_pair(int64_t n, int c1, int c2, const uint8_t* qt, int64_t ldt, int k, const uint8_t* pl1, const int* ex1,
-                const uint8_t* pl2, const int* ex2, double* part, size_t part_b, int* splits, cudaStream_t st) {
-  Half2 h2;
-  h2.pairs = 2;
-  h2.ncols = c2;
-  h2.planes = pl2;
-  h2.exps = ex2;
-  return launch_np<NP>(n, c1, qt, ldt, k, pl1, ex1, part, part_b, splits, st, h2);
+// one launch for every (NP, DIG) the sketch supports
+int launch_any(int NP, int dig, int64_t n, int ncols, const uint8_t* qt, int64_t ldt, int k, const uint8_t* planes,
+               const int* exps, double* part, size_t part_b, int* splits, cudaStream_t st, const Half2& h2, bool lean) {
+#define RB_LA(NPV, DG) \
+  return launch_np<NPV, DG>(n, ncols, qt, ldt, k, planes, exps, part, part_b, splits, st, h2, lean)
+  if (dig == 3) {
+    switch (NP) {
+      case 16: RB_LA(16, 3);
+      case 32: RB_LA(32, 3);
+      case 48: RB_LA(48, 3);
+      default: RB_LA(64, 3);
+    }
+  }
+  if (dig == 4) {
+    switch (NP) {
+      case 16: RB_LA(16, 4);
+      case 32: RB_LA(32, 4);
+      case 40: RB_LA(40, 4);
+      case 48: RB_LA(48, 4);
+      default: RB_LA(64, 4);
+    }
+  }
+  switch (NP) {
+    case 16: RB_LA(16, 6);
+    case 32: RB_LA(32, 6);
+    case 40: RB_LA(40, 6);
+    case 48: RB_LA(48, 6);
+    default: RB_LA(64, 6);
+  }
+#undef RB_LA
 }
 
 // [out1 | out2] for c1 + c2 > 64 (each <= 64): the two inputs are split into
@@ -744,15 +819,16 @@ int launch_pair(int64_t n, int c1, int c2, const uint8_t* qt, int64_t ldt, int k
 // every q tile (one HBM read of the table per pair instead of per input).
 int sketch_gaussian_tc_pair(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2,
                             int c2, int64_t n, const uint8_t* qt, int64_t ldt, int k, double scale, double* out1,
-                            int64_t ldo1, double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st) {
+                            int64_t ldo1, double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st,
+                            int dig) {
   RB_REQUIRE(c1 >= 1 && c2 >= 1 && c1 <= 64 && c2 <= 64 && k >= 1 && out1 && out2 && ldo1 >= k && ldo2 >= k,
              "rb_sketch_gaussian (tensor pair): bad args (c1 %d, c2 %d)", c1, c2);
   RB_REQUIRE(n == 0 || (X1 && ld1 >= n && X2 && ld2 >= n && qt && ldt >= n && ldt % kBK == 0),
              "rb_sketch_gaussian (tensor pair): bad X/theta (ldt %% 128 required)");
-  const int NP = std::max(np_for(c1), np_for(c2));
+  const int NP = std::max(np_for(c1, dig), np_for(c2, dig));
   const int nchunks = (int)((n + kChunk - 1) / kChunk);
   const int64_t ktiles = (int64_t)nchunks * kTPC;
-  const size_t planes_b = (size_t)ktiles * gl::kXDig * kBK * NP;
+  const size_t planes_b = (size_t)ktiles * dig * kBK * NP;
   const size_t exps_b = ((size_t)NP * nchunks * sizeof(int) + 255) / 256 * 256;
   RB_REQUIRE(ws && wsb > 2 * (planes_b + exps_b) + 2048, "rb_sketch_gaussian (tensor pair): workspace too small");
   uint8_t* pl1 = (uint8_t*)ws;
@@ -764,18 +840,16 @@ int sketch_gaussian_tc_pair(int xd1, const void* X1, int64_t ld1, int c1, int xd
   int splits = 0;
   if (n > 0) {
     dim3 g(nchunks, NP / 2);
-    if (xd1 == RB_F32) launch_split<float>(RB_F32, g, n, c1, X1, ld1, 0, nullptr, 0, NP, pl1, ex1, st);
-    else launch_split<double>(RB_F32, g, n, c1, X1, ld1, 0, nullptr, 0, NP, pl1, ex1, st);
-    if (xd2 == RB_F32) launch_split<float>(RB_F32, g, n, c2, X2, ld2, 0, nullptr, 0, NP, pl2, ex2, st);
-    else launch_split<double>(RB_F32, g, n, c2, X2, ld2, 0, nullptr, 0, NP, pl2, ex2, st);
-    int rc;
-    switch (NP) {
-      case 16: rc = launch_pair<16>(n, c1, c2, qt, ldt, k, pl1, ex1, pl2, ex2, part, part_b, &splits, st); break;
-      case 32: rc = launch_pair<32>(n, c1, c2, qt, ldt, k, pl1, ex1, pl2, ex2, part, part_b, &splits, st); break;
-      case 40: rc = launch_pair<40>(n, c1, c2, qt, ldt, k, pl1, ex1, pl2, ex2, part, part_b, &splits, st); break;
-      case 48: rc = launch_pair<48>(n, c1, c2, qt, ldt, k, pl1, ex1, pl2, ex2, part, part_b, &splits, st); break;
-      default: rc = launch_pair<64>(n, c1, c2, qt, ldt, k, pl1, ex1, pl2, ex2, part, part_b, &splits, st); break;
-    }
+    if (xd1 == RB_F32) launch_split<float>(RB_F32, g, n, c1, X1, ld1, 0, nullptr, 0, NP, pl1, ex1, st, dig);
+    else launch_split<double>(RB_F32, g, n, c1, X1, ld1, 0, nullptr, 0, NP, pl1, ex1, st, dig);
+    if (xd2 == RB_F32) launch_split<float>(RB_F32, g, n, c2, X2, ld2, 0, nullptr, 0, NP, pl2, ex2, st, dig);
+    else launch_split<double>(RB_F32, g, n, c2, X2, ld2, 0, nullptr, 0, NP, pl2, ex2, st, dig);
+    Half2 h2;
+    h2.pairs = 2;
+    h2.ncols = c2;
+    h2.planes = pl2;
+    h2.exps = ex2;
+    const int rc = launch_any(NP, dig, n, c1, qt, ldt, k, pl1, ex1, part, part_b, &splits, st, h2, false);
     if (rc != RB_OK) return rc;
   }
   const size_t half_b = (part_b / 2) & ~(size_t)255;
@@ -804,19 +878,20 @@ size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k) {
 // binary32 or binary64 (n rows); c2 may be 0.
 int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2, int c2,
                        int64_t n, const uint8_t* qt, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
-                       double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st, bool lean) {
+                       double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st, bool lean, int dig) {
   const int ncols = c1 + c2;
+  RB_REQUIRE(dig == 6 || dig == 4 || dig == 3, "rb_sketch_gaussian (tensor): digits must be 6, 4 or 3 (got %d)", dig);
   if (ncols > 64)
     return sketch_gaussian_tc_pair(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, qt, ldt, k, scale, out1, ldo1, out2, ldo2,
-                                   acc, ws, wsb, st);
+                                   acc, ws, wsb, st, dig);
   RB_REQUIRE(c1 >= 1 && c2 >= 0 && ncols <= 64 && k >= 1 && ldo1 >= k && out1 && (c2 == 0 || (out2 && ldo2 >= k)),
              "rb_sketch_gaussian (tensor): bad args (c1 %d, c2 %d)", c1, c2);
   RB_REQUIRE(n == 0 || (X1 && ld1 >= n && (c2 == 0 || (X2 && ld2 >= n)) && qt && ldt >= n && ldt % kBK == 0),
              "rb_sketch_gaussian (tensor): bad X/theta (ldt %% 128 required)");
-  const int NP = np_for(ncols);
+  const int NP = np_for(ncols, dig);
   const int nchunks = (int)((n + kChunk - 1) / kChunk);
   const int64_t ktiles = (int64_t)nchunks * kTPC;
-  const size_t planes_b = (size_t)ktiles * gl::kXDig * kBK * NP;
+  const size_t planes_b = (size_t)ktiles * dig * kBK * NP;
   const size_t exps_b = ((size_t)NP * nchunks * sizeof(int) + 255) / 256 * 256;
   RB_REQUIRE(ws && wsb > planes_b + exps_b + 1024, "rb_sketch_gaussian (tensor): workspace too small");
   uint8_t* planes = (uint8_t*)ws;
@@ -826,17 +901,9 @@ int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, co
   int splits = 0;
   if (n > 0) {
     dim3 g(nchunks, NP / 2);
-    if (xd1 == RB_F32) launch_split<float>(xd2, g, n, c1, X1, ld1, c2, X2, ld2, NP, planes, exps, st);
-    else launch_split<double>(xd2, g, n, c1, X1, ld1, c2, X2, ld2, NP, planes, exps, st);
-    int rc;
-    switch (NP) {
-      case 16: rc = launch_np<16>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st, Half2(), lean); break;
-      case 32: rc = launch_np<32>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st, Half2(), lean); break;
-      case 40: rc = launch_np<40>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st, Half2(), lean); break;
-      case 48: rc = launch_np<48>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st, Half2(), lean); break;
-      case 64: rc = launch_np<64>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st, Half2(), lean); break;
-      default: rc = launch_np<64>(n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st, Half2(), lean); break;
-    }
+    if (xd1 == RB_F32) launch_split<float>(xd2, g, n, c1, X1, ld1, c2, X2, ld2, NP, planes, exps, st, dig);
+    else launch_split<double>(xd2, g, n, c1, X1, ld1, c2, X2, ld2, NP, planes, exps, st, dig);
+    const int rc = launch_any(NP, dig, n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st, Half2(), lean);
     if (rc != RB_OK) return rc;
   }
   const int64_t tot = (int64_t)k * ncols;

@@ -118,6 +118,11 @@ class DeviceConfig:
                       not bit-identical -- for inputs whose R is insensitive
                       to the Step-3 rounding order (bench.py gates them on
                       the measured oracle drift).
+    sketch_digits     gaussian kind on the tensor pipe: byte digits kept of
+                      each binary32 entry inside Theta X (6, 4 or 3; default:
+                      the operator's own, 6 = binary64-grade).  Fewer digits
+                      cost proportionally less tensor work; like the fast
+                      projection orders, for inputs whose R tolerates it.
     comm / shard      row sharding: this rank's rows and the group that owns
                       the other shards (comm.py).  Default: all rows here.
     overwrite_w       one-shot rbgs() only: Q is written over W's own device
@@ -133,6 +138,7 @@ class DeviceConfig:
     device: object = None
     q_dtype: torch.dtype = None
     projection_order: str = "reference"
+    sketch_digits: int = None
     comm: Comm = None
     shard: RowShard = None
     overwrite_w: bool = False
@@ -371,6 +377,9 @@ class RbgsSweep:
         if dc.projection_order not in ("reference", "fma", "tc"):
             raise ValueError("projection_order must be 'reference', 'fma' or 'tc'")
         self.order = {"fma": ORDER_FMA, "tc": ORDER_TC}.get(dc.projection_order, ORDER_REFERENCE)
+        if dc.sketch_digits not in (None, 6, 4, 3):
+            raise ValueError("sketch_digits must be 6, 4 or 3")
+        self._gmode = sketching.gauss_mode(theta, dc.sketch_digits) if theta.kind == "gaussian" else "auto"
         dev = self.device
         k = theta.k
         if _q_storage is not None:  # Q over W's storage (DeviceConfig.overwrite_w)
@@ -410,7 +419,7 @@ class RbgsSweep:
 
     # -- small utilities ---------------------------------------------------
     def _sketch(self, X, out):
-        sketching.sketch_into(self.theta, X, out, self.row0)
+        sketching.sketch_into(self.theta, X, out, self.row0, gauss=self._gmode if self.theta.kind == "gaussian" else None)
 
     def _sketch_reduce(self, X, out):
         self._sketch(X, out)
@@ -657,7 +666,7 @@ class RbgsSweep:
         tab = self.theta.device_tables(A.device, self.row0, A.shape[0])
         D.sketch_gaussian2(A, B, tab["theta"], tab["ldt"], self.theta.k,
                            1.0 / (sketching.GAUSS_GRID * math.sqrt(self.theta.k)), outA, outB,
-                           False, sketching.GAUSS_MODE)
+                           False, self._gmode)
         self._reduce(outA, outB)
 
     # -- sketch / projection overlap -------------------------------------------
@@ -906,8 +915,9 @@ class RbgsSweep:
         thr = self.n * U_FINE * q_norm
         for t in range(w):
             if not r[t] > thr:
-                raise DependentBlockError(i, f"dependent column: block {t + 1} numerically "
-                                             f"dependent: sketched norm {r[t]:.3e} below dependence threshold")
+                # rbgs.py:258-260 raised inside interblock_rgs, re-raised by the sweep (rbgs.py:381)
+                inner = DependentBlockError(t + 1, f"sketched norm {r[t]:.3e} below dependence threshold")
+                raise DependentBlockError(i, f"dependent column: {inner}") from inner
 
     def _certify_block(self, Si, Rii, Sp):
         w = Si.shape[1]

@@ -138,10 +138,28 @@ class _ExtendedSketchOperator(SketchOperator):
     _allowed = KINDS + EXTENDED_KINDS
 
 
-def gaussian_operator(k: int, n: int, seed: int) -> SketchOperator:
+def gaussian_operator(k: int, n: int, seed: int, digits: int = 6) -> SketchOperator:
     """Dense gaussian sketch, entries q / (2048 sqrt(k)) with q the int16
-    Box-Muller normal of Philox4x32-10."""
-    return _ExtendedSketchOperator("gaussian", int(k), int(n), int(seed))
+    Box-Muller normal of Philox4x32-10.
+
+    digits  byte digits of each binary32 X entry the tensor-pipe sketch
+            keeps: 6 (default; fixed point at 2^-47 of each 16384-row chunk's
+            max -- binary64-grade sketches), 4 (2^-31) or 3 (2^-23); the
+            tensor work is proportional to it.  The operator (Theta) is the
+            same; only the rounding of X inside Theta X changes."""
+    if digits not in (6, 4, 3):
+        raise ValueError("digits must be 6, 4 or 3")
+    op = _ExtendedSketchOperator("gaussian", int(k), int(n), int(seed))
+    object.__setattr__(op, "digits", int(digits))
+    return op
+
+
+def gauss_mode(theta, digits=None) -> str:
+    """rb_sketch_gaussian mode of an operator (RB_GAUSS_MODE overrides)."""
+    if GAUSS_MODE != "auto":
+        return GAUSS_MODE
+    d = digits or getattr(theta, "digits", 6)
+    return {6: "auto", 4: "tensor4", 3: "tensor3"}[d]
 
 
 def sparse_sign_operator(k: int, n: int, seed: int, nnz: int = 8) -> SketchOperator:
@@ -158,7 +176,7 @@ def make_operator(kind: str, k: int, n: int, seed: int) -> SketchOperator:
 
 
 def sketch_into(theta: SketchOperator, X: torch.Tensor, out: torch.Tensor, row0: int = 0,
-                accumulate: bool = False) -> None:
+                accumulate: bool = False, gauss: str = None) -> None:
     """out (k x cols, fp64, device) = Theta[:, row0:row0+rows] @ X (device,
     column-major).  The building block of every sketch in the sweep."""
     n, cols = X.shape
@@ -179,7 +197,7 @@ def sketch_into(theta: SketchOperator, X: torch.Tensor, out: torch.Tensor, row0:
         D.sketch_signs(X, tab["bits"], tab["ldb"], k, 1.0 / math.sqrt(k), out, accumulate)
     elif theta.kind == "gaussian":
         D.sketch_gaussian(X, tab["theta"], tab["ldt"], k, 1.0 / (GAUSS_GRID * math.sqrt(k)), out,
-                          accumulate, GAUSS_MODE)
+                          accumulate, gauss or gauss_mode(theta))
     else:
         # the pre-bucketed table of exactly this row range (cached on the
         # operator; shards and whole-matrix calls each get their own)

@@ -1,81 +1,76 @@
 """pytest plugin for the boundary conformance run (SURVEY.md section 7 step 1,
-VERDICT r01 item 8): the reference's OWN hot-path test files are collected
-unmodified, then every name a test module imported from `sketch_krylov`
-that the drop-in package exports under the same module / name is rebound
-to the drop-in's object -- so `rbgs`, `RbgsSweep`, `RbgsConfig`,
-`SketchOperator`, `apply`, `certify`, `rbgs_arnoldi`, `block_gmres`,
-`Matrix`, `BlockPartition`, the LS / inter-block functions, the operators
-and the error classes under test are this repository's; names the drop-in
-does not provide (the out-of-scope classical BGS baselines, generators,
-naive oracles) stay the reference's and serve as the checker.
+VERDICT r01 item 8): the reference's OWN test files run unmodified against
+the drop-in package.
+
+Before any test module is imported, the reference package `sketch_krylov`
+is imported module by module in dependency order (errors, kernels,
+sketching, operators, rbgs, krylov) and, after each import, every public
+name the drop-in module of the same name exports is overwritten with the
+drop-in's object.  `from sketch_krylov.rbgs import rbgs, RbgsSweep, ...` in
+a test (and in the reference's own out-of-scope modules: classic BGS,
+FOM / Rayleigh-Ritz / s-step drivers, generators) then binds THIS
+repository's `rbgs`, `RbgsSweep`, `RbgsConfig`, `SketchOperator`, `apply`,
+`certify`, `rbgs_arnoldi`, `block_gmres`, `Matrix`, `BlockPartition`, LS /
+inter-block functions and operators; names the drop-in does not provide stay
+the reference's and act as the checker.  The exception classes are unified
+the other way round (the drop-in's modules are pointed at the reference's
+classes, same names / attributes / messages) so that `pytest.raises` matches
+whichever side raises.
 
 The reference package and tests are NOT part of this repository: the run
 script stages them from /root/reference into the git-ignored oracle/_ref/
 for the duration of one GPU call (tools/conformance.sh)."""
 
 import importlib
+import json
+import os
 import sys
 import types
 
 DROPIN = "paper_2111_14641_b200"
-MODULES = ("rbgs", "sketching", "krylov", "operators", "kernels", "errors")
-REPORT = {"rebound": {}, "kept_reference": {}}
+ORDER = ("kernels", "sketching", "operators", "rbgs", "krylov")
+REPORT = {"overridden": {}, "kept_reference": {}}
 
 
-def _dropin_modules():
-    out = {}
-    for m in MODULES:
-        out[m] = importlib.import_module(f"{DROPIN}.{m}")
-    return out
+def install():
+    ours = {m: importlib.import_module(f"{DROPIN}.{m}") for m in ORDER + ("errors",)}
+    # 1. one set of exception classes: the reference's
+    ref_err = importlib.import_module("sketch_krylov.errors")
+    names = [n for n, o in vars(ours["errors"]).items() if isinstance(o, type) and issubclass(o, Exception)
+             and hasattr(ref_err, n)]
+    pairs = {getattr(ours["errors"], n): getattr(ref_err, n) for n in names}
+    for modname, mod in list(sys.modules.items()):
+        if modname.startswith(DROPIN) and mod is not None:
+            for k, v in list(vars(mod).items()):
+                if isinstance(v, type) and v in pairs:
+                    setattr(mod, k, pairs[v])
+    REPORT["overridden"]["errors"] = ["(drop-in raises the reference's classes: " + ", ".join(sorted(names)) + ")"]
+    # 2. hot-path modules: the drop-in's public names replace the reference's
+    for m in ORDER:
+        ref = importlib.import_module(f"sketch_krylov.{m}")
+        mine = ours[m]
+        public = getattr(mine, "__all__", None) or [n for n in vars(mine) if not n.startswith("_")]
+        over, kept = [], []
+        for n in list(vars(ref)):
+            if n.startswith("_") or isinstance(getattr(ref, n), types.ModuleType):
+                continue
+            if n in public and hasattr(mine, n):
+                obj = getattr(mine, n)
+                if isinstance(obj, types.ModuleType):
+                    continue
+                setattr(ref, n, obj)
+                over.append(n)
+            elif getattr(getattr(ref, n), "__module__", None) == ref.__name__:
+                kept.append(n)
+        REPORT["overridden"][m] = sorted(over)
+        REPORT["kept_reference"][m] = sorted(kept)
 
 
-def _rebind(mod, ours):
-    ref_pkg = "sketch_krylov"
-    for name, obj in list(vars(mod).items()):
-        if name.startswith("__"):
-            continue
-        if isinstance(obj, types.ModuleType):
-            short = obj.__name__.rsplit(".", 1)[-1]
-            if obj.__name__.startswith(ref_pkg + ".") and short in ours:
-                setattr(mod, name, ours[short])
-                REPORT["rebound"].setdefault(mod.__name__, []).append(f"module {short}")
-            continue
-        home = getattr(obj, "__module__", None)
-        if not isinstance(home, str) or not home.startswith(ref_pkg + "."):
-            continue
-        short = home.rsplit(".", 1)[-1]
-        target = ours.get(short)
-        cand = getattr(target, getattr(obj, "__name__", name), None) if target else None
-        if cand is None and target is not None:
-            cand = getattr(target, name, None)
-        if cand is not None:
-            setattr(mod, name, cand)
-            REPORT["rebound"].setdefault(mod.__name__, []).append(name)
-        else:
-            REPORT["kept_reference"].setdefault(mod.__name__, []).append(f"{short}.{name}")
-    # module-level constants built from reference objects (FINE / COARSE
-    # PrecisionSpec instances, configs) are matched by name
-    for name in ("FINE", "COARSE"):
-        if hasattr(mod, name) and hasattr(ours["kernels"], name):
-            setattr(mod, name, getattr(ours["kernels"], name))
-
-
-def pytest_collection_modifyitems(session, config, items):
-    ours = _dropin_modules()
-    seen = set()
-    for it in items:
-        mod = getattr(it, "module", None)
-        if mod is None or mod.__name__ in seen:
-            continue
-        seen.add(mod.__name__)
-        _rebind(mod, ours)
+install()
 
 
 def pytest_sessionfinish(session, exitstatus):
-    import json
-    import os
-
     out = os.environ.get("RB_CONFORMANCE_REPORT")
     if out:
         with open(out, "w") as fh:
-            json.dump({k: {m: sorted(set(v)) for m, v in d.items()} for k, d in REPORT.items()}, fh, indent=1)
+            json.dump(REPORT, fh, indent=1)
