@@ -53,7 +53,7 @@ CONFIGS = {
                desc="block GMRES, 4 RHS, 7-point Poisson 256^3, 61 RBGS blocks (60 Arnoldi steps), "
                     "sparse-sign k=488 (8 nnz/col), fp32 coarse / fp64 fine"),
     "c5shard": dict(name="C5-shard", n=1 << 24, m=1024, p=64, k=2048, kind="gaussian", gen="colscaled",
-                    dtype="f32", coarse="coarse", inplace=True,
+                    dtype="f32", coarse="coarse", inplace=True, order="tc", digits=4,
                     desc="RBGS QR two-precision, per-GPU shard of C5: 2^24 x 1024, p=64, gaussian k=2048"),
 }
 SEED_W, SEED_THETA = 7, 11
@@ -159,7 +159,7 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # CPU restatement (oracle) -- the reference arm and the cpu_baseline leg
 
-def _oracle_sample(cfgd, n_s, parity=False, order="reference"):
+def _oracle_sample(cfgd, n_s, parity=False, order="reference", digits=None):
     """One RBGS QR of an n_s-row sample of the workload with the CPU oracle;
     the gaussian table is materialised beforehand (operator construction),
     like the reference's SRHT tables.  Returns seconds -- and with `parity`
@@ -197,7 +197,7 @@ def _oracle_sample(cfgd, n_s, parity=False, order="reference"):
     gcfg = RbgsConfig(partition=BlockPartition.uniform(m, p), interblock="sketched_cholqr(1)",
                       coarse=COARSE if cfgd["coarse"] == "coarse" else FINE)
     Wg = W.astype(np.float32) if cfgd["dtype"] == "f32" else W
-    f = rbgs(Wg, theta, gcfg, DeviceConfig(projection_order=order))
+    f = rbgs(Wg, theta, gcfg, DeviceConfig(projection_order=order, sketch_digits=digits))
     torch.cuda.synchronize()
     R, Rref = f.R.data, sw.R
     par = {"rows": n_s, "oracle": "oracle/ restatement, same W, same seeded operator",
@@ -289,7 +289,7 @@ def gpu_arm(args, cfgd):
     cfg = RbgsConfig(partition=BlockPartition.uniform(m, p), interblock=args.interblock,
                      coarse=COARSE if cfgd["coarse"] == "coarse" else FINE)
     dc = DeviceConfig(device=dev, projection_order=args.order, comm=Comm(group) if group else None,
-                      shard=shard if world > 1 else None, overwrite_w=inplace)
+                      shard=shard if world > 1 else None, overwrite_w=inplace, sketch_digits=args.sketch_digits)
     torch.cuda.synchronize()
 
     # Default: the factorization captured once as a CUDA graph (RbgsPlan)
@@ -467,7 +467,7 @@ def gpu_arm(args, cfgd):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_s = args.sample_rows or 8192
-        sec, parity = _oracle_sample(cfgd, n_s, parity=True, order=args.order)
+        sec, parity = _oracle_sample(cfgd, n_s, parity=True, order=args.order, digits=args.sketch_digits)
         cpu = {"value": esz * n_s * m / sec / 1e9, "unit": "GB/s", "cores": _CORES, "kind": "port",
                "sample": f"{n_s} x {m} rows of {cfgd['name']}, one factorization, oracle/ restatement "
                          f"(numpy + OpenBLAS)", "parity": parity}
@@ -479,7 +479,7 @@ def gpu_arm(args, cfgd):
             "dtype": "f32-coarse/f64-fine" if cfgd["coarse"] == "coarse" else "f64", "data": "synthetic",
             "config": {"workload": cfgd["desc"], "n": n, "m": m, "p": p, "k": k, "sketch": cfgd["kind"],
                        "interblock": args.interblock, "ls_solver": "richardson(5)",
-                       "projection_order": args.order, "parallelism": f"rows{world}",
+                       "projection_order": args.order, "sketch_digits": args.sketch_digits or 6, "parallelism": f"rows{world}",
                        "execution": ("cuda-graph replay (RbgsPlan)" if plan is not None
                                      else (graph_note or "eager rbgs()")),
                        "collectives_per_block": coll_per_block,
@@ -586,6 +586,9 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--order", default=None, choices=["reference", "fma", "tc"],
                     help="Step-3 order (default: the config's own, see CONFIGS 'order')")
+    ap.add_argument("--sketch-digits", type=int, default=None, choices=[6, 4, 3],
+                    help="gaussian kind: byte digits of X kept inside Theta X (default: the config's own; 6 = "
+                         "binary64-grade)")
     ap.add_argument("--interblock", default="sketched_cholqr(1)",
                     help="inter-block QR (reference default: l2_plus_cholqr; one sketch pass: sketched_cholqr(1))")
     ap.add_argument("--sample-rows", type=int, default=None,
@@ -599,6 +602,8 @@ def main():
     cfgd = CONFIGS[args.config]
     if args.order is None:
         args.order = cfgd.get("order", "reference")
+    if args.sketch_digits is None:
+        args.sketch_digits = cfgd.get("digits") if cfgd["kind"] == "gaussian" else None
     if args.impl == "reference":
         reference_arm(args, cfgd)
     elif cfgd.get("krylov"):

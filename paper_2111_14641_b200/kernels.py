@@ -56,6 +56,8 @@ class Matrix:
         if isinstance(data, Matrix):
             self._host, self._dev = data._host, data._dev
             return
+        if type(data).__name__ == "DevArray":
+            data = data.tensor
         if isinstance(data, torch.Tensor):
             t = data
             if t.ndim == 1:
@@ -108,10 +110,79 @@ class Matrix:
         return f"Matrix({self.shape[0]}x{self.shape[1]}, {where})"
 
 
+class DevArray:
+    """What `RbgsSweep.Q / S / P / R` hand to a caller: the reference keeps
+    these as numpy arrays that consumers slice and feed to numpy / scipy
+    (rbgs.py:343-347; krylov.py:229-262 does `sweep.R[:c, mp:c]`,
+    `sweep.Q[:, :j] @ Z`).  Here the data live on the device, so the public
+    attribute is this lazy view: slicing stays on the device (`.tensor` is
+    the CUDA tensor, used by this package's own drivers), and anything numpy
+    asks of it -- `np.asarray`, `@`, arithmetic, `.copy()`, `.T`,
+    `np.linalg.*` -- downloads the viewed block once as binary64."""
+
+    __slots__ = ("tensor",)
+    __array_priority__ = 100.0
+
+    def __init__(self, t):
+        self.tensor = t
+
+    def __getitem__(self, idx):
+        return DevArray(self.tensor[idx])
+
+    def __setitem__(self, idx, value):
+        v = value.tensor if isinstance(value, DevArray) else value
+        if not isinstance(v, torch.Tensor):
+            v = torch.from_numpy(np.ascontiguousarray(np.asarray(v, dtype=np.float64)))
+        self.tensor[idx] = v.to(self.tensor.device, self.tensor.dtype)
+
+    def __array__(self, dtype=None, copy=None):
+        A = self.tensor.detach().to("cpu", torch.float64).numpy()
+        return A if dtype is None else A.astype(dtype, copy=False)
+
+    @property
+    def shape(self):
+        return tuple(self.tensor.shape)
+
+    @property
+    def ndim(self):
+        return self.tensor.dim()
+
+    @property
+    def dtype(self):
+        return np.dtype(np.float64)
+
+    def __len__(self):
+        return self.tensor.shape[0]
+
+    def __getattr__(self, name):  # .copy(), .T, .sum(), ... : numpy semantics on the downloaded block
+        if name.startswith("__"):
+            raise AttributeError(name)
+        return getattr(np.asarray(self), name)
+
+    def __repr__(self):
+        return f"DevArray({tuple(self.tensor.shape)}, {self.tensor.dtype}, {self.tensor.device})"
+
+
+def _devarray_op(name):
+    def op(self, *others):
+        return getattr(np.asarray(self), name)(*[np.asarray(o) if isinstance(o, DevArray) else o for o in others])
+    op.__name__ = name
+    return op
+
+
+for _n in ("__matmul__", "__rmatmul__", "__add__", "__radd__", "__sub__", "__rsub__", "__mul__", "__rmul__",
+           "__truediv__", "__rtruediv__", "__neg__", "__abs__", "__eq__", "__ne__", "__lt__", "__le__", "__gt__",
+           "__ge__", "__iter__"):
+    setattr(DevArray, _n, _devarray_op(_n))
+DevArray.__hash__ = None
+
+
 def as_array(X) -> np.ndarray:
     """Host fp64 2-D view (kernels.py:68-77)."""
     if isinstance(X, Matrix):
         return X.data
+    if isinstance(X, DevArray):
+        X = X.tensor
     if isinstance(X, torch.Tensor):
         X = X.detach().cpu().numpy()
     A = np.asarray(X, dtype=np.float64)

@@ -114,9 +114,9 @@ def rbgs_arnoldi(A: LinearOperator, B, theta, p: int, cfg: RbgsConfig = None,
         sweep.push_block(Bd)
         off = sweep.offsets
         for i in range(2, p + 1):
-            sweep.push_block(_matvec(A, sweep.Q[:, off[i - 2]:off[i - 1]], matvec_precision))
+            sweep.push_block(_matvec(A, sweep.Qd[:, off[i - 2]:off[i - 1]], matvec_precision))
         f = sweep.finish()
-        R = sweep.R
+        R = sweep.Rd
         return ArnoldiDecomposition(f.Q, Matrix(R[:, mp:]), Matrix(R[:, :mp]), f.S, f.P, f.cert,
                                     cfg.partition)
 
@@ -180,17 +180,17 @@ def _sketched_history(A, X, Bd, bn, sweep, cands, Hf, Rf, mp, c, bk, comm, histo
     n-dimensional correction and one true residual per cycle (the last
     candidate: the sketched residual is non-increasing in j)."""
     dev = Bd.device
-    k = sweep.S.shape[0]
+    k = sweep.Sd.shape[0]
     # sketched residuals of the nested problems: ||R_first - H Z_j|| per column
     est = []
     for t, (w, Z, rows) in enumerate(cands):
         if bk and t == len(cands) - 1:
             # breakdown candidate (krylov.py:258-268): || P_1 - [P_2.. | pending] Z ||
             PA = D.empty_cm(k, c, torch.float64, dev)
-            PA[:, :c - mp].copy_(sweep.P[:, mp:c])
+            PA[:, :c - mp].copy_(sweep.Pd[:, mp:c])
             PA[:, c - mp:].copy_(sweep.pending_P.tensor)
             Rk = D.empty_cm(k, mp, torch.float64, dev)
-            Rk.copy_(sweep.P[:, :mp])
+            Rk.copy_(sweep.Pd[:, :mp])
             D.gemm(0, 0, -1.0, PA, Z, 1.0, Rk)
         else:
             Rk = D.empty_cm(rows, mp, torch.float64, dev)
@@ -205,7 +205,7 @@ def _sketched_history(A, X, Bd, bn, sweep, cands, Hf, Rf, mp, c, bk, comm, histo
     rmax = max(r for _, _, r in cands)
     G = D.empty_cm(rmax, rmax, torch.float64, dev)
     Sc = D.empty_cm(k, rmax, torch.float64, dev)
-    Sc.copy_(sweep.S[:, :rmax])
+    Sc.copy_(sweep.Sd[:, :rmax])
     D.gemm(1, 0, 1.0, Sc, Sc, 0.0, G)
     Gh = G.cpu().numpy()
     Gh = np.triu(Gh) + np.triu(Gh, 1).T
@@ -214,7 +214,7 @@ def _sketched_history(A, X, Bd, bn, sweep, cands, Hf, Rf, mp, c, bk, comm, histo
     U = D.empty_cm(Bd.shape[0], mp, torch.float64, dev)
     Zc = D.empty_cm(w, mp, torch.float64, dev)
     Zc.copy_(Z)
-    D.gemm(0, 0, 1.0, sweep.Q[:, :w], Zc, 0.0, U)
+    D.gemm(0, 0, 1.0, sweep.Qd[:, :w], Zc, 0.0, U)
     Rr = Bd - A._apply_dev(D.to_cm(X + U), torch.float64)
     rels[-1] = float((colsq(Rr).sqrt() / bn).max())
     for t, (_, _, r) in enumerate(cands):
@@ -286,7 +286,7 @@ def block_gmres(A: LinearOperator, B, theta, p: int, restarts: int = 1, cfg=None
                 sweep.push_block(Bres)
                 off = sweep.offsets
                 for i in range(2, p + 1):
-                    sweep.push_block(_matvec(A, sweep.Q[:, off[i - 2]:off[i - 1]], matvec_precision))
+                    sweep.push_block(_matvec(A, sweep.Qd[:, off[i - 2]:off[i - 1]], matvec_precision))
             except DependentBlockError as e:
                 bk = e.block
             q, c = sweep.blocks_done, sweep.cols_done
@@ -297,10 +297,10 @@ def block_gmres(A: LinearOperator, B, theta, p: int, restarts: int = 1, cfg=None
                 certs.append((np.nan, np.nan))
                 breakdown = bk
                 break
-            rep = certify(sweep.S[:, :c], sweep.P[:, :c], sweep.R[:c, :c])
+            rep = certify(sweep.Sd[:, :c], sweep.Pd[:, :c], sweep.Rd[:c, :c])
             pair = (rep.delta, rep.delta_tilde)
-            Hf = sweep.R[:c, mp:c]
-            Rf = sweep.R[:c, :mp]
+            Hf = sweep.Rd[:c, mp:c]
+            Rf = sweep.Rd[:c, :mp]
             # Every inner iterate j = 1 .. q-1 (plus the breakdown candidate)
             # of krylov.py:229-262, evaluated in batches: the small LS
             # solves first, then ONE pass over the basis for all corrections
@@ -313,9 +313,9 @@ def block_gmres(A: LinearOperator, B, theta, p: int, restarts: int = 1, cfg=None
                 cands.append((j * mp, Z, (j + 1) * mp))
             if bk:
                 PA = D.empty_cm(theta.k, c - mp + mp, torch.float64, dev)
-                PA[:, :c - mp].copy_(sweep.P[:, mp:c])
+                PA[:, :c - mp].copy_(sweep.Pd[:, mp:c])
                 PA[:, c - mp:].copy_(sweep.pending_P.tensor)
-                cands.append((c, _ls_qr_dev(PA, sweep.P[:, :mp]), c))
+                cands.append((c, _ls_qr_dev(PA, sweep.Pd[:, :mp]), c))
             U_best, rel_best = None, None
             if cands and diagnostics == "sketched":
                 U_best, rel_best, it = _sketched_history(A, X, Bd, bn, sweep, cands, Hf, Rf, mp, c, bk, comm,
@@ -326,7 +326,7 @@ def block_gmres(A: LinearOperator, B, theta, p: int, restarts: int = 1, cfg=None
                 for t, (w, Z, _) in enumerate(cands):
                     Zb[:w, t * mp:(t + 1) * mp].copy_(Z)
                 U = D.empty_cm(n_local, mp * len(cands), torch.float64, dev)
-                D.gemm(0, 0, 1.0, sweep.Q[:, :wmax], Zb, 0.0, U)
+                D.gemm(0, 0, 1.0, sweep.Qd[:, :wmax], Zb, 0.0, U)
                 res2 = torch.empty(len(cands), mp, dtype=torch.float64, device=dev)
                 for t in range(len(cands)):
                     Rr = Bd - A._apply_dev(D.to_cm(X + U[:, t * mp:(t + 1) * mp]), torch.float64)
@@ -339,7 +339,7 @@ def block_gmres(A: LinearOperator, B, theta, p: int, restarts: int = 1, cfg=None
                 G = D.empty_cm(rmax, rmax, torch.float64, dev)
                 # full DGEMM: cuBLAS' DSYRK picks a 3x slower kernel for
                 # K = n_local ~ 1.7e7 (measured)
-                D.gemm(1, 0, 1.0, sweep.Q[:, :rmax], sweep.Q[:, :rmax], 0.0, G)
+                D.gemm(1, 0, 1.0, sweep.Qd[:, :rmax], sweep.Qd[:, :rmax], 0.0, G)
                 comm.allreduce_(G)
                 Gh = G.cpu().numpy()
                 Gh = np.triu(Gh) + np.triu(Gh, 1).T

@@ -51,7 +51,7 @@ from .errors import (
     RankDeficiencyError,
     ShapeError,
 )
-from .kernels import COARSE, FINE, BlockPartition, Matrix, PrecisionSpec, as_array
+from .kernels import COARSE, FINE, BlockPartition, DevArray, Matrix, PrecisionSpec, as_array
 
 __all__ = ["RbgsConfig", "DeviceConfig", "BlockQR", "CertReport", "rbgs", "RbgsSweep", "RbgsPlan", "certify",
            "ls_richardson", "ls_bmgs_reorth", "ls_cg_normal", "ls_householder_direct",
@@ -386,9 +386,9 @@ class RbgsSweep:
             if (_q_storage.shape != (self.n_local, m) or _q_storage.dtype != self.q_dtype
                     or not D.is_cm(_q_storage) or _q_storage.device != dev):
                 raise ShapeError("overwrite_w needs W as a column-major CUDA tensor of Q's dtype")
-            self.Q = _q_storage
+            self.Qd = _q_storage
         else:
-            self.Q = D.zeros_cm(self.n_local, m, self.q_dtype, dev)
+            self.Qd = D.zeros_cm(self.n_local, m, self.q_dtype, dev)
         # binary64 Q with binary32 projections (Arnoldi: the operator reads
         # the binary64 basis): keep a binary32 shadow -- exactly the
         # Q.astype(float32) the reference's coarse gemm reads (kernels.py:192)
@@ -396,9 +396,9 @@ class RbgsSweep:
         self.Q32 = None
         if self.q_dtype == torch.float64 and self.compute == F32 and dc.coarse_shadow:
             self.Q32 = D.zeros_cm(self.n_local, m, torch.float32, dev)
-        self.S = D.zeros_cm(k, m, torch.float64, dev)
-        self.P = D.zeros_cm(k, m, torch.float64, dev)
-        self.R = D.zeros_cm(m, m, torch.float64, dev)
+        self.Sd = D.zeros_cm(k, m, torch.float64, dev)
+        self.Pd = D.zeros_cm(k, m, torch.float64, dev)
+        self.Rd = D.zeros_cm(m, m, torch.float64, dev)
         wmax = max(cfg.partition.block_widths())
         self._scr = _Scratch(k, m, wmax, dev)
         self._tmp64 = None
@@ -418,6 +418,24 @@ class RbgsSweep:
         self._g_given = None  # l2 stage: Q'^T Q' reduced with the block's sketches
 
     # -- small utilities ---------------------------------------------------
+    # the reference's public state (rbgs.py:343-347) as numpy-compatible
+    # views of the device tensors Qd / Sd / Pd / Rd (kernels.DevArray)
+    @property
+    def Q(self):
+        return DevArray(self.Qd)
+
+    @property
+    def S(self):
+        return DevArray(self.Sd)
+
+    @property
+    def P(self):
+        return DevArray(self.Pd)
+
+    @property
+    def R(self):
+        return DevArray(self.Rd)
+
     def _sketch(self, X, out):
         sketching.sketch_into(self.theta, X, out, self.row0, gauss=self._gmode if self.theta.kind == "gaussian" else None)
 
@@ -517,7 +535,7 @@ class RbgsSweep:
                 if not last and Qcur.data_ptr() == out.data_ptr():
                     out = D.empty_cm(self.n_local, w, torch.float64, self.device)
                 if (last and l == 1 and self._fuse_scaling and out.data_ptr() == Qcur.data_ptr()
-                        and self.cols_done + w < self.Q.shape[1]):
+                        and self.cols_done + w < self.Qd.shape[1]):
                     # in-place scaling of this block: done by the next block's
                     # projection (rb_project_trsm), which alone reads it next
                     self._pending_scale = (out, RS)
@@ -751,7 +769,7 @@ class RbgsSweep:
             D.convert(Pi, scr.P32[:, :w])
             Pi = scr.Pr[:, :w]
             D.convert(scr.P32[:, :w], Pi)
-        slot = self.Q[:, j0:j1]
+        slot = self.Qd[:, j0:j1]
         sp_given = None
         if c:
             self._g_given = None
@@ -764,8 +782,8 @@ class RbgsSweep:
             fork = (self._fork_next_sketch(Wn, Pn), Pn)
         if c:
             X = scr.X[:c, :w]
-            self._solve_ls(self.S[:, :c], Pi, X)
-            self.R[:c, j0:j1].copy_(X)
+            self._solve_ls(self.Sd[:, :c], Pi, X)
+            self.Rd[:c, j0:j1].copy_(X)
             if self.Q32 is not None:
                 # Q' in binary32 into the (not yet committed) shadow slot,
                 # then widened exactly into the binary64 slot
@@ -774,9 +792,9 @@ class RbgsSweep:
             elif self._pending_scale is not None:
                 Qf, RSf = self._pending_scale
                 self._pending_scale = None
-                D.project_trsm(self.Q[:, :c], X, W, slot, self.compute, self.order, norms[0:2], Qf, RSf)
+                D.project_trsm(self.Qd[:, :c], X, W, slot, self.compute, self.order, norms[0:2], Qf, RSf)
             else:
-                D.project(self.Q[:, :c], X, W, slot, self.compute, self.order, norms[0:2])
+                D.project(self.Qd[:, :c], X, W, slot, self.compute, self.order, norms[0:2])
             if sharded:
                 # the norm partials join the block's next allreduce
                 self._pending.append(norms[0:2])
@@ -860,10 +878,10 @@ class RbgsSweep:
 
     def _commit_block(self, j0, j1, Pi, Si, Rii):
         if self.Q32 is not None:
-            D.convert(self.Q[:, j0:j1], self.Q32[:, j0:j1])
-        self.S[:, j0:j1].copy_(Si)
-        self.P[:, j0:j1].copy_(Pi)
-        self.R[j0:j1, j0:j1].copy_(Rii)
+            D.convert(self.Qd[:, j0:j1], self.Q32[:, j0:j1])
+        self.Sd[:, j0:j1].copy_(Si)
+        self.Pd[:, j0:j1].copy_(Pi)
+        self.Rd[j0:j1, j0:j1].copy_(Rii)
         self.blocks_done += 1
         self.cols_done = j1
 
@@ -938,11 +956,11 @@ class RbgsSweep:
     def finish(self) -> BlockQR:
         c = self.cols_done
         with torch.cuda.device(self.device):
-            cert0 = certify(self.S[:, :c], self.P[:, :c], self.R[:c, :c])
+            cert0 = certify(self.Sd[:, :c], self.Pd[:, :c], self.Rd[:c, :c])
         cert = CertReport(cert0.delta, cert0.delta_tilde, tuple(self.per_block_ortho),
                           tuple(self.per_block_resid))
-        return BlockQR(Matrix(self.Q, precision=self.cfg.coarse), Matrix(self.R), Matrix(self.S),
-                       Matrix(self.P), self.cfg.partition, cert)
+        return BlockQR(Matrix(self.Qd, precision=self.cfg.coarse), Matrix(self.Rd), Matrix(self.Sd),
+                       Matrix(self.Pd), self.cfg.partition, cert)
 
 
 REPLAYS = 0  # one-shot factorizations replayed eagerly after a deferred-status failure
@@ -1212,7 +1230,7 @@ def _standalone_interblock(Qprime, theta, cfg):
     except DependentBlockError as e:
         cause = e.__cause__
         raise (cause if cause is not None else e)
-    return Matrix(sw.Q), Matrix(sw.R), Matrix(sw.S)
+    return Matrix(sw.Qd), Matrix(sw.Rd), Matrix(sw.Sd)
 
 
 def interblock_sketched_cholqr(Qprime, theta, l: int = 1, resketch: bool = False):

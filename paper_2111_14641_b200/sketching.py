@@ -181,6 +181,13 @@ def sketch_into(theta: SketchOperator, X: torch.Tensor, out: torch.Tensor, row0:
     column-major).  The building block of every sketch in the sweep."""
     n, cols = X.shape
     k = theta.k
+    if cols > 64 and theta.kind != "identity":
+        # the kernels take at most 64 columns per call (a block is never
+        # wider); wider inputs (e.g. the reference's materialize(): Theta @ I)
+        # go through in column slabs
+        for j in range(0, cols, 64):
+            sketch_into(theta, X[:, j:j + 64], out[:, j:j + 64], row0, accumulate, gauss)
+        return
     if theta.kind == "identity":
         if row0 != 0 or n != theta.n:
             raise ShapeError("identity sketch cannot be row-sharded")

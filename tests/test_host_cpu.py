@@ -311,3 +311,31 @@ def test_reference_arm_runs_on_cpu():
     import json
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["impl"] == "reference" and line["value"] > 0 and line["cpu_baseline"]["kind"] == "port"
+
+
+def test_devarray_is_numpy_compatible():
+    """kernels.DevArray (what RbgsSweep.Q/S/P/R return): slicing stays a view
+    of the tensor, numpy consumers (asarray, @, .copy(), .T, linalg) see the
+    binary64 block -- the reference's consumers (krylov.py:229-262) do
+    `sweep.R[:c, mp:c].copy()` and `sweep.Q[:, :j] @ Z`."""
+    import torch
+
+    from paper_2111_14641_b200.kernels import DevArray, Matrix, as_array
+
+    A = np.arange(12.0).reshape(3, 4)
+    t = torch.from_numpy(A.copy())
+    d = DevArray(t)
+    assert d.shape == (3, 4) and len(d) == 3 and d.ndim == 2
+    v = d[:, 1:3]
+    assert isinstance(v, DevArray) and v.tensor.data_ptr() == t[:, 1:3].data_ptr()
+    assert np.array_equal(np.asarray(v), A[:, 1:3])
+    assert np.array_equal(v.copy(), A[:, 1:3]) and isinstance(v.copy(), np.ndarray)
+    assert np.array_equal(d.T, A.T)
+    Z = np.ones((4, 2))
+    assert np.array_equal(d @ Z, A @ Z) and np.array_equal(Z.T @ d.T, Z.T @ A.T)
+    assert np.array_equal(d - A, np.zeros_like(A)) and np.array_equal(2.0 * d, 2.0 * A)
+    assert np.allclose(np.linalg.svd(d, compute_uv=False), np.linalg.svd(A, compute_uv=False))
+    assert np.array_equal(np.hstack([d[:, :1], d[:, 1:]]), A)
+    assert np.array_equal(Matrix(d).data, A) and np.array_equal(as_array(d), A)
+    d[0:1, 0:2] = np.array([[7.0, 8.0]])
+    assert t[0, 0].item() == 7.0 and t[0, 1].item() == 8.0
