@@ -194,7 +194,8 @@ int rb_sumsq3(int64_t m1, int n1, const double* A1, int64_t lda1,
               int64_t m3, int n3, const double* A3, int64_t lda3, double* out,
               void* ws, size_t ws_bytes, void* stream);
 /* Symmetric rank-k update: C = alpha A^T A + beta C for a tall binary64 A
- * (k x n, C n x n; the full product is formed) -- the basis Gram of the
+ * (k x n, C n x n; the upper triangle is valid: 128 x 64 tiles wholly below
+ * the diagonal are not formed) -- the basis Gram of the
  * GMRES conditioning history (krylov.py:98-103, 247-257). */
 int rb_syrk_f64(int n, int64_t k, double alpha, const double* A, int64_t lda, double beta,
                 double* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream);

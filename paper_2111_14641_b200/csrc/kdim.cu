@@ -815,40 +815,73 @@ constexpr int kGM = 128, kGN = 64, kGK = 16;
 template <typename T, bool TRANS_A>
 __global__ void __launch_bounds__(256)
 gemm_tiles(int m, int n, int64_t K, const T* __restrict__ A, int64_t lda, const T* __restrict__ B, int64_t ldb,
-           int64_t chunk, T alpha, T beta, T* __restrict__ C, int64_t ldc, T* __restrict__ ws) {
+           int64_t chunk, T alpha, T beta, T* __restrict__ C, int64_t ldc, T* __restrict__ ws, int upper) {
   using V4 = typename std::conditional<sizeof(T) == 8, double4, float4>::type;
-  __shared__ __align__(32) T sA[kGK][kGM];
-  __shared__ __align__(32) T sB[kGK][kGN];
+  // double-buffered tiles: the next K step is fetched into registers while
+  // the current one is multiplied (one barrier per step)
+  // rows padded by 4 entries: the K-fastest stores of a fetched tile (16
+  // consecutive k per row of op(A) / B) would otherwise all hit one bank
+  extern __shared__ __align__(32) unsigned char gemm_smem[];
+  T (*sA)[kGK][kGM + 4] = reinterpret_cast<T (*)[kGK][kGM + 4]>(gemm_smem);
+  T (*sB)[kGK][kGN + 4] = reinterpret_cast<T (*)[kGK][kGN + 4]>(gemm_smem + 2 * kGK * (kGM + 4) * sizeof(T));
   const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;  // rows 8 ty.., cols 4 tx..
   const int m0 = blockIdx.x * kGM, n0 = blockIdx.y * kGN;
+  // symmetric product (A^T A): tiles entirely below the diagonal are not formed
+  if (upper && m0 >= n0 + kGN) return;
   const int64_t kb = (int64_t)blockIdx.z * chunk, ke = min(K, kb + chunk);
+  constexpr int kEA = kGK * kGM / 256, kEB = kGK * kGN / 256;
+  T ra[kEA], rb[kEB];
+  auto fetch = [&](int64_t k0) {
+#pragma unroll
+    for (int u = 0; u < kEA; ++u) {
+      const int e = tid + 256 * u;
+      int i, kk;
+      if (TRANS_A) { kk = e % kGK; i = e / kGK; } else { i = e % kGM; kk = e / kGM; }
+      const int64_t kg = k0 + kk;
+      ra[u] = (m0 + i < m && kg < ke) ? (TRANS_A ? A[kg + (int64_t)(m0 + i) * lda] : A[(m0 + i) + kg * lda]) : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < kEB; ++u) {
+      const int e = tid + 256 * u;
+      const int kk = e % kGK, jj = e / kGK;
+      const int64_t kg = k0 + kk;
+      rb[u] = (n0 + jj < n && kg < ke) ? B[kg + (int64_t)(n0 + jj) * ldb] : T(0);
+    }
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < kEA; ++u) {
+      const int e = tid + 256 * u;
+      int i, kk;
+      if (TRANS_A) { kk = e % kGK; i = e / kGK; } else { i = e % kGM; kk = e / kGM; }
+      sA[buf][kk][i] = ra[u];
+    }
+#pragma unroll
+    for (int u = 0; u < kEB; ++u) {
+      const int e = tid + 256 * u;
+      sB[buf][e % kGK][e / kGK] = rb[u];
+    }
+  };
   T acc[8][4];
 #pragma unroll
   for (int a = 0; a < 8; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = T(0);
+  int buf = 0;
+  if (kb < ke) {
+    fetch(kb);
+    stash(0);
+  }
+  __syncthreads();
   for (int64_t k0 = kb; k0 < ke; k0 += kGK) {
-    __syncthreads();
-    for (int e = tid; e < kGK * kGM; e += 256) {
-      int i, kk;
-      if (TRANS_A) { kk = e % kGK; i = e / kGK; } else { i = e % kGM; kk = e / kGM; }
-      const int64_t kg = k0 + kk;
-      T v = T(0);
-      if (m0 + i < m && kg < ke) v = TRANS_A ? A[kg + (int64_t)(m0 + i) * lda] : A[(m0 + i) + kg * lda];
-      sA[kk][i] = v;
-    }
-    for (int e = tid; e < kGK * kGN; e += 256) {
-      const int kk = e % kGK, j = e / kGK;
-      const int64_t kg = k0 + kk;
-      sB[kk][j] = (n0 + j < n && kg < ke) ? B[kg + (int64_t)(n0 + j) * ldb] : T(0);
-    }
-    __syncthreads();
+    const bool more = k0 + kGK < ke;
+    if (more) fetch(k0 + kGK);
 #pragma unroll
     for (int kk = 0; kk < kGK; ++kk) {
       T a[8], b[4];
-      const V4 a0 = *reinterpret_cast<const V4*>(&sA[kk][8 * ty]);
-      const V4 a1 = *reinterpret_cast<const V4*>(&sA[kk][8 * ty + 4]);
-      const V4 b0 = *reinterpret_cast<const V4*>(&sB[kk][4 * tx]);
+      const V4 a0 = *reinterpret_cast<const V4*>(&sA[buf][kk][8 * ty]);
+      const V4 a1 = *reinterpret_cast<const V4*>(&sA[buf][kk][8 * ty + 4]);
+      const V4 b0 = *reinterpret_cast<const V4*>(&sB[buf][kk][4 * tx]);
       a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
       a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
       b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
@@ -857,29 +890,50 @@ gemm_tiles(int m, int n, int64_t K, const T* __restrict__ A, int64_t lda, const 
 #pragma unroll
         for (int t = 0; t < 4; ++t) acc[q][t] = fma(a[q], b[t], acc[q][t]);
     }
+    if (more) stash(buf ^ 1);
+    __syncthreads();
+    buf ^= 1;
   }
+  // a thread's 8 rows are contiguous: whole-vector stores (full sectors)
+  // when the tile is interior and C is aligned -- the tall n x 240 outputs
+  // of the GMRES corrections are write-bound otherwise
+  T* Cd = ws ? ws + (int64_t)blockIdx.z * m * n : C;
+  const int64_t ldd = ws ? m : ldc;
+  const bool vec = m0 + kGM <= m && ldd % 4 == 0 && ((uintptr_t)Cd % (4 * sizeof(T))) == 0 &&
+                   (ws || beta == T(0));
 #pragma unroll
-  for (int q = 0; q < 8; ++q)
+  for (int t = 0; t < 4; ++t) {
+    const int jj = n0 + 4 * tx + t;
+    if (jj >= n) continue;
+    const T sc = ws ? T(1) : alpha;
+    if (vec) {
+      V4 v0, v1;
+      v0.x = sc * acc[0][t]; v0.y = sc * acc[1][t]; v0.z = sc * acc[2][t]; v0.w = sc * acc[3][t];
+      v1.x = sc * acc[4][t]; v1.y = sc * acc[5][t]; v1.z = sc * acc[6][t]; v1.w = sc * acc[7][t];
+      V4* dst = reinterpret_cast<V4*>(Cd + (m0 + 8 * ty) + (int64_t)jj * ldd);
+      dst[0] = v0;
+      dst[1] = v1;
+    } else {
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int i = m0 + 8 * ty + q, j = n0 + 4 * tx + t;
-      if (i < m && j < n) {
-        if (ws) {
-          ws[(int64_t)blockIdx.z * m * n + i + (int64_t)j * m] = acc[q][t];
-        } else {
-          T* c = C + i + (int64_t)j * ldc;
-          *c = beta == T(0) ? alpha * acc[q][t] : alpha * acc[q][t] + beta * *c;
+      for (int q = 0; q < 8; ++q) {
+        const int i = m0 + 8 * ty + q;
+        if (i < m) {
+          T* c = Cd + i + (int64_t)jj * ldd;
+          if (ws) *c = acc[q][t];
+          else *c = beta == T(0) ? alpha * acc[q][t] : alpha * acc[q][t] + beta * *c;
         }
       }
     }
+  }
 }
 
 template <typename T>
 __global__ void gemm_reduce(const T* __restrict__ ws, int splits, int m, int n, T alpha, T beta, T* __restrict__ C,
-                            int64_t ldc) {
+                            int64_t ldc, int upper) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t tot = (int64_t)m * n;
   if (e >= tot) return;
+  if (upper && (int)(e % m) / kGM * kGM >= (int)(e / m) / kGN * kGN + kGN) return;  // tile not formed
   T s = T(0);
   for (int q = 0; q < splits; ++q) s += ws[(int64_t)q * tot + e];
   const int i = (int)(e % m), j = (int)(e / m);
@@ -889,7 +943,7 @@ __global__ void gemm_reduce(const T* __restrict__ ws, int splits, int m, int n, 
 
 template <typename T>
 int gemm_generic(int tA, int m, int n, int64_t K, T alpha, const T* A, int64_t lda, const T* B, int64_t ldb, T beta,
-                 T* C, int64_t ldc, void* ws, size_t wsb, cudaStream_t st, const char* what) {
+                 T* C, int64_t ldc, void* ws, size_t wsb, cudaStream_t st, const char* what, int upper = 0) {
   if (m == 0 || n == 0) return RB_OK;
   const int mt = (m + kGM - 1) / kGM, nt = (n + kGN - 1) / kGN;
   const int64_t tiles = (int64_t)mt * nt;
@@ -906,10 +960,18 @@ int gemm_generic(int tA, int m, int n, int64_t K, T alpha, const T* A, int64_t l
   T* part = splits > 1 ? (T*)ws : nullptr;
   RB_REQUIRE(mt <= INT32_MAX && nt <= 65535, "%s: too large", what);
   const dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)splits);
-  if (tA) RB_KLAUNCH gemm_tiles<T, true><<<grid, 256, 0, st>>>(m, n, K, A, lda, B, ldb, chunk, alpha, beta, C, ldc, part);
-  else RB_KLAUNCH gemm_tiles<T, false><<<grid, 256, 0, st>>>(m, n, K, A, lda, B, ldb, chunk, alpha, beta, C, ldc, part);
+  const size_t smem = 2 * kGK * (kGM + 4 + kGN + 4) * sizeof(T);
+  if (tA) {
+    cudaFuncSetAttribute(gemm_tiles<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    RB_KLAUNCH gemm_tiles<T, true><<<grid, 256, smem, st>>>(m, n, K, A, lda, B, ldb, chunk, alpha, beta, C, ldc, part,
+                                                            upper);
+  } else {
+    cudaFuncSetAttribute(gemm_tiles<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    RB_KLAUNCH gemm_tiles<T, false><<<grid, 256, smem, st>>>(m, n, K, A, lda, B, ldb, chunk, alpha, beta, C, ldc, part,
+                                                             upper);
+  }
   if (part) RB_KLAUNCH gemm_reduce<T><<<ceil_div((int64_t)m * n, 256), 256, 0, st>>>(part, (int)splits, m, n, alpha,
-                                                                                     beta, C, ldc);
+                                                                                     beta, C, ldc, upper);
   return check_launch(what);
 }
 
@@ -1092,7 +1154,9 @@ int gemm_f32(int tA, int tB, int m, int n, int k, float alpha, const float* A, i
 int syrk_f64(int n, int64_t k, double alpha, const double* A, int64_t lda, double beta, double* C, int64_t ldc,
              void* ws, size_t wsb, cudaStream_t st) {
   RB_REQUIRE(n >= 0 && k >= 0 && C && ldc >= std::max(n, 1) && (k == 0 || (A && lda >= k)), "rb_syrk_f64: bad args");
-  return gemm_generic<double>(1, n, n, k, alpha, A, lda, A, lda, beta, C, ldc, ws, wsb, st, "rb_syrk_f64");
+  // tiles entirely below the diagonal are skipped (C's strictly lower tiles
+  // are left untouched): 6 of 8 tiles at n = 244
+  return gemm_generic<double>(1, n, n, k, alpha, A, lda, A, lda, beta, C, ldc, ws, wsb, st, "rb_syrk_f64", 1);
 }
 
 }  // namespace rb

@@ -337,9 +337,8 @@ def block_gmres(A: LinearOperator, B, theta, p: int, restarts: int = 1, cfg=None
                 # cond(Q[:, :rows]) is that of a leading principal block
                 rmax = max(r for _, _, r in cands)
                 G = D.empty_cm(rmax, rmax, torch.float64, dev)
-                # full DGEMM: cuBLAS' DSYRK picks a 3x slower kernel for
-                # K = n_local ~ 1.7e7 (measured)
-                D.gemm(1, 0, 1.0, sweep.Qd[:, :rmax], sweep.Qd[:, :rmax], 0.0, G)
+                G.zero_()
+                D.syrk(sweep.Qd[:, :rmax], G)  # upper triangle (tiles below the diagonal are skipped)
                 comm.allreduce_(G)
                 Gh = G.cpu().numpy()
                 Gh = np.triu(Gh) + np.triu(Gh, 1).T

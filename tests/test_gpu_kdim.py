@@ -106,3 +106,20 @@ def test_gemm_vs_numpy(D, tA, m, n, k, dt):
         scale = np.abs(Aw.T if tA else Aw) @ np.abs(Bw) + np.abs(Cw)
         u = 2.0 ** -24 if dt == torch.float32 else 2.0 ** -53
         assert np.all(np.abs(C.double().cpu().numpy() - want) <= 4 * k * u * scale + 1e-300)
+
+
+@pytest.mark.parametrize("n,k", [(244, 200_000), (64, 5000), (130, 777), (8, 64)])
+def test_syrk_upper_vs_numpy(D, n, k):
+    """rb_syrk_f64 (the GMRES basis Gram, krylov.py:98-103): the upper
+    triangle of A^T A; 128 x 64 tiles wholly below the diagonal are not formed
+    and stay as they were."""
+    g = np.random.Generator(np.random.Philox(n))
+    A = g.standard_normal((k, n))
+    C = _dev(np.full((n, n), 7.0), torch.float64)
+    D.syrk(_dev(A, torch.float64), C)
+    got = C.cpu().numpy()
+    want = A.T @ A
+    iu = np.triu_indices(n)
+    assert np.all(np.abs(got[iu] - want[iu]) <= 4 * k * 2.0 ** -53 * (np.abs(A).T @ np.abs(A))[iu])
+    if n == 244:  # tile (rows 128.., cols 0..63) lies below the diagonal: untouched
+        assert np.all(got[128:, :64] == 7.0)
