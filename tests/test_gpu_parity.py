@@ -708,3 +708,55 @@ def test_bench_workload_sample_vs_oracle(pkg, config):
     assert par["rel_R_diff"] <= tol, par
     d, do = par["delta"]
     assert abs(d - do) <= 0.05 * do + 1e-12, par
+
+
+def test_repeat_and_two_stream_determinism(pkg):
+    """Race evidence in place of compute-sanitizer (closed on this pool,
+    profiles/r02_sanitizer_record.txt): the warp-specialised kernels
+    (gauss_tc_partial, project_staged, project_tc2), the last-CTA combine of
+    sumsq3 and the cooperative k-dimensional kernels give bitwise identical
+    factors (a) run after run and (b) when two factorizations are in flight
+    on two streams of the same device at once (the C ABI's per-stream
+    workspaces; formerly one constant bank / counter per device)."""
+    rbgs, sketching, D = pkg
+    from paper_2111_14641_b200.kernels import BlockPartition
+    import goldens as G
+
+    n, m, p, k = 65536, 120, 40, 256
+    W = G.trig_family(n, m, 5).astype(np.float32)
+    Wd = _dev(W.astype(np.float64), torch.float32)
+    th = sketching.gaussian_operator(k, n, 3)
+    cfg = rbgs.RbgsConfig(partition=BlockPartition.uniform(m, p), interblock="sketched_cholqr(1)")
+    for order in ("reference", "tc"):
+        dc = rbgs.DeviceConfig(projection_order=order)
+        base = rbgs.rbgs(Wd, th, cfg, dc)
+        torch.cuda.synchronize()
+        Rb, Qb = base.R.data.copy(), base.Q.data.copy()
+        for _ in range(3):
+            f = rbgs.rbgs(Wd, th, cfg, dc)
+            torch.cuda.synchronize()
+            assert np.array_equal(f.R.data, Rb) and np.array_equal(f.Q.data, Qb), order
+        import threading
+
+        outs, errs = [], []
+
+        def worker():
+            try:
+                s = torch.cuda.Stream()
+                with torch.cuda.stream(s):
+                    for _ in range(3):  # (each call ends with one status read of its own stream)
+                        outs.append(rbgs.rbgs(Wd, th, cfg, dc))
+                s.synchronize()
+            except Exception as e:  # noqa: BLE001
+                errs.append(e)
+
+        ts = [threading.Thread(target=worker) for _ in range(2)]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        torch.cuda.synchronize()
+        assert not errs, errs
+        assert len(outs) == 6
+        for f in outs:
+            assert np.array_equal(f.R.data, Rb) and np.array_equal(f.Q.data, Qb), order
