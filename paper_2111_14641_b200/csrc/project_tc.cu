@@ -327,8 +327,11 @@ __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* t
       : "memory");
 }
 
+constexpr int kTc2Threads = 512;  // 4 role warps + 8 converter warps + 4 epilogue warps
+constexpr int kConvThreads = 256;
+
 template <int NP, typename TW>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kTc2Threads, 1)
 project_tc2(const __grid_constant__ CUtensorMap tmq, int64_t n, int c, int p, const float* __restrict__ Xs,
             const TW* W, int64_t ldw, float* Qp, int64_t ldqp, double* __restrict__ partial) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -351,7 +354,7 @@ project_tc2(const __grid_constant__ CUtensorMap tmq, int64_t n, int c, int p, co
       tc::mbar_init(&S.full[s], 1);
       tc::mbar_init(&S.done[s], 1);
     }
-    for (int s = 0; s < kRL; ++s) tc::mbar_init(&S.conv[s], 128);
+    for (int s = 0; s < kRL; ++s) tc::mbar_init(&S.conv[s], kConvThreads);
     for (int s = 0; s < kRX; ++s) {
       tc::mbar_init(&S.xfull[s], 1);
       tc::mbar_init(&S.xempty[s], 1);
@@ -429,9 +432,9 @@ project_tc2(const __grid_constant__ CUtensorMap tmq, int64_t n, int c, int p, co
         tc::mma_commit(&S.tfull[buf]);
       }
     }
-  } else if (warp >= 4 && warp < 8) {
-    // ---------------- converters: elementwise split, in place ----------------
-    const int t128 = tid - 128;
+  } else if (warp >= 4 && warp < 12) {
+    // ---------------- converters: elementwise split ----------------
+    const int t128 = tid - 128;  // 0 .. kConvThreads - 1
     int64_t total = 0;
     for (int64_t it = 0; it < my_super; ++it) total += (int64_t)nsub_of(it) * nch;
     for (int64_t g = 0; g < total; ++g) {
@@ -442,22 +445,22 @@ project_tc2(const __grid_constant__ CUtensorMap tmq, int64_t n, int c, int p, co
       const float4* src = reinterpret_cast<const float4*>(&S.raw[s][0][0][0]);
       float4* dlo = reinterpret_cast<float4*>(&S.lo[sl][0][0][0]);
 #pragma unroll
-      for (int i = 0; i < (int)(kABytes / 16 / 128); ++i) {
+      for (int i = 0; i < (int)(kABytes / 16 / kConvThreads); ++i) {
         // hi = the entry truncated to tf32 -- what the tensor pipe reads from
         // the raw binary32 word (it ignores the low 13 bits), so the raw
         // stage is used as it arrived; lo = rna_tf32(q - hi), q - hi exact
-        const float4 v = src[i * 128 + t128];
+        const float4 v = src[i * kConvThreads + t128];
         float4 l;
         l.x = rna_tf32(v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u));
         l.y = rna_tf32(v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u));
         l.z = rna_tf32(v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u));
         l.w = rna_tf32(v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u));
-        dlo[i * 128 + t128] = l;
+        dlo[i * kConvThreads + t128] = l;
       }
       tc::fence_proxy_async_smem();  // generic-proxy stores -> tensor-core reads
       tc::mbar_arrive(&S.conv[sl]);
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 12) {
     // ---------------- epilogue: one row per thread ----------------
     const int q = warp & 3;
     const int rr = q * 32 + lane;
@@ -468,30 +471,37 @@ project_tc2(const __grid_constant__ CUtensorMap tmq, int64_t n, int c, int p, co
       const int64_t row0 = (blockIdx.x + it * gridDim.x) * kSub * kTM;
       for (int t = 0; t < nsub; ++t) {
         const int64_t row = row0 + (int64_t)t * kTM + rr;
-        // this row of W into registers while the accumulators are busy
-        TW wv[NP];
-#pragma unroll
-        for (int j = 0; j < NP; ++j) wv[j] = j < p ? ld_stream(W + row + (int64_t)j * ldw) : TW(0);
-        if (t == 0) {
-          tc::mbar_wait(&S.tfull[buf], (uint32_t)((it >> 1) & 1));
-          tc::tc_fence_after();
-        }
+        // this row of W into registers while the accumulators are busy, in
+        // column groups of <= 32 (512 threads: 128 registers per thread)
+        constexpr int kCG = NP < 32 ? NP : 32;
         const uint32_t la = tbase + buf * kAccCols + t * 2 * NP + ((uint32_t)(q * 32) << 16);
 #pragma unroll
-        for (int j0 = 0; j0 < NP; j0 += 16) {
-          uint32_t v[16], u[16];
-          tc::tmem_ld16(la + j0, v);
-          tc::tmem_ld16(la + NP + j0, u);
-          tc::tmem_ld_wait();
+        for (int c0 = 0; c0 < NP; c0 += kCG) {
+          TW wv[kCG];
 #pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {
-            const int j = j0 + jj;
-            if (j < p) {
-              w2 += (double)wv[j] * (double)wv[j];
-              const float dsum = __fadd_rn(__uint_as_float(v[jj]), __uint_as_float(u[jj]));
-              const float out = __fsub_rn((float)wv[j], dsum);
-              __stcs(Qp + row + (int64_t)j * ldqp, out);
-              q2 += (double)out * (double)out;
+          for (int j = 0; j < kCG; ++j)
+            wv[j] = (c0 + j < p) ? ld_stream(W + row + (int64_t)(c0 + j) * ldw) : TW(0);
+          if (t == 0 && c0 == 0) {
+            tc::mbar_wait(&S.tfull[buf], (uint32_t)((it >> 1) & 1));
+            tc::tc_fence_after();
+          }
+#pragma unroll
+          for (int j0 = 0; j0 < kCG; j0 += 16) {
+            uint32_t v[16], u[16];
+            tc::tmem_ld16(la + c0 + j0, v);
+            tc::tmem_ld16(la + NP + c0 + j0, u);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              const int j = c0 + j0 + jj;
+              if (j < p) {
+                const TW w = wv[j0 + jj];
+                w2 += (double)w * (double)w;
+                const float dsum = __fadd_rn(__uint_as_float(v[jj]), __uint_as_float(u[jj]));
+                const float out = __fsub_rn((float)w, dsum);
+                __stcs(Qp + row + (int64_t)j * ldqp, out);
+                q2 += (double)out * (double)out;
+              }
             }
           }
         }
@@ -509,7 +519,7 @@ project_tc2(const __grid_constant__ CUtensorMap tmq, int64_t n, int c, int p, co
       S.red[q][1] = q2;
     }
     asm volatile("bar.sync 1, 128;" ::: "memory");
-    if (partial && tid == 256) {
+    if (partial && tid == 384) {
       double a = 0.0, b = 0.0;
       for (int i = 0; i < 4; ++i) {
         a += S.red[i][0];
@@ -599,7 +609,7 @@ int project_tc_launch(int w_dtype, int64_t n, int c, int p, const float* Q, int6
   {                                                                                                          \
     const size_t smem = sizeof(Tc2Smem<V>) + 2048;                                                           \
     cudaFuncSetAttribute(project_tc2<V, TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);        \
-    RB_KLAUNCH project_tc2<V, TW><<<grid2, kTcThreads, smem, st>>>(tm, n, c, p, Xs, (const TW*)W, ldw, Qp,   \
+    RB_KLAUNCH project_tc2<V, TW><<<grid2, kTc2Threads, smem, st>>>(tm, n, c, p, Xs, (const TW*)W, ldw, Qp,   \
                                                                    ldqp, partial);                        \
   }
     if (w_dtype == RB_F32) {

@@ -37,7 +37,7 @@ def main():
     o2 = torch.empty((p, k), dtype=torch.float64, device=dev).t()
 
     def call():
-        D.sketch_gaussian2(X1, X2, tab["theta"], tab["ldt"], k, 1.0, o1, o2, mode="tensor")
+        D.sketch_gaussian2(X1, X2, tab["theta"], tab["ldt"], k, 1.0, o1, o2, mode=os.environ.get("SB_MODE", "tensor"))
 
     for _ in range(3):
         call()
