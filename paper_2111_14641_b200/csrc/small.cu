@@ -172,6 +172,57 @@ trsm_right_kernel(int64_t n, int p, const TI* B, int64_t ldb, TO* Xo, int64_t ld
     if (j < p) Xo[r + (int64_t)j * ldx] = (TO)x[j];
 }
 
+// More than 40 columns: `x[64]` in binary64 is 128 registers and spilled
+// (4.97 ms at 2^24 x 64).  Here the first 32 solved entries of the row stay
+// in registers and the later ones go to shared memory ([l - 32][thread],
+// conflict-free), columns 32.. solved four at a time as independent chains.
+// Every column keeps the reference chain -- s = x_j; s = fma(-x_l, R_lj, s)
+// for l ascending; x_j = s / R_jj (as s * (1 / R_jj), like tri_solve_row) --
+// so the output is bitwise that of trsm_right_kernel.
+constexpr int kTrsmHiThreads = 256;
+template <typename TI, typename TO, int PB>
+__global__ void __launch_bounds__(kTrsmHiThreads, 2)
+trsm_right_hi_kernel(int64_t n, int p, const TI* B, int64_t ldb, TO* Xo, int64_t ldx) {  // B, Xo may alias
+  static_assert(PB > 32 && PB <= 64 && PB % 4 == 0, "columns 33 .. 64");
+  extern __shared__ double trsm_sh[];  // [PB - 32][kTrsmHiThreads]
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double* xh = trsm_sh + threadIdx.x;
+  double x[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) x[j] = (double)B[r + (int64_t)j * ldb];  // p > 32 here
+  tri_solve_row<32, 4>(x, 32);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) Xo[r + (int64_t)j * ldx] = (TO)x[j];
+#pragma unroll
+  for (int j = 32; j < PB; j += 4) {
+    if (j >= p) break;
+    double s[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) s[c] = j + c < p ? (double)B[r + (int64_t)(j + c) * ldb] : 0.0;
+#pragma unroll
+    for (int l = 0; l < 32; ++l)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) s[c] = fma(-x[l], c_tri_R[l + (j + c) * kTriLd], s[c]);
+#pragma unroll
+    for (int l = 32; l < j; ++l) {
+      const double xl = xh[(l - 32) * kTrsmHiThreads];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) s[c] = fma(-xl, c_tri_R[l + (j + c) * kTriLd], s[c]);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (j + c < p) {
+        const double xj = s[c] * c_tri_inv[j + c];
+        xh[(j + c - 32) * kTrsmHiThreads] = xj;
+        Xo[r + (int64_t)(j + c) * ldx] = (TO)xj;
+#pragma unroll
+        for (int c2 = c + 1; c2 < 4; ++c2) s[c2] = fma(-xj, c_tri_R[j + c + (j + c2) * kTriLd], s[c2]);
+      }
+    }
+  }
+}
+
 // Left solve R X = B in place, one warp per right-hand side.
 __global__ void trsm_left_upper_kernel(int m, int nrhs, const double* __restrict__ R, int64_t ldr,
                                        double* __restrict__ B, int64_t ldb, int* __restrict__ info) {
@@ -338,7 +389,23 @@ void trsm_right_launch(int64_t n, int p, const void* B, int64_t ldb, const doubl
     tri_const_done_locked(st);                                                                            \
     return;                                                                                               \
   }
-  RB_TR(4) RB_TR(8) RB_TR(12) RB_TR(16) RB_TR(24) RB_TR(32) RB_TR(40) RB_TR(48) RB_TR(64)
+  RB_TR(4) RB_TR(8) RB_TR(12) RB_TR(16) RB_TR(24) RB_TR(32) RB_TR(40)
+  static const int hi = getenv("RB_TRSM_HI") ? atoi(getenv("RB_TRSM_HI")) : 1;
+  if (hi) {
+#define RB_TRH(V)                                                                                              \
+  if (p <= V) {                                                                                                \
+    const size_t smem = (size_t)(V - 32) * kTrsmHiThreads * sizeof(double);                                    \
+    cudaFuncSetAttribute(trsm_right_hi_kernel<TI, TO, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                         (int)smem);                                                                           \
+    RB_KLAUNCH trsm_right_hi_kernel<TI, TO, V><<<ceil_div(n, (int64_t)kTrsmHiThreads), kTrsmHiThreads, smem,   \
+                                                 st>>>(n, p, (const TI*)B, ldb, (TO*)X, ldx);                  \
+    tri_const_done_locked(st);                                                                                 \
+    return;                                                                                                    \
+  }
+    RB_TRH(48) RB_TRH(64)
+#undef RB_TRH
+  }
+  RB_TR(48) RB_TR(64)
 #undef RB_TR
 }
 

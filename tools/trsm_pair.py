@@ -19,7 +19,7 @@ from paper_2111_14641_b200 import _device as D  # noqa: E402
 dev = torch.device("cuda:0")
 g = torch.Generator(device=dev).manual_seed(7)
 res = {}
-for n, p in [(1_000_000, 40), (1 << 24, 32), (1 << 24, 40), (1 << 24, 64)]:
+for n, p in [(1_000_000, 40), (1 << 24, 32), (1 << 24, 40), (1 << 24, 48), (1 << 24, 61), (1 << 24, 64)]:
     B = D.empty_cm(n, p, torch.float32, dev)
     B.copy_(torch.randn(n, p, generator=g, device=dev))
     R = torch.eye(p, dtype=torch.float64, device=dev) + 0.05 * torch.triu(
