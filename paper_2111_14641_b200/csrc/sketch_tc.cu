@@ -411,6 +411,69 @@ encode_planes(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2,
   }
 }
 
+// encode_tile (default): one CTA per 128-row K tile.  A warp reads 128 rows
+// of one column as ONE coalesced 512-byte run (lane L: rows 4 L .. 4 L + 3)
+// -- encode_planes' thread-per-(16 rows, column pair) mapping made every
+// warp load touch 32 lines 64 MB apart at the C5 shape (ncu: lg_throttle,
+// 2.8 TB/s) -- converts its four entries per column into one 32-bit word
+// per plane, stages the tile in shared memory in the operand layout (rows
+// of a K chunk padded by 16 bytes: conflict-free) and the CTA writes the
+// tile's DIG x 128 x NP bytes, contiguous in HBM, as whole lines.  Same
+// exponents, integers and plane bytes as encode_planes.
+template <typename T1, typename T2, int DIG>
+__global__ void __launch_bounds__(256, 4)
+encode_tile(int64_t n, int c1, const T1* __restrict__ X1, int64_t ld1, int c2, const T2* __restrict__ X2,
+            int64_t ld2, int NP, bool vec1, bool vec2, const int* __restrict__ exps, uint8_t* __restrict__ planes) {
+  extern __shared__ __align__(16) uint32_t enc_sm[];
+  using TV = typename std::conditional<sizeof(T1) == 4 && sizeof(T2) == 4, float, double>::type;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t base = (int64_t)blockIdx.x * kBK;
+  const int64_t chunk = base / kChunk;
+  const int NG = gl::np_group(NP, DIG);
+  const int rowW = DIG * NP * 4;   // words per K chunk (16 rows) of the tile
+  const int S = rowW + 4;          // padded: the 8 K chunks of a warp store hit distinct banks
+  const int kc = lane >> 2, b4 = lane & 3;
+  constexpr int kMaxCols = 8;      // NP / 8 columns per warp, NP <= 64
+  TV v[kMaxCols][4];
+  const int ncw = NP / 8;
+  const int64_t r0 = base + 4 * lane;
+#pragma unroll
+  for (int i = 0; i < kMaxCols; ++i) {
+    if (i >= ncw) break;
+    const int j = warp + 8 * i;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[i][e] = TV(0);
+    if (j < c1) loadL<4, T1, TV>(X1 + (int64_t)j * ld1, r0, n, vec1, v[i]);
+    else if (j < c1 + c2) loadL<4, T2, TV>(X2 + (int64_t)(j - c1) * ld2, r0, n, vec2, v[i]);
+  }
+#pragma unroll
+  for (int i = 0; i < kMaxCols; ++i) {
+    if (i >= ncw) break;
+    const int j = warp + 8 * i;
+    const int E = __ldg(exps + chunk * NP + j);
+    constexpr int kBits = 8 * DIG - 2;
+    Scale sc;
+    sc.s = ldexp(1.0, kBits - E);
+    sc.fast = kBits - E >= -126 && kBits - E <= 127;
+    sc.sf = sc.fast ? (float)sc.s : 1.f;
+    long long xi[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) xi[e] = fixed_of(v[i][e], sc);
+    uint32_t pw[DIG];
+    planes4d<DIG>(xi, pw);
+    const int g = j / NG, jj = j % NG;
+#pragma unroll
+    for (int pl = 0; pl < DIG; ++pl) enc_sm[kc * S + ((g * DIG + pl) * NG + jj) * 4 + b4] = pw[pl];
+  }
+  __syncthreads();
+  const int nq = (kBK / 16) * DIG * NP;  // 16-byte words of the tile
+  uint4* dst = reinterpret_cast<uint4*>(planes + (int64_t)blockIdx.x * ((int64_t)DIG * kBK * NP));
+  for (int q = threadIdx.x; q < nq; q += 256) {
+    const int kq = q / (DIG * NP), rem = q % (DIG * NP);
+    __stcs(dst + q, *reinterpret_cast<const uint4*>(&enc_sm[kq * S + rem * 4]));
+  }
+}
+
 template <int NP, int ST, int DIG = gl::kXDig>
 struct Smem {
   static constexpr int S = ST;
@@ -748,7 +811,7 @@ void launch_split(int xd2, dim3 g, int64_t n, int c1, const void* X1, int64_t ld
   static int mode = -1, slow = 0;
   if (mode < 0) {
     const char* e = getenv("RB_SPLIT_MODE");
-    mode = e ? atoi(e) : 2;
+    mode = e ? atoi(e) : 3;
     const char* s = getenv("RB_SPLIT_SLOW");
     slow = s ? atoi(s) : 0;
   }
@@ -765,7 +828,23 @@ void launch_split(int xd2, dim3 g, int64_t n, int c1, const void* X1, int64_t ld
       RB_KLAUNCH chunk_max<T1, T2><<<dim3(g.x, NP), 256, 0, st>>>(n, c1, (const T1*)X1, ld1, c2, (const T2*)X2,   \
                                                                   ld2, NP, v1, v2, exps);                        \
       const unsigned eg = (unsigned)ceil_div(nseg * (NP / 2), 256);                                              \
-      if (dig == 3) {                                                                                            \
+      const unsigned tg = (unsigned)(nseg * 16 / kBK);                                                           \
+      const size_t tsm = (size_t)(kBK / 16) * ((size_t)dig * NP * 4 + 4) * 4;                                     \
+      if (mode == 3) {                                                                                           \
+        if (dig == 3) {                                                                                          \
+          cudaFuncSetAttribute(encode_tile<T1, T2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);   \
+          RB_KLAUNCH encode_tile<T1, T2, 3><<<tg, 256, tsm, st>>>(n, c1, (const T1*)X1, ld1, c2, (const T2*)X2,  \
+                                                                  ld2, NP, v1, v2, exps, planes);                \
+        } else if (dig == 4) {                                                                                   \
+          cudaFuncSetAttribute(encode_tile<T1, T2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);   \
+          RB_KLAUNCH encode_tile<T1, T2, 4><<<tg, 256, tsm, st>>>(n, c1, (const T1*)X1, ld1, c2, (const T2*)X2,  \
+                                                                  ld2, NP, v1, v2, exps, planes);                \
+        } else {                                                                                                 \
+          cudaFuncSetAttribute(encode_tile<T1, T2, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm);   \
+          RB_KLAUNCH encode_tile<T1, T2, 6><<<tg, 256, tsm, st>>>(n, c1, (const T1*)X1, ld1, c2, (const T2*)X2,  \
+                                                                  ld2, NP, v1, v2, exps, planes);                \
+        }                                                                                                        \
+      } else if (dig == 3) {                                                                                     \
         RB_KLAUNCH encode_planes<T1, T2, 3><<<eg, 256, 0, st>>>(n, c1, (const T1*)X1, ld1, c2, (const T2*)X2,    \
                                                                 ld2, NP, v1, v2, nseg, exps, planes);            \
       } else if (dig == 4) {                                                                                     \

@@ -1,6 +1,9 @@
-for cfg in "4096 512 1 1" "4096 1024 1 1"; do
-  set -- $cfg
-  echo "== LBO=$1 SBO=$2 LAYOUT=$3 AMAJOR=$4"
-  RB_TC_DEBUG=1 RB_TC_LBO=$1 RB_TC_SBO=$2 RB_TC_LAYOUT=$3 RB_TC_AMAJOR=$4 timeout 60 python tools/tc_probe.py map 2>&1 | grep -E "raw k|acc row|mismatches|out\[|rror" | head -50
+for rep in 1 2; do
+for mode in 2 3; do
+  echo "== split mode $mode tensor4 C5"; RB_SPLIT_MODE=$mode SB_N=16777216 SB_P=64 SB_K=2048 SB_MODE=tensor4 python tools/split_bench.py 2>/dev/null | tail -1 | cut -c60-330
 done
-timeout 200 python tools/tc_probe.py check 2>&1 | tail -12
+done
+for mode in 2 3; do
+  echo "== split mode $mode tensor C2"; RB_SPLIT_MODE=$mode python tools/split_bench.py 2>/dev/null | tail -1 | cut -c60-330
+done
+nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,power.draw,power.limit,temperature.gpu --format=csv

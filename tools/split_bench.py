@@ -59,7 +59,7 @@ def main():
     for ev in prof.events():
         if ev.device_type.name != "CUDA":
             continue
-        for key in ("split_planes", "chunk_max", "encode_planes", "gauss_tc_partial", "reduce_splits"):
+        for key in ("split_planes", "chunk_max", "encode_planes", "encode_tile", "gauss_tc_partial", "reduce_splits"):
             if key in ev.name:
                 d = per.setdefault(key, [0, 0.0])
                 d[0] += 1
