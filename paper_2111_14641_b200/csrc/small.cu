@@ -4,6 +4,7 @@
 // (rbgs.py:284, kernels.py:250-270) and the Householder QR used by the
 // direct LS solver and the GMRES least-squares problem (kernels.py:216-231).
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 #include "tri_const.cuh"
@@ -476,6 +477,137 @@ int cross_small(int64_t n, int p, int q, const TA* A, int64_t lda, const TB* B, 
   return check_launch("rb_cross (small)");
 }
 
+// Tall cross product out = A^T B for 8 < max(p, q) <= 64 (the l2 stage's
+// Q'^T Q' at block widths 16 .. 64, rbgs.py:293-302) on the FP64 tensor pipe:
+// mma.sync m16n8k4 f64.  The split-K tile kernel above issued 8 scalar
+// shared loads per 16 DFMA and padded a 40 x 40 output to 64 x 64 (0.95 ms
+// per 1e6 x 40 block, 3.4 TFLOP/s).  Here a CTA walks its row range in
+// 64-row chunks (coalesced column reads, staged as binary64 [column][row]
+// with a pitch of 68: staging stores and fragment loads are conflict-free), a warp owns one 16-row tile of
+// the output for a quarter / half of the chunk's rows and all its 8-column
+// tiles (one A fragment per k-step serves every column tile); for a Gram
+// (A == B) tiles wholly below the diagonal are skipped and mirrored by the
+// reduction.  Fixed orders throughout: per-warp k ascending, warps, then
+// CTAs in index order.
+constexpr int kCrossKC = 64, kCrossPitch = 68, kCrossThreads = 256;
+
+template <typename TA, typename TB>
+__global__ void __launch_bounds__(kCrossThreads, 2)
+cross_dmma_partial(int64_t n, int p, int q, const TA* __restrict__ A, int64_t lda, const TB* __restrict__ B,
+                   int64_t ldb, int64_t rows_per_cta, int sym, double* __restrict__ ws) {
+  extern __shared__ double cross_sm[];
+  double* sA = cross_sm;                                  // [column][kCrossPitch]
+  double* sB = sym ? sA : cross_sm + 64 * kCrossPitch;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int mt = (p + 15) / 16, nt = (q + 7) / 8;
+  const int groups = 8 / mt;                              // k-groups (warps per output row tile)
+  const int mtile = warp % mt, kg = warp / mt;
+  const bool active = kg < groups;
+  const int m0 = mtile * 16;
+  const int kper = kCrossKC / groups;                     // rows of a chunk per k-group (multiple of 4)
+  double acc[8][4];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  const int64_t beg = (int64_t)blockIdx.x * rows_per_cta, end = min(n, beg + rows_per_cta);
+  for (int64_t r0 = beg; r0 < end; r0 += kCrossKC) {
+    __syncthreads();
+    // stage: lanes along rows (64 consecutive rows of one column per two warps' worth of lanes)
+    for (int e = tid; e < kCrossKC * p; e += kCrossThreads) {
+      const int kk = e % kCrossKC, j = e / kCrossKC;
+      const int64_t r = r0 + kk;
+      sA[j * kCrossPitch + kk] = r < end ? (double)A[r + (int64_t)j * lda] : 0.0;
+    }
+    if (!sym)
+      for (int e = tid; e < kCrossKC * q; e += kCrossThreads) {
+        const int kk = e % kCrossKC, j = e / kCrossKC;
+        const int64_t r = r0 + kk;
+        sB[j * kCrossPitch + kk] = r < end ? (double)B[r + (int64_t)j * ldb] : 0.0;
+      }
+    __syncthreads();
+    if (active) {
+      const int kb = kg * kper;
+      for (int k0 = kb; k0 < kb + kper; k0 += 4) {
+        const double a0 = (m0 + g < p) ? sA[(m0 + g) * kCrossPitch + k0 + t] : 0.0;
+        const double a1 = (m0 + g + 8 < p) ? sA[(m0 + g + 8) * kCrossPitch + k0 + t] : 0.0;
+#pragma unroll
+        for (int nn = 0; nn < 8; ++nn) {
+          if (nn < nt && !(sym && 8 * (nn + 1) <= m0)) {
+            const int col = nn * 8 + g;
+            const double b0 = col < q ? sB[col * kCrossPitch + k0 + t] : 0.0;
+            asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                         : "+d"(acc[nn][0]), "+d"(acc[nn][1]), "+d"(acc[nn][2]), "+d"(acc[nn][3])
+                         : "d"(a0), "d"(a1), "d"(b0));
+          }
+        }
+      }
+    }
+  }
+  // CTA reduction over the k-groups in group order (through shared memory)
+  __syncthreads();
+  double* red = cross_sm;  // [groups][16 mt x 64], reuses the staging area (sized by the launcher)
+  const size_t gstride = (size_t)16 * mt * 64;
+  if (active) {
+#pragma unroll
+    for (int nn = 0; nn < 8; ++nn) {
+      if (nn < nt) {
+        const int c0 = nn * 8 + 2 * t;
+        double* d = red + (size_t)kg * gstride;
+        d[(m0 + g) * 64 + c0] = acc[nn][0];
+        d[(m0 + g) * 64 + c0 + 1] = acc[nn][1];
+        d[(m0 + g + 8) * 64 + c0] = acc[nn][2];
+        d[(m0 + g + 8) * 64 + c0 + 1] = acc[nn][3];
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < p * q; e += kCrossThreads) {
+    const int i = e % p, j = e / p;
+    double v = 0.0;
+    for (int w = 0; w < groups; ++w) v += red[(size_t)w * gstride + i * 64 + j];
+    ws[(int64_t)blockIdx.x * p * q + e] = v;  // column-major p x q partial
+  }
+}
+
+__global__ void cross_dmma_reduce(const double* __restrict__ ws, int parts, int p, int q, int sym, double beta,
+                                  double* __restrict__ out, int64_t ldo) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= p * q) return;
+  const int i = e % p, j = e / p;
+  if (sym && i > j) return;  // written by (j, i)
+  double v = 0.0;
+  for (int c = 0; c < parts; ++c) v += ws[(int64_t)c * p * q + e];
+  double* o = out + i + (int64_t)j * ldo;
+  *o = beta == 0.0 ? v : v + beta * *o;
+  if (sym && i < j) {
+    double* o2 = out + j + (int64_t)i * ldo;
+    *o2 = beta == 0.0 ? v : v + beta * *o2;
+  }
+}
+
+template <typename TA, typename TB>
+int cross_dmma(int64_t n, int p, int q, const TA* A, int64_t lda, const TB* B, int64_t ldb, double beta, double* out,
+               int64_t ldo, void* ws, size_t wsb, cudaStream_t st) {
+  const bool sym = (const void*)A == (const void*)B && p == q && lda == ldb && std::is_same<TA, TB>::value;
+  const size_t per = (size_t)p * q * sizeof(double);
+  int ctas = (int)std::min<int64_t>(2 * (int64_t)sm_count(), std::max<int64_t>(1, (n + kCrossKC - 1) / kCrossKC));
+  if ((size_t)ctas * per > wsb) ctas = (int)std::max<size_t>(1, wsb / per);
+  RB_REQUIRE(ws && (size_t)ctas * per <= wsb, "rb_cross: workspace too small");
+  int64_t rows = (n + ctas - 1) / ctas;
+  rows = (rows + kCrossKC - 1) / kCrossKC * kCrossKC;
+  ctas = (int)std::max<int64_t>(1, (n + rows - 1) / rows);
+  const int mt = (p + 15) / 16, groups = 8 / mt;
+  const size_t stage = (size_t)(sym ? 1 : 2) * 64 * kCrossPitch * sizeof(double);
+  const size_t smem = std::max(stage, (size_t)groups * 16 * mt * 64 * sizeof(double));
+  cudaFuncSetAttribute(cross_dmma_partial<TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  RB_KLAUNCH cross_dmma_partial<TA, TB><<<ctas, kCrossThreads, smem, st>>>(n, p, q, A, lda, B, ldb, rows, sym ? 1 : 0,
+                                                                           (double*)ws);
+  RB_KLAUNCH cross_dmma_reduce<<<ceil_div((int64_t)p * q, 256), 256, 0, st>>>((const double*)ws, ctas, p, q, sym ? 1 : 0,
+                                                                              beta, out, ldo);
+  return check_launch("rb_cross (dmma)");
+}
+
 int cross(int ad, int bd, int64_t n, int p, int q, const void* A, int64_t lda, const void* B, int64_t ldb,
           double* out, int64_t ldo, int acc, void* ws, size_t wsb, cudaStream_t st) {
   RB_REQUIRE(n >= 0 && p >= 1 && q >= 1 && out && ldo >= p, "rb_cross: bad args");
@@ -488,6 +620,16 @@ int cross(int ad, int bd, int64_t n, int p, int q, const void* A, int64_t lda, c
     if (bd == RB_F32)
       return cross_small<double, float>(n, p, q, (const double*)A, lda, (const float*)B, ldb, beta, out, ldo, ws, wsb, st);
     return cross_small<double, double>(n, p, q, (const double*)A, lda, (const double*)B, ldb, beta, out, ldo, ws, wsb, st);
+  }
+  static const int use_dmma = getenv("RB_CROSS_DMMA") ? atoi(getenv("RB_CROSS_DMMA")) : 1;
+  if (use_dmma && p <= 64 && q <= 64 && n > 0) {
+    if (ad == RB_F32 && bd == RB_F32)
+      return cross_dmma<float, float>(n, p, q, (const float*)A, lda, (const float*)B, ldb, beta, out, ldo, ws, wsb, st);
+    if (ad == RB_F32)
+      return cross_dmma<float, double>(n, p, q, (const float*)A, lda, (const double*)B, ldb, beta, out, ldo, ws, wsb, st);
+    if (bd == RB_F32)
+      return cross_dmma<double, float>(n, p, q, (const double*)A, lda, (const float*)B, ldb, beta, out, ldo, ws, wsb, st);
+    return cross_dmma<double, double>(n, p, q, (const double*)A, lda, (const double*)B, ldb, beta, out, ldo, ws, wsb, st);
   }
   if (ad == RB_F32 && bd == RB_F32)
     return gemm_t<float, float>(1, 0, p, q, n, 1.0, (const float*)A, lda, (const float*)B, ldb, beta, out, ldo, ws, wsb, st);

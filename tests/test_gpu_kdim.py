@@ -123,3 +123,26 @@ def test_syrk_upper_vs_numpy(D, n, k):
     assert np.all(np.abs(got[iu] - want[iu]) <= 4 * k * 2.0 ** -53 * (np.abs(A).T @ np.abs(A))[iu])
     if n == 244:  # tile (rows 128.., cols 0..63) lies below the diagonal: untouched
         assert np.all(got[128:, :64] == 7.0)
+
+
+@pytest.mark.parametrize("n,p,q,sym", [(100_003, 40, 40, True), (65536, 64, 64, True), (5000, 16, 16, True),
+                                       (33_000, 33, 20, False), (70_000, 64, 9, False), (64, 48, 48, True)])
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_cross_dmma_vs_numpy(D, n, p, q, sym, dt):
+    """rb_cross for 8 < max(p, q) <= 64 (the l2 stage's tall Gram Q'^T Q',
+    rbgs.py:293-302) on the FP64 tensor pipe, Gram (mirrored upper tiles) and
+    general A^T B, accumulate flag included."""
+    g = np.random.Generator(np.random.Philox(n + p))
+    A = g.standard_normal((n, p))
+    B = A if sym else g.standard_normal((n, q))
+    Ad = _dev(A, dt)
+    Bd = Ad if sym else _dev(B, dt)
+    Aw = Ad.double().cpu().numpy()
+    Bw = Aw if sym else Bd.double().cpu().numpy()
+    want = Aw.T @ Bw
+    bound = 4 * n * 2.0 ** -53 * (np.abs(Aw).T @ np.abs(Bw))
+    out = _dev(np.ones((p, q)), torch.float64)
+    D.cross(Ad, Bd, out)
+    assert np.all(np.abs(out.cpu().numpy() - want) <= bound)
+    D.cross(Ad, Bd, out, accumulate=True)
+    assert np.all(np.abs(out.cpu().numpy() - 2 * want) <= 2 * bound)
