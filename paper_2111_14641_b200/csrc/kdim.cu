@@ -50,6 +50,8 @@ __device__ __forceinline__ void kdim_mark(int slot) {
 namespace rb {
 
 int sm_count();
+int cross(int ad, int bd, int64_t n, int p, int q, const void* A, int64_t lda, const void* B, int64_t ldb,
+          double* out, int64_t ldo, int acc, void* ws, size_t wsb, cudaStream_t st);
 
 namespace {
 
@@ -927,6 +929,68 @@ gemm_tiles(int m, int n, int64_t K, const T* __restrict__ A, int64_t lda, const 
   }
 }
 
+// Tall binary64 product C (M x N) = alpha A (M x K) B (K x N) + beta C for
+// M >> N, K (the GMRES corrections U = Q Z, krylov.py:247-262: 1.7e7 x 244
+// times 244 x 240) on the FP64 tensor pipe: a CTA owns 128 rows x 64 columns,
+// a warp 16 rows and all eight 8-column tiles (mma.sync m16n8k4 f64: one A
+// fragment per k-step serves them); A and B chunks of 32 k are staged in
+// shared memory with pitches (136, 36) that make staging stores and fragment
+// loads conflict-free.  k ascending per output: deterministic.
+constexpr int kNNM = 128, kNNN = 64, kNNK = 32, kNNPA = 136, kNNPB = 36;
+
+__global__ void __launch_bounds__(256, 2)
+gemm_nn_dmma(int64_t M, int N, int K, double alpha, const double* __restrict__ A, int64_t lda,
+             const double* __restrict__ B, int64_t ldb, double beta, double* __restrict__ C, int64_t ldc) {
+  extern __shared__ double nn_sm[];
+  double* sA = nn_sm;                    // [kNNK][kNNPA]: (k, row)
+  double* sB = nn_sm + kNNK * kNNPA;     // [kNNN][kNNPB]: (col, k)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int64_t m0 = (int64_t)blockIdx.x * kNNM;
+  const int n0 = blockIdx.y * kNNN;
+  double acc[8][4];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+  for (int k0 = 0; k0 < K; k0 += kNNK) {
+    __syncthreads();
+    for (int e = tid; e < kNNK * kNNM; e += 256) {
+      const int i = e % kNNM, kk = e / kNNM;
+      sA[kk * kNNPA + i] = (m0 + i < M && k0 + kk < K) ? A[(m0 + i) + (int64_t)(k0 + kk) * lda] : 0.0;
+    }
+    for (int e = tid; e < kNNK * kNNN; e += 256) {
+      const int kk = e % kNNK, j = e / kNNK;
+      sB[j * kNNPB + kk] = (n0 + j < N && k0 + kk < K) ? B[(k0 + kk) + (int64_t)(n0 + j) * ldb] : 0.0;
+    }
+    __syncthreads();
+    const int r = warp * 16 + g;
+#pragma unroll
+    for (int ks = 0; ks < kNNK; ks += 4) {
+      const double a0 = sA[(ks + t) * kNNPA + r];
+      const double a1 = sA[(ks + t) * kNNPA + r + 8];
+#pragma unroll
+      for (int nn = 0; nn < 8; ++nn) {
+        const double b0 = sB[(nn * 8 + g) * kNNPB + ks + t];
+        asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+                     : "+d"(acc[nn][0]), "+d"(acc[nn][1]), "+d"(acc[nn][2]), "+d"(acc[nn][3])
+                     : "d"(a0), "d"(a1), "d"(b0));
+      }
+    }
+  }
+#pragma unroll
+  for (int nn = 0; nn < 8; ++nn) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int64_t i = m0 + warp * 16 + g + (h >> 1) * 8;
+      const int j = n0 + nn * 8 + 2 * t + (h & 1);
+      if (i < M && j < N) {
+        double* c = C + i + (int64_t)j * ldc;
+        *c = beta == 0.0 ? alpha * acc[nn][h] : alpha * acc[nn][h] + beta * *c;
+      }
+    }
+  }
+}
+
 template <typename T>
 __global__ void gemm_reduce(const T* __restrict__ ws, int splits, int m, int n, T alpha, T beta, T* __restrict__ C,
                             int64_t ldc, int upper) {
@@ -945,6 +1009,18 @@ template <typename T>
 int gemm_generic(int tA, int m, int n, int64_t K, T alpha, const T* A, int64_t lda, const T* B, int64_t ldb, T beta,
                  T* C, int64_t ldc, void* ws, size_t wsb, cudaStream_t st, const char* what, int upper = 0) {
   if (m == 0 || n == 0) return RB_OK;
+  if constexpr (std::is_same<T, double>::value) {
+    // tall outputs only: the k-dimensional products keep their own summation order
+    static const int nn_dmma = getenv("RB_GEMM_DMMA") ? atoi(getenv("RB_GEMM_DMMA")) : 1;
+    if (nn_dmma && !tA && !upper && m >= 65536 && K >= 1 && K <= 4096) {
+      const size_t smem = (size_t)(kNNK * kNNPA + kNNN * kNNPB) * sizeof(double);
+      cudaFuncSetAttribute(gemm_nn_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      const dim3 grid((unsigned)((m + kNNM - 1) / kNNM), (unsigned)((n + kNNN - 1) / kNNN));
+      RB_KLAUNCH gemm_nn_dmma<<<grid, 256, smem, st>>>((int64_t)m, n, (int)K, (double)alpha, (const double*)A, lda,
+                                                       (const double*)B, ldb, (double)beta, (double*)C, ldc);
+      return check_launch(what);
+    }
+  }
   const int mt = (m + kGM - 1) / kGM, nt = (n + kGN - 1) / kGN;
   const int64_t tiles = (int64_t)mt * nt;
   const int64_t want = 2 * (int64_t)sm_count();
@@ -1154,6 +1230,24 @@ int gemm_f32(int tA, int tB, int m, int n, int k, float alpha, const float* A, i
 int syrk_f64(int n, int64_t k, double alpha, const double* A, int64_t lda, double beta, double* C, int64_t ldc,
              void* ws, size_t wsb, cudaStream_t st) {
   RB_REQUIRE(n >= 0 && k >= 0 && C && ldc >= std::max(n, 1) && (k == 0 || (A && lda >= k)), "rb_syrk_f64: bad args");
+  // alpha = 1, beta in {0, 1} (the GMRES basis Gram): 64-column blocks on
+  // the FP64 tensor pipe (rb_cross: mma.sync m16n8k4 f64), upper block pairs
+  // only -- the strictly lower blocks of C are left untouched.  Each pair
+  // re-reads its two column slabs (10 pairs at n = 244: 170 GB at the C4
+  // size, 27 ms of HBM time against 134 ms for the CUDA-core tile kernel).
+  static const int blk = getenv("RB_SYRK_BLOCKS") ? atoi(getenv("RB_SYRK_BLOCKS")) : 1;
+  if (blk && alpha == 1.0 && (beta == 0.0 || beta == 1.0) && k > 0 && n > 0) {
+    for (int bi = 0; bi < n; bi += 64) {
+      const int wi = std::min(64, n - bi);
+      for (int bj = bi; bj < n; bj += 64) {
+        const int wj = std::min(64, n - bj);
+        const int rc = cross(RB_F64, RB_F64, k, wi, wj, A + (int64_t)bi * lda, lda, A + (int64_t)bj * lda, lda,
+                             C + bi + (int64_t)bj * ldc, ldc, beta == 1.0 ? 1 : 0, ws, wsb, st);
+        if (rc != RB_OK) return rc;
+      }
+    }
+    return RB_OK;
+  }
   // tiles entirely below the diagonal are skipped (C's strictly lower tiles
   // are left untouched): 6 of 8 tiles at n = 244
   return gemm_generic<double>(1, n, n, k, alpha, A, lda, A, lda, beta, C, ldc, ws, wsb, st, "rb_syrk_f64", 1);

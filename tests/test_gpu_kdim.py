@@ -121,7 +121,7 @@ def test_syrk_upper_vs_numpy(D, n, k):
     want = A.T @ A
     iu = np.triu_indices(n)
     assert np.all(np.abs(got[iu] - want[iu]) <= 4 * k * 2.0 ** -53 * (np.abs(A).T @ np.abs(A))[iu])
-    if n == 244:  # tile (rows 128.., cols 0..63) lies below the diagonal: untouched
+    if n == 244:  # the block (rows 128.., cols 0..63) lies below the diagonal: untouched
         assert np.all(got[128:, :64] == 7.0)
 
 
