@@ -339,3 +339,22 @@ def test_devarray_is_numpy_compatible():
     assert np.array_equal(Matrix(d).data, A) and np.array_equal(as_array(d), A)
     d[0:1, 0:2] = np.array([[7.0, 8.0]])
     assert t[0, 0].item() == 7.0 and t[0, 1].item() == 8.0
+
+
+def test_device_knobs_validate_without_a_gpu():
+    """Round-2 device-only knobs: operator digits and the rb_sketch_gaussian
+    mode they select; block_gmres diagnostics modes are validated before any
+    device work."""
+    from paper_2111_14641_b200 import krylov, sketching
+    from paper_2111_14641_b200._device import GAUSS_MODE
+
+    op = sketching.gaussian_operator(8, 64, 1)
+    assert op.digits == 6 and sketching.gauss_mode(op) in ("auto", sketching.GAUSS_MODE)
+    if sketching.GAUSS_MODE == "auto":
+        assert sketching.gauss_mode(sketching.gaussian_operator(8, 64, 1, digits=4)) == "tensor4"
+        assert sketching.gauss_mode(op, 3) == "tensor3"
+    assert GAUSS_MODE["tensor4"] == 4 and GAUSS_MODE["tensor3"] == 5
+    with pytest.raises(ValueError):
+        sketching.gaussian_operator(8, 64, 1, digits=5)
+    with pytest.raises(ValueError):
+        krylov.block_gmres(None, None, None, 4, diagnostics="none")
