@@ -24,8 +24,10 @@ import os
 
 _CORES = len(os.sched_getaffinity(0))
 if "--impl" in os.sys.argv and "reference" in os.sys.argv:
+    # all host threads for the CPU arm (torchrun presets OMP_NUM_THREADS=1 for
+    # its workers; only rank 0 runs this arm)
     for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
-        os.environ.setdefault(_v, str(_CORES))
+        os.environ[_v] = str(_CORES)
 
 import argparse  # noqa: E402
 import json  # noqa: E402
