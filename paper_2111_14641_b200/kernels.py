@@ -14,9 +14,10 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
-from .errors import ShapeError
+from .errors import NotPositiveDefiniteError, ShapeError, SingularTriangularError
 
-__all__ = ["PrecisionSpec", "COARSE", "FINE", "Matrix", "BlockPartition", "as_array", "cond_estimate"]
+__all__ = ["PrecisionSpec", "COARSE", "FINE", "Matrix", "BlockPartition", "as_array", "cond_estimate",
+           "gemm", "householder_qr", "cholesky", "triangular_solve"]
 
 
 @dataclass(frozen=True)
@@ -240,3 +241,148 @@ def cond_estimate(A, device=None) -> float:
     from .post import cond_estimate as _ce
 
     return _ce(A, device)
+
+
+# ---------------------------------------------------------------------------
+# The reference's kernel-level entry points (kernels.py:171-270) on the device.
+# The sweep calls the device kernels directly; these wrappers keep the module
+# API for callers that use them standalone.
+
+
+def _dev_cm(X, dtype, device=None):
+    from . import _device as D
+
+    if isinstance(X, Matrix):
+        X = X._dev if X._dev is not None else X.data
+    if isinstance(X, DevArray):
+        X = X.tensor
+    if isinstance(X, torch.Tensor):
+        t = X if X.dim() == 2 else X.reshape(-1, 1)
+        return D.to_cm(t, dtype, device if device is not None else (t.device if t.is_cuda else None))
+    return D.to_cm(torch.from_numpy(np.asfortranarray(as_array(X))), dtype, device)
+
+
+def gemm(alpha: float, A, B, beta: float = 0.0, C=None, prec: PrecisionSpec = FINE, device=None) -> Matrix:
+    """fl(alpha A B + beta C) with every elementary multiply / add rounded per
+    `prec`, l ascending (kernels.py:171-209) -- bit-identical to the
+    reference.  alpha = +-1 (every call of the RBGS path) runs on rb_project's
+    separately-rounded multiply-add kernels in 64-column slabs; any other
+    alpha keeps the reference's extra rounding fl(alpha fl(a b)) with one
+    elementwise device pass per l."""
+    from . import _device as D
+    from ._lib import F32, F64, ORDER_REFERENCE, require_cuda
+
+    require_cuda()
+    Ad = _dev_cm(A, prec.torch_dtype, device)
+    dev = Ad.device
+    Bd = _dev_cm(B, torch.float64, dev)
+    if Ad.shape[1] != Bd.shape[0]:
+        raise ShapeError(f"gemm inner dimensions disagree: {tuple(Ad.shape)} x {tuple(Bd.shape)}")
+    n, m = Ad.shape[0], Bd.shape[1]
+    dt = prec.torch_dtype
+    if C is not None:
+        Cd = _dev_cm(C, torch.float64, dev)
+        if tuple(Cd.shape) != (n, m):
+            raise ShapeError(f"gemm C has shape {tuple(Cd.shape)}, expected {(n, m)}")
+    elif beta != 0.0:
+        raise ShapeError("gemm beta != 0 requires C")
+    with torch.cuda.device(dev):
+        acc = D.zeros_cm(n, m, dt, dev)
+        if C is not None and beta != 0.0:
+            acc.copy_(Cd)  # rounds to prec.dtype like C.astype(dt)
+            if beta != 1.0:
+                acc.mul_(torch.tensor(beta, dtype=dt, device=dev))
+        K = Ad.shape[1]
+        if K and alpha in (1.0, -1.0):
+            compute = F32 if prec.format == "coarse" else F64
+            X = Bd if alpha == -1.0 else D.to_cm(-Bd)  # acc - A (-B): negation is exact
+            for j in range(0, m, 64):
+                D.project(Ad, X[:, j:j + 64], acc[:, j:j + 64], acc[:, j:j + 64], compute, ORDER_REFERENCE)
+        elif K:
+            a = torch.tensor(alpha, dtype=dt, device=dev)
+            Bt = Bd.to(dt)
+            for l in range(K):
+                term = Ad[:, l:l + 1] * Bt[l:l + 1, :]
+                acc += a * term
+        return Matrix(D.to_cm(acc, torch.float64), precision=prec)
+
+
+def householder_qr(A, device=None) -> tuple:
+    """Economic Householder QR with diag(R) >= 0 (kernels.py:216-231) on the
+    device (single-CTA Householder kernel: meant for the k-dimensional
+    problems of the path; a tall n runs, slowly)."""
+    from . import _device as D
+    from ._lib import require_cuda
+
+    require_cuda()
+    Ad = _dev_cm(A, torch.float64, device)
+    n, m = Ad.shape
+    if n < m:
+        raise ShapeError(f"householder_qr requires rows >= cols, got {(n, m)}")
+    with torch.cuda.device(Ad.device):
+        Q = D.empty_cm(n, m, torch.float64, Ad.device)
+        Q.copy_(Ad)
+        R = D.zeros_cm(m, m, torch.float64, Ad.device)
+        D.geqrf(Q, R)
+    return Matrix(Q), Matrix(R)
+
+
+def cholesky(G, device=None) -> Matrix:
+    """Upper-triangular R with R^T R = G (kernels.py:234-247), dpotrf
+    semantics: NotPositiveDefiniteError(column) at the first bad pivot."""
+    from . import _device as D
+    from ._lib import require_cuda
+
+    require_cuda()
+    Gd = _dev_cm(G, torch.float64, device)
+    n, m = Gd.shape
+    if n != m:
+        raise ShapeError(f"cholesky requires a square matrix, got {(n, m)}")
+    if n > 128:
+        raise ShapeError(f"cholesky on the device handles n <= 128 (block-sized Gram matrices), got {n}")
+    with torch.cuda.device(Gd.device):
+        tol = 1e-10 * max(1.0, float(Gd.abs().max()))
+        if float((Gd - Gd.t()).abs().max()) > tol:
+            raise ShapeError("cholesky input is not symmetric")
+        R = D.zeros_cm(n, n, torch.float64, Gd.device)
+        info = torch.zeros(1, dtype=torch.int32, device=Gd.device)
+        D.potrf(Gd, R, info)
+        bad = int(info.item())
+    if bad > 0:
+        raise NotPositiveDefiniteError(bad)
+    return Matrix(R)
+
+
+def triangular_solve(R, B, side: str = "left", device=None) -> Matrix:
+    """Solve R X = B ('left') or X R = B ('right') for upper-triangular R
+    (kernels.py:250-270)."""
+    from . import _device as D
+    from ._lib import require_cuda
+
+    require_cuda()
+    Rd = _dev_cm(R, torch.float64, device)
+    n = Rd.shape[0]
+    if Rd.shape[1] != n:
+        raise ShapeError(f"triangular_solve requires square R, got {tuple(Rd.shape)}")
+    Bd = _dev_cm(B, torch.float64, Rd.device)
+    d = Rd.diagonal().abs()
+    if bool((d == 0.0).any()):
+        raise SingularTriangularError(int(torch.argmax((d == 0.0).to(torch.int32)).item()))
+    with torch.cuda.device(Rd.device):
+        if side == "left":
+            if Bd.shape[0] != n:
+                raise ShapeError(f"RX=B shape mismatch: {tuple(Rd.shape)} vs {tuple(Bd.shape)}")
+            X = D.empty_cm(Bd.shape[0], Bd.shape[1], torch.float64, Rd.device)
+            X.copy_(Bd)
+            info = torch.zeros(1, dtype=torch.int32, device=Rd.device)
+            D.trsm_left_upper(Rd, X, info)
+        elif side == "right":
+            if Bd.shape[1] != n:
+                raise ShapeError(f"XR=B shape mismatch: {tuple(Bd.shape)} vs {tuple(Rd.shape)}")
+            if n > 64:
+                raise ShapeError(f"right solves on the device handle n <= 64 (one block), got {n}")
+            X = D.empty_cm(Bd.shape[0], n, torch.float64, Rd.device)
+            D.trsm_right(Bd, Rd, X)
+        else:
+            raise ValueError(f"side must be 'left' or 'right', got {side!r}")
+    return Matrix(X)

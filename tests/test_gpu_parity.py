@@ -760,3 +760,64 @@ def test_repeat_and_two_stream_determinism(pkg):
         assert len(outs) == 6
         for f in outs:
             assert np.array_equal(f.R.data, Rb) and np.array_equal(f.Q.data, Qb), order
+
+
+@pytest.mark.parametrize("fmt", ["coarse", "fine"])
+def test_kernels_gemm_bit_identical_to_reference_order(pkg, fmt):
+    """kernels.gemm (kernels.py:171-209) on the device: every alpha / beta
+    branch of the reference loop, bit for bit against the oracle's
+    restatement (itself pinned bit-exact to the reference's golden vectors)."""
+    from paper_2111_14641_b200 import kernels as K
+    from paper_2111_14641_b200.errors import ShapeError
+
+    prec = K.COARSE if fmt == "coarse" else K.FINE
+    g = np.random.Generator(np.random.Philox(31))
+    for n, kk, m in [(257, 33, 5), (1024, 96, 70), (64, 1, 3)]:
+        A, B, C = g.standard_normal((n, kk)), g.standard_normal((kk, m)), g.standard_normal((n, m))
+        for alpha, beta, Cin in [(-1.0, 1.0, C), (1.0, 0.0, None), (1.0, 1.0, C), (-1.0, 2.5, C), (0.5, 1.0, C),
+                                 (-2.0, 0.0, None)]:
+            got = K.gemm(alpha, A, B, beta, Cin, prec).data
+            want = osw.gemm_ordered(alpha, A, B, beta, Cin, fmt)
+            assert np.array_equal(got, want), (fmt, n, kk, m, alpha, beta)
+    with pytest.raises(ShapeError):
+        K.gemm(1.0, np.ones((3, 2)), np.ones((3, 2)))
+    with pytest.raises(ShapeError):
+        K.gemm(1.0, np.ones((3, 2)), np.ones((2, 2)), beta=1.0)
+
+
+def test_kernels_factorizations_vs_oracle(pkg):
+    """kernels.householder_qr / cholesky / triangular_solve (kernels.py:216-270)
+    on the device: values against the oracle's LAPACK restatement, errors with
+    the reference's classes and attributes."""
+    from paper_2111_14641_b200 import kernels as K
+    from paper_2111_14641_b200.errors import NotPositiveDefiniteError, ShapeError, SingularTriangularError
+
+    g = np.random.Generator(np.random.Philox(32))
+    A = g.standard_normal((300, 12))
+    Q, R = K.householder_qr(A)
+    Qo, Ro = osw.householder_qr(A)
+    assert np.all(np.diag(R.data) >= 0) and np.allclose(R.data, Ro, rtol=0, atol=1e-12 * np.abs(Ro).max())
+    assert np.allclose(Q.data, Qo, rtol=0, atol=1e-12) and np.allclose(Q.data @ R.data, A, atol=1e-12)
+    with pytest.raises(ShapeError):
+        K.householder_qr(np.ones((2, 3)))
+    G = A.T @ A
+    Rc = K.cholesky(G).data
+    assert np.allclose(Rc, osw.cholesky_upper(G), rtol=1e-12, atol=1e-12) and np.array_equal(Rc, np.triu(Rc))
+    Gb = G.copy()
+    Gb[4, 4] = -1.0
+    with pytest.raises(NotPositiveDefiniteError) as e:
+        K.cholesky(Gb)
+    assert e.value.column == 5
+    with pytest.raises(ShapeError):
+        K.cholesky(np.triu(G) + 1.0)
+    Bl, Br = g.standard_normal((12, 4)), g.standard_normal((500, 12))
+    assert np.allclose(K.triangular_solve(Ro, Bl).data, osw.trsm(Ro, Bl, "left"), rtol=1e-10, atol=1e-12)
+    assert np.allclose(K.triangular_solve(Ro, Br, side="right").data, osw.trsm(Ro, Br, "right"), rtol=1e-10,
+                       atol=1e-12)
+    Rs = Ro.copy()
+    Rs[3, 3] = 0.0
+    with pytest.raises(SingularTriangularError) as e:
+        K.triangular_solve(Rs, Bl)
+    assert e.value.index == 3
+    with pytest.raises(ValueError):
+        K.triangular_solve(Ro, Bl, side="up")

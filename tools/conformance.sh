@@ -11,7 +11,7 @@ case "${1:-}" in
 stage)
   rm -rf $DIR; mkdir -p $DIR/tests
   cp -r /root/reference/pkg/src/sketch_krylov $DIR/sketch_krylov
-  for f in conftest.py oracles.py test_rbgs.py test_sketching.py test_krylov.py; do
+  for f in conftest.py oracles.py test_rbgs.py test_sketching.py test_krylov.py test_kernels.py test_operators.py; do
     cp /root/reference/pkg/tests/$f $DIR/tests/
   done
   ;;
@@ -23,7 +23,7 @@ run)
   cd $DIR/tests
   timeout 2400 python -m pytest -p rb_conformance_plugin -q --no-header -rA -p no:cacheprovider \
     --deselect test_rbgs.py::test_rbgs_coarse_cg_less_stable_than_direct_solver_at_scale ${CONF_ARGS:-} \
-    test_rbgs.py test_sketching.py test_krylov.py 2>&1 | grep -v "^$" > $OLDPWD/gpurun_out/${TAG}_conformance.log
+    test_rbgs.py test_sketching.py test_krylov.py test_kernels.py test_operators.py 2>&1 | grep -v "^$" > $OLDPWD/gpurun_out/${TAG}_conformance.log
   echo "rc=${PIPESTATUS[0]}" >> $OLDPWD/gpurun_out/${TAG}_conformance.log
   ;;
 clean)
