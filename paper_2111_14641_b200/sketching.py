@@ -31,7 +31,8 @@ from .errors import ShapeError
 from .kernels import Matrix, as_array
 
 __all__ = ["KINDS", "EXTENDED_KINDS", "SketchOperator", "make_operator", "apply", "sketch_into",
-           "gaussian_operator", "sparse_sign_operator", "to_line", "from_line"]
+           "gaussian_operator", "sparse_sign_operator", "to_line", "from_line", "srht_apply", "materialize",
+           "gauss_mode"]
 
 KINDS = ("rademacher", "srht", "identity")
 EXTENDED_KINDS = ("gaussian", "sparse_sign")
@@ -227,6 +228,34 @@ def apply(theta: SketchOperator, X, device=None) -> Matrix:
     with torch.cuda.device(Xd.device):
         sketch_into(theta, Xd, out)
     return Matrix(out)
+
+
+def srht_apply(X, sign_diagonal, sample_indices, k: int, device=None):
+    """Core SRHT path (sketching.py:129-137): zero-pad to len(sign_diagonal),
+    sign-flip, Walsh-Hadamard transform (the pruned warp FWHT, same stage
+    order as `_fwht_rows`), subsample, scale 1 / sqrt(k).  Returns the
+    k x cols numpy array like the reference (the device result downloaded)."""
+    A = as_array(X)
+    signs = np.asarray(sign_diagonal, dtype=np.float64)
+    n_pad = len(signs)
+    if n_pad & (n_pad - 1) or n_pad < A.shape[0]:
+        raise ShapeError(f"sign diagonal of length {n_pad} must be a power of two >= rows {A.shape[0]}")
+    sample = np.asarray(sample_indices, dtype=np.int64)
+    Xd = D.to_cm(torch.from_numpy(np.asfortranarray(A)), torch.float64, device)
+    dev = Xd.device
+    words = -(-n_pad // 2048) * 64
+    bits = torch.from_numpy(_pack_bits(signs < 0, words).view(np.int32)).to(dev)
+    out = D.empty_cm(len(sample), Xd.shape[1], torch.float64, dev)
+    with torch.cuda.device(dev):
+        for j in range(0, Xd.shape[1], 64):
+            D.sketch_srht(Xd[:, j:j + 64], 0, n_pad, bits, torch.from_numpy(sample).to(dev), len(sample),
+                          1.0 / math.sqrt(k), out[:, j:j + 64], False)
+    return out.cpu().numpy()
+
+
+def materialize(theta: SketchOperator, device=None) -> np.ndarray:
+    """Dense k x n realization (sketching.py:158-160); test-scale diagnostics only."""
+    return apply(theta, np.eye(theta.n), device).data
 
 
 def to_line(theta: SketchOperator) -> str:

@@ -821,3 +821,38 @@ def test_kernels_factorizations_vs_oracle(pkg):
     assert e.value.index == 3
     with pytest.raises(ValueError):
         K.triangular_solve(Ro, Bl, side="up")
+
+
+def test_srht_apply_and_materialize_vs_reference_recipe(pkg):
+    """sketching.srht_apply / materialize (sketching.py:129-160) on the device
+    against the reference recipe restated in numpy (zero-pad, signs, FWHT in
+    ascending-h stage order, subsample, 1 / sqrt(k))."""
+    rbgs, sketching, D = pkg
+
+    def fwht(Z):
+        n = Z.shape[0]
+        h = 1
+        while h < n:
+            Y = Z.reshape(n // (2 * h), 2, -1)
+            a = Y[:, 0, :].copy()
+            Y[:, 0, :] += Y[:, 1, :]
+            Y[:, 1, :] = a - Y[:, 1, :]
+            h *= 2
+        return Z
+
+    g = np.random.Generator(np.random.Philox(41))
+    for n, n_pad, k, cols in [(1, 4, 4, 1), (300, 512, 64, 5), (5000, 8192, 700, 3), (2048, 2048, 1500, 70)]:
+        X = g.standard_normal((n, cols))
+        signs = g.integers(0, 2, n_pad) * 2.0 - 1.0
+        sample = g.permutation(n_pad)[:k]
+        Z = np.zeros((n_pad, cols))
+        Z[:n] = signs[:n, None] * X
+        want = fwht(Z.copy())[sample] / math.sqrt(k)
+        got = sketching.srht_apply(X, signs, sample, k)
+        assert got.shape == want.shape
+        assert np.linalg.norm(got - want) <= 1e-13 * max(np.linalg.norm(want), 1e-300)
+    th = sketching.SketchOperator("srht", 24, 100, 3)
+    M = sketching.materialize(th)
+    Xr = g.standard_normal((100, 4))
+    assert M.shape == (24, 100)
+    assert np.allclose(M @ Xr, sketching.apply(th, Xr).data, rtol=0, atol=1e-12)
