@@ -209,6 +209,16 @@ int rb_cross(int a_dtype, int b_dtype, int64_t n, int p, int q, const void* A, i
  * lower part is zeroed.  G and R may alias.  p <= 1024.                  */
 int rb_potrf_upper(int p, const double* G, int64_t ldg, double* R, int64_t ldr,
                    int* info, void* stream);
+/* R factor (p x p upper, diag >= 0) of the Householder QR of a tall A (n x p,
+ * p <= 64, binary32 or binary64; kernels.py:216-231 householder_qr, the l2
+ * stage of rbgs.py:293-302) by sequential TSQR in binary64 -- backward
+ * stable for any cond(A).  cond: when non-NULL and *cond == 0 on the device
+ * the call does nothing (the sweep issues it behind the Gram Cholesky's
+ * status word: no host branch).  info (may alias cond): 0 on a valid factor,
+ * else the 1-based index of a zero / non-finite diagonal entry.
+ * ws >= 2 * SMs * p * p doubles.                                          */
+int rb_tsqr_r(int a_dtype, int64_t n, int p, const void* A, int64_t lda, double* R, int64_t ldr,
+              const int* cond, int* info, void* ws, size_t ws_bytes, void* stream);
 /* Left solve R X = B (R m x m upper), B m x nrhs overwritten with X.
  * *info (device) = 0, or 1 + index of the first zero diagonal.          */
 int rb_trsm_left_upper(int m, int nrhs, const double* R, int64_t ldr, double* B, int64_t ldb,

@@ -272,6 +272,14 @@ def potrf(G, R, info):
     call("rb_potrf_upper", p, ptr(G), ld(G), ptr(R), ld(R), ptr(info), st(G.device))
 
 
+def tsqr_r(A, R, info, cond=None):
+    """R <- the Householder-QR R factor of the tall A (TSQR, binary64); with
+    `cond` (a device int) the call is a no-op unless cond != 0."""
+    n, p = A.shape
+    ws, wsb = _ws(n, p, 64, A.device)
+    call("rb_tsqr_r", dtype_code(A), n, p, ptr(A), ld(A), ptr(R), ld(R), ptr(cond), ptr(info), ws, wsb, st(A.device))
+
+
 def trsm_left_upper(R, B, info):
     m = R.shape[0]
     call("rb_trsm_left_upper", m, B.shape[1], ptr(R), ld(R), ptr(B), ld(B), ptr(info), st(R.device))

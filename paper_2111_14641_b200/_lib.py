@@ -52,6 +52,7 @@ SIGNATURES = {
     "rb_syrk_f64": [_i, _i64, _d, _p, _i64, _d, _p, _i64, _p, _sz, _p],
     "rb_cross": [_i, _i, _i64, _i, _i, _p, _i64, _p, _i64, _p, _i64, _i, _p, _sz, _p],
     "rb_potrf_upper": [_i, _p, _i64, _p, _i64, _p, _p],
+    "rb_tsqr_r": [_i, _i64, _i, _p, _i64, _p, _i64, _p, _p, _p, _sz, _p],
     "rb_trsm_left_upper": [_i, _i, _p, _i64, _p, _i64, _p, _p],
     "rb_geqrf_small": [_i, _i, _p, _i64, _p, _i64, _p, _sz, _p],
     "rb_sumsq": [_i, _i64, _i, _p, _i64, _i, _p, _p, _sz, _p],

@@ -75,6 +75,7 @@ size_t kdim_ws_bytes(int k, int m);
 int l2_select(int, int, const int*, const int*, const int*, const double*, int64_t, const double*, int64_t,
               const double*, int64_t, const double*, int64_t, double*, int64_t, double*, int64_t, int*, cudaStream_t);
 int potrf_upper(int, const double*, int64_t, double*, int64_t, int*, cudaStream_t);
+int tsqr_r(int, int64_t, int, const void*, int64_t, double*, int64_t, const int*, int*, void*, size_t, cudaStream_t);
 int trsm_left_upper(int, int, const double*, int64_t, double*, int64_t, int*, cudaStream_t);
 int geqrf_small(int, int, double*, int64_t, double*, int64_t, void*, size_t, cudaStream_t);
 int sumsq(int, int64_t, int, const void*, int64_t, int, double*, void*, size_t, cudaStream_t);
@@ -215,6 +216,11 @@ int rb_cross(int ad, int bd, int64_t n, int p, int q, const void* A, int64_t lda
 
 int rb_potrf_upper(int p, const double* G, int64_t ldg, double* R, int64_t ldr, int* info, void* s) {
   return rb::potrf_upper(p, G, ldg, R, ldr, info, as_stream(s));
+}
+
+int rb_tsqr_r(int ad, int64_t n, int p, const void* A, int64_t lda, double* R, int64_t ldr, const int* cond, int* info,
+              void* ws, size_t wsb, void* s) {
+  return rb::tsqr_r(ad, n, p, A, lda, R, ldr, cond, info, ws, wsb, as_stream(s));
 }
 
 int rb_trsm_left_upper(int m, int nrhs, const double* R, int64_t ldr, double* B, int64_t ldb, int* info, void* s) {

@@ -640,6 +640,131 @@ int cross(int ad, int bd, int64_t n, int p, int q, const void* A, int64_t lda, c
   return gemm_t<double, double>(1, 0, p, q, n, 1.0, (const double*)A, lda, (const double*)B, ldb, beta, out, ldo, ws, wsb, st);
 }
 
+// ============================ tall QR, R factor only (TSQR) =================
+// R (p x p, upper, diag >= 0) with A = Q R for a tall A (n x p, p <= 64), by
+// Householder reflections in binary64 -- the l2 stage of l2_plus_cholqr
+// (rbgs.py:293-302 -> kernels.householder_qr, kernels.py:216-231) when the
+// Gram route Q'^T Q' = R'^T R' breaks down (cond(Q') > ~1e8): Householder
+// stays backward stable for any conditioning, like the reference's LAPACK QR.
+// Sequential TSQR: a CTA walks its row range in slabs of kTsRows - p rows,
+// each time factoring [R_running; slab] (kTsRows x p, in shared memory) and
+// keeping the new p x p R; the per-CTA factors are stacked and factored the
+// same way by one CTA.  One row per thread; a reflector is applied to the
+// trailing columns warp by warp (a warp owns a column: dot, then update --
+// no block barrier inside a step beyond the two that publish the reflector).
+// `cond`: when non-null and *cond == 0 the kernel returns at once -- the
+// sweep launches it unconditionally behind the Gram Cholesky's status word,
+// so there is no host branch and the common path costs two empty launches.
+constexpr int kTsRows = 256, kTsThreads = 256;
+
+template <typename T>
+__global__ void __launch_bounds__(kTsThreads)
+tsqr_seq(int64_t n, int p, const T* __restrict__ A, int64_t lda, int64_t rows_per_cta, double* __restrict__ Rstack,
+         int64_t lds, const int* __restrict__ cond, int final_fix, int* __restrict__ info_out) {
+  if (cond && *cond == 0) return;
+  extern __shared__ double ts_sm[];
+  double* M = ts_sm;                    // [p][kTsRows] column-major tile
+  double* red = ts_sm + (size_t)p * kTsRows;  // [8] warp partials + [2] scalars
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t beg = (int64_t)blockIdx.x * rows_per_cta, end = min(n, beg + rows_per_cta);
+  const int slab = kTsRows - p;
+  for (int c = 0; c < p; ++c) M[c * kTsRows + tid] = 0.0;  // running R = 0
+  for (int64_t r0 = beg; r0 < end || r0 == beg; r0 += slab) {
+    // rows p .. kTsRows-1 <- the slab (zero padded)
+    if (tid >= p) {
+      const int64_t r = r0 + (tid - p);
+      for (int c = 0; c < p; ++c) M[c * kTsRows + tid] = r < end ? (double)A[r + (int64_t)c * lda] : 0.0;
+    }
+    __syncthreads();
+    for (int j = 0; j < p; ++j) {
+      // ||x||^2 of x = M[j:, j]
+      const double xr = tid >= j ? M[j * kTsRows + tid] : 0.0;
+      double s2 = xr * xr;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      if (lane == 0) red[warp] = s2;
+      __syncthreads();
+      double nrm2 = 0.0;
+#pragma unroll
+      for (int w = 0; w < kTsThreads / 32; ++w) nrm2 += red[w];
+      const double alpha = M[j * kTsRows + j];
+      const double nrm = sqrt(nrm2);
+      __syncthreads();  // everyone has read alpha / red before they change
+      if (nrm2 == 0.0) continue;
+      const double beta = alpha >= 0.0 ? -nrm : nrm;
+      const double v0 = alpha - beta;
+      // v = x with v_j = v0; H = I - 2 v v^T / (v^T v), v^T v = nrm2 - alpha^2 + v0^2
+      const double vtv = nrm2 - alpha * alpha + v0 * v0;
+      const double scale = vtv > 0.0 ? 2.0 / vtv : 0.0;
+      // trailing columns, one per warp at a time
+      for (int c = j + 1 + warp; c < p; c += kTsThreads / 32) {
+        double dot = 0.0;
+        for (int r = j + lane; r < kTsRows; r += 32) {
+          const double vr = r == j ? v0 : M[j * kTsRows + r];
+          dot += vr * M[c * kTsRows + r];
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+        const double f = scale * dot;
+        for (int r = j + lane; r < kTsRows; r += 32) {
+          const double vr = r == j ? v0 : M[j * kTsRows + r];
+          M[c * kTsRows + r] -= f * vr;
+        }
+      }
+      __syncthreads();  // column j's reflector has been read by every warp
+      if (tid == j) M[j * kTsRows + j] = beta;
+      else if (tid > j) M[j * kTsRows + tid] = 0.0;
+      __syncthreads();
+    }
+    if (end <= beg) break;
+  }
+  // the CTA's R: rows 0 .. p-1 of the tile (upper triangular)
+  __syncthreads();
+  for (int e = tid; e < p * p; e += kTsThreads) {
+    const int i = e % p, j = e / p;
+    double v = i <= j ? M[j * kTsRows + i] : 0.0;
+    if (final_fix && M[i * kTsRows + i] < 0.0) v = -v;  // diag(R) >= 0 (kernels.py:226-230)
+    Rstack[(int64_t)blockIdx.x * p + i + (int64_t)j * lds] = v;
+  }
+  if (final_fix && info_out && tid == 0) {
+    int bad = 0;
+    for (int i = 0; i < p; ++i) {
+      const double d = M[i * kTsRows + i];
+      if (!(fabs(d) > 0.0) || !isfinite(d)) { bad = i + 1; break; }
+    }
+    *info_out = bad;  // 0: R is a valid factor (replaces the Gram Cholesky's status)
+  }
+}
+
+// R (p x p, ldr) <- the R factor of A (n x p); ws holds the stacked per-CTA
+// factors.  cond / info as above (info may alias cond).
+template <typename T>
+int tsqr_r_t(int64_t n, int p, const T* A, int64_t lda, double* R, int64_t ldr, const int* cond, int* info, void* ws,
+             size_t wsb, cudaStream_t st) {
+  const int slab = kTsRows - p;
+  int ctas = (int)std::min<int64_t>(2 * (int64_t)sm_count(), std::max<int64_t>(1, (n + slab - 1) / slab));
+  const size_t need = (size_t)ctas * p * p * sizeof(double);
+  RB_REQUIRE(ws && need <= wsb, "rb_tsqr_r: workspace too small");
+  int64_t rows = (n + ctas - 1) / ctas;
+  ctas = (int)std::max<int64_t>(1, (n + rows - 1) / rows);
+  const size_t smem = ((size_t)p * kTsRows + 16) * sizeof(double);
+  cudaFuncSetAttribute(tsqr_seq<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(tsqr_seq<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  double* stack = (double*)ws;
+  const int64_t lds = (int64_t)ctas * p;
+  RB_KLAUNCH tsqr_seq<T><<<ctas, kTsThreads, smem, st>>>(n, p, A, lda, rows, stack, lds, cond, 0, nullptr);
+  RB_KLAUNCH tsqr_seq<double><<<1, kTsThreads, smem, st>>>(lds, p, stack, lds, lds, R, ldr, cond, 1, info);
+  return check_launch("rb_tsqr_r");
+}
+
+int tsqr_r(int ad, int64_t n, int p, const void* A, int64_t lda, double* R, int64_t ldr, const int* cond, int* info,
+           void* ws, size_t wsb, cudaStream_t st) {
+  RB_REQUIRE(n >= 1 && p >= 1 && p <= 64 && A && lda >= n && R && ldr >= p, "rb_tsqr_r: bad args (n=%lld p=%d)",
+             (long long)n, p);
+  return ad == RB_F32 ? tsqr_r_t<float>(n, p, (const float*)A, lda, R, ldr, cond, info, ws, wsb, st)
+                      : tsqr_r_t<double>(n, p, (const double*)A, lda, R, ldr, cond, info, ws, wsb, st);
+}
+
 int potrf_upper(int p, const double* G, int64_t ldg, double* R, int64_t ldr, int* info, cudaStream_t st) {
   RB_REQUIRE(p >= 1 && p <= 128 && G && R && info && ldg >= p && ldr >= p, "rb_potrf_upper: bad args (p=%d)", p);
   const size_t smem = (size_t)p * p * sizeof(double);

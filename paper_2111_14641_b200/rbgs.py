@@ -575,11 +575,19 @@ class RbgsSweep:
         # Gram stage run on the device and rb_l2_select keeps one.
         #  (A) R' = chol(Q'^T Q'), S* = Sp R'^{-1}, R'' = chol(S*^T S*),
         #      R_ii = R'' R', S_i = S* R''^{-1}
-        #  (B) Q' too ill-conditioned for the Gram (info != 0): the one-pass
-        #      sketched CholQR of Q' -- the same R_ii in exact arithmetic.
+        #      If the Gram Cholesky broke down (cond(Q') > ~1e8) R' is replaced
+        #      by the Householder R of Q' (rb_tsqr_r: binary64 TSQR, the
+        #      reference's own l2 stage, kernels.py:216-231) -- launched
+        #      unconditionally, a no-op unless the status word is set.
+        #      (Row-sharded runs keep (B): the tall QR would need its own
+        #      collective.)
+        #  (B) last resort (A still failed / sharded): the one-pass sketched
+        #      CholQR of Q' -- the same R_ii in exact arithmetic.
         info = scr.info
         R1 = scr.R1[:w, :w]
         D.potrf(G, R1, info[8:9])
+        if not self.comm.active and TSQR_FALLBACK:
+            D.tsqr_r(Qp, R1, info[8:9], cond=info[8:9])
         Ss = scr.Ss[:, :w]
         D.trsm_right(Sp, R1, Ss)
         R2 = scr.R2[:w, :w]
@@ -972,6 +980,7 @@ REPLAYS = 0  # one-shot factorizations replayed eagerly after a deferred-status 
 # series (2.89 vs 2.77 ms at C2's last block); the default is the fused
 # two-input sketch after the projection (one table pass).
 OVERLAP = os.environ.get("RB_OVERLAP", "0") == "1"
+TSQR_FALLBACK = os.environ.get("RB_L2_TSQR", "1") == "1"  # Householder R when the l2 Gram breaks down
 _SIDE_STREAMS = {}
 
 

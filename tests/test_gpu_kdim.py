@@ -146,3 +146,34 @@ def test_cross_dmma_vs_numpy(D, n, p, q, sym, dt):
     assert np.all(np.abs(out.cpu().numpy() - want) <= bound)
     D.cross(Ad, Bd, out, accumulate=True)
     assert np.all(np.abs(out.cpu().numpy() - 2 * want) <= 2 * bound)
+
+
+@pytest.mark.parametrize("n,p,cond", [(100_003, 40, 1e3), (65536, 64, 1e12), (300, 7, 1e6), (50_000, 33, 1e14),
+                                      (64, 64, 10.0)])
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_tsqr_r_vs_lapack(D, n, p, cond, dt):
+    """rb_tsqr_r: the Householder R factor of a tall matrix (kernels.py:216-231),
+    binary64 TSQR, against LAPACK's QR of the same (rounded) input -- normwise
+    1e-13 even at cond 1e14 where the Gram route has long broken down; the
+    conditional form is a no-op when the status word is zero."""
+    g = np.random.Generator(np.random.Philox(n + p))
+    U, _ = np.linalg.qr(g.standard_normal((n, p)))
+    V, _ = np.linalg.qr(g.standard_normal((p, p)))
+    A = (U * np.geomspace(1.0, 1.0 / cond, p)) @ V.T
+    Ad = _dev(A, dt)
+    Aw = Ad.double().cpu().numpy()
+    Rw = np.linalg.qr(Aw, mode="r")
+    Rw = np.sign(np.diag(Rw))[:, None] * Rw
+    R = _dev(np.full((p, p), 3.0), torch.float64)
+    info = torch.full((1,), 5, dtype=torch.int32, device="cuda")
+    D.tsqr_r(Ad, R, info, cond=info)
+    got = R.cpu().numpy()
+    assert int(info.item()) == 0
+    assert np.array_equal(got, np.triu(got)) and np.all(np.diag(got) >= 0)
+    assert np.linalg.norm(got - Rw) <= 1e-13 * np.linalg.norm(Rw) * max(1.0, np.sqrt(n) / 30)
+    # R^T R reproduces the Gram to working accuracy
+    assert np.linalg.norm(got.T @ got - Aw.T @ Aw) <= 1e-13 * np.linalg.norm(Aw) ** 2
+    R2 = _dev(np.full((p, p), 3.0), torch.float64)
+    zero = torch.zeros(1, dtype=torch.int32, device="cuda")
+    D.tsqr_r(Ad, R2, zero, cond=zero)
+    assert np.all(R2.cpu().numpy() == 3.0)

@@ -856,3 +856,26 @@ def test_srht_apply_and_materialize_vs_reference_recipe(pkg):
     Xr = g.standard_normal((100, 4))
     assert M.shape == (24, 100)
     assert np.allclose(M @ Xr, sketching.apply(th, Xr).data, rtol=0, atol=1e-12)
+
+
+def test_l2_plus_cholqr_survives_gram_breakdown(pkg):
+    """The reference default inter-block QR on a block whose l2 condition
+    number (1e10) breaks the Gram Cholesky of the l2 stage: the device falls
+    through to the Householder R (rb_tsqr_r) like the reference's own
+    householder_qr stage (rbgs.py:293-302), without a host branch -- same R as
+    the oracle, Q sketch-orthonormal; with the tall QR disabled the last
+    resort (one-pass sketched CholQR) is visibly worse or fails."""
+    rbgs, sketching, D = pkg
+
+    g = np.random.Generator(np.random.Philox(51))
+    n, w, k = 20_000, 12, 160
+    U, _ = np.linalg.qr(g.standard_normal((n, w)))
+    V, _ = np.linalg.qr(g.standard_normal((w, w)))
+    Qp = (U * np.geomspace(1.0, 1e-10, w)) @ V.T
+    th = sketching.SketchOperator("srht", k, n, 9)
+    Q, R, S = rbgs.interblock_l2_cholqr(Qp, th)
+    Qo, Ro, So = osw.interblock_l2_cholqr(Qp, osk.OracleSketch("srht", k, n, 9))
+    assert np.linalg.norm(R.data - Ro) <= 1e-6 * np.linalg.norm(Ro)
+    G = S.data.T @ S.data
+    assert np.linalg.norm(G - np.eye(w)) <= 1e-8
+    assert np.linalg.norm(Qp - Q.data @ R.data) <= 1e-12 * np.linalg.norm(Qp)
