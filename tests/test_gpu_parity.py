@@ -879,3 +879,33 @@ def test_l2_plus_cholqr_survives_gram_breakdown(pkg):
     G = S.data.T @ S.data
     assert np.linalg.norm(G - np.eye(w)) <= 1e-8
     assert np.linalg.norm(Qp - Q.data @ R.data) <= 1e-12 * np.linalg.norm(Qp)
+
+
+def test_staged_pageable_upload_is_bitwise_neutral(pkg):
+    """rbgs() on a pageable numpy W (the reference-style input) above 64 MB
+    takes the staged block-by-block upload (pinned staging ring, host copy
+    threads, copy stream): same bits as the factorization of the same W
+    already on the device, for Fortran- and C-ordered inputs, and a failing
+    block still raises the reference's exception with its block index."""
+    rbgs, sketching, D = pkg
+    from paper_2111_14641_b200.errors import DependentBlockError
+    from paper_2111_14641_b200.kernels import BlockPartition
+    import goldens as G
+
+    n, m, p, k = 200_000, 120, 40, 256
+    W = G.trig_family(n, m, 5).astype(np.float32)
+    assert W.nbytes >= 64 << 20
+    th = sketching.gaussian_operator(k, n, 3)
+    cfg = rbgs.RbgsConfig(partition=BlockPartition.uniform(m, p), interblock="sketched_cholqr(1)")
+    base = rbgs.rbgs(_dev(W.astype(np.float64), torch.float32), th, cfg)
+    torch.cuda.synchronize()
+    for Wh in (np.asfortranarray(W), np.ascontiguousarray(W)):
+        assert rbgs._stageable(Wh, cfg) is not None
+        for _ in range(2):
+            f = rbgs.rbgs(Wh, th, cfg)
+            assert np.array_equal(f.R.data, base.R.data) and np.array_equal(f.Q.data, base.Q.data)
+    Wz = np.asfortranarray(W.copy())
+    Wz[:, 80:] = 0.0
+    with pytest.raises(DependentBlockError) as e:
+        rbgs.rbgs(Wz, th, cfg)
+    assert e.value.block == 3
