@@ -582,6 +582,29 @@ def gpu_arm_krylov(args, cfgd):
     wbytes = 8 * n * cfgd["m"]
     value = wbytes / (ms * 1e-3) / 1e9
     hbm, _, src = _peaks()
+    parity = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        # the oracle as the checker on the same family at a grid it finishes in
+        # seconds: 32^3, 16 blocks, same sketch kind and precisions
+        from oracle import krylov as okr
+        from oracle import sketches as osk
+        gs, ps = 32, 16
+        ns, ks = gs ** 3, 2 * mp * ps
+        Bs = np.random.Generator(np.random.Philox(SEED_W)).standard_normal((ns, mp))
+        t0 = time.perf_counter()
+        orc = okr.gmres(okr.poisson3d_apply(gs, gs, gs), Bs, osk.OracleSketch("sparse_sign", ks, ns, SEED_THETA), ps)
+        sec = time.perf_counter() - t0
+        reps = krylov.block_gmres(operators.Poisson3D(gs, gs, gs, device=dev), Bs,
+                                  sketching.sparse_sign_operator(ks, ns, SEED_THETA, cfgd["nnz"]), ps, cfg=cfg,
+                                  diagnostics=args.diagnostics)
+        h, ho = np.array(reps.residual_history), np.array(orc["residual_history"])
+        xo = orc["solution"]
+        parity = {"grid": gs, "blocks": ps, "oracle": "oracle/ restatement (block GMRES, same B, same seeded operator)",
+                  "final_rel_residual": [float(h[-1, 1]), float(ho[-1, 1])],
+                  "max_rel_residual_history_diff": (float(np.max(np.abs(h[:, 1] / ho[:, 1] - 1.0)))
+                                                    if args.diagnostics == "full" else None),
+                  "rel_solution_diff": float(np.linalg.norm(reps.solution.data - xo) / np.linalg.norm(xo)),
+                  "pairs": "[device, oracle]", "oracle_seconds": sec}
     if rank == 0:
         line = {
             "metric": "RBGS QR GB/s of W processed", "value": value, "unit": "GB/s", "n_gpus": world,
@@ -591,6 +614,7 @@ def gpu_arm_krylov(args, cfgd):
                        "k": k, "sketch": "sparse_sign(8)", "restarts": 1, "diagnostics": args.diagnostics, "parallelism": f"zslab{world}",
                        "l2": "inputs larger than L2 (basis = %.1f GB)" % (wbytes / 1e9)},
             "rel_residual": rep.residual_history[-1][1], "iterations": len(rep.residual_history),
+            "parity": parity,
             "basis_cond_last": rep.basis_cond_history[-1], "cert_last": list(rep.cert_history[-1]),
             "host_wall_ms_per_step": wall * 1e3, "gpu_launches": launches, "clocks": clk.summary(),
             "peak_hbm_GBps": hbm, "peak_source": src,
