@@ -464,15 +464,17 @@ def gpu_arm(args, cfgd):
                                      "peak": fpeak, "unit": "TFLOP/s", "frac": fach / fpeak,
                                      "flops_per_launch": d["flops"] / d["calls"]}
         if name == "sketch_gaussian" and esz == 4:
-            # The exact six-digit split runs 12 int8 byte
-            # products per (Theta entry, X entry) on the tensor pipe, with M
+            # The exact digit split runs 2 x digits int8 byte
+            # products per (Theta entry, X entry) on the tensor pipe (12 at
+            # the default six digits), with M
             # padded to 128 sketch rows: the binding roofline is the int8
             # tensor pipe, 148 SMs x 16384 int8 ops per SM clock (dense).
             mhz = (clk_summary or {}).get("sm_mhz") or 1965.0
             ipeak = 148 * 16384 * mhz * 1e6 / 1e12
             kpad = -(-k // 128) * 128
-            iops = d["flops"] * 12 * kpad / k
-            roof["compute_bound"] = {"pipe": "int8 tensor (tcgen05 kind::i8, 12 byte products per entry)",
+            nprod = 2 * (args.sketch_digits or 6)
+            iops = d["flops"] * nprod * kpad / k
+            roof["compute_bound"] = {"pipe": f"int8 tensor (tcgen05 kind::i8, {nprod} byte products per entry)",
                                      "achieved": iops / (d["ms"] * 1e-3) / 1e12, "peak": ipeak,
                                      "unit": "TOP/s", "frac": iops / (d["ms"] * 1e-3) / 1e12 / ipeak,
                                      "ops_per_launch": iops / d["calls"],

@@ -555,7 +555,7 @@ class RbgsSweep:
             else:
                 Si = scr.Ss[:, :w]  # the last pass's Sp R_S^{-1}
             return Rt, Si, sp_qp
-        # l2_plus_cholqr -- Gram realisation of the l2 stage (DESIGN.md 4.3):
+        # l2_plus_cholqr -- Gram realisation of the l2 stage (DESIGN.md 4.5):
         # R' = chol(Q'^T Q'), S* = (Theta Q') R'^{-1} = Theta Q*, then the
         # sketched CholQR of Q*: R'' = chol(S*^T S*), R_ii = R'' R',
         # Q_i = Q' R_ii^{-1}, S_i = S* R''^{-1}.
