@@ -125,6 +125,20 @@ int rb_sketch_gaussian2(int x1_dtype, const void* X1, int64_t ldx1, int c1,
                         const uint8_t* theta, int64_t ldt, int k, double scale,
                         double* out1, int64_t ldo1, double* out2, int64_t ldo2,
                         int accumulate, int mode, void* ws, size_t ws_bytes, void* stream);
+/* The pre-pass (chunk exponents + digit planes) of the SECOND input of a
+ * paired call (c1 + c2 > 64) on its own, so a caller can run it early on
+ * another stream -- the sweep encodes W_(i+1) beside block i's projection --
+ * and hand the buffer to rb_sketch_gaussian2_pre, which then skips it.  Same
+ * plane bytes as the fused call.  out: rb_gauss_prepass_bytes(n, c2, c1,
+ * digits) bytes, 256-byte aligned; digits must match the later call's mode. */
+size_t rb_gauss_prepass_bytes(int64_t n, int c, int c_partner, int digits);
+int rb_gauss_prepass(int x_dtype, const void* X, int64_t ldx, int c, int c_partner, int64_t n, int digits,
+                     void* out, size_t out_bytes, void* stream);
+int rb_sketch_gaussian2_pre(int x1_dtype, const void* X1, int64_t ldx1, int c1,
+                            int x2_dtype, const void* X2, int64_t ldx2, int c2, int64_t n,
+                            const uint8_t* theta, int64_t ldt, int k, double scale,
+                            double* out1, int64_t ldo1, double* out2, int64_t ldo2,
+                            int accumulate, int mode, const void* pre2, void* ws, size_t ws_bytes, void* stream);
 /* srht kind (sketching.py:129-137): signs as a bitmask over the GLOBAL
  * padded index space (bit i set <=> sign_diagonal[i] = -1), sample = the
  * k global sample indices, scale = 1/sqrt(k).  Rows >= n_valid (global)

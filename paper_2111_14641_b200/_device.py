@@ -164,15 +164,37 @@ def sketch_gaussian(X, theta, ldt, k, scale, out, accumulate=False, mode="auto")
     _t1(e0, "sketch_gaussian", n * (cols * X.element_size() + 2 * k), 2.0 * k * n * cols)
 
 
-def sketch_gaussian2(X1, X2, theta, ldt, k, scale, out1, out2, accumulate=False, mode="auto"):
-    """[out1 | out2] = Theta [X1 | X2] in one pass over the gaussian table."""
+GAUSS_DIGITS = {"auto": 6, "tensor": 6, "tensor4": 4, "tensor3": 3}
+
+
+def gauss_prepass_bytes(n, c, c_partner, mode):
+    from ._lib import require_cuda
+    return int(require_cuda().rb_gauss_prepass_bytes(int(n), int(c), int(c_partner), GAUSS_DIGITS[mode]))
+
+
+def gauss_prepass(X, c_partner, mode, buf):
+    """Digit planes + chunk exponents of X (the second input of a later
+    paired sketch_gaussian2 with a c_partner-column first input) into buf."""
+    n, c = X.shape
+    call("rb_gauss_prepass", dtype_code(X), ptr(X), ld(X), c, int(c_partner), n, GAUSS_DIGITS[mode], ptr(buf),
+         buf.numel() * buf.element_size(), st(X.device))
+
+
+def sketch_gaussian2(X1, X2, theta, ldt, k, scale, out1, out2, accumulate=False, mode="auto", pre2=None):
+    """[out1 | out2] = Theta [X1 | X2] in one pass over the gaussian table;
+    pre2: X2's pre-pass already done (gauss_prepass)."""
     n, c1 = X1.shape
     c2 = X2.shape[1]
     ws, wsb = _ws(n, c1 + c2, k, X1.device)
     e0 = _t0()
-    call("rb_sketch_gaussian2", dtype_code(X1), ptr(X1), ld(X1), c1, dtype_code(X2), ptr(X2), ld(X2), c2, n,
-         ptr(theta), ldt, k, scale, ptr(out1), ld(out1), ptr(out2), ld(out2), int(accumulate), GAUSS_MODE[mode],
-         ws, wsb, st(X1.device))
+    if pre2 is not None:
+        call("rb_sketch_gaussian2_pre", dtype_code(X1), ptr(X1), ld(X1), c1, dtype_code(X2), ptr(X2), ld(X2), c2, n,
+             ptr(theta), ldt, k, scale, ptr(out1), ld(out1), ptr(out2), ld(out2), int(accumulate), GAUSS_MODE[mode],
+             ptr(pre2), ws, wsb, st(X1.device))
+    else:
+        call("rb_sketch_gaussian2", dtype_code(X1), ptr(X1), ld(X1), c1, dtype_code(X2), ptr(X2), ld(X2), c2, n,
+             ptr(theta), ldt, k, scale, ptr(out1), ld(out1), ptr(out2), ld(out2), int(accumulate), GAUSS_MODE[mode],
+             ws, wsb, st(X1.device))
     _t1(e0, "sketch_gaussian", n * ((c1 + c2) * X1.element_size() + 2 * k), 2.0 * k * n * (c1 + c2))
 
 

@@ -31,11 +31,15 @@ SIGNATURES = {
     "rb_last_error": [],
     "rb_launch_count": [],
     "rb_workspace_bytes": [_i64, _i, _i],
+    "rb_gauss_prepass_bytes": [_i64, _i, _i, _i],
     "rb_project": [_i, _i, _i, _i, _i64, _i, _i, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, _p, _sz, _p],
     "rb_project_trsm": [_i, _i, _i, _i, _i64, _i, _i, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p,
                         _p, _i64, _p, _i64, _i, _p, _sz, _p],
     "rb_gaussian_fill": [_u64, _i, _i64, _i64, _p, _i64, _p],
     "rb_sketch_gaussian": [_i, _i64, _i, _p, _i64, _p, _i64, _i, _d, _p, _i64, _i, _i, _p, _sz, _p],
+    "rb_gauss_prepass": [_i, _p, _i64, _i, _i, _i64, _i, _p, _sz, _p],
+    "rb_sketch_gaussian2_pre": [_i, _p, _i64, _i, _i, _p, _i64, _i, _i64, _p, _i64, _i, _d, _p, _i64, _p, _i64, _i, _i,
+                                _p, _p, _sz, _p],
     "rb_sketch_gaussian2": [_i, _p, _i64, _i, _i, _p, _i64, _i, _i64, _p, _i64, _i, _d, _p, _i64, _p, _i64, _i, _i,
                             _p, _sz, _p],
     "rb_sketch_srht": [_i, _i64, _i, _p, _i64, _i64, _i64, _p, _p, _i, _d, _p, _i64, _i, _p, _sz, _p],
@@ -63,7 +67,8 @@ SIGNATURES = {
     "rb_convert": [_i, _i, _i64, _i, _p, _i64, _p, _i64, _p],
 }
 _RESTYPE = {"rb_version": ctypes.c_char_p, "rb_last_error": ctypes.c_char_p,
-            "rb_workspace_bytes": ctypes.c_size_t, "rb_launch_count": ctypes.c_ulonglong}
+            "rb_workspace_bytes": ctypes.c_size_t, "rb_gauss_prepass_bytes": ctypes.c_size_t,
+            "rb_launch_count": ctypes.c_ulonglong}
 
 
 def launch_count() -> int:

@@ -49,7 +49,10 @@ int sketch_gaussian(int, int64_t, int, const void*, int64_t, const uint8_t*, int
                     int, int, void*, size_t, cudaStream_t);
 size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k);
 int sketch_gaussian2(int, const void*, int64_t, int, int, const void*, int64_t, int, int64_t, const uint8_t*, int64_t,
-                     int, double, double*, int64_t, double*, int64_t, int, int, void*, size_t, cudaStream_t);
+                     int, double, double*, int64_t, double*, int64_t, int, int, void*, size_t, cudaStream_t,
+                     const void* pre2);
+size_t gauss_prepass_bytes(int64_t n, int c, int c_partner, int dig);
+int gauss_prepass(int, const void*, int64_t, int, int, int64_t, int, void*, size_t, cudaStream_t);
 int sketch_signs(int, int64_t, int, const void*, int64_t, const uint32_t*, int64_t, int, double, double*, int64_t, int,
                  void*, size_t, cudaStream_t);
 int sketch_srht(int, int64_t, int, const void*, int64_t, int64_t, int64_t, const uint32_t*, const int64_t*, int,
@@ -141,7 +144,24 @@ int rb_sketch_gaussian2(int xd1, const void* X1, int64_t ld1, int c1, int xd2, c
                         int64_t n, const uint8_t* theta, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
                         double* out2, int64_t ldo2, int acc, int mode, void* ws, size_t wsb, void* s) {
   return rb::sketch_gaussian2(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, theta, ldt, k, scale, out1, ldo1, out2, ldo2, acc,
-                              mode, ws, wsb, as_stream(s));
+                              mode, ws, wsb, as_stream(s), nullptr);
+}
+
+int rb_sketch_gaussian2_pre(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2, int c2,
+                            int64_t n, const uint8_t* theta, int64_t ldt, int k, double scale, double* out1,
+                            int64_t ldo1, double* out2, int64_t ldo2, int acc, int mode, const void* pre2, void* ws,
+                            size_t wsb, void* s) {
+  return rb::sketch_gaussian2(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, theta, ldt, k, scale, out1, ldo1, out2, ldo2, acc,
+                              mode, ws, wsb, as_stream(s), pre2);
+}
+
+size_t rb_gauss_prepass_bytes(int64_t n, int c, int c_partner, int digits) {
+  return rb::gauss_prepass_bytes(n, c, c_partner, digits);
+}
+
+int rb_gauss_prepass(int xd, const void* X, int64_t ldx, int c, int c_partner, int64_t n, int digits, void* out,
+                     size_t out_bytes, void* s) {
+  return rb::gauss_prepass(xd, X, ldx, c, c_partner, n, digits, out, out_bytes, as_stream(s));
 }
 
 int rb_sketch_srht(int xd, int64_t n, int ncols, const void* X, int64_t ldx, int64_t row0, int64_t n_pad,

@@ -986,7 +986,7 @@ size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k);
 int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2, int c2,
                        int64_t n, const uint8_t* qt, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
                        double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st, bool lean = false,
-                       int dig = 6);
+                       int dig = 6, const void* pre2 = nullptr);
 
 // [out1 | out2] = scale * (q @ [X1 | X2]).  mode 0 = auto (tensor pipe when
 // every input is binary32), 1 = fp64 CUDA cores, 2 = tensor pipe, 3 = tensor
@@ -996,7 +996,8 @@ int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, co
 // instead of 2^(E-47); 2/3 and 1/2 of the tensor work).
 int sketch_gaussian2(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2, int c2,
                      int64_t n, const uint8_t* theta, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
-                     double* out2, int64_t ldo2, int acc, int mode, void* ws, size_t wsb, cudaStream_t st) {
+                     double* out2, int64_t ldo2, int acc, int mode, void* ws, size_t wsb, cudaStream_t st,
+                     const void* pre2) {
   RB_REQUIRE(c1 >= 1 && c2 >= 0 && c1 <= 64 && c2 <= 64 && k >= 1 && ldo1 >= k && out1 &&
                  (c2 == 0 || (out2 && ldo2 >= k)),
              "rb_sketch_gaussian: bad args");
@@ -1010,9 +1011,11 @@ int sketch_gaussian2(int xd1, const void* X1, int64_t ld1, int c1, int xd2, cons
   const bool tc = mode >= 2 || (mode == 0 && xd1 == RB_F32 && (c2 == 0 || xd2 == RB_F32));
   // > 64 columns: CTA pairs sharing the table stream (RB_TC_PAIR=0: two passes)
   static const int pair = getenv("RB_TC_PAIR") ? atoi(getenv("RB_TC_PAIR")) : 1;
+  RB_REQUIRE(!pre2 || (tc && pair && c2 > 0 && c1 + c2 > 64 && mode != 3),
+             "rb_sketch_gaussian2_pre: the pre-encoded input needs the paired tensor form");
   if (tc && (c1 + c2 <= 64 || (pair && c2 > 0)))
     return sketch_gaussian_tc(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, theta, ldt, k, scale, out1, ldo1, out2, ldo2,
-                              acc, ws, wsb, st, false, dig);
+                              acc, ws, wsb, st, false, dig, pre2);
   if (tc) {
     int rc = sketch_gaussian_tc(xd1, X1, ld1, c1, RB_F32, nullptr, 0, 0, n, theta, ldt, k, scale, out1, ldo1,
                                 nullptr, 0, acc, ws, wsb, st, false, dig);
@@ -1036,7 +1039,7 @@ int sketch_gaussian(int xd, int64_t n, int ncols, const void* X, int64_t ldx, co
                     int k, double scale, double* out, int64_t ldo, int acc, int mode, void* ws, size_t wsb,
                     cudaStream_t st) {
   return sketch_gaussian2(xd, X, ldx, ncols, RB_F32, nullptr, 0, 0, n, theta, ldt, k, scale, out, ldo, nullptr, 0,
-                          acc, mode, ws, wsb, st);
+                          acc, mode, ws, wsb, st, nullptr);
 }
 
 int sketch_signs(int xd, int64_t n, int ncols, const void* X, int64_t ldx, const uint32_t* bits, int64_t ldb,

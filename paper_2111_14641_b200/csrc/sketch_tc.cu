@@ -899,7 +899,7 @@ int launch_any(int NP, int dig, int64_t n, int ncols, const uint8_t* qt, int64_t
 int sketch_gaussian_tc_pair(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2,
                             int c2, int64_t n, const uint8_t* qt, int64_t ldt, int k, double scale, double* out1,
                             int64_t ldo1, double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st,
-                            int dig) {
+                            int dig, const void* pre2 = nullptr) {
   RB_REQUIRE(c1 >= 1 && c2 >= 1 && c1 <= 64 && c2 <= 64 && k >= 1 && out1 && out2 && ldo1 >= k && ldo2 >= k,
              "rb_sketch_gaussian (tensor pair): bad args (c1 %d, c2 %d)", c1, c2);
   RB_REQUIRE(n == 0 || (X1 && ld1 >= n && X2 && ld2 >= n && qt && ldt >= n && ldt % kBK == 0),
@@ -915,13 +915,18 @@ int sketch_gaussian_tc_pair(int xd1, const void* X1, int64_t ld1, int c1, int xd
   uint8_t* pl2 = pl1 + planes_b + exps_b;
   int* ex2 = (int*)(pl2 + planes_b);
   double* part = (double*)(pl2 + planes_b + exps_b);
+  if (pre2) {  // the second input's planes and exponents, encoded earlier (rb_gauss_prepass)
+    pl2 = (uint8_t*)const_cast<void*>(pre2);
+    ex2 = (int*)(pl2 + planes_b);
+  }
   const size_t part_b = wsb - 2 * (planes_b + exps_b);
   int splits = 0;
   if (n > 0) {
     dim3 g(nchunks, NP / 2);
     if (xd1 == RB_F32) launch_split<float>(RB_F32, g, n, c1, X1, ld1, 0, nullptr, 0, NP, pl1, ex1, st, dig);
     else launch_split<double>(RB_F32, g, n, c1, X1, ld1, 0, nullptr, 0, NP, pl1, ex1, st, dig);
-    if (xd2 == RB_F32) launch_split<float>(RB_F32, g, n, c2, X2, ld2, 0, nullptr, 0, NP, pl2, ex2, st, dig);
+    if (pre2) {
+    } else if (xd2 == RB_F32) launch_split<float>(RB_F32, g, n, c2, X2, ld2, 0, nullptr, 0, NP, pl2, ex2, st, dig);
     else launch_split<double>(RB_F32, g, n, c2, X2, ld2, 0, nullptr, 0, NP, pl2, ex2, st, dig);
     Half2 h2;
     h2.pairs = 2;
@@ -942,6 +947,32 @@ int sketch_gaussian_tc_pair(int xd1, const void* X1, int64_t ld1, int c1, int xd
 
 }  // namespace
 
+// The pre-pass of ONE input of a paired sketch on its own (planes, then
+// exponents, in `out`): the sweep encodes W_(i+1) on a side stream while
+// block i's projection runs, and hands the buffer to the paired call.
+size_t gauss_prepass_bytes(int64_t n, int c, int c_partner, int dig) {
+  const int NP = std::max(np_for(c, dig), np_for(c_partner, dig));
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  return (size_t)nchunks * kTPC * dig * kBK * NP + ((size_t)NP * nchunks * sizeof(int) + 255) / 256 * 256;
+}
+
+int gauss_prepass(int xd, const void* X, int64_t ld, int c, int c_partner, int64_t n, int dig, void* out, size_t outb,
+                  cudaStream_t st) {
+  RB_REQUIRE(c >= 1 && c <= 64 && c_partner >= 1 && c_partner <= 64 && n >= 1 && X && ld >= n && out &&
+                 (dig == 6 || dig == 4 || dig == 3) && outb >= gauss_prepass_bytes(n, c, c_partner, dig) &&
+                 (uintptr_t)out % 256 == 0,
+             "rb_gauss_prepass: bad args");
+  const int NP = std::max(np_for(c, dig), np_for(c_partner, dig));
+  const int nchunks = (int)((n + kChunk - 1) / kChunk);
+  const size_t planes_b = (size_t)nchunks * kTPC * dig * kBK * NP;
+  uint8_t* pl = (uint8_t*)out;
+  int* ex = (int*)(pl + planes_b);
+  dim3 g(nchunks, NP / 2);
+  if (xd == RB_F32) launch_split<float>(RB_F32, g, n, c, X, ld, 0, nullptr, 0, NP, pl, ex, st, dig);
+  else launch_split<double>(RB_F32, g, n, c, X, ld, 0, nullptr, 0, NP, pl, ex, st, dig);
+  return check_launch("rb_gauss_prepass");
+}
+
 size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k) {
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
   // room for a fused two-input call: <= 64 columns in one CTA, else two
@@ -957,12 +988,14 @@ size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k) {
 // binary32 or binary64 (n rows); c2 may be 0.
 int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2, int c2,
                        int64_t n, const uint8_t* qt, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
-                       double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st, bool lean, int dig) {
+                       double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st, bool lean, int dig,
+                       const void* pre2) {
   const int ncols = c1 + c2;
   RB_REQUIRE(dig == 6 || dig == 4 || dig == 3, "rb_sketch_gaussian (tensor): digits must be 6, 4 or 3 (got %d)", dig);
+  RB_REQUIRE(!pre2 || ncols > 64, "rb_sketch_gaussian (tensor): a pre-encoded second input needs the paired form");
   if (ncols > 64)
     return sketch_gaussian_tc_pair(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, qt, ldt, k, scale, out1, ldo1, out2, ldo2,
-                                   acc, ws, wsb, st, dig);
+                                   acc, ws, wsb, st, dig, pre2);
   RB_REQUIRE(c1 >= 1 && c2 >= 0 && ncols <= 64 && k >= 1 && ldo1 >= k && out1 && (c2 == 0 || (out2 && ldo2 >= k)),
              "rb_sketch_gaussian (tensor): bad args (c1 %d, c2 %d)", c1, c2);
   RB_REQUIRE(n == 0 || (X1 && ld1 >= n && (c2 == 0 || (X2 && ld2 >= n)) && qt && ldt >= n && ldt % kBK == 0),

@@ -412,6 +412,8 @@ class RbgsSweep:
         # one-shot sweeps: the Step-5 scaling of the previous block, deferred
         # into the next projection (rb_project_trsm): (slot, R_S) or None
         self._fuse_scaling = False
+        self._prepass_bufs = None
+        self._prepass_flip = 0
         self._pending_scale = None
         self._lookahead_event = None  # upload event of the lookahead block (pinned host W)
         self._pending = []  # this block's partials (norms, l2 Gram) not yet allreduced
@@ -688,12 +690,48 @@ class RbgsSweep:
                 and not self.cfg.certify_blocks and A.dtype == torch.float32 and B.dtype == torch.float32
                 and A.shape[1] <= 64 and B.shape[1] <= 64 and sketching.GAUSS_MODE != "fp64")
 
-    def _sketch_pair(self, A, B, outA, outB):
+    def _sketch_pair(self, A, B, outA, outB, pre=None):
         tab = self.theta.device_tables(A.device, self.row0, A.shape[0])
+        pre2 = None
+        if pre is not None:  # B's pre-pass ran on the side stream (_fork_prepass)
+            pre2, ev = pre
+            torch.cuda.current_stream(self.device).wait_event(ev)
         D.sketch_gaussian2(A, B, tab["theta"], tab["ldt"], self.theta.k,
                            1.0 / (sketching.GAUSS_GRID * math.sqrt(self.theta.k)), outA, outB,
-                           False, self._gmode)
+                           False, self._gmode, pre2=pre2)
         self._reduce(outA, outB)
+
+    def _fork_prepass(self, slot, Wn):
+        """The digit pre-pass of W_(i+1) (chunk exponents + planes: two small
+        streaming kernels that depend on nothing block i computes) on the
+        side stream while this stream runs block i's projection, for the
+        paired sketch [Q'_i | W_(i+1)] that follows it.  Returns (buffer,
+        event) or None when the paired tensor form will not be taken."""
+        if not (PREPASS_OVERLAP and self._fusable(slot, Wn) and slot.shape[1] + Wn.shape[1] > 64
+                and self._gmode in ("auto", "tensor", "tensor4", "tensor3") and Wn.shape[0] >= 1):
+            return None
+        dev = self.device
+        nb = D.gauss_prepass_bytes(Wn.shape[0], Wn.shape[1], slot.shape[1], self._gmode)
+        bufs = self._prepass_bufs
+        if bufs is None or bufs[0].numel() < nb:
+            bufs = self._prepass_bufs = [torch.empty(nb, dtype=torch.uint8, device=dev) for _ in range(2)]
+            self._prepass_flip = 0
+        buf = bufs[self._prepass_flip]
+        self._prepass_flip ^= 1
+        cur = torch.cuda.current_stream(dev)
+        side = _SIDE_STREAMS.get(dev.index)
+        if side is None:
+            side = _SIDE_STREAMS[dev.index] = torch.cuda.Stream(dev, priority=-1)
+        side.wait_stream(cur)
+        ev = self._lookahead_event
+        self._lookahead_event = None
+        with torch.cuda.stream(side):
+            if ev is not None:
+                side.wait_event(ev)  # W_(i+1)'s upload (pinned / staged host W)
+            D.gauss_prepass(Wn, slot.shape[1], self._gmode, buf)
+            done = torch.cuda.Event()
+            done.record(side)
+        return buf, done
 
     # -- sketch / projection overlap -------------------------------------------
     def _overlap_ok(self, Wn):
@@ -782,6 +820,9 @@ class RbgsSweep:
         if c:
             self._g_given = None
         fork = None
+        pre = None
+        if c and Wn is not None and self._next_P is None and not self._overlap_ok(Wn):
+            pre = self._fork_prepass(slot, Wn)
         if c and Wn is not None and self._next_P is None and self._overlap_ok(Wn):
             # the next block's Step 1 does not depend on this block: issue it
             # first, on the side stream, so it overlaps the projection
@@ -819,7 +860,7 @@ class RbgsSweep:
                 Pn = scr.Pn[scr.pn_flip][:, :Wn.shape[1]]
                 scr.pn_flip ^= 1
                 self._wait_lookahead()
-                self._sketch_pair(slot, Wn, sp_given, Pn)
+                self._sketch_pair(slot, Wn, sp_given, Pn, pre=pre)
                 self._next_P = (self._key(Wn), Pn)
             elif (Wn is not None and self._next_P is None and sharded and not cfg.certify_blocks
                   and self.inter[0] in ("sketched_cholqr", "l2_plus_cholqr")):
@@ -980,6 +1021,10 @@ REPLAYS = 0  # one-shot factorizations replayed eagerly after a deferred-status 
 # series (2.89 vs 2.77 ms at C2's last block); the default is the fused
 # two-input sketch after the projection (one table pass).
 OVERLAP = os.environ.get("RB_OVERLAP", "0") == "1"
+# W_(i+1)'s digit pre-pass on a side stream beside the projection: built, bitwise neutral, measured without
+# gain at C2 (54.3 / 54.8 ms off, 54.4 / 54.1 ms on: the staged projection fills every SM's shared memory, so
+# the side kernels run in its tail) -- off by default
+PREPASS_OVERLAP = os.environ.get("RB_PREPASS_OVERLAP", "0") == "1"
 TSQR_FALLBACK = os.environ.get("RB_L2_TSQR", "1") == "1"  # Householder R when the l2 Gram breaks down
 _SIDE_STREAMS = {}
 
