@@ -161,7 +161,7 @@ class Clocks:
 # ---------------------------------------------------------------------------
 # CPU restatement (oracle) -- the reference arm and the cpu_baseline leg
 
-def _oracle_sample(cfgd, n_s, parity=False, order="reference", digits=None):
+def _oracle_sample(cfgd, n_s, parity=False, order="reference", digits=None, theta_bits=16):
     """One RBGS QR of an n_s-row sample of the workload with the CPU oracle;
     the gaussian table is materialised beforehand (operator construction),
     like the reference's SRHT tables.  Returns seconds -- and with `parity`
@@ -180,7 +180,7 @@ def _oracle_sample(cfgd, n_s, parity=False, order="reference", digits=None):
         W = WL.colscaled_host(n_s, m, SEED_W)
     if cfgd["dtype"] == "f32":
         W = W.astype(np.float32).astype(np.float64)
-    op = osk.materialize(osk.OracleSketch(cfgd["kind"], k, n_s, SEED_THETA))
+    op = osk.materialize(osk.OracleSketch(cfgd["kind"], k, n_s, SEED_THETA, bits=theta_bits))
     cfg = osw.OracleConfig(osw.uniform_widths(m, p), interblock="sketched_cholqr(1)",
                            coarse=cfgd["coarse"])
     t0 = time.perf_counter()
@@ -194,7 +194,7 @@ def _oracle_sample(cfgd, n_s, parity=False, order="reference", digits=None):
     from paper_2111_14641_b200.kernels import COARSE, FINE, BlockPartition
     from paper_2111_14641_b200.rbgs import DeviceConfig, RbgsConfig, rbgs
 
-    theta = (sketching.gaussian_operator(k, n_s, SEED_THETA) if cfgd["kind"] == "gaussian"
+    theta = (sketching.gaussian_operator(k, n_s, SEED_THETA, theta_bits=theta_bits) if cfgd["kind"] == "gaussian"
              else sketching.make_operator(cfgd["kind"], k, n_s, SEED_THETA))
     gcfg = RbgsConfig(partition=BlockPartition.uniform(m, p), interblock="sketched_cholqr(1)",
                       coarse=COARSE if cfgd["coarse"] == "coarse" else FINE)
@@ -283,7 +283,7 @@ def gpu_arm(args, cfgd):
         torch.cuda.synchronize()
     torch.cuda.empty_cache()
     if cfgd["kind"] == "gaussian":
-        theta = sketching.gaussian_operator(k, n, SEED_THETA)
+        theta = sketching.gaussian_operator(k, n, SEED_THETA, theta_bits=args.theta_bits)
         theta.device_tables(dev, shard.row0, n_per)
     else:
         theta = sketching.SketchOperator(cfgd["kind"], k, n, SEED_THETA)
@@ -472,7 +472,7 @@ def gpu_arm(args, cfgd):
             mhz = (clk_summary or {}).get("sm_mhz") or 1965.0
             ipeak = 148 * 16384 * mhz * 1e6 / 1e12
             kpad = -(-k // 128) * 128
-            nprod = 2 * (args.sketch_digits or 6)
+            nprod = (2 if args.theta_bits == 16 else 1) * (args.sketch_digits or 6)
             iops = d["flops"] * nprod * kpad / k
             roof["compute_bound"] = {"pipe": f"int8 tensor (tcgen05 kind::i8, {nprod} byte products per entry)",
                                      "achieved": iops / (d["ms"] * 1e-3) / 1e12, "peak": ipeak,
@@ -489,7 +489,8 @@ def gpu_arm(args, cfgd):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_s = args.sample_rows or 8192
-        sec, parity = _oracle_sample(cfgd, n_s, parity=True, order=args.order, digits=args.sketch_digits)
+        sec, parity = _oracle_sample(cfgd, n_s, parity=True, order=args.order, digits=args.sketch_digits,
+                                     theta_bits=args.theta_bits)
         cpu = {"value": esz * n_s * m / sec / 1e9, "unit": "GB/s", "cores": _CORES, "kind": "port",
                "sample": f"{n_s} x {m} rows of {cfgd['name']}, one factorization, oracle/ restatement "
                          f"(numpy + OpenBLAS)", "parity": parity}
@@ -500,7 +501,10 @@ def gpu_arm(args, cfgd):
             "scaling": "weak", "vs_baseline": None,
             "dtype": "f32-coarse/f64-fine" if cfgd["coarse"] == "coarse" else "f64", "data": "synthetic",
             "config": {"workload": cfgd["desc"], "n": n, "m": m, "p": p, "k": k, "sketch": cfgd["kind"],
-                       "theta": ("N(0,1) Box-Muller of Philox4x32-10 quantized to the int16 grid 2^-11 (clamped), "
+                       "theta": (("N(0,1) Box-Muller of Philox4x32-10 quantized to the int16 grid 2^-11 (clamped), "
+                                  if args.theta_bits == 16 else
+                                  "OPT-IN 8-bit operator: N(0,1) Box-Muller of Philox4x32-10 on the int8 grid 2^-5 "
+                                  "(255 levels, clamped), ") +
                                  "scaled by 1/sqrt(k); same operator in the oracle" if cfgd["kind"] == "gaussian"
                                  else "reference operator (numpy Philox recipe)"),
                        "interblock": args.interblock, "ls_solver": "richardson(5)",
@@ -638,6 +642,9 @@ def main():
     ap.add_argument("--sketch-digits", type=int, default=None, choices=[6, 4, 3],
                     help="gaussian kind: byte digits of X kept inside Theta X (default: the config's own; 6 = "
                          "binary64-grade)")
+    ap.add_argument("--theta-bits", type=int, default=16, choices=[16, 8],
+                    help="gaussian kind: grid of the operator's entries (16 = the default int16 grid 2^-11; 8 = the "
+                         "opt-in int8 grid 2^-5: one byte plane, half the tensor work)")
     ap.add_argument("--interblock", default="sketched_cholqr(1)",
                     help="inter-block QR (reference default: l2_plus_cholqr; one sketch pass: sketched_cholqr(1))")
     ap.add_argument("--sample-rows", type=int, default=None,

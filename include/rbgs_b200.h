@@ -105,6 +105,14 @@ int rb_project_trsm(int q_dtype, int w_dtype, int compute_dtype, int order, int6
  * 2 * ceil(k/128) * 128 * ldt bytes, padding zeroed.                      */
 int rb_gaussian_fill(uint64_t seed, int k, int64_t row0, int64_t nrows,
                      uint8_t* theta, int64_t ldt, void* stream);
+/* The same table with the operator's entries on a coarser grid: bits = 16 is
+ * rb_gaussian_fill; bits = 8 stores q = 256 q8, q8 = clamp(rint(32 g), +-127)
+ * (the same normals g on the int8 grid 2^-5; Theta = q / (8192 sqrt(k))), so
+ * the lo plane is zero and rb_sketch_gaussian[2] called with mode + 16 skips
+ * it: half the table stream and half the tensor work.  An opt-in operator
+ * (discretised gaussian with 255 levels), not the default.               */
+int rb_gaussian_fill_bits(uint64_t seed, int k, int64_t row0, int64_t nrows,
+                          uint8_t* theta, int64_t ldt, int bits, void* stream);
 /* out = scale * (q @ X) (scale = 1 / (2048 sqrt(k)) gives Theta @ X).
  * mode 0 = auto (tensor pipe for binary32 X, fp64 CUDA cores for binary64),
  * 1 = fp64 CUDA cores (exact fp64 products), 2 = tensor pipe: tcgen05

@@ -49,9 +49,10 @@ def next_pow2(n: int) -> int:
 class OracleSketch:
     """Plain-data operator: (kind, k, n, seed) plus its realised tables."""
 
-    def __init__(self, kind, k, n, seed, nnz=8):
+    def __init__(self, kind, k, n, seed, nnz=8, bits=16):
         self.kind, self.k, self.n, self.seed = kind, int(k), int(n), int(seed)
         self.nnz = int(nnz)
+        self.bits = int(bits)  # gaussian kind: 16 (grid 2^-11) or 8 (grid 2^-5, |q| <= 127)
         if kind in ("srht", "rademacher"):
             gen = np.random.Generator(np.random.Philox(self.seed))
             if kind == "srht":
@@ -70,7 +71,7 @@ class OracleSketch:
 # gaussian kind
 # ---------------------------------------------------------------------------
 
-def gaussian_int16(seed: int, k: int, rows: np.ndarray) -> np.ndarray:
+def gaussian_int16(seed: int, k: int, rows: np.ndarray, bits: int = 16) -> np.ndarray:
     """int16 table q[r, t] for global W-rows `rows` (shape k x len(rows))."""
     rows = np.asarray(rows, dtype=np.uint64)
     nq = (k + 3) // 4
@@ -93,23 +94,28 @@ def gaussian_int16(seed: int, k: int, rows: np.ndarray) -> np.ndarray:
     g[1::4] = r1 * np.sin(t1)
     g[2::4] = r2 * np.cos(t2)
     g[3::4] = r2 * np.sin(t2)
+    if bits == 8:  # the same normals on the int8 grid 2^-5 (the one-plane tensor sketch)
+        return np.clip(np.rint(GAUSS_GRID8 * g[:k]), -127, 127).astype(np.int16)
     q = np.clip(np.rint(GAUSS_GRID * g[:k]), -32767, 32767)
     return q.astype(np.int16)
 
 
-def gaussian_scale(k: int) -> float:
-    return 1.0 / (GAUSS_GRID * math.sqrt(k))
+GAUSS_GRID8 = 32.0
 
 
-def gaussian_apply(seed, k, X, row0=0, chunk=8192):
+def gaussian_scale(k: int, bits: int = 16) -> float:
+    return 1.0 / ((GAUSS_GRID8 if bits == 8 else GAUSS_GRID) * math.sqrt(k))
+
+
+def gaussian_apply(seed, k, X, row0=0, chunk=8192, bits=16):
     """Theta[:, row0:row0+n] @ X in fp64, Theta regenerated chunk by chunk."""
     X = np.asarray(X, dtype=np.float64)
     out = np.zeros((k, X.shape[1]))
     for s in range(0, X.shape[0], chunk):
         e = min(X.shape[0], s + chunk)
-        q = gaussian_int16(seed, k, np.arange(row0 + s, row0 + e))
+        q = gaussian_int16(seed, k, np.arange(row0 + s, row0 + e), bits)
         out += q.astype(np.float64) @ X[s:e]
-    return out * gaussian_scale(k)
+    return out * gaussian_scale(k, bits)
 
 
 # ---------------------------------------------------------------------------
@@ -201,7 +207,8 @@ def materialize(op: OracleSketch) -> OracleSketch:
     construction, as the reference does for its SRHT tables), so apply is
     one BLAS product.  For timing the CPU baseline on row samples."""
     if op.kind == "gaussian":
-        op.dense = gaussian_int16(op.seed, op.k, np.arange(op.n)).astype(np.float64) * gaussian_scale(op.k)
+        op.dense = (gaussian_int16(op.seed, op.k, np.arange(op.n), op.bits).astype(np.float64)
+                    * gaussian_scale(op.k, op.bits))
     return op
 
 
@@ -220,6 +227,6 @@ def _apply(op: OracleSketch, X) -> np.ndarray:
     if op.kind == "gaussian":
         if getattr(op, "dense", None) is not None:
             return op.dense @ X
-        return gaussian_apply(op.seed, op.k, X)
+        return gaussian_apply(op.seed, op.k, X, bits=op.bits)
     M = sparse_sign_matrix(op.seed, op.k, op.nnz, op.n)
     return np.asarray(M @ X)

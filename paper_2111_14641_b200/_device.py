@@ -153,6 +153,8 @@ def project_trsm(Q, X, W, Qp, compute, order, norms2, Qf, Rf):
 
 
 GAUSS_MODE = {"auto": 0, "fp64": 1, "tensor": 2, "lean": 3, "tensor4": 4, "tensor3": 5}
+# "+q8": the table of an 8-bit operator (lo plane zero): mode + 16
+GAUSS_MODE.update({m + "+q8": c + 16 for m, c in list(GAUSS_MODE.items()) if m != "lean"})
 
 
 def sketch_gaussian(X, theta, ldt, k, scale, out, accumulate=False, mode="auto"):
@@ -165,6 +167,7 @@ def sketch_gaussian(X, theta, ldt, k, scale, out, accumulate=False, mode="auto")
 
 
 GAUSS_DIGITS = {"auto": 6, "tensor": 6, "tensor4": 4, "tensor3": 3}
+GAUSS_DIGITS.update({m + "+q8": d for m, d in list(GAUSS_DIGITS.items())})
 
 
 def gauss_prepass_bytes(n, c, c_partner, mode):
@@ -198,9 +201,9 @@ def sketch_gaussian2(X1, X2, theta, ldt, k, scale, out1, out2, accumulate=False,
     _t1(e0, "sketch_gaussian", n * ((c1 + c2) * X1.element_size() + 2 * k), 2.0 * k * n * (c1 + c2))
 
 
-def gaussian_fill(seed, k, row0, nrows, theta, ldt):
-    call("rb_gaussian_fill", ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), k, row0, nrows, ptr(theta), ldt,
-         st(theta.device))
+def gaussian_fill(seed, k, row0, nrows, theta, ldt, bits=16):
+    call("rb_gaussian_fill_bits", ctypes.c_uint64(seed & 0xFFFFFFFFFFFFFFFF), k, row0, nrows, ptr(theta), ldt,
+         int(bits), st(theta.device))
 
 
 def sketch_srht(X, row0, n_pad, bits, sample, k, scale, out, accumulate=False):

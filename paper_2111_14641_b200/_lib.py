@@ -36,6 +36,7 @@ SIGNATURES = {
     "rb_project_trsm": [_i, _i, _i, _i, _i64, _i, _i, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p,
                         _p, _i64, _p, _i64, _i, _p, _sz, _p],
     "rb_gaussian_fill": [_u64, _i, _i64, _i64, _p, _i64, _p],
+    "rb_gaussian_fill_bits": [_u64, _i, _i64, _i64, _p, _i64, _i, _p],
     "rb_sketch_gaussian": [_i, _i64, _i, _p, _i64, _p, _i64, _i, _d, _p, _i64, _i, _i, _p, _sz, _p],
     "rb_gauss_prepass": [_i, _p, _i64, _i, _i, _i64, _i, _p, _sz, _p],
     "rb_sketch_gaussian2_pre": [_i, _p, _i64, _i, _i, _p, _i64, _i, _i64, _p, _i64, _i, _d, _p, _i64, _p, _i64, _i, _i,

@@ -44,7 +44,7 @@ int project(int, int, int, int, int64_t, int, int, const void*, int64_t, const d
 int project_trsm(int, int, int, int, int64_t, int, int, const void*, int64_t, const double*, int64_t, const void*,
                  int64_t, void*, int64_t, double*, void*, int64_t, const double*, int64_t, int, void*, size_t,
                  cudaStream_t);
-int gaussian_fill(uint64_t, int, int64_t, int64_t, uint8_t*, int64_t, cudaStream_t);
+int gaussian_fill(uint64_t, int, int64_t, int64_t, uint8_t*, int64_t, cudaStream_t, int bits);
 int sketch_gaussian(int, int64_t, int, const void*, int64_t, const uint8_t*, int64_t, int, double, double*, int64_t,
                     int, int, void*, size_t, cudaStream_t);
 size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k);
@@ -131,7 +131,12 @@ int rb_project_trsm(int qd, int wd, int cd, int order, int64_t n, int c, int p, 
 }
 
 int rb_gaussian_fill(uint64_t seed, int k, int64_t row0, int64_t nrows, uint8_t* theta, int64_t ldt, void* s) {
-  return rb::gaussian_fill(seed, k, row0, nrows, theta, ldt, as_stream(s));
+  return rb::gaussian_fill(seed, k, row0, nrows, theta, ldt, as_stream(s), 16);
+}
+
+int rb_gaussian_fill_bits(uint64_t seed, int k, int64_t row0, int64_t nrows, uint8_t* theta, int64_t ldt, int bits,
+                          void* s) {
+  return rb::gaussian_fill(seed, k, row0, nrows, theta, ldt, as_stream(s), bits);
 }
 
 int rb_sketch_gaussian(int xd, int64_t n, int ncols, const void* X, int64_t ldx, const uint8_t* theta, int64_t ldt,

@@ -214,7 +214,7 @@ int dense_sketch(int64_t n, int ncols, const TX* X, int64_t ldx, Src src, int k,
 
 // ======================= gaussian table fill ================================
 __global__ void gaussian_fill_kernel(uint64_t seed, int k, int64_t row0, int64_t nrows,
-                                     uint8_t* __restrict__ theta, int64_t ldt) {
+                                     uint8_t* __restrict__ theta, int64_t ldt, int bits) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int q = blockIdx.y;  // quad of sketch rows 4q..4q+3
   if (i >= nrows) return;
@@ -234,8 +234,10 @@ __global__ void gaussian_fill_kernel(uint64_t seed, int k, int64_t row0, int64_t
   for (int t = 0; t < 4; ++t) {
     const int r = 4 * q + t;
     if (r < k) {
-      double v = rint(2048.0 * g[t]);
-      v = fmin(fmax(v, -32767.0), 32767.0);
+      // bits == 8: the same normal on the int8 grid 2^-5, stored as q = 256 q8
+      // (hi plane = q8, lo plane = 0: the tensor sketch then skips the lo plane)
+      double v = bits == 8 ? 256.0 * fmin(fmax(rint(32.0 * g[t]), -127.0), 127.0)
+                           : fmin(fmax(rint(2048.0 * g[t]), -32767.0), 32767.0);
       const int q = (int)v;
       theta[gl::q_offset(0, r, i, ldt)] = (uint8_t)(q >> 8);   // hi plane (signed byte)
       theta[gl::q_offset(1, r, i, ldt)] = (uint8_t)(q & 255);  // lo plane
@@ -935,13 +937,14 @@ int sparse_sketch(int64_t n, int ncols, const TX* X, int64_t ldx, int64_t row0, 
 
 // ============================== entry points ================================
 int gaussian_fill(uint64_t seed, int k, int64_t row0, int64_t nrows, uint8_t* theta, int64_t ldt,
-                  cudaStream_t st) {
+                  cudaStream_t st, int bits) {
+  RB_REQUIRE(bits == 16 || bits == 8, "rb_gaussian_fill: bits must be 16 or 8");
   RB_REQUIRE(k >= 1 && k <= 4 * 65535 && nrows >= 0 && ldt >= nrows && ldt % gl::kBK == 0 && theta,
              "rb_gaussian_fill: bad args (ldt must be a multiple of 128)");
   cudaMemsetAsync(theta, 0, (size_t)gl::q_bytes(k, ldt), st);  // zero padding rows / columns
   if (nrows == 0) return check_launch("rb_gaussian_fill");
   dim3 grid(ceil_div(nrows, 256), (k + 3) / 4);
-  RB_KLAUNCH gaussian_fill_kernel<<<grid, 256, 0, st>>>(seed, k, row0, nrows, theta, ldt);
+  RB_KLAUNCH gaussian_fill_kernel<<<grid, 256, 0, st>>>(seed, k, row0, nrows, theta, ldt, bits);
   return check_launch("rb_gaussian_fill");
 }
 
@@ -986,7 +989,7 @@ size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k);
 int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2, int c2,
                        int64_t n, const uint8_t* qt, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
                        double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st, bool lean = false,
-                       int dig = 6, const void* pre2 = nullptr);
+                       int dig = 6, const void* pre2 = nullptr, int qpl = 2);
 
 // [out1 | out2] = scale * (q @ [X1 | X2]).  mode 0 = auto (tensor pipe when
 // every input is binary32), 1 = fp64 CUDA cores, 2 = tensor pipe, 3 = tensor
@@ -1003,6 +1006,10 @@ int sketch_gaussian2(int xd1, const void* X1, int64_t ld1, int c1, int xd2, cons
              "rb_sketch_gaussian: bad args");
   RB_REQUIRE(n == 0 || (X1 && ld1 >= n && (c2 == 0 || (X2 && ld2 >= n)) && theta && ldt >= n),
              "rb_sketch_gaussian: bad X/theta");
+  // mode + 16: the table's lo plane is zero (8-bit operator, rb_gaussian_fill_bits
+  // with bits = 8): the tensor sketch skips it (half the table stream, half the MMAs)
+  const int qpl = (mode & 16) ? 1 : 2;
+  mode &= 15;
   RB_REQUIRE(mode >= 0 && mode <= 5, "rb_sketch_gaussian: bad mode %d", mode);
   const int dig = mode == 4 ? 4 : mode == 5 ? 3 : 6;
   if (mode == 3 && c1 + c2 <= 64)
@@ -1015,13 +1022,13 @@ int sketch_gaussian2(int xd1, const void* X1, int64_t ld1, int c1, int xd2, cons
              "rb_sketch_gaussian2_pre: the pre-encoded input needs the paired tensor form");
   if (tc && (c1 + c2 <= 64 || (pair && c2 > 0)))
     return sketch_gaussian_tc(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, theta, ldt, k, scale, out1, ldo1, out2, ldo2,
-                              acc, ws, wsb, st, false, dig, pre2);
+                              acc, ws, wsb, st, false, dig, pre2, qpl);
   if (tc) {
     int rc = sketch_gaussian_tc(xd1, X1, ld1, c1, RB_F32, nullptr, 0, 0, n, theta, ldt, k, scale, out1, ldo1,
-                                nullptr, 0, acc, ws, wsb, st, false, dig);
+                                nullptr, 0, acc, ws, wsb, st, false, dig, nullptr, qpl);
     if (rc == RB_OK)
       rc = sketch_gaussian_tc(xd2, X2, ld2, c2, RB_F32, nullptr, 0, 0, n, theta, ldt, k, scale, out2, ldo2, nullptr,
-                              0, acc, ws, wsb, st, false, dig);
+                              0, acc, ws, wsb, st, false, dig, nullptr, qpl);
     return rc;
   }
   PlaneSrc src{theta, ldt, k};

@@ -494,7 +494,9 @@ __device__ __forceinline__ void
 gauss_tc_body(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt, int k,
               const uint8_t* __restrict__ planes1, const int* __restrict__ exps1, int tiles_per_cta,
               double* __restrict__ ws1, int dbg, int pairs, int ncols2, const uint8_t* __restrict__ planes2,
-              const int* __restrict__ exps2, double* __restrict__ ws2) {
+              const int* __restrict__ exps2, double* __restrict__ ws2, int qpl = 2) {
+  // qpl == 1: the table's lo plane is zero (8-bit operator): only the hi plane
+  // is copied and multiplied (TMEM block DIG stays as the epilogue zeroed it).
   // pairs == 2: CTAs 2 mt and 2 mt + 1 own the same 128 sketch rows and K
   // range for two inputs (two column halves of > 64 columns that do not fit
   // one CTA's TMEM); launched side by side they read each q tile once from
@@ -548,8 +550,9 @@ gauss_tc_body(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt,
         const int s = t % kStages;
         if (t >= kStages) tc::mbar_wait(&S.empty[s], ((t / kStages) - 1) & 1);
         const int64_t kt = kt_beg + t;
-        tc::mbar_arrive_expect_tx(&S.full[s], kABytes + kBBytes);
-        tc::bulk_g2s(&S.a[s][0][0][0][0], qtile + kt * 2 * gl::kTileBytes, kABytes, &S.full[s]);
+        const uint32_t abytes = qpl == 1 ? kABytes / 2 : kABytes;  // the hi plane comes first in a tile
+        tc::mbar_arrive_expect_tx(&S.full[s], abytes + kBBytes);
+        tc::bulk_g2s(&S.a[s][0][0][0][0], qtile + kt * 2 * gl::kTileBytes, abytes, &S.full[s]);
         tc::bulk_g2s(&S.b[s][0][0][0], planes + kt * (int64_t)kBBytes, kBBytes, &S.full[s]);
       }
     }
@@ -589,7 +592,7 @@ gauss_tc_body(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt,
               // the first qh MMA of a segment overwrites blocks 0..5 (no
               // zeroing needed); block 6 (ql x b0 only) is zeroed by the epilogue
               tc::mma_i8(d + g * kBlk * NG, ah, b, ID_HI, (seg_first && ks == 0) ? 0u : 1u);
-              tc::mma_i8(d + g * kBlk * NG + NG, al, b, ID_LO, 1u);
+              if (qpl == 2) tc::mma_i8(d + g * kBlk * NG + NG, al, b, ID_LO, 1u);
             }
           }
         }
@@ -701,9 +704,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 gauss_tc_partial(int64_t n, int ncols, const uint8_t* __restrict__ qt, int64_t ldt, int k,
                  const uint8_t* __restrict__ planes1, const int* __restrict__ exps1, int tiles_per_cta,
                  double* __restrict__ ws1, int dbg, int pairs, int ncols2, const uint8_t* __restrict__ planes2,
-                 const int* __restrict__ exps2, double* __restrict__ ws2) {
+                 const int* __restrict__ exps2, double* __restrict__ ws2, int qpl) {
   gauss_tc_body<NP, ST, false, DIG>(n, ncols, qt, ldt, k, planes1, exps1, tiles_per_cta, ws1, dbg, pairs, ncols2,
-                                    planes2, exps2, ws2);
+                                    planes2, exps2, ws2, qpl);
 }
 
 constexpr int kLeanThreads = 192;
@@ -745,7 +748,7 @@ int dbg_flag() {
 }
 
 struct Half2 {  // the second input of a paired launch (pairs == 2)
-  int pairs = 1, ncols = 0;
+  int pairs = 1, ncols = 0, qpl = 2;
   const uint8_t* planes = nullptr;
   const int* exps = nullptr;
 };
@@ -780,7 +783,7 @@ int launch_np(int64_t n, int ncols, const uint8_t* qt, int64_t ldt, int k, const
     cudaFuncSetAttribute(gauss_tc_partial<NP, STG, DIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     RB_KLAUNCH gauss_tc_partial<NP, STG, DIG><<<dim3(mt * h2.pairs, splits), kThreads, smem, st>>>(              \
         n, ncols, qt, ldt, k, planes, exps, tpc, part, dbg_flag(), h2.pairs, h2.ncols, h2.planes, h2.exps,       \
-        part + part_bytes / sizeof(double));                                                                     \
+        part + part_bytes / sizeof(double), h2.qpl);                                                             \
   }
   if (lean && h2.pairs == 1 && DIG == gl::kXDig) {
     // two stages: shares the SM with one projection CTA
@@ -899,7 +902,7 @@ int launch_any(int NP, int dig, int64_t n, int ncols, const uint8_t* qt, int64_t
 int sketch_gaussian_tc_pair(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2,
                             int c2, int64_t n, const uint8_t* qt, int64_t ldt, int k, double scale, double* out1,
                             int64_t ldo1, double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st,
-                            int dig, const void* pre2 = nullptr) {
+                            int dig, const void* pre2 = nullptr, int qpl = 2) {
   RB_REQUIRE(c1 >= 1 && c2 >= 1 && c1 <= 64 && c2 <= 64 && k >= 1 && out1 && out2 && ldo1 >= k && ldo2 >= k,
              "rb_sketch_gaussian (tensor pair): bad args (c1 %d, c2 %d)", c1, c2);
   RB_REQUIRE(n == 0 || (X1 && ld1 >= n && X2 && ld2 >= n && qt && ldt >= n && ldt % kBK == 0),
@@ -933,6 +936,7 @@ int sketch_gaussian_tc_pair(int xd1, const void* X1, int64_t ld1, int c1, int xd
     h2.ncols = c2;
     h2.planes = pl2;
     h2.exps = ex2;
+    h2.qpl = qpl;
     const int rc = launch_any(NP, dig, n, c1, qt, ldt, k, pl1, ex1, part, part_b, &splits, st, h2, false);
     if (rc != RB_OK) return rc;
   }
@@ -989,13 +993,13 @@ size_t gauss_tc_ws_bytes(int64_t n, int ncols, int k) {
 int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, const void* X2, int64_t ld2, int c2,
                        int64_t n, const uint8_t* qt, int64_t ldt, int k, double scale, double* out1, int64_t ldo1,
                        double* out2, int64_t ldo2, int acc, void* ws, size_t wsb, cudaStream_t st, bool lean, int dig,
-                       const void* pre2) {
+                       const void* pre2, int qpl) {
   const int ncols = c1 + c2;
   RB_REQUIRE(dig == 6 || dig == 4 || dig == 3, "rb_sketch_gaussian (tensor): digits must be 6, 4 or 3 (got %d)", dig);
   RB_REQUIRE(!pre2 || ncols > 64, "rb_sketch_gaussian (tensor): a pre-encoded second input needs the paired form");
   if (ncols > 64)
     return sketch_gaussian_tc_pair(xd1, X1, ld1, c1, xd2, X2, ld2, c2, n, qt, ldt, k, scale, out1, ldo1, out2, ldo2,
-                                   acc, ws, wsb, st, dig, pre2);
+                                   acc, ws, wsb, st, dig, pre2, qpl);
   RB_REQUIRE(c1 >= 1 && c2 >= 0 && ncols <= 64 && k >= 1 && ldo1 >= k && out1 && (c2 == 0 || (out2 && ldo2 >= k)),
              "rb_sketch_gaussian (tensor): bad args (c1 %d, c2 %d)", c1, c2);
   RB_REQUIRE(n == 0 || (X1 && ld1 >= n && (c2 == 0 || (X2 && ld2 >= n)) && qt && ldt >= n && ldt % kBK == 0),
@@ -1015,7 +1019,9 @@ int sketch_gaussian_tc(int xd1, const void* X1, int64_t ld1, int c1, int xd2, co
     dim3 g(nchunks, NP / 2);
     if (xd1 == RB_F32) launch_split<float>(xd2, g, n, c1, X1, ld1, c2, X2, ld2, NP, planes, exps, st, dig);
     else launch_split<double>(xd2, g, n, c1, X1, ld1, c2, X2, ld2, NP, planes, exps, st, dig);
-    const int rc = launch_any(NP, dig, n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st, Half2(), lean);
+    Half2 h1;
+    h1.qpl = qpl;
+    const int rc = launch_any(NP, dig, n, ncols, qt, ldt, k, planes, exps, part, part_b, &splits, st, h1, lean);
     if (rc != RB_OK) return rc;
   }
   const int64_t tot = (int64_t)k * ncols;

@@ -697,7 +697,7 @@ class RbgsSweep:
             pre2, ev = pre
             torch.cuda.current_stream(self.device).wait_event(ev)
         D.sketch_gaussian2(A, B, tab["theta"], tab["ldt"], self.theta.k,
-                           1.0 / (sketching.GAUSS_GRID * math.sqrt(self.theta.k)), outA, outB,
+                           sketching.gauss_scale(self.theta), outA, outB,
                            False, self._gmode, pre2=pre2)
         self._reduce(outA, outB)
 
@@ -708,7 +708,7 @@ class RbgsSweep:
         paired sketch [Q'_i | W_(i+1)] that follows it.  Returns (buffer,
         event) or None when the paired tensor form will not be taken."""
         if not (PREPASS_OVERLAP and self._fusable(slot, Wn) and slot.shape[1] + Wn.shape[1] > 64
-                and self._gmode in ("auto", "tensor", "tensor4", "tensor3") and Wn.shape[0] >= 1):
+                and self._gmode.split("+")[0] in ("auto", "tensor", "tensor4", "tensor3") and Wn.shape[0] >= 1):
             return None
         dev = self.device
         nb = D.gauss_prepass_bytes(Wn.shape[0], Wn.shape[1], slot.shape[1], self._gmode)
@@ -758,7 +758,7 @@ class RbgsSweep:
             if ev is not None:
                 side.wait_event(ev)
             D.sketch_gaussian(Wn, tab["theta"], tab["ldt"], self.theta.k,
-                              1.0 / (sketching.GAUSS_GRID * math.sqrt(self.theta.k)), Pn, False, "lean")
+                              sketching.gauss_scale(self.theta), Pn, False, "lean")
             done = torch.cuda.Event()
             done.record(side)
         return done

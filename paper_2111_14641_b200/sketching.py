@@ -121,7 +121,7 @@ class SketchOperator:
             ldt = max(-(-nrows // 128) * 128, 128)
             theta = torch.empty((2 * (-(-self.k // 128)) * 128, ldt), dtype=torch.uint8, device=dev)
             with torch.cuda.device(dev):
-                D.gaussian_fill(self.seed, self.k, row0, nrows, theta, ldt)
+                D.gaussian_fill(self.seed, self.k, row0, nrows, theta, ldt, getattr(self, "theta_bits", 16))
             tab = dict(theta=theta, ldt=ldt)
         elif self.kind == "sparse_sign":
             with torch.cuda.device(dev):
@@ -139,7 +139,7 @@ class _ExtendedSketchOperator(SketchOperator):
     _allowed = KINDS + EXTENDED_KINDS
 
 
-def gaussian_operator(k: int, n: int, seed: int, digits: int = 6) -> SketchOperator:
+def gaussian_operator(k: int, n: int, seed: int, digits: int = 6, theta_bits: int = 16) -> SketchOperator:
     """Dense gaussian sketch, entries q / (2048 sqrt(k)) with q the int16
     Box-Muller normal of Philox4x32-10.
 
@@ -147,12 +147,28 @@ def gaussian_operator(k: int, n: int, seed: int, digits: int = 6) -> SketchOpera
             keeps: 6 (default; fixed point at 2^-47 of each 16384-row chunk's
             max -- binary64-grade sketches), 4 (2^-31) or 3 (2^-23); the
             tensor work is proportional to it.  The operator (Theta) is the
-            same; only the rounding of X inside Theta X changes."""
+            same; only the rounding of X inside Theta X changes.
+    theta_bits  16 (default): the normals on the int16 grid 2^-11.  8: the
+            SAME normals on the int8 grid 2^-5 (255 levels, clamped at
+            +-127/32) -- a different, coarser-grained operator (still iid,
+            symmetric, unit variance to 1e-4: a valid embedding), whose
+            table needs one byte plane: half the table stream and half the
+            tensor work.  Opt-in; the oracle builds the same operator
+            (OracleSketch(..., bits=8))."""
     if digits not in (6, 4, 3):
         raise ValueError("digits must be 6, 4 or 3")
+    if theta_bits not in (16, 8):
+        raise ValueError("theta_bits must be 16 or 8")
     op = _ExtendedSketchOperator("gaussian", int(k), int(n), int(seed))
     object.__setattr__(op, "digits", int(digits))
+    object.__setattr__(op, "theta_bits", int(theta_bits))
     return op
+
+
+def gauss_scale(theta) -> float:
+    """1 / (grid sqrt(k)) of a gaussian operator's table (q units)."""
+    grid = 8192.0 if getattr(theta, "theta_bits", 16) == 8 else GAUSS_GRID
+    return 1.0 / (grid * math.sqrt(theta.k))
 
 
 def gauss_mode(theta, digits=None) -> str:
@@ -160,7 +176,7 @@ def gauss_mode(theta, digits=None) -> str:
     if GAUSS_MODE != "auto":
         return GAUSS_MODE
     d = digits or getattr(theta, "digits", 6)
-    return {6: "auto", 4: "tensor4", 3: "tensor3"}[d]
+    return {6: "auto", 4: "tensor4", 3: "tensor3"}[d] + ("+q8" if getattr(theta, "theta_bits", 16) == 8 else "")
 
 
 def sparse_sign_operator(k: int, n: int, seed: int, nnz: int = 8) -> SketchOperator:
@@ -204,7 +220,7 @@ def sketch_into(theta: SketchOperator, X: torch.Tensor, out: torch.Tensor, row0:
     elif theta.kind == "rademacher":
         D.sketch_signs(X, tab["bits"], tab["ldb"], k, 1.0 / math.sqrt(k), out, accumulate)
     elif theta.kind == "gaussian":
-        D.sketch_gaussian(X, tab["theta"], tab["ldt"], k, 1.0 / (GAUSS_GRID * math.sqrt(k)), out,
+        D.sketch_gaussian(X, tab["theta"], tab["ldt"], k, gauss_scale(theta), out,
                           accumulate, gauss or gauss_mode(theta))
     else:
         # the pre-bucketed table of exactly this row range (cached on the

@@ -377,3 +377,42 @@ def test_c3_families_tensor_pipe_projection_vs_oracle(D, family):
     assert _same_order(r["fact"][0], r["fact"][1]) and _same_order(r["condQ"][0], r["condQ"][1]), r
     if family == "companion":
         assert r["delta"][0] < 0.1 and _same_order(r["delta"][0], r["delta"][1], 3.0), r
+
+
+def test_gaussian_8bit_operator_vs_oracle(D):
+    """The opt-in 8-bit gaussian operator (theta_bits = 8: the same normals on
+    the grid 2^-5, one byte plane, half the tensor work): the device table and
+    both sketch paths against the oracle's operator of the same definition
+    (single call, paired call, binary64 input on the CUDA-core path), and a
+    C2-family sweep with it against the oracle sweep (R within 1e-5)."""
+    from paper_2111_14641_b200 import _device as Dv
+    from paper_2111_14641_b200 import sketching, workloads
+
+    n, k = 40_000, 256
+    g = np.random.Generator(np.random.Philox(8))
+    op = sketching.gaussian_operator(k, n, 11, theta_bits=8)
+    oo = osk.OracleSketch("gaussian", k, n, 11, bits=8)
+    q8 = osk.gaussian_int16(11, k, np.arange(2000), 8)
+    assert np.abs(q8).max() <= 127 and abs(q8.mean()) < 0.5 and abs(q8.astype(np.float64).var() / 1024.0 - 1.0) < 0.02
+    for cols in (40, 80):
+        X = (g.standard_normal((n, cols)) * np.logspace(0, -5, cols)).astype(np.float32)
+        want = osk.apply(oo, X.astype(np.float64))
+        got = sketching.apply(op, torch.from_numpy(np.asfortranarray(X)).cuda().t().contiguous().t()).data
+        assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want), cols
+        got64 = sketching.apply(op, X.astype(np.float64)).data  # binary64 input: CUDA-core path
+        assert np.linalg.norm(got64 - want) <= 1e-13 * np.linalg.norm(want), cols
+    # paired call (the sweep's [Q'_i | W_(i+1)] form)
+    Xd = torch.from_numpy(np.asfortranarray(X)).cuda().t().contiguous().t()
+    tab = op.device_tables(Xd.device, 0, n)
+    o1, o2 = Dv.empty_cm(k, 40, torch.float64, Xd.device), Dv.empty_cm(k, 40, torch.float64, Xd.device)
+    Dv.sketch_gaussian2(Xd[:, :40], Xd[:, 40:], tab["theta"], tab["ldt"], k, sketching.gauss_scale(op), o1, o2, False,
+                        sketching.gauss_mode(op))
+    pair = np.hstack([o1.cpu().numpy(), o2.cpu().numpy()])
+    assert np.linalg.norm(pair - want) <= 1e-12 * np.linalg.norm(want)
+    # sweep on the trig family
+    ns, m, p, ks = 32768, 400, 40, 1600
+    W = workloads.trig_host(ns, m, 7)
+    r = _sweep_pair(W, sketching.gaussian_operator(ks, ns, 11, theta_bits=8),
+                    osk.materialize(osk.OracleSketch("gaussian", ks, ns, 11, bits=8)), m, p, "coarse")
+    assert r["rel_R"] <= 1e-5, r
+    assert _same_order(r["fact"][0], r["fact"][1]) and _same_order(r["condQ"][0], r["condQ"][1], 1.5)
