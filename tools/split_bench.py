@@ -31,13 +31,14 @@ def main():
     g = torch.Generator(device=dev).manual_seed(3)
     W[:, :p] = torch.randn(n, p, device=dev, generator=g) * torch.logspace(0, -6, p, device=dev)
     X1, X2 = W[:, :p], W[:, p:]
-    theta = sketching.gaussian_operator(k, n, 11)
+    theta = sketching.gaussian_operator(k, n, 11, theta_bits=int(os.environ.get("SB_THETA_BITS", "16")))
     tab = theta.device_tables(dev, 0, n)
     o1 = torch.empty((p, k), dtype=torch.float64, device=dev).t()
     o2 = torch.empty((p, k), dtype=torch.float64, device=dev).t()
 
     def call():
-        D.sketch_gaussian2(X1, X2, tab["theta"], tab["ldt"], k, 1.0, o1, o2, mode=os.environ.get("SB_MODE", "tensor"))
+        D.sketch_gaussian2(X1, X2, tab["theta"], tab["ldt"], k, 1.0, o1, o2,
+                           mode=os.environ.get("SB_MODE", "tensor") + ("+q8" if theta.theta_bits == 8 else ""))
 
     for _ in range(3):
         call()
